@@ -1,0 +1,145 @@
+/*
+ * hetoc_b200.h -- C ABI of the B200-native batched-hash engine.
+ *
+ * Plain pointers and sizes only (no torch / CUDA types in the signatures;
+ * `stream` is an opaque cudaStream_t passed as void*).  Every entry point
+ * returns an hb_status; on failure hb_last_error() (thread-local) says why.
+ * The Python package paper_2407_09333_b200.crypto binds these with ctypes,
+ * mirroring the reference API (hetoc.crypto); INTEGRATION.md shows the
+ * binding.
+ *
+ * Which reference interface each entry point replaces (paths relative to the
+ * reference repo root):
+ *
+ *   hb_hash_fixed     batch_digest(alg, data)            pkg/src/hetoc/crypto/batch.py:274-290
+ *                     (+ the hyper staging contract of _emit_dev_launch,
+ *                      pkg/src/hetoc/passes/lower_hyper_for.py:279-368, the
+ *                      message-range split partition_range,
+ *                      pkg/src/hetoc/passes/partition.py:17-31, and the
+ *                      capacity sub-batching of _run_group,
+ *                      pkg/src/hetoc/runtime/executor.py:603-699)
+ *   hb_hash_varlen    digest(alg, msg) mapped over an offsets array
+ *                     (pkg/src/hetoc/crypto/batch.py:102-109; the reference has
+ *                      no variable-length batch layout)
+ *   hb_hash_fixed_dev _CHUNK_FN[alg](rows) on device-resident rows
+ *                     pkg/src/hetoc/crypto/batch.py:263 / dev.launch body,
+ *                     pkg/src/hetoc/runtime/executor.py:562-599
+ *   hb_hash_decimal   hash_batch(alg, gen_messages(start, count, width))
+ *                     pkg/src/hetoc/crypto/batch.py:86-99, :293-316
+ *   hb_partition_range partition_range  pkg/src/hetoc/passes/partition.py:17-31
+ *   hb_device_count / hb_device_info   detect_hardware
+ *                     pkg/src/hetoc/runtime/devices.py:169-184
+ *   hb_digest_len     DIGEST_LEN         pkg/src/hetoc/crypto/batch.py:23
+ */
+#ifndef HETOC_B200_H
+#define HETOC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HB_ABI_VERSION 1
+
+typedef enum {
+    HB_OK = 0,
+    HB_ERR_ALG = 1,      /* unknown algorithm          -> UnknownAlgorithmError */
+    HB_ERR_INVAL = 2,    /* bad argument               -> ValueError            */
+    HB_ERR_CUDA = 3,     /* CUDA runtime/driver error  -> RuntimeError          */
+    HB_ERR_NOMEM = 4,    /* device or pinned allocation failed                  */
+    HB_ERR_NODEV = 5     /* no CUDA device / bad device ordinal                 */
+} hb_status;
+
+typedef enum { HB_SHA1 = 0, HB_MD5 = 1, HB_SM3 = 2 } hb_alg;
+
+/* flags */
+#define HB_FLAG_NO_TMA   0x1u  /* fixed width: direct-load kernel instead of TMA staging */
+#define HB_FLAG_NO_SORT  0x2u  /* varlen: skip the length-bucket sort                    */
+#define HB_FLAG_SYNC_H2D 0x4u  /* engine: no copy/compute overlap (diagnostics)          */
+
+typedef struct {
+    double total_ms;       /* host wall time of the call                              */
+    double kernel_ms;      /* max over GPUs of summed hash-kernel device time         */
+    double h2d_ms;         /* max over GPUs of summed H2D device time                 */
+    double d2h_ms;         /* max over GPUs of summed D2H device time                 */
+    uint64_t h2d_bytes;    /* total bytes copied host -> device                       */
+    uint64_t d2h_bytes;    /* total bytes copied device -> host                       */
+    uint64_t chunks;       /* sub-batches (chunks) executed over all GPUs             */
+    uint64_t launches;     /* kernels launched by this call                           */
+} hb_timing;
+
+typedef struct {
+    int ordinal;
+    int sm_count;
+    int cc_major, cc_minor;
+    uint64_t total_mem;
+    uint64_t free_mem;
+    int pci_bus_id;
+    int clock_khz;
+    char name[96];
+} hb_device_info_t;
+
+/* ---- introspection ---------------------------------------------------- */
+int hb_abi_version(void);
+const char *hb_last_error(void);          /* thread-local message of the last failure */
+int hb_digest_len(int alg);               /* 20 / 16 / 32, or -1                      */
+int hb_device_count(int *n);
+int hb_device_info(int ordinal, hb_device_info_t *info);
+uint64_t hb_launch_count(void);           /* kernels launched by this process so far   */
+
+/* ---- host-buffer engine (staging + sharding + chunked streaming) ------- */
+/* Hash n fixed-width messages (row i = msgs[i*msg_len, (i+1)*msg_len)) into
+ * out[i*dlen, (i+1)*dlen).  [0,n) is split over gpus[0..n_gpus) with
+ * partition_range's cumulative round-half-up rule and equal ratios; each GPU
+ * streams its slice through a ring of pinned/device chunk buffers (H2D, kernel,
+ * D2H overlapped on separate streams).  Host buffers may be pageable or
+ * pinned (pinned is copied directly).  gpus == NULL / n_gpus == 0 means "all
+ * devices".  t may be NULL.  msg_len 0 hashes empty messages.                */
+int hb_hash_fixed(int alg, const uint8_t *msgs, uint64_t n, uint64_t msg_len, uint8_t *out,
+                  const int *gpus, int n_gpus, uint32_t flags, hb_timing *t);
+
+/* Variable-length: message i = data[offsets[i], offsets[i+1]); offsets has n+1
+ * non-decreasing entries, offsets[0] may be non-zero.                        */
+int hb_hash_varlen(int alg, const uint8_t *data, const uint64_t *offsets, uint64_t n, uint8_t *out,
+                   const int *gpus, int n_gpus, uint32_t flags, hb_timing *t);
+
+/* Paper workload (gen_messages): digests of the zero-padded decimal strings
+ * of start .. start+count-1, width bytes each, generated on the GPU.       */
+int hb_hash_decimal(int alg, uint64_t start, uint64_t count, int width, uint8_t *out,
+                    const int *gpus, int n_gpus, uint32_t flags, hb_timing *t);
+
+/* ---- device-resident (kernel-only) entry points ------------------------ */
+/* All pointers are device pointers on `gpu`; work is enqueued on `stream`
+ * (NULL = legacy default stream) and NOT synchronised.                       */
+int hb_hash_fixed_dev(int alg, int gpu, const void *d_msgs, uint64_t n, uint64_t msg_len, void *d_out,
+                      void *stream, uint32_t flags);
+/* d_data must be readable up to round_up(d_offsets[n] - offset_base, 4).
+ * d_scratch: hb_varlen_scratch_bytes(n) bytes, or NULL (unsorted).          */
+int hb_hash_varlen_dev(int alg, int gpu, const void *d_data, uint64_t data_bytes, const uint64_t *d_offsets,
+                       uint64_t offset_base, uint64_t n, void *d_out, void *d_scratch, void *stream,
+                       uint32_t flags);
+uint64_t hb_varlen_scratch_bytes(uint64_t n);
+int hb_hash_decimal_dev(int alg, int gpu, uint64_t start, uint64_t count, int width, void *d_out, void *stream);
+
+/* Synthetic message bytes: the counter-based generator (seed, byte_offset
+ * multiple of 8) shared with the CPU oracle.  d_buf 8-byte aligned.          */
+int hb_fill_random_dev(int gpu, void *d_buf, uint64_t nbytes, uint64_t seed, uint64_t byte_offset, void *stream);
+/* gen_messages bytes on the device (count*width bytes).                     */
+int hb_gen_decimal_dev(int gpu, uint64_t start, uint64_t count, int width, void *d_out, void *stream);
+
+/* ---- staging memory ---------------------------------------------------- */
+void *hb_alloc_pinned(uint64_t bytes);   /* page-locked, portable; NULL on failure */
+int hb_free_pinned(void *p);
+int hb_sync_device(int gpu);
+/* Release every cached per-GPU context (streams, chunk buffers).            */
+int hb_shutdown(void);
+
+/* ---- task splitting ---------------------------------------------------- */
+/* partition_range(lb, ub, ratios[0..k)): writes k+1 bounds.                 */
+int hb_partition_range(int64_t lb, int64_t ub, const double *ratios, int k, int64_t *bounds_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HETOC_B200_H */

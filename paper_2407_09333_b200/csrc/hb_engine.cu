@@ -1,0 +1,717 @@
+// hb_engine.cu -- host-side engine and C ABI of the batched-hash engine.
+//
+// This is the B200 realisation of the reference's *hyper* data management and
+// task splitting for crypto.hash_batch:
+//   * message-range split across GPUs   = partition_range (passes/partition.py:17-31)
+//                                          as applied by lower_loop (passes/lower_hyper_for.py:207-254)
+//   * per-device staging                = _emit_dev_launch (passes/lower_hyper_for.py:279-368):
+//       hyper.alloc(slice) -> hyper.memcpy(src_off = s*stride) -> dev.launch[0,n) offset s
+//       -> hyper.memcpy(dst_off = s*dlen) -> hyper.dealloc
+//   * capacity sub-batching             = _run_group (runtime/executor.py:603-699),
+//       here a ring of kSlots chunk buffers per GPU whose H2D / kernel / D2H run
+//       on separate streams so copies overlap compute.
+// One host thread per GPU drives its shard; all CUDA work of a shard is
+// asynchronous on that GPU's slot streams.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/hetoc_b200.h"
+#include "hb_internal.h"
+
+namespace hb {
+uint64_t launches_total();
+
+// ------------------------------------------------------------ error state --
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define HB_CK(expr)                                                                                        \
+    do {                                                                                                   \
+        cudaError_t e_ = (expr);                                                                           \
+        if (e_ != cudaSuccess) {                                                                           \
+            const char* extra_ = (e_ == cudaErrorNotSupported || e_ == cudaErrorInvalidValue) ? tma_error() : ""; \
+            return fail(e_ == cudaErrorMemoryAllocation ? HB_ERR_NOMEM : HB_ERR_CUDA, "%s failed: %s %s (%s:%d)", \
+                        #expr, cudaGetErrorString(e_), extra_, __FILE__, __LINE__);                        \
+        }                                                                                                  \
+    } while (0)
+
+static int digest_len(int alg) {
+    switch (alg) {
+    case HB_SHA1: return 20;
+    case HB_MD5: return 16;
+    case HB_SM3: return 32;
+    default: return -1;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d) {
+        cudaGetDevice(&prev);
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+static int device_count() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// ---------------------------------------------------------------- tuning --
+static uint64_t env_u64(const char* name, uint64_t dflt) {
+    const char* v = getenv(name);
+    if (!v || !*v) return dflt;
+    char* end = nullptr;
+    unsigned long long x = strtoull(v, &end, 0);
+    return (end && *end == '\0' && x > 0) ? (uint64_t)x : dflt;
+}
+static uint64_t chunk_bytes() { return env_u64("HB_CHUNK_BYTES", 256ull << 20); }
+static int memcpy_threads(int n_gpus) {
+    uint64_t t = env_u64("HB_MEMCPY_THREADS", 0);
+    if (t) return (int)t;
+    unsigned hw = std::thread::hardware_concurrency();
+    int per = (int)(hw ? hw : 8) / std::max(1, n_gpus);
+    return std::max(1, std::min(8, per));
+}
+
+// Host memcpy split across threads (pageable <-> pinned staging).
+static void parallel_memcpy(void* dst, const void* src, uint64_t bytes, int nthreads) {
+    if (bytes < (8ull << 20) || nthreads <= 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> ts;
+    const uint64_t per = ((bytes / nthreads) + 4095) & ~4095ull;
+    for (int k = 0; k < nthreads; ++k) {
+        const uint64_t lo = per * k;
+        if (lo >= bytes) break;
+        const uint64_t len = std::min(per, bytes - lo);
+        ts.emplace_back([=] { memcpy((uint8_t*)dst + lo, (const uint8_t*)src + lo, len); });
+    }
+    for (auto& t : ts) t.join();
+}
+
+static bool is_pinned(const void* p, uint64_t bytes) {
+    if (!p || !bytes) return false;
+    const void* probes[2] = {p, (const uint8_t*)p + bytes - 1};
+    for (const void* q : probes) {
+        cudaPointerAttributes a;
+        if (cudaPointerGetAttributes(&a, q) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        if (a.type != cudaMemoryTypeHost) return false;
+    }
+    return true;
+}
+
+// ------------------------------------------------------- per-GPU context --
+constexpr int kSlots = 3;
+
+struct DevBuf {
+    void* p = nullptr;
+    uint64_t cap = 0;
+    cudaError_t ensure(uint64_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const uint64_t want = (bytes + 4095) & ~4095ull;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+};
+struct HostBuf {
+    void* p = nullptr;
+    uint64_t cap = 0;
+    cudaError_t ensure(uint64_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        const uint64_t want = (bytes + 4095) & ~4095ull;
+        cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocPortable);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+};
+
+struct Slot {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[6] = {};  // h2d0, h2d1, k0, k1, d2h0, d2h1
+    DevBuf d_in, d_out, d_off, d_scratch;
+    HostBuf h_in, h_out, h_off;
+    bool in_use = false;
+    bool has_h2d = false;
+    // deferred copy-out (pageable destination)
+    uint8_t* pend_dst = nullptr;
+    uint64_t pend_bytes = 0;
+};
+
+struct GpuCtx {
+    int dev = -1;
+    std::mutex mu;
+    bool ready = false;
+    Slot slots[kSlots];
+};
+
+static std::mutex g_ctx_mu;
+static std::vector<std::unique_ptr<GpuCtx>> g_ctx;
+
+static int get_ctx(int dev, GpuCtx** out) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    const int nd = device_count();
+    if (dev < 0 || dev >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", dev, nd);
+    if ((int)g_ctx.size() < nd) g_ctx.resize(nd);
+    if (!g_ctx[dev]) {
+        g_ctx[dev].reset(new GpuCtx());
+        g_ctx[dev]->dev = dev;
+    }
+    *out = g_ctx[dev].get();
+    return HB_OK;
+}
+
+static int ctx_init(GpuCtx& c) {  // caller holds c.mu and has set the device
+    if (c.ready) return HB_OK;
+    for (Slot& s : c.slots) {
+        HB_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+        for (auto& e : s.ev) HB_CK(cudaEventCreate(&e));
+    }
+    c.ready = true;
+    return HB_OK;
+}
+
+struct ShardStats {
+    double kernel_ms = 0, h2d_ms = 0, d2h_ms = 0;
+    uint64_t h2d_bytes = 0, d2h_bytes = 0, chunks = 0, launches = 0;
+    int status = HB_OK;
+    std::string err;
+};
+
+// Wait for a slot's previous chunk, land its deferred copy-out, bank timings.
+static int retire_slot(Slot& s, ShardStats& st, int mt) {
+    if (!s.in_use) return HB_OK;
+    HB_CK(cudaEventSynchronize(s.ev[5]));
+    float ms = 0;
+    if (s.has_h2d && cudaEventElapsedTime(&ms, s.ev[0], s.ev[1]) == cudaSuccess) st.h2d_ms += ms;
+    if (cudaEventElapsedTime(&ms, s.ev[2], s.ev[3]) == cudaSuccess) st.kernel_ms += ms;
+    if (cudaEventElapsedTime(&ms, s.ev[4], s.ev[5]) == cudaSuccess) st.d2h_ms += ms;
+    if (s.pend_bytes) parallel_memcpy(s.pend_dst, s.h_out.p, s.pend_bytes, mt);
+    s.pend_bytes = 0;
+    s.in_use = false;
+    return HB_OK;
+}
+
+// Stage a host range into a slot's device buffer (direct DMA when pinned).
+static int stage_in(Slot& s, DevBuf& dst, HostBuf& stage, const void* src, uint64_t bytes, bool pinned, int mt) {
+    if (!bytes) return HB_OK;
+    if (pinned) {
+        HB_CK(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, s.stream));
+    } else {
+        HB_CK(stage.ensure(bytes));
+        parallel_memcpy(stage.p, src, bytes, mt);
+        HB_CK(cudaMemcpyAsync(dst.p, stage.p, bytes, cudaMemcpyHostToDevice, s.stream));
+    }
+    return HB_OK;
+}
+
+static int stage_out(Slot& s, uint8_t* dst, uint64_t bytes, bool pinned) {
+    if (!bytes) return HB_OK;
+    if (pinned) {
+        HB_CK(cudaMemcpyAsync(dst, s.d_out.p, bytes, cudaMemcpyDeviceToHost, s.stream));
+    } else {
+        HB_CK(s.h_out.ensure(bytes));
+        HB_CK(cudaMemcpyAsync(s.h_out.p, s.d_out.p, bytes, cudaMemcpyDeviceToHost, s.stream));
+        s.pend_dst = dst;
+        s.pend_bytes = bytes;
+    }
+    return HB_OK;
+}
+
+// A unit of work for one GPU: the shard [lo, hi) of the global message range.
+struct ShardJob {
+    int kind = 0;  // 0 fixed, 1 varlen, 2 decimal
+    int alg = 0;
+    int dev = 0;
+    uint64_t lo = 0, hi = 0;
+    // fixed
+    const uint8_t* msgs = nullptr;
+    uint64_t msg_len = 0;
+    // varlen
+    const uint8_t* data = nullptr;
+    const uint64_t* offsets = nullptr;
+    // decimal
+    uint64_t start = 0;
+    int width = 0;
+    uint8_t* out = nullptr;
+    bool in_pinned = false, off_pinned = false, out_pinned = false;
+    uint32_t flags = 0;
+    int mt = 1;
+};
+
+static int run_shard_locked(GpuCtx& c, const ShardJob& j, ShardStats& st) {
+    int rc = ctx_init(c);
+    if (rc) return rc;
+    const int dlen = digest_len(j.alg);
+    const uint64_t budget = chunk_bytes();
+    uint64_t slot_k = 0;
+    const uint64_t l0 = hb::launches_total();
+    uint64_t i = j.lo;
+    while (i < j.hi) {
+        // ---- plan the chunk [i, e)
+        uint64_t e, in_bytes = 0, in_off = 0;
+        if (j.kind == 0) {
+            uint64_t per = j.msg_len ? std::max<uint64_t>(1, budget / j.msg_len) : (j.hi - j.lo);
+            if (per >= 256) per &= ~127ull;
+            e = std::min(j.hi, i + per);
+            in_bytes = (e - i) * j.msg_len;
+            in_off = i * j.msg_len;
+        } else if (j.kind == 1) {
+            const uint64_t lim = j.offsets[i] + budget;
+            const uint64_t* ub = std::upper_bound(j.offsets + i + 1, j.offsets + j.hi + 1, lim);
+            e = (uint64_t)(ub - j.offsets) - 1;  // last index whose offset <= lim
+            if (e <= i) e = i + 1;                // one over-budget message: its own chunk
+            const uint64_t max_msgs = std::max<uint64_t>(1024, budget / 64);
+            e = std::min(e, i + max_msgs);
+            in_off = j.offsets[i];
+            in_bytes = j.offsets[e] - j.offsets[i];
+        } else {
+            const uint64_t per = std::max<uint64_t>(1, budget / 32);
+            e = std::min(j.hi, i + per);
+        }
+        const uint64_t cn = e - i;
+        Slot& s = c.slots[slot_k % kSlots];
+        ++slot_k;
+        rc = retire_slot(s, st, j.mt);
+        if (rc) return rc;
+        HB_CK(s.d_out.ensure(cn * dlen));
+        if (in_bytes) HB_CK(s.d_in.ensure(in_bytes + 64));
+        s.has_h2d = false;
+        // ---- copy in
+        HB_CK(cudaEventRecord(s.ev[0], s.stream));
+        if (j.kind == 0 && in_bytes) {
+            rc = stage_in(s, s.d_in, s.h_in, j.msgs + in_off, in_bytes, j.in_pinned, j.mt);
+            if (rc) return rc;
+            s.has_h2d = true;
+        } else if (j.kind == 1) {
+            HB_CK(s.d_off.ensure((cn + 1) * 8));
+            rc = stage_in(s, s.d_off, s.h_off, j.offsets + i, (cn + 1) * 8, j.off_pinned, j.mt);
+            if (rc) return rc;
+            if (in_bytes) {
+                rc = stage_in(s, s.d_in, s.h_in, j.data + in_off, in_bytes, j.in_pinned, j.mt);
+                if (rc) return rc;
+            }
+            s.has_h2d = true;
+        }
+        HB_CK(cudaEventRecord(s.ev[1], s.stream));
+        st.h2d_bytes += in_bytes + (j.kind == 1 ? (cn + 1) * 8 : 0);
+        // ---- kernel
+        HB_CK(cudaEventRecord(s.ev[2], s.stream));
+        uint8_t* dout = static_cast<uint8_t*>(s.d_out.p);
+        if (j.kind == 0) {
+            HB_CK(launch_fixed(j.alg, static_cast<const uint8_t*>(s.d_in.p), cn, j.msg_len, dout, s.stream, j.flags));
+        } else if (j.kind == 1) {
+            void* scratch = nullptr;
+            if (!(j.flags & HB_FLAG_NO_SORT)) {
+                HB_CK(s.d_scratch.ensure(varlen_scratch_bytes(cn)));
+                scratch = s.d_scratch.p;
+            }
+            HB_CK(launch_varlen(j.alg, static_cast<const uint8_t*>(s.d_in.p), in_bytes,
+                                static_cast<const uint64_t*>(s.d_off.p), j.offsets[i], cn, dout, scratch, s.stream,
+                                j.flags));
+        } else {
+            HB_CK(launch_decimal(j.alg, j.start + i, cn, j.width, dout, s.stream));
+        }
+        HB_CK(cudaEventRecord(s.ev[3], s.stream));
+        // ---- copy out (dst_off = s*dlen)
+        HB_CK(cudaEventRecord(s.ev[4], s.stream));
+        rc = stage_out(s, j.out + i * dlen, cn * dlen, j.out_pinned);
+        if (rc) return rc;
+        HB_CK(cudaEventRecord(s.ev[5], s.stream));
+        st.d2h_bytes += cn * dlen;
+        st.chunks += 1;
+        s.in_use = true;
+        if (j.flags & HB_FLAG_SYNC_H2D) {
+            rc = retire_slot(s, st, j.mt);
+            if (rc) return rc;
+        }
+        i = e;
+    }
+    for (Slot& s : c.slots) {
+        rc = retire_slot(s, st, j.mt);
+        if (rc) return rc;
+    }
+    st.launches = hb::launches_total() - l0;
+    return HB_OK;
+}
+
+static void run_shard(const ShardJob& j, ShardStats& st) {
+    GpuCtx* c = nullptr;
+    int rc = get_ctx(j.dev, &c);
+    if (rc == HB_OK) {
+        std::lock_guard<std::mutex> lk(c->mu);
+        DeviceGuard g(j.dev);
+        rc = run_shard_locked(*c, j, st);
+        if (rc != HB_OK) {
+            // leave the context reusable: drain whatever is in flight
+            for (Slot& s : c->slots) {
+                if (s.stream) cudaStreamSynchronize(s.stream);
+                s.in_use = false;
+                s.pend_bytes = 0;
+            }
+            cudaGetLastError();
+        }
+    }
+    st.status = rc;
+    if (rc != HB_OK) st.err = g_err;
+}
+
+// partition_range, pkg/src/hetoc/passes/partition.py:17-31 (same double
+// arithmetic as the Python: cum += r; b = lb + floor(n*cum + 0.5)).
+static int partition(int64_t lb, int64_t ub, const double* ratios, int k, int64_t* bounds) {
+    if (lb > ub) return fail(HB_ERR_INVAL, "range [%lld, %lld) is inverted", (long long)lb, (long long)ub);
+    if (k < 1 || !ratios) return fail(HB_ERR_INVAL, "need at least one ratio");
+    const int64_t n = ub - lb;
+    bounds[0] = lb;
+    double cum = 0.0;
+    for (int i = 0; i < k - 1; ++i) {
+        cum += ratios[i];
+        int64_t b = lb + (int64_t)std::floor((double)n * cum + 0.5);
+        b = std::min(std::max(b, bounds[i]), ub);
+        bounds[i + 1] = b;
+    }
+    bounds[k] = ub;
+    return HB_OK;
+}
+
+static int resolve_gpus(const int* gpus, int n_gpus, std::vector<int>& out) {
+    const int nd = device_count();
+    if (nd == 0) return fail(HB_ERR_NODEV, "no CUDA device visible");
+    out.clear();
+    if (!gpus || n_gpus <= 0) {
+        for (int d = 0; d < nd; ++d) out.push_back(d);
+    } else {
+        for (int k = 0; k < n_gpus; ++k) {
+            if (gpus[k] < 0 || gpus[k] >= nd)
+                return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpus[k], nd);
+            out.push_back(gpus[k]);
+        }
+    }
+    return HB_OK;
+}
+
+// Split [0, n) over the GPUs, run one host thread per shard, merge stats.
+static int run_sharded(ShardJob proto, uint64_t n, const std::vector<int>& devs, hb_timing* t) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int k = (int)devs.size();
+    std::vector<double> ratios(k, 1.0 / k);
+    std::vector<int64_t> bounds(k + 1);
+    int rc = partition(0, (int64_t)n, ratios.data(), k, bounds.data());
+    if (rc) return rc;
+    proto.mt = memcpy_threads(k);
+    std::vector<ShardJob> jobs;
+    for (int d = 0; d < k; ++d) {
+        if (bounds[d + 1] <= bounds[d]) continue;
+        ShardJob j = proto;
+        j.dev = devs[d];
+        j.lo = (uint64_t)bounds[d];
+        j.hi = (uint64_t)bounds[d + 1];
+        jobs.push_back(j);
+    }
+    std::vector<ShardStats> stats(jobs.size());
+    if (jobs.size() == 1) {
+        run_shard(jobs[0], stats[0]);
+    } else {
+        std::vector<std::thread> ts;
+        for (size_t q = 0; q < jobs.size(); ++q) ts.emplace_back(run_shard, std::cref(jobs[q]), std::ref(stats[q]));
+        for (auto& th : ts) th.join();
+    }
+    hb_timing agg;
+    memset(&agg, 0, sizeof agg);
+    for (auto& s : stats) {
+        if (s.status != HB_OK) {
+            g_err = s.err;
+            return s.status;
+        }
+        agg.kernel_ms = std::max(agg.kernel_ms, s.kernel_ms);
+        agg.h2d_ms = std::max(agg.h2d_ms, s.h2d_ms);
+        agg.d2h_ms = std::max(agg.d2h_ms, s.d2h_ms);
+        agg.h2d_bytes += s.h2d_bytes;
+        agg.d2h_bytes += s.d2h_bytes;
+        agg.chunks += s.chunks;
+        agg.launches += s.launches;
+    }
+    agg.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (t) *t = agg;
+    return HB_OK;
+}
+
+}  // namespace hb
+
+using namespace hb;
+
+// =========================================================================
+// C ABI
+// =========================================================================
+extern "C" {
+
+int hb_abi_version(void) { return HB_ABI_VERSION; }
+const char* hb_last_error(void) { return g_err.c_str(); }
+int hb_digest_len(int alg) { return digest_len(alg); }
+uint64_t hb_launch_count(void) { return hb::launches_total(); }
+
+int hb_device_count(int* n) {
+    if (!n) return fail(HB_ERR_INVAL, "null pointer");
+    *n = device_count();
+    return HB_OK;
+}
+
+int hb_device_info(int ordinal, hb_device_info_t* info) {
+    if (!info) return fail(HB_ERR_INVAL, "null pointer");
+    const int nd = device_count();
+    if (ordinal < 0 || ordinal >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range", ordinal);
+    cudaDeviceProp p;
+    HB_CK(cudaGetDeviceProperties(&p, ordinal));
+    memset(info, 0, sizeof *info);
+    info->ordinal = ordinal;
+    info->sm_count = p.multiProcessorCount;
+    info->cc_major = p.major;
+    info->cc_minor = p.minor;
+    info->total_mem = p.totalGlobalMem;
+    info->pci_bus_id = p.pciBusID;
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, ordinal);
+    info->clock_khz = clk;
+    {
+        DeviceGuard g(ordinal);
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) info->free_mem = fr;
+        cudaGetLastError();
+    }
+    snprintf(info->name, sizeof info->name, "%s", p.name);
+    return HB_OK;
+}
+
+int hb_partition_range(int64_t lb, int64_t ub, const double* ratios, int k, int64_t* bounds_out) {
+    if (!bounds_out) return fail(HB_ERR_INVAL, "null pointer");
+    return partition(lb, ub, ratios, k, bounds_out);
+}
+
+int hb_hash_fixed(int alg, const uint8_t* msgs, uint64_t n, uint64_t msg_len, uint8_t* out, const int* gpus,
+                  int n_gpus, uint32_t flags, hb_timing* t) {
+    const int dlen = digest_len(alg);
+    if (dlen < 0) return fail(HB_ERR_ALG, "unknown hash algorithm id %d", alg);
+    if (t) memset(t, 0, sizeof *t);
+    if (n == 0) return HB_OK;
+    if (!out || (!msgs && msg_len)) return fail(HB_ERR_INVAL, "null buffer");
+    if (msg_len && n > UINT64_MAX / msg_len) return fail(HB_ERR_INVAL, "n*msg_len overflows");
+    std::vector<int> devs;
+    int rc = resolve_gpus(gpus, n_gpus, devs);
+    if (rc) return rc;
+    ShardJob j;
+    j.kind = 0;
+    j.alg = alg;
+    j.msgs = msgs;
+    j.msg_len = msg_len;
+    j.out = out;
+    j.flags = flags;
+    j.in_pinned = is_pinned(msgs, n * msg_len);
+    j.out_pinned = is_pinned(out, n * (uint64_t)dlen);
+    return run_sharded(j, n, devs, t);
+}
+
+int hb_hash_varlen(int alg, const uint8_t* data, const uint64_t* offsets, uint64_t n, uint8_t* out,
+                   const int* gpus, int n_gpus, uint32_t flags, hb_timing* t) {
+    const int dlen = digest_len(alg);
+    if (dlen < 0) return fail(HB_ERR_ALG, "unknown hash algorithm id %d", alg);
+    if (t) memset(t, 0, sizeof *t);
+    if (n == 0) return HB_OK;
+    if (!out || !offsets) return fail(HB_ERR_INVAL, "null buffer");
+    for (uint64_t i = 0; i < n; ++i)
+        if (offsets[i + 1] < offsets[i]) return fail(HB_ERR_INVAL, "offsets must be non-decreasing (at %llu)", (unsigned long long)i);
+    if (!data && offsets[n] > offsets[0]) return fail(HB_ERR_INVAL, "null data");
+    std::vector<int> devs;
+    int rc = resolve_gpus(gpus, n_gpus, devs);
+    if (rc) return rc;
+    ShardJob j;
+    j.kind = 1;
+    j.alg = alg;
+    j.data = data;
+    j.offsets = offsets;
+    j.out = out;
+    j.flags = flags;
+    j.in_pinned = is_pinned(data + offsets[0], offsets[n] - offsets[0]);
+    j.off_pinned = is_pinned(offsets, (n + 1) * 8);
+    j.out_pinned = is_pinned(out, n * (uint64_t)dlen);
+    return run_sharded(j, n, devs, t);
+}
+
+int hb_hash_decimal(int alg, uint64_t start, uint64_t count, int width, uint8_t* out, const int* gpus, int n_gpus,
+                    uint32_t flags, hb_timing* t) {
+    const int dlen = digest_len(alg);
+    if (dlen < 0) return fail(HB_ERR_ALG, "unknown hash algorithm id %d", alg);
+    if (t) memset(t, 0, sizeof *t);
+    if (width < 1 || width > 20) return fail(HB_ERR_INVAL, "width must be in [1, 20] for on-device generation");
+    if (count == 0) return HB_OK;
+    if (!out) return fail(HB_ERR_INVAL, "null buffer");
+    std::vector<int> devs;
+    int rc = resolve_gpus(gpus, n_gpus, devs);
+    if (rc) return rc;
+    ShardJob j;
+    j.kind = 2;
+    j.alg = alg;
+    j.start = start;
+    j.width = width;
+    j.out = out;
+    j.flags = flags;
+    j.out_pinned = is_pinned(out, count * (uint64_t)dlen);
+    return run_sharded(j, count, devs, t);
+}
+
+int hb_hash_fixed_dev(int alg, int gpu, const void* d_msgs, uint64_t n, uint64_t msg_len, void* d_out, void* stream,
+                      uint32_t flags) {
+    if (digest_len(alg) < 0) return fail(HB_ERR_ALG, "unknown hash algorithm id %d", alg);
+    if (n == 0) return HB_OK;
+    if (!d_out || (!d_msgs && msg_len)) return fail(HB_ERR_INVAL, "null buffer");
+    const int nd = device_count();
+    if (gpu < 0 || gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
+    DeviceGuard g(gpu);
+    HB_CK(launch_fixed(alg, static_cast<const uint8_t*>(d_msgs), n, msg_len, static_cast<uint8_t*>(d_out),
+                       static_cast<cudaStream_t>(stream), flags));
+    return HB_OK;
+}
+
+uint64_t hb_varlen_scratch_bytes(uint64_t n) { return varlen_scratch_bytes(n); }
+
+int hb_hash_varlen_dev(int alg, int gpu, const void* d_data, uint64_t data_bytes, const uint64_t* d_offsets,
+                       uint64_t offset_base, uint64_t n, void* d_out, void* d_scratch, void* stream, uint32_t flags) {
+    if (digest_len(alg) < 0) return fail(HB_ERR_ALG, "unknown hash algorithm id %d", alg);
+    if (n == 0) return HB_OK;
+    if (!d_out || !d_offsets) return fail(HB_ERR_INVAL, "null buffer");
+    const int nd = device_count();
+    if (gpu < 0 || gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
+    DeviceGuard g(gpu);
+    HB_CK(launch_varlen(alg, static_cast<const uint8_t*>(d_data), data_bytes, d_offsets, offset_base, n,
+                        static_cast<uint8_t*>(d_out), d_scratch, static_cast<cudaStream_t>(stream), flags));
+    return HB_OK;
+}
+
+int hb_hash_decimal_dev(int alg, int gpu, uint64_t start, uint64_t count, int width, void* d_out, void* stream) {
+    if (digest_len(alg) < 0) return fail(HB_ERR_ALG, "unknown hash algorithm id %d", alg);
+    if (width < 1 || width > 20) return fail(HB_ERR_INVAL, "width must be in [1, 20]");
+    if (count == 0) return HB_OK;
+    if (!d_out) return fail(HB_ERR_INVAL, "null buffer");
+    const int nd = device_count();
+    if (gpu < 0 || gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
+    DeviceGuard g(gpu);
+    HB_CK(launch_decimal(alg, start, count, width, static_cast<uint8_t*>(d_out), static_cast<cudaStream_t>(stream)));
+    return HB_OK;
+}
+
+int hb_fill_random_dev(int gpu, void* d_buf, uint64_t nbytes, uint64_t seed, uint64_t byte_offset, void* stream) {
+    if (nbytes == 0) return HB_OK;
+    if (!d_buf || (reinterpret_cast<uintptr_t>(d_buf) & 7u) || (byte_offset & 7u))
+        return fail(HB_ERR_INVAL, "d_buf and byte_offset must be 8-byte aligned");
+    const int nd = device_count();
+    if (gpu < 0 || gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
+    DeviceGuard g(gpu);
+    HB_CK(launch_fill_random(static_cast<uint8_t*>(d_buf), nbytes, seed, byte_offset, static_cast<cudaStream_t>(stream)));
+    return HB_OK;
+}
+
+int hb_gen_decimal_dev(int gpu, uint64_t start, uint64_t count, int width, void* d_out, void* stream) {
+    if (width < 1) return fail(HB_ERR_INVAL, "width must be positive");
+    if (count == 0) return HB_OK;
+    if (!d_out) return fail(HB_ERR_INVAL, "null buffer");
+    const int nd = device_count();
+    if (gpu < 0 || gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
+    DeviceGuard g(gpu);
+    HB_CK(launch_gen_decimal(start, count, width, static_cast<uint8_t*>(d_out), static_cast<cudaStream_t>(stream)));
+    return HB_OK;
+}
+
+void* hb_alloc_pinned(uint64_t bytes) {
+    if (!bytes) bytes = 1;
+    void* p = nullptr;
+    cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(HB_ERR_NOMEM, "cudaHostAlloc(%llu) failed: %s", (unsigned long long)bytes, cudaGetErrorString(e));
+        return nullptr;
+    }
+    return p;
+}
+
+int hb_free_pinned(void* p) {
+    if (!p) return HB_OK;
+    HB_CK(cudaFreeHost(p));
+    return HB_OK;
+}
+
+int hb_sync_device(int gpu) {
+    const int nd = device_count();
+    if (gpu < 0 || gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
+    DeviceGuard g(gpu);
+    HB_CK(cudaDeviceSynchronize());
+    return HB_OK;
+}
+
+int hb_shutdown(void) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    for (auto& cp : g_ctx) {
+        if (!cp) continue;
+        std::lock_guard<std::mutex> lk2(cp->mu);
+        DeviceGuard g(cp->dev);
+        for (Slot& s : cp->slots) {
+            if (s.stream) cudaStreamSynchronize(s.stream);
+            if (s.d_in.p) cudaFree(s.d_in.p);
+            if (s.d_out.p) cudaFree(s.d_out.p);
+            if (s.d_off.p) cudaFree(s.d_off.p);
+            if (s.d_scratch.p) cudaFree(s.d_scratch.p);
+            if (s.h_in.p) cudaFreeHost(s.h_in.p);
+            if (s.h_out.p) cudaFreeHost(s.h_out.p);
+            if (s.h_off.p) cudaFreeHost(s.h_off.p);
+            for (auto& e : s.ev)
+                if (e) cudaEventDestroy(e);
+            if (s.stream) cudaStreamDestroy(s.stream);
+        }
+        cp.reset();
+    }
+    g_ctx.clear();
+    return HB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,547 @@
+// hb_kernels.cu -- sm_100a kernels of the batched-hash engine and their
+// launchers.  One thread owns one message: chaining state and message
+// schedule live in registers; message bytes reach the thread either through a
+// TMA-staged, 64B-swizzled shared-memory ring (fixed width, 16B-aligned rows:
+// the HBM-streaming hot path) or through direct unaligned loads (any width,
+// variable length).  Padding is generated in registers (md_finish) -- the
+// padded (n, nblocks, 16) array of the reference (batch.py:128-138) never
+// exists in memory.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <mutex>
+
+#include "hb_algos.cuh"
+#include "hb_internal.h"
+#include "hb_ptx.cuh"
+#include "../../include/hetoc_b200.h"
+
+namespace hb {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launches(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+uint64_t launches_total() { return g_launches.load(std::memory_order_relaxed); }
+
+// =========================================================================
+// Fixed-width, TMA-staged kernel (the hot path).
+//
+// CTA = 4 warps; warp w owns 32 consecutive messages (rows).  Each warp runs
+// its own kStages-deep ring of 2 KiB stages: lane 0 issues one 2-D TMA load
+// per 64-byte message block ({64 B, 32 rows} box over the (n, msg_len) byte
+// matrix, SWIZZLE_64B), completion lands on the stage's mbarrier, all lanes
+// wait on the phase and read their row with four conflict-free 16-byte
+// shared loads.  TMA zero-fills columns >= msg_len, so the final partial
+// block arrives already masked.
+// =========================================================================
+constexpr int kTmaWarps = 4;
+constexpr int kRowsPerWarp = 32;
+constexpr int kStages = 3;
+constexpr int kStageBytes = 64 * kRowsPerWarp;  // 2 KiB
+constexpr int kTmaSmemBytes = kTmaWarps * kStages * kStageBytes + 1024 /*align slack*/ + kTmaWarps * kStages * 8;
+
+template <int ALG> struct Occupancy { static constexpr int kMinCtas = 8; };   // 1024 threads/SM
+template <> struct Occupancy<kSm3> { static constexpr int kMinCtas = 6; };    // SM3 needs more registers
+
+template <int ALG>
+__global__ void __launch_bounds__(kTmaWarps * 32, Occupancy<ALG>::kMinCtas)
+k_fixed_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t row0 = (blockIdx.x * kTmaWarps + warp) * kRowsPerWarp;
+    if (row0 >= n) return;  // warp-uniform
+
+    // 1024-align the ring (the swizzle pattern is a function of address bits 7:8).
+    const uint32_t base_s = smem_u32(smem_raw);
+    uint8_t* ring = smem_raw + (((base_s + 1023u) & ~1023u) - base_s);
+    uint8_t* wring = ring + warp * (kStages * kStageBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kTmaWarps * kStages * kStageBytes) + warp * kStages;
+
+    const uint32_t nload = (msg_len + 63u) >> 6;  // blocks holding message bytes
+    if (lane == 0) {
+        prefetch_tmap(&tmap);
+#pragma unroll
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        const uint32_t pro = nload < (uint32_t)kStages ? nload : (uint32_t)kStages;
+        for (uint32_t b = 0; b < pro; ++b) {
+            mbar_arrive_expect_tx(&bars[b], kStageBytes);
+            tma_load_2d(wring + b * kStageBytes, &tmap, &bars[b], (int)(b * 64u), (int)row0);
+        }
+    }
+    __syncwarp();
+
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    const uint32_t swz = (lane >> 1) & 3u;  // SWIZZLE_64B: 16B-chunk index ^= addr bits 7:8
+    uint32_t stage = 0, phase = 0;
+    uint32_t raw[16];
+    auto read_stage = [&](uint32_t s) {
+        const uint8_t* rowp = wring + s * kStageBytes + lane * 64u;
+#pragma unroll
+        for (uint32_t c = 0; c < 4; ++c) {
+            const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((c ^ swz) << 4));
+            raw[4 * c + 0] = v.x; raw[4 * c + 1] = v.y; raw[4 * c + 2] = v.z; raw[4 * c + 3] = v.w;
+        }
+    };
+    const uint32_t nfull = msg_len >> 6;
+    for (uint32_t b = 0; b < nfull; ++b) {
+        mbar_wait_parity(&bars[stage], phase);
+        read_stage(stage);
+        H::compress(st, raw);
+        __syncwarp();  // every lane has consumed this stage (its registers fed compress)
+        if (lane == 0 && b + kStages < nload) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&bars[stage], kStageBytes);
+            tma_load_2d(wring + stage * kStageBytes, &tmap, &bars[stage], (int)((b + kStages) * 64u), (int)row0);
+        }
+        if (++stage == (uint32_t)kStages) { stage = 0; phase ^= 1u; }
+    }
+    const uint32_t r = msg_len & 63u;
+    if (r) {  // partial data block: TMA zero-filled the columns >= msg_len
+        mbar_wait_parity(&bars[stage], phase);
+        read_stage(stage);
+    } else {  // padding-only final block (0x80, zeros, length)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) raw[j] = 0u;
+    }
+    md_finish<ALG>(st, raw, r, msg_len);
+    const uint32_t row = row0 + lane;
+    if (row < n) store_digest<ALG>(out + (uint64_t)row * H::kDigestBytes, st);
+}
+
+// =========================================================================
+// Fixed-width direct-load kernel (HB_FLAG_NO_TMA; 16B-aligned rows only).
+// Kept as the A/B baseline for the TMA staging: each thread streams its own
+// row with 128-bit read-only loads.
+// =========================================================================
+template <int ALG>
+__global__ void __launch_bounds__(128, Occupancy<ALG>::kMinCtas)
+k_fixed_direct(const uint8_t* __restrict__ msgs, uint64_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint4* p = reinterpret_cast<const uint4*>(msgs + i * msg_len);
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    const uint32_t nfull = msg_len >> 6;
+    for (uint32_t b = 0; b < nfull; ++b) {
+        uint32_t raw[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const uint4 v = __ldg(p + 4 * b + c);
+            raw[4 * c + 0] = v.x; raw[4 * c + 1] = v.y; raw[4 * c + 2] = v.z; raw[4 * c + 3] = v.w;
+        }
+        H::compress(st, raw);
+    }
+    const uint32_t r = msg_len & 63u;
+    uint32_t raw[16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if ((uint32_t)(16 * c) < r) v = __ldg(p + 4 * nfull + c);  // r is a multiple of 16 here
+        raw[4 * c + 0] = v.x; raw[4 * c + 1] = v.y; raw[4 * c + 2] = v.z; raw[4 * c + 3] = v.w;
+    }
+    md_finish<ALG>(st, raw, r, msg_len);
+    store_digest<ALG>(out + i * H::kDigestBytes, st);
+}
+
+// =========================================================================
+// Generic kernel: any width / alignment, and variable length.
+// Message bytes are fetched as aligned 32-bit words and realigned with one
+// funnel shift per word; the tail is masked and padded in registers.
+// For variable length, `perm` (optional) is a length-descending permutation
+// so the 32 lanes of a warp run (nearly) the same number of blocks.
+// =========================================================================
+__device__ __forceinline__ void load_block_unaligned(const uint8_t* p, const uint8_t* end, uint32_t raw[16]) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* q = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t sh = (uint32_t)(a & 3u) * 8u;
+    uint32_t c[17];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) c[k] = __ldg(q + k);
+    c[16] = (sh != 0u && reinterpret_cast<const uint8_t*>(q + 16) < end) ? __ldg(q + 16) : 0u;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) raw[j] = __funnelshift_r(c[j], c[j + 1], sh);
+}
+
+__device__ __forceinline__ void load_partial_unaligned(const uint8_t* p, uint32_t r, uint32_t raw[16]) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* q = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t sh = (uint32_t)(a & 3u) * 8u;
+    const uint8_t* e = p + r;
+    uint32_t c[17];
+#pragma unroll
+    for (int k = 0; k < 17; ++k) c[k] = (reinterpret_cast<const uint8_t*>(q + k) < e) ? __ldg(q + k) : 0u;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) raw[j] = __funnelshift_r(c[j], c[j + 1], sh);
+    mask_tail(raw, r);
+}
+
+template <int ALG, bool VARLEN>
+__global__ void __launch_bounds__(128)
+k_generic(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+          uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t msg_len, uint64_t n,
+          uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = (VARLEN && perm) ? (uint64_t)perm[t] : t;
+    uint64_t start, len;
+    if (VARLEN) {
+        start = offsets[i] - offset_base;
+        len = offsets[i + 1] - offsets[i];
+    } else {
+        start = i * msg_len;
+        len = msg_len;
+    }
+    const uint8_t* p = data + start;
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    const uint64_t nfull = len >> 6;
+    for (uint64_t b = 0; b < nfull; ++b) {
+        uint32_t raw[16];
+        load_block_unaligned(p + 64 * b, data_end, raw);
+        H::compress(st, raw);
+    }
+    uint32_t raw[16];
+    load_partial_unaligned(p + 64 * nfull, (uint32_t)(len & 63u), raw);
+    md_finish<ALG>(st, raw, (uint32_t)(len & 63u), len);
+    store_digest<ALG>(out + i * H::kDigestBytes, st);
+}
+
+// ---------------------------------------------------- length-bucket sort --
+// Counting sort of message indices by block count, longest first.  Three
+// small kernels: per-CTA shared-memory histograms -> global histogram, one
+// exclusive scan, per-CTA reservation + scatter.  Order inside a bucket is
+// irrelevant (digests are written to out[i]).
+constexpr int kSortBuckets = 2048;
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;  // per thread
+
+__device__ __forceinline__ uint32_t sort_bucket(const uint64_t* offsets, uint64_t i) {
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uint64_t nb = (len + 8u) / 64u + 1u;
+    const uint64_t c = nb < (uint64_t)(kSortBuckets - 1) ? nb : (uint64_t)(kSortBuckets - 1);
+    return (uint32_t)(kSortBuckets - 1) - (uint32_t)c;
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __restrict__ offsets, uint64_t n,
+                                                            uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[kSortBuckets];
+    for (int k = threadIdx.x; k < kSortBuckets; k += kSortThreads) h[k] = 0;
+    __syncthreads();
+    const uint64_t base = (uint64_t)blockIdx.x * kSortThreads * kSortItems;
+#pragma unroll 4
+    for (int it = 0; it < kSortItems; ++it) {
+        const uint64_t i = base + (uint64_t)it * kSortThreads + threadIdx.x;
+        if (i < n) atomicAdd(&h[sort_bucket(offsets, i)], 1u);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < kSortBuckets; k += kSortThreads)
+        if (h[k]) atomicAdd(&hist[k], h[k]);
+}
+
+__global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* __restrict__ hist) {
+    // exclusive scan of kSortBuckets (2 per thread) in place
+    __shared__ uint32_t warp_sums[32];
+    const int t = threadIdx.x;
+    const uint32_t a = hist[2 * t], b = hist[2 * t + 1];
+    uint32_t s = a + b, incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if ((t & 31) >= o) incl += v;
+    }
+    if ((t & 31) == 31) warp_sums[t >> 5] = incl;
+    __syncthreads();
+    if (t < 32) {
+        uint32_t w = warp_sums[t], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (t >= o) wi += v;
+        }
+        warp_sums[t] = wi - w;  // exclusive warp prefix
+    }
+    __syncthreads();
+    const uint32_t excl = warp_sums[t >> 5] + incl - s;
+    hist[2 * t] = excl;
+    hist[2 * t + 1] = excl + a;
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const uint64_t* __restrict__ offsets, uint64_t n,
+                                                               uint32_t* __restrict__ cursor,
+                                                               uint32_t* __restrict__ perm) {
+    __shared__ uint32_t h[kSortBuckets];
+    __shared__ uint32_t base[kSortBuckets];
+    for (int k = threadIdx.x; k < kSortBuckets; k += kSortThreads) h[k] = 0;
+    __syncthreads();
+    const uint64_t b0 = (uint64_t)blockIdx.x * kSortThreads * kSortItems;
+    uint32_t bucket[kSortItems];
+#pragma unroll
+    for (int it = 0; it < kSortItems; ++it) {
+        const uint64_t i = b0 + (uint64_t)it * kSortThreads + threadIdx.x;
+        bucket[it] = (i < n) ? sort_bucket(offsets, i) : 0xFFFFFFFFu;
+        if (i < n) atomicAdd(&h[bucket[it]], 1u);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < kSortBuckets; k += kSortThreads) {
+        base[k] = h[k] ? atomicAdd(&cursor[k], h[k]) : 0u;
+        h[k] = 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < kSortItems; ++it) {
+        const uint64_t i = b0 + (uint64_t)it * kSortThreads + threadIdx.x;
+        if (bucket[it] != 0xFFFFFFFFu) perm[base[bucket[it]] + atomicAdd(&h[bucket[it]], 1u)] = (uint32_t)i;
+    }
+}
+
+// ------------------------------------------------------- synthetic bytes --
+__device__ __forceinline__ uint64_t mix64(uint64_t seed, uint64_t idx) {  // == oracle mix64
+    uint64_t z = (idx + 1ull) * 0x9E3779B97F4A7C15ull + seed * 0xD1B54A32D192ED03ull;
+    z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27; z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+__global__ void k_fill_random(uint8_t* __restrict__ buf, uint64_t nbytes, uint64_t seed, uint64_t w0) {
+    const uint64_t nwords = (nbytes + 7) / 8;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = mix64(seed, w0 + w);
+        if (8 * w + 8 <= nbytes) {
+            reinterpret_cast<uint64_t*>(buf)[w] = v;
+        } else {
+            for (uint64_t k = 0; 8 * w + k < nbytes; ++k) buf[8 * w + k] = (uint8_t)(v >> (8 * k));
+        }
+    }
+}
+
+// -------------------------------------------- decimal messages in-register --
+// gen_messages (batch.py:86-99): message i is the zero-padded decimal
+// rendering of start+i, WIDTH bytes.  The bytes are built in registers and
+// hashed directly; only digests touch HBM.
+template <int ALG, int WIDTH>
+__global__ void __launch_bounds__(128) k_decimal(uint64_t start, uint64_t count, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    static_assert(WIDTH >= 1 && WIDTH <= 20, "width");
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    uint64_t v = start + i;
+    uint32_t raw[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) raw[j] = 0u;
+#pragma unroll
+    for (int pos = WIDTH - 1; pos >= 0; --pos) {  // batch.py:96-98
+        const uint32_t d = (uint32_t)(v % 10u);
+        v /= 10u;
+        raw[pos >> 2] |= (0x30u + d) << ((pos & 3) * 8);
+    }
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    md_finish<ALG>(st, raw, (uint32_t)WIDTH, (uint64_t)WIDTH);
+    store_digest<ALG>(out + i * H::kDigestBytes, st);
+}
+
+__global__ void k_gen_decimal(uint64_t start, uint64_t count, int width, uint8_t* __restrict__ out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    uint64_t v = start + i;
+    for (int pos = width - 1; pos >= 0; --pos) {
+        out[i * (uint64_t)width + pos] = (uint8_t)('0' + v % 10u);
+        v /= 10u;
+    }
+}
+
+// =========================================================================
+// Host-side launchers
+// =========================================================================
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode_tiled() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    });
+    return fn;
+}
+
+static thread_local char g_tma_err[160];
+const char* tma_error() { return g_tma_err; }
+
+template <int ALG>
+static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
+                                        cudaStream_t stream) {
+    PFN_encodeTiled enc = get_encode_tiled();
+    if (!enc) {
+        snprintf(g_tma_err, sizeof g_tma_err, "cuTensorMapEncodeTiled unavailable");
+        return cudaErrorNotSupported;
+    }
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {L, n};
+    const cuuint64_t strides[1] = {L};
+    const cuuint32_t box[2] = {64, (cuuint32_t)kRowsPerWarp};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult rc = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_msgs), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) {
+        snprintf(g_tma_err, sizeof g_tma_err, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)rc);
+        return cudaErrorInvalidValue;
+    }
+    static std::once_flag attr_once;
+    static cudaError_t attr_rc = cudaSuccess;
+    std::call_once(attr_once, [] {
+        attr_rc = cudaFuncSetAttribute(k_fixed_tma<ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemBytes);
+    });
+    if (attr_rc != cudaSuccess) return attr_rc;
+    const uint32_t rows_per_cta = kTmaWarps * kRowsPerWarp;
+    const uint32_t grid = (n + rows_per_cta - 1) / rows_per_cta;
+    k_fixed_tma<ALG><<<grid, kTmaWarps * 32, kTmaSmemBytes, stream>>>(map, n, L, d_out);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+template <int ALG>
+static cudaError_t launch_fixed_alg(const uint8_t* d_msgs, uint64_t n, uint64_t L, uint8_t* d_out,
+                                    cudaStream_t stream, uint32_t flags) {
+    using H = HashAlg<ALG>;
+    const bool aligned = L > 0 && (L % 16) == 0 && (reinterpret_cast<uintptr_t>(d_msgs) % 16) == 0 &&
+                         L < (1ull << 31);
+    if (aligned && !(flags & HB_FLAG_NO_TMA)) {
+        // TMA coordinates are int32: split very large batches into row slabs.
+        const uint64_t slab = 1ull << 30;
+        for (uint64_t r0 = 0; r0 < n; r0 += slab) {
+            const uint64_t rn = (n - r0) < slab ? (n - r0) : slab;
+            cudaError_t e = launch_fixed_tma_alg<ALG>(d_msgs + r0 * L, (uint32_t)rn, (uint32_t)L,
+                                                      d_out + r0 * H::kDigestBytes, stream);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
+    const uint64_t grid = (n + 127) / 128;
+    if (aligned) {
+        k_fixed_direct<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, (uint32_t)L, d_out);
+    } else {
+        k_generic<ALG, false><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, d_msgs + n * L, nullptr, 0, nullptr, L, n,
+                                                                  d_out);
+    }
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fixed(int alg, const uint8_t* d_msgs, uint64_t n, uint64_t msg_len, uint8_t* d_out,
+                         cudaStream_t stream, uint32_t flags) {
+    if (n == 0) return cudaSuccess;
+    switch (alg) {
+    case kSha1: return launch_fixed_alg<kSha1>(d_msgs, n, msg_len, d_out, stream, flags);
+    case kMd5: return launch_fixed_alg<kMd5>(d_msgs, n, msg_len, d_out, stream, flags);
+    case kSm3: return launch_fixed_alg<kSm3>(d_msgs, n, msg_len, d_out, stream, flags);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+uint64_t varlen_scratch_bytes(uint64_t n) { return (uint64_t)kSortBuckets * 4u + n * 4u + 256u; }
+
+template <int ALG>
+static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes, const uint64_t* d_offsets,
+                                     uint64_t offset_base, uint64_t n, uint8_t* d_out, void* d_scratch,
+                                     cudaStream_t stream, uint32_t flags) {
+    const uint32_t* perm = nullptr;
+    if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch) {
+        uint32_t* hist = static_cast<uint32_t*>(d_scratch);
+        uint32_t* p = hist + kSortBuckets;
+        cudaError_t e = cudaMemsetAsync(hist, 0, kSortBuckets * sizeof(uint32_t), stream);
+        if (e != cudaSuccess) return e;
+        const uint64_t per_cta = (uint64_t)kSortThreads * kSortItems;
+        const unsigned g = (unsigned)((n + per_cta - 1) / per_cta);
+        k_sort_hist<<<g, kSortThreads, 0, stream>>>(d_offsets, n, hist);
+        k_sort_scan<<<1, 1024, 0, stream>>>(hist);
+        k_sort_scatter<<<g, kSortThreads, 0, stream>>>(d_offsets, n, hist, p);
+        note_launches(3);
+        perm = p;
+    }
+    const uint64_t grid = (n + 127) / 128;
+    k_generic<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets, offset_base,
+                                                             perm, 0, n, d_out);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_varlen(int alg, const uint8_t* d_data, uint64_t data_bytes, const uint64_t* d_offsets,
+                          uint64_t offset_base, uint64_t n, uint8_t* d_out, void* d_scratch, cudaStream_t stream,
+                          uint32_t flags) {
+    if (n == 0) return cudaSuccess;
+    if (n >= (1ull << 32)) return cudaErrorInvalidValue;
+    switch (alg) {
+    case kSha1: return launch_varlen_alg<kSha1>(d_data, data_bytes, d_offsets, offset_base, n, d_out, d_scratch, stream, flags);
+    case kMd5: return launch_varlen_alg<kMd5>(d_data, data_bytes, d_offsets, offset_base, n, d_out, d_scratch, stream, flags);
+    case kSm3: return launch_varlen_alg<kSm3>(d_data, data_bytes, d_offsets, offset_base, n, d_out, d_scratch, stream, flags);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_fill_random(uint8_t* d_buf, uint64_t nbytes, uint64_t seed, uint64_t byte_offset,
+                               cudaStream_t stream) {
+    if (nbytes == 0) return cudaSuccess;
+    const uint64_t nwords = (nbytes + 7) / 8;
+    uint64_t grid = (nwords + 255) / 256;
+    if (grid > 148ull * 64) grid = 148ull * 64;
+    k_fill_random<<<(unsigned)grid, 256, 0, stream>>>(d_buf, nbytes, seed, byte_offset / 8);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+template <int ALG, int W>
+static void dec_launch(uint64_t start, uint64_t count, uint8_t* d_out, cudaStream_t s) {
+    k_decimal<ALG, W><<<(unsigned)((count + 127) / 128), 128, 0, s>>>(start, count, d_out);
+}
+
+template <int ALG>
+static cudaError_t launch_decimal_alg(uint64_t start, uint64_t count, int width, uint8_t* d_out, cudaStream_t s) {
+    switch (width) {
+#define HB_DEC_CASE(W) case W: dec_launch<ALG, W>(start, count, d_out, s); break;
+    HB_DEC_CASE(1) HB_DEC_CASE(2) HB_DEC_CASE(3) HB_DEC_CASE(4) HB_DEC_CASE(5) HB_DEC_CASE(6) HB_DEC_CASE(7)
+    HB_DEC_CASE(8) HB_DEC_CASE(9) HB_DEC_CASE(10) HB_DEC_CASE(11) HB_DEC_CASE(12) HB_DEC_CASE(13)
+    HB_DEC_CASE(14) HB_DEC_CASE(15) HB_DEC_CASE(16) HB_DEC_CASE(17) HB_DEC_CASE(18) HB_DEC_CASE(19)
+    HB_DEC_CASE(20)
+#undef HB_DEC_CASE
+    default: return cudaErrorInvalidValue;
+    }
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decimal(int alg, uint64_t start, uint64_t count, int width, uint8_t* d_out, cudaStream_t stream) {
+    if (count == 0) return cudaSuccess;
+    if (count >= (1ull << 40)) return cudaErrorInvalidValue;
+    switch (alg) {
+    case kSha1: return launch_decimal_alg<kSha1>(start, count, width, d_out, stream);
+    case kMd5: return launch_decimal_alg<kMd5>(start, count, width, d_out, stream);
+    case kSm3: return launch_decimal_alg<kSm3>(start, count, width, d_out, stream);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_gen_decimal(uint64_t start, uint64_t count, int width, uint8_t* d_out, cudaStream_t stream) {
+    if (count == 0) return cudaSuccess;
+    k_gen_decimal<<<(unsigned)((count + 127) / 128), 128, 0, stream>>>(start, count, width, d_out);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace hb

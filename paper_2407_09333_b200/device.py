@@ -1,0 +1,84 @@
+"""Device-resident (kernel-only) entry points over torch CUDA tensors.
+
+PyTorch is plumbing here: it owns device memory and streams; the hashing is
+the C ABI (``hb_hash_fixed_dev`` / ``hb_hash_varlen_dev`` / ...).  Work is
+enqueued on the tensor's device's *current* torch stream and is not
+synchronised, so CUDA events recorded on that stream bracket exactly the
+engine's kernels.
+"""
+
+from __future__ import annotations
+
+from . import _native
+from .crypto.batch import DIGEST_LEN, _check_alg
+
+
+def _stream_ptr(torch, dev: int) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def hash_fixed(alg: str, msgs, out=None, flags: int = 0):
+    """Digest each row of a 2-D uint8 CUDA tensor; returns (n, dlen) uint8 CUDA tensor."""
+    import torch
+
+    _check_alg(alg)
+    if msgs.dim() != 2 or msgs.dtype != torch.uint8 or not msgs.is_cuda:
+        raise ValueError("msgs must be a 2-D uint8 CUDA tensor")
+    msgs = msgs.contiguous()
+    n, L = msgs.shape
+    dev = msgs.device.index
+    if out is None:
+        out = torch.empty((n, DIGEST_LEN[alg]), dtype=torch.uint8, device=msgs.device)
+    if n:
+        rc = _native.lib().hb_hash_fixed_dev(_native.ALG_ID[alg], dev, msgs.data_ptr(), n, L, out.data_ptr(),
+                                             _stream_ptr(torch, dev), int(flags))
+        _native.check(rc, "hb_hash_fixed_dev")
+    return out
+
+
+def hash_varlen(alg: str, data, offsets, out=None, scratch=None, flags: int = 0):
+    """Digest message i = data[offsets[i]-offsets[0] : offsets[i+1]-offsets[0]] (CUDA tensors)."""
+    import torch
+
+    _check_alg(alg)
+    if data.dtype != torch.uint8 or offsets.dtype not in (torch.int64, torch.uint64) or not data.is_cuda:
+        raise ValueError("data must be uint8 and offsets int64/uint64 CUDA tensors")
+    n = offsets.numel() - 1
+    dev = data.device.index
+    if out is None:
+        out = torch.empty((max(n, 0), DIGEST_LEN[alg]), dtype=torch.uint8, device=data.device)
+    if n <= 0:
+        return out
+    if scratch is None and not (flags & _native.HB_FLAG_NO_SORT):
+        scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch.uint8, device=data.device)
+    base = int(offsets[0].item())
+    rc = _native.lib().hb_hash_varlen_dev(_native.ALG_ID[alg], dev, data.data_ptr(), data.numel(),
+                                          offsets.data_ptr(), base, n, out.data_ptr(),
+                                          scratch.data_ptr() if scratch is not None else None,
+                                          _stream_ptr(torch, dev), int(flags))
+    _native.check(rc, "hb_hash_varlen_dev")
+    return out
+
+
+def hash_decimal(alg: str, start: int, count: int, width: int = 9, device: int = 0, out=None):
+    import torch
+
+    _check_alg(alg)
+    if out is None:
+        out = torch.empty((count, DIGEST_LEN[alg]), dtype=torch.uint8, device=f"cuda:{device}")
+    if count:
+        rc = _native.lib().hb_hash_decimal_dev(_native.ALG_ID[alg], device, start, count, width, out.data_ptr(),
+                                               _stream_ptr(torch, device))
+        _native.check(rc, "hb_hash_decimal_dev")
+    return out
+
+
+def fill_random(buf, seed: int, byte_offset: int = 0):
+    """Fill a uint8 CUDA tensor with the oracle-compatible counter-based bytes."""
+    import torch
+
+    dev = buf.device.index
+    rc = _native.lib().hb_fill_random_dev(dev, buf.data_ptr(), buf.numel(), int(seed), int(byte_offset),
+                                          _stream_ptr(torch, dev))
+    _native.check(rc, "hb_fill_random_dev")
+    return buf

@@ -1,0 +1,154 @@
+"""The C-ABI library loads and exports every symbol include/hetoc_b200.h
+declares, and its host-only logic (partition, digest lengths, argument
+validation, error mapping) behaves like the reference.  No compute calls
+that need a GPU (CPU suite)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2407_09333_b200 as hb
+from paper_2407_09333_b200 import _native
+from paper_2407_09333_b200.crypto import (
+    ALGORITHMS,
+    DIGEST_LEN,
+    Digest,
+    MessageBatch,
+    UnknownAlgorithmError,
+    batch_digest,
+    batch_digest_varlen,
+    gen_messages,
+    hash_batch,
+)
+from paper_2407_09333_b200.passes import partition_range
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "hetoc_b200.h")
+
+
+def header_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(hb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _native.lib()
+    syms = header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_native.EXPORTS)
+
+
+def test_library_is_sm100a():
+    # the cubin inside the .so is sm_100a (checked without a GPU)
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "-lelf", _native.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_abi_basics():
+    lib = _native.lib()
+    assert lib.hb_abi_version() == 1
+    assert [lib.hb_digest_len(i) for i in range(3)] == [20, 16, 32]
+    assert lib.hb_digest_len(7) == -1
+    assert hb.launch_count() >= 0
+
+
+def test_partition_matches_reference_golden(golden):
+    for row in golden("partition.json"):
+        assert [list(x) for x in partition_range(row["lb"], row["ub"], row["ratios"])] == row["ranges"]
+
+
+def test_partition_spec_examples():
+    # SPEC.md:188-190
+    assert partition_range(0, 10, [0.5, 0.5]) == [(0, 5), (5, 10)]
+    assert partition_range(0, 1000, [0.3, 0.7]) == [(0, 300), (300, 1000)]
+    assert partition_range(0, 7, [0.33, 0.33, 0.34]) == [(0, 2), (2, 5), (5, 7)]
+    with pytest.raises(ValueError):
+        partition_range(5, 1, [1.0])
+    with pytest.raises(ValueError):
+        partition_range(0, 1, [])
+
+
+def test_partition_totality_random():
+    # SPEC.md:506 partition totality
+    rng = np.random.default_rng(11)
+    for _ in range(2000):
+        k = int(rng.integers(1, 9))
+        w = rng.random(k)
+        r = list(w / w.sum())
+        lb = int(rng.integers(0, 100))
+        ub = lb + int(rng.integers(0, 10**7))
+        got = partition_range(lb, ub, r)
+        assert got[0][0] == lb and got[-1][1] == ub
+        assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
+        assert all(lo <= hi for lo, hi in got)
+
+
+def test_api_constants_and_types():
+    assert ALGORITHMS == ("md5", "sha1", "sm3")
+    assert DIGEST_LEN == {"sha1": 20, "md5": 16, "sm3": 32}
+    assert issubclass(UnknownAlgorithmError, ValueError)
+    with pytest.raises(ValueError):
+        Digest("md5", b"\0" * 15)
+    with pytest.raises(UnknownAlgorithmError):
+        Digest("sha256", b"")
+    with pytest.raises(ValueError):
+        MessageBatch(1, 0, b"")
+    with pytest.raises(ValueError):
+        MessageBatch(2, 3, b"12345")
+    b = MessageBatch(2, 3, b"abcdef")
+    assert b.message(1) == b"def"
+    assert b.as_array().shape == (2, 3)
+
+
+def test_gen_messages(golden):
+    import hashlib
+
+    for row in golden("decimal_batches.json"):
+        b = gen_messages(row["start"], row["count"], row["width"])
+        assert hashlib.sha256(b.data).hexdigest() == row["input_sha256"]
+    assert gen_messages(0, 1).data == b"000000000"
+    assert gen_messages(999999999, 1).data == b"999999999"
+    with pytest.raises(ValueError):
+        gen_messages(999999999, 2)
+    with pytest.raises(ValueError):
+        gen_messages(0, 1, 0)
+
+
+def test_validation_before_device():
+    # argument errors surface before any device work (and identically with or without a GPU)
+    with pytest.raises(UnknownAlgorithmError):
+        batch_digest("sha256", np.zeros((1, 4), np.uint8))
+    with pytest.raises(ValueError):
+        batch_digest("md5", np.zeros(4, np.uint8))
+    with pytest.raises(ValueError):
+        hash_batch("md5", MessageBatch(1, 1, b"a"), threads=0)
+    assert hash_batch("md5", MessageBatch(0, 1, b"")) == []
+    assert batch_digest("sm3", np.zeros((0, 7), np.uint8)).shape == (0, 32)
+    with pytest.raises(ValueError):
+        batch_digest_varlen("md5", np.zeros(4, np.uint8), np.array([0, 5], np.uint64))
+
+
+def test_bad_alg_id_maps_to_unknown_algorithm():
+    lib = _native.lib()
+    rc = lib.hb_hash_fixed(9, None, 1, 1, None, None, 0, 0, None)
+    assert rc == _native.HB_ERR_ALG
+    with pytest.raises(UnknownAlgorithmError):
+        _native.check(rc)
+
+
+def test_no_cpu_fallback_without_gpu():
+    # with no CUDA device the product path raises instead of computing on the CPU
+    if _native.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        batch_digest("md5", np.zeros((4, 16), np.uint8))
+    lib = _native.lib()
+    assert lib.hb_hash_fixed_dev(1, 0, ctypes.c_void_p(16), 1, 16, ctypes.c_void_p(16), None, 0) == _native.HB_ERR_NODEV
