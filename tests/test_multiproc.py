@@ -1,0 +1,73 @@
+"""world_size-2 gloo test of the N>1 host path: message-range shards
+(partition_range) hashed independently per rank, then the optional digest
+gather, reproduce the single-rank result.  CPU only: the per-rank "kernel"
+here is the oracle (a test stand-in; on GPUs each rank calls the engine)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from paper_2407_09333_b200.distributed import gather_digests, shard_bounds, shard_for_rank
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n, L, q):
+    import torch.distributed as dist
+
+    import oracle
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = shard_for_rank(n, world, rank)
+        # the bytes of global messages [lo, hi): counter-based, shard-independent
+        mine = oracle.fill_random((hi - lo) * L, 17, lo * L).reshape(hi - lo, L)
+        res = {}
+        for alg in ("sha1", "md5", "sm3"):
+            local = torch.from_numpy(oracle.batch_fixed(alg, mine))
+            full = gather_digests(local, n)
+            res[alg] = full.numpy().copy()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [1001, 7, 1])
+def test_two_rank_shard_and_gather(n):
+    import oracle
+
+    L = 40  # multiple of 8 so every shard starts on a generator word
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, L, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    data = oracle.fill_random(n * L, 17).reshape(n, L)
+    for alg in ("sha1", "md5", "sm3"):
+        ref = oracle.batch_fixed(alg, data)
+        for r in range(world):
+            assert np.array_equal(got[r][alg], ref), (alg, r)
+
+
+def test_shard_bounds_rules():
+    assert shard_bounds(10, 2) == [(0, 5), (5, 10)]
+    assert shard_bounds(1 << 24, 8)[-1] == ((1 << 24) * 7 // 8, 1 << 24)
+    assert shard_bounds(3, 8)[0] == (0, 0)  # empty shards are legal
+    with pytest.raises(ValueError):
+        shard_for_rank(10, 2, 2)
