@@ -1,10 +1,15 @@
-// hb_algos.cuh -- SHA-1 / MD5 / SM3 compression for one message per thread.
+// hb_algos.cuh -- SHA-1 / MD5 / SM3 compression, one message per lane-slot.
 //
 // Each function keeps the chaining state and the whole message schedule in
 // registers (fully unrolled, constant indices only) and compiles to
-// LOP3 (boolean functions), SHF.L.W (rotates), IADD3/IMAD (adds) and PRMT
-// (byte swaps).  Inputs are the 16 RAW little-endian words of a 64-byte
-// block as loaded from memory; the big-endian algorithms byte-swap inside.
+// LOP3 (boolean functions), SHF.L.W / LEA.HI (rotates, rotate+add), IADD3 /
+// IMAD / VIADD (adds) and PRMT (byte swaps).  Inputs are the 16 RAW
+// little-endian words of a 64-byte block as loaded from memory; the
+// big-endian algorithms byte-swap inside.
+//
+// compress_n<NB> runs NB independent messages (of one thread) round by round,
+// interleaved in source order, so the scheduler can overlap their dependency
+// chains (instruction-level parallelism on top of warp parallelism).
 //
 // Reference semantics followed (paths relative to the reference repo):
 //   SHA-1  pkg/src/hetoc/crypto/sha1.py:21-37   (batch kernel batch.py:145-170)
@@ -21,47 +26,99 @@ enum Alg : int { kSha1 = 0, kMd5 = 1, kSm3 = 2 };
 __device__ __forceinline__ uint32_t rotl(uint32_t x, int n) { return __funnelshift_l(x, x, n); }
 __device__ __forceinline__ uint32_t bswap(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-// x ^ y ^ z as one LOP3 (immLut 0x96); the compiler already fuses these, the
-// explicit forms below keep the intent visible in the source.
-__device__ __forceinline__ uint32_t xor3(uint32_t x, uint32_t y, uint32_t z) { return x ^ y ^ z; }
-__device__ __forceinline__ uint32_t ch(uint32_t x, uint32_t y, uint32_t z) { return z ^ (x & (y ^ z)); }   // 0xCA
+// Boolean round functions; each lowers to one LOP3.
+__device__ __forceinline__ uint32_t xor3(uint32_t x, uint32_t y, uint32_t z) { return x ^ y ^ z; }             // 0x96
+__device__ __forceinline__ uint32_t ch(uint32_t x, uint32_t y, uint32_t z) { return z ^ (x & (y ^ z)); }       // 0xCA
 __device__ __forceinline__ uint32_t maj(uint32_t x, uint32_t y, uint32_t z) { return (x & y) | (z & (x | y)); } // 0xE8
 
-template <int ALG> struct HashAlg;
+// ------------------------------------------------------- pipe balancing --
+// On sm_100 LOP3 / SHF / PRMT / IADD3 / LEA.HI all issue to the ALU pipe (64
+// lanes/clk/SM, tools/pipe_bench.cu), while IMAD runs on the FMA pipe at the
+// same rate and VIADD (register + immediate) does not occupy the ALU pipe.
+// ptxas lowers every hash round to ALU ops, so the kernels start out
+// ALU-bound with the FMA pipe idle (ncu: ALU 92-97 %, FMA 5-17 %).
+// Multiplying by an *opaque* 1 (a __constant__ word ptxas cannot fold)
+// forces an addition onto the FMA pipe as IMAD; rotl_f does a rotate as IMAD +
+// IMAD.HI (the latter is half rate, so it is used sparingly).  Which rounds use
+// which form is a compile-time "variant" (A/B-measured on the B200).
+__constant__ uint32_t c_opaque[33] = {
+    1u, 2u, 4u, 8u, 16u, 32u, 64u, 128u, 256u, 512u, 1024u, 2048u, 4096u, 8192u, 16384u, 32768u, 65536u,
+    1u << 17, 1u << 18, 1u << 19, 1u << 20, 1u << 21, 1u << 22, 1u << 23, 1u << 24, 1u << 25, 1u << 26,
+    1u << 27, 1u << 28, 1u << 29, 1u << 30, 1u << 31, 1u};
+__device__ __forceinline__ uint32_t add_f(uint32_t a, uint32_t b) { return a * c_opaque[32] + b; }   // IMAD
+// A second, distinct opaque 1 (c_opaque[0]): ptxas may not factor x*one + y*one
+// into (x + y)*one across the two, which would pull adds back onto the
+// round's critical path.
+__device__ __forceinline__ uint32_t add_g(uint32_t a, uint32_t b) { return a * c_opaque[0] + b; }    // IMAD
+__device__ __forceinline__ uint32_t rotl_f(uint32_t x, int n) {                                       // IMAD.HI + IMAD
+    return __umulhi(x, c_opaque[n]) + x * c_opaque[n];
+}
+
+// Variant ids (template parameter V of the compress functions).
+constexpr int kVarPlain = 0;  // plain C arithmetic, ptxas' choice (ALU-heavy)
+constexpr int kVarBal = 1;    // additions partly routed to IMAD
+constexpr int kVarBal2 = 2;   // + more FMA-pipe work (algorithm specific, see below)
+constexpr int kVarBal3 = 3;
+constexpr int kNumVariants = 4;
+
+template <int ALG, int V = -1> struct HashAlg;
+
+// Default (tuned) variant per algorithm -- used by every kernel that does not
+// take an explicit variant (generic / varlen / decimal).  Measured A/B on the
+// B200 (profiles/variant_sweep_r1.txt): variant 1 is best for all three.
+template <int ALG> struct DefaultVariant { static constexpr int value = kVarBal; };
 
 // ------------------------------------------------------------------ SHA-1 --
-template <> struct HashAlg<kSha1> {
+// Variants: 1 = round adds e+W+K+f via IMAD/VIADD (then LEA.HI for +rotl(a,5));
+// 2 = 1 + schedule rotl1 via IMAD/IMAD.HI on every expanded word;
+// 3 = 1 + schedule rotl1 via IMAD/IMAD.HI on every other expanded word.
+template <int V> struct HashAlg<kSha1, V> {
     static constexpr int kStateWords = 5;
     static constexpr int kDigestBytes = 20;
     static constexpr bool kBigEndian = true;
+    static constexpr int kV = V < 0 ? DefaultVariant<kSha1>::value : V;
 
     __device__ __forceinline__ static void init(uint32_t s[5]) {   // sha1.py:5
         s[0] = 0x67452301u; s[1] = 0xEFCDAB89u; s[2] = 0x98BADCFEu; s[3] = 0x10325476u; s[4] = 0xC3D2E1F0u;
     }
 
-    __device__ __forceinline__ static void compress(uint32_t s[5], const uint32_t raw[16]) {
-        uint32_t w[16];
+    template <int NB>
+    __device__ __forceinline__ static void compress_n(uint32_t (&s)[NB][5], const uint32_t (&raw)[NB][16]) {
+        uint32_t w[NB][16], a[NB], b[NB], c[NB], d[NB], e[NB];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) w[t] = bswap(raw[t]);            // sha1.py:22 (">16I")
-        uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4];
+        for (int q = 0; q < NB; ++q) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t) w[q][t] = bswap(raw[q][t]);  // sha1.py:22 (">16I")
+            a[q] = s[q][0]; b[q] = s[q][1]; c[q] = s[q][2]; d[q] = s[q][3]; e[q] = s[q][4];
+        }
 #pragma unroll
         for (int t = 0; t < 80; ++t) {
-            uint32_t wt;
-            if (t < 16) {
-                wt = w[t];
-            } else {                                                  // batch.py:156-157 circular schedule
-                wt = rotl(w[(t - 3) & 15] ^ w[(t - 8) & 15] ^ w[(t - 14) & 15] ^ w[t & 15], 1);
-                w[t & 15] = wt;
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                uint32_t wt;
+                if (t < 16) {
+                    wt = w[q][t];
+                } else {                                              // batch.py:156-157 circular schedule
+                    const uint32_t x = w[q][(t - 3) & 15] ^ w[q][(t - 8) & 15] ^ w[q][(t - 14) & 15] ^ w[q][t & 15];
+                    const bool fma_rot = (kV == 2) || (kV == 3 && (t & 1));
+                    wt = fma_rot ? rotl_f(x, 1) : rotl(x, 1);
+                    w[q][t & 15] = wt;
+                }
+                uint32_t f, k;
+                if (t < 20)      { f = ch(b[q], c[q], d[q]);   k = 0x5A827999u; }   // sha1.py:27-34
+                else if (t < 40) { f = xor3(b[q], c[q], d[q]); k = 0x6ED9EBA1u; }
+                else if (t < 60) { f = maj(b[q], c[q], d[q]);  k = 0x8F1BBCDCu; }
+                else             { f = xor3(b[q], c[q], d[q]); k = 0xCA62C1D6u; }
+                uint32_t tmp;                                         // sha1.py:35
+                if (kV >= kVarBal) tmp = add_g(f, add_f(e[q], wt + k)) + rotl(a[q], 5);
+                else tmp = rotl(a[q], 5) + f + e[q] + k + wt;
+                e[q] = d[q]; d[q] = c[q]; c[q] = rotl(b[q], 30); b[q] = a[q]; a[q] = tmp;   // sha1.py:36
             }
-            uint32_t f, k;
-            if (t < 20)      { f = ch(b, c, d);   k = 0x5A827999u; }    // sha1.py:27-34
-            else if (t < 40) { f = xor3(b, c, d); k = 0x6ED9EBA1u; }
-            else if (t < 60) { f = maj(b, c, d);  k = 0x8F1BBCDCu; }
-            else             { f = xor3(b, c, d); k = 0xCA62C1D6u; }
-            const uint32_t tmp = rotl(a, 5) + f + e + k + wt;         // sha1.py:35
-            e = d; d = c; c = rotl(b, 30); b = a; a = tmp;             // sha1.py:36
         }
-        s[0] += a; s[1] += b; s[2] += c; s[3] += d; s[4] += e;         // sha1.py:37
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {                                // sha1.py:37
+            s[q][0] += a[q]; s[q][1] += b[q]; s[q][2] += c[q]; s[q][3] += d[q]; s[q][4] += e[q];
+        }
     }
 
     __device__ __forceinline__ static void digest_words(const uint32_t s[5], uint32_t o[5]) {
@@ -71,100 +128,80 @@ template <> struct HashAlg<kSha1> {
 };
 
 // -------------------------------------------------------------------- MD5 --
-template <> struct HashAlg<kMd5> {
+// K[i] = floor(|sin(i+1)|*2^32) (md5.py:9), S (md5.py:11-16), g (md5.py:38-49).
+__host__ __device__ constexpr uint32_t md5_k(int i) {
+    constexpr uint32_t K[64] = {
+        0xd76aa478, 0xe8c7b756, 0x242070db, 0xc1bdceee, 0xf57c0faf, 0x4787c62a, 0xa8304613, 0xfd469501,
+        0x698098d8, 0x8b44f7af, 0xffff5bb1, 0x895cd7be, 0x6b901122, 0xfd987193, 0xa679438e, 0x49b40821,
+        0xf61e2562, 0xc040b340, 0x265e5a51, 0xe9b6c7aa, 0xd62f105d, 0x02441453, 0xd8a1e681, 0xe7d3fbc8,
+        0x21e1cde6, 0xc33707d6, 0xf4d50d87, 0x455a14ed, 0xa9e3e905, 0xfcefa3f8, 0x676f02d9, 0x8d2a4c8a,
+        0xfffa3942, 0x8771f681, 0x6d9d6122, 0xfde5380c, 0xa4beea44, 0x4bdecfa9, 0xf6bb4b60, 0xbebfbc70,
+        0x289b7ec6, 0xeaa127fa, 0xd4ef3085, 0x04881d05, 0xd9d4d039, 0xe6db99e5, 0x1fa27cf8, 0xc4ac5665,
+        0xf4292244, 0x432aff97, 0xab9423a7, 0xfc93a039, 0x655b59c3, 0x8f0ccc92, 0xffeff47d, 0x85845dd1,
+        0x6fa87e4f, 0xfe2ce6e0, 0xa3014314, 0x4e0811a1, 0xf7537e82, 0xbd3af235, 0x2ad7d2bb, 0xeb86d391};
+    return K[i];
+}
+__host__ __device__ constexpr int md5_s(int i) {
+    constexpr int S[4][4] = {{7, 12, 17, 22}, {5, 9, 14, 20}, {4, 11, 16, 23}, {6, 10, 15, 21}};
+    return S[i / 16][i % 4];
+}
+__host__ __device__ constexpr int md5_g(int i) {
+    return i < 16 ? i : i < 32 ? (5 * i + 1) % 16 : i < 48 ? (3 * i + 5) % 16 : (7 * i) % 16;
+}
+
+// Variants: 1 = two of every three rounds add a+M(+K)+F through IMAD/VIADD,
+// the third through IADD3 (balances ALU vs FMA issue); 2 = every round via IMAD;
+// 3 = as 1 but written so K stays attached to M (3-op dependency chain).
+template <int V> struct HashAlg<kMd5, V> {
     static constexpr int kStateWords = 4;
     static constexpr int kDigestBytes = 16;
     static constexpr bool kBigEndian = false;
+    static constexpr int kV = V < 0 ? DefaultVariant<kMd5>::value : V;
 
     __device__ __forceinline__ static void init(uint32_t s[4]) {   // md5.py:6
         s[0] = 0x67452301u; s[1] = 0xEFCDAB89u; s[2] = 0x98BADCFEu; s[3] = 0x10325476u;
     }
 
-    // One step of md5.py:36-53: b' = b + rotl(a + f(b,c,d) + K[i] + m[g], S), with
-    // the (a,b,c,d) <- (d,b',b,c) rename folded into the macro's argument order.
-#define HB_MD5_F(x, y, z) (ch((x), (y), (z)))                  // i<16: (b&c)|(~b&d)
-#define HB_MD5_G(x, y, z) (ch((z), (x), (y)))                  // i<32: (d&b)|(~d&c)
-#define HB_MD5_H(x, y, z) (xor3((x), (y), (z)))                // i<48
-#define HB_MD5_I(x, y, z) ((y) ^ ((x) | ~(z)))                 // i<64: c^(b|~d)
-#define HB_MD5_STEP(FN, a, b, c, d, m, k, s) a = (b) + rotl((a) + FN((b), (c), (d)) + (m) + (k), (s))
-
-    __device__ __forceinline__ static void compress(uint32_t st[4], const uint32_t m[16]) {
-        uint32_t a = st[0], b = st[1], c = st[2], d = st[3];
-        // K[i] = floor(|sin(i+1)|*2^32) (md5.py:9), S (md5.py:11-16), g (md5.py:38-49)
-        HB_MD5_STEP(HB_MD5_F, a, b, c, d, m[0], 0xd76aa478u, 7);
-        HB_MD5_STEP(HB_MD5_F, d, a, b, c, m[1], 0xe8c7b756u, 12);
-        HB_MD5_STEP(HB_MD5_F, c, d, a, b, m[2], 0x242070dbu, 17);
-        HB_MD5_STEP(HB_MD5_F, b, c, d, a, m[3], 0xc1bdceeeu, 22);
-        HB_MD5_STEP(HB_MD5_F, a, b, c, d, m[4], 0xf57c0fafu, 7);
-        HB_MD5_STEP(HB_MD5_F, d, a, b, c, m[5], 0x4787c62au, 12);
-        HB_MD5_STEP(HB_MD5_F, c, d, a, b, m[6], 0xa8304613u, 17);
-        HB_MD5_STEP(HB_MD5_F, b, c, d, a, m[7], 0xfd469501u, 22);
-        HB_MD5_STEP(HB_MD5_F, a, b, c, d, m[8], 0x698098d8u, 7);
-        HB_MD5_STEP(HB_MD5_F, d, a, b, c, m[9], 0x8b44f7afu, 12);
-        HB_MD5_STEP(HB_MD5_F, c, d, a, b, m[10], 0xffff5bb1u, 17);
-        HB_MD5_STEP(HB_MD5_F, b, c, d, a, m[11], 0x895cd7beu, 22);
-        HB_MD5_STEP(HB_MD5_F, a, b, c, d, m[12], 0x6b901122u, 7);
-        HB_MD5_STEP(HB_MD5_F, d, a, b, c, m[13], 0xfd987193u, 12);
-        HB_MD5_STEP(HB_MD5_F, c, d, a, b, m[14], 0xa679438eu, 17);
-        HB_MD5_STEP(HB_MD5_F, b, c, d, a, m[15], 0x49b40821u, 22);
-
-        HB_MD5_STEP(HB_MD5_G, a, b, c, d, m[1], 0xf61e2562u, 5);
-        HB_MD5_STEP(HB_MD5_G, d, a, b, c, m[6], 0xc040b340u, 9);
-        HB_MD5_STEP(HB_MD5_G, c, d, a, b, m[11], 0x265e5a51u, 14);
-        HB_MD5_STEP(HB_MD5_G, b, c, d, a, m[0], 0xe9b6c7aau, 20);
-        HB_MD5_STEP(HB_MD5_G, a, b, c, d, m[5], 0xd62f105du, 5);
-        HB_MD5_STEP(HB_MD5_G, d, a, b, c, m[10], 0x02441453u, 9);
-        HB_MD5_STEP(HB_MD5_G, c, d, a, b, m[15], 0xd8a1e681u, 14);
-        HB_MD5_STEP(HB_MD5_G, b, c, d, a, m[4], 0xe7d3fbc8u, 20);
-        HB_MD5_STEP(HB_MD5_G, a, b, c, d, m[9], 0x21e1cde6u, 5);
-        HB_MD5_STEP(HB_MD5_G, d, a, b, c, m[14], 0xc33707d6u, 9);
-        HB_MD5_STEP(HB_MD5_G, c, d, a, b, m[3], 0xf4d50d87u, 14);
-        HB_MD5_STEP(HB_MD5_G, b, c, d, a, m[8], 0x455a14edu, 20);
-        HB_MD5_STEP(HB_MD5_G, a, b, c, d, m[13], 0xa9e3e905u, 5);
-        HB_MD5_STEP(HB_MD5_G, d, a, b, c, m[2], 0xfcefa3f8u, 9);
-        HB_MD5_STEP(HB_MD5_G, c, d, a, b, m[7], 0x676f02d9u, 14);
-        HB_MD5_STEP(HB_MD5_G, b, c, d, a, m[12], 0x8d2a4c8au, 20);
-
-        HB_MD5_STEP(HB_MD5_H, a, b, c, d, m[5], 0xfffa3942u, 4);
-        HB_MD5_STEP(HB_MD5_H, d, a, b, c, m[8], 0x8771f681u, 11);
-        HB_MD5_STEP(HB_MD5_H, c, d, a, b, m[11], 0x6d9d6122u, 16);
-        HB_MD5_STEP(HB_MD5_H, b, c, d, a, m[14], 0xfde5380cu, 23);
-        HB_MD5_STEP(HB_MD5_H, a, b, c, d, m[1], 0xa4beea44u, 4);
-        HB_MD5_STEP(HB_MD5_H, d, a, b, c, m[4], 0x4bdecfa9u, 11);
-        HB_MD5_STEP(HB_MD5_H, c, d, a, b, m[7], 0xf6bb4b60u, 16);
-        HB_MD5_STEP(HB_MD5_H, b, c, d, a, m[10], 0xbebfbc70u, 23);
-        HB_MD5_STEP(HB_MD5_H, a, b, c, d, m[13], 0x289b7ec6u, 4);
-        HB_MD5_STEP(HB_MD5_H, d, a, b, c, m[0], 0xeaa127fau, 11);
-        HB_MD5_STEP(HB_MD5_H, c, d, a, b, m[3], 0xd4ef3085u, 16);
-        HB_MD5_STEP(HB_MD5_H, b, c, d, a, m[6], 0x04881d05u, 23);
-        HB_MD5_STEP(HB_MD5_H, a, b, c, d, m[9], 0xd9d4d039u, 4);
-        HB_MD5_STEP(HB_MD5_H, d, a, b, c, m[12], 0xe6db99e5u, 11);
-        HB_MD5_STEP(HB_MD5_H, c, d, a, b, m[15], 0x1fa27cf8u, 16);
-        HB_MD5_STEP(HB_MD5_H, b, c, d, a, m[2], 0xc4ac5665u, 23);
-
-        HB_MD5_STEP(HB_MD5_I, a, b, c, d, m[0], 0xf4292244u, 6);
-        HB_MD5_STEP(HB_MD5_I, d, a, b, c, m[7], 0x432aff97u, 10);
-        HB_MD5_STEP(HB_MD5_I, c, d, a, b, m[14], 0xab9423a7u, 15);
-        HB_MD5_STEP(HB_MD5_I, b, c, d, a, m[5], 0xfc93a039u, 21);
-        HB_MD5_STEP(HB_MD5_I, a, b, c, d, m[12], 0x655b59c3u, 6);
-        HB_MD5_STEP(HB_MD5_I, d, a, b, c, m[3], 0x8f0ccc92u, 10);
-        HB_MD5_STEP(HB_MD5_I, c, d, a, b, m[10], 0xffeff47du, 15);
-        HB_MD5_STEP(HB_MD5_I, b, c, d, a, m[1], 0x85845dd1u, 21);
-        HB_MD5_STEP(HB_MD5_I, a, b, c, d, m[8], 0x6fa87e4fu, 6);
-        HB_MD5_STEP(HB_MD5_I, d, a, b, c, m[15], 0xfe2ce6e0u, 10);
-        HB_MD5_STEP(HB_MD5_I, c, d, a, b, m[6], 0xa3014314u, 15);
-        HB_MD5_STEP(HB_MD5_I, b, c, d, a, m[13], 0x4e0811a1u, 21);
-        HB_MD5_STEP(HB_MD5_I, a, b, c, d, m[4], 0xf7537e82u, 6);
-        HB_MD5_STEP(HB_MD5_I, d, a, b, c, m[11], 0xbd3af235u, 10);
-        HB_MD5_STEP(HB_MD5_I, c, d, a, b, m[2], 0x2ad7d2bbu, 15);
-        HB_MD5_STEP(HB_MD5_I, b, c, d, a, m[9], 0xeb86d391u, 21);
-        st[0] += a; st[1] += b; st[2] += c; st[3] += d;                // md5.py:54
+    __device__ __forceinline__ static constexpr bool use_fma(int i) {
+        return kV == kVarPlain ? false : kV == kVarBal2 ? true : (i % 3) != 2;
     }
-#undef HB_MD5_F
-#undef HB_MD5_G
-#undef HB_MD5_H
-#undef HB_MD5_I
-#undef HB_MD5_STEP
+
+    template <int NB>
+    __device__ __forceinline__ static void compress_n(uint32_t (&st)[NB][4], const uint32_t (&m)[NB][16]) {
+        uint32_t a[NB], b[NB], c[NB], d[NB];
+#pragma unroll
+        for (int q = 0; q < NB; ++q) { a[q] = st[q][0]; b[q] = st[q][1]; c[q] = st[q][2]; d[q] = st[q][3]; }
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {                                // md5.py:35-53
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                uint32_t f;
+                if (i < 16)      f = ch(b[q], c[q], d[q]);            // (b&c)|(~b&d)
+                else if (i < 32) f = ch(d[q], b[q], c[q]);            // (d&b)|(~d&c)
+                else if (i < 48) f = xor3(b[q], c[q], d[q]);
+                else             f = c[q] ^ (b[q] | ~d[q]);
+                const uint32_t mg = m[q][md5_g(i)];
+                // t = a + M[g] + K is off the critical path (a is four rounds
+                // old); only f -> IMAD -> LEA.HI depends on the previous round.
+                // Written so ptxas keeps K attached to M (it sinks immediate adds
+                // to the end of an add chain otherwise, lengthening the chain).
+                // Variant 1 (B200-measured best, profiles/variant_sweep_r1c.txt):
+                // ptxas lowers it to IMAD.IADD(f+a) -> IMAD(x*1+M) -> VIADD(+K),
+                // keeping two of the three adds off the ALU pipe.  Variant 3
+                // keeps K attached to M (shorter dependency chain, 2 IMADs).
+                uint32_t u;
+                if (kV == kVarBal3) u = use_fma(i) ? add_g(f, add_f(a[q], mg + md5_k(i))) : add_g(f, a[q] + (mg + md5_k(i)));
+                else if (use_fma(i)) u = add_f(f, add_f(a[q], mg) + md5_k(i));
+                else u = a[q] + f + mg + md5_k(i);
+                const uint32_t nb = b[q] + rotl(u, md5_s(i));         // one LEA.HI
+                a[q] = d[q]; d[q] = c[q]; c[q] = b[q]; b[q] = nb;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {                                // md5.py:54
+            st[q][0] += a[q]; st[q][1] += b[q]; st[q][2] += c[q]; st[q][3] += d[q];
+        }
+    }
 
     __device__ __forceinline__ static void digest_words(const uint32_t s[4], uint32_t o[4]) {
 #pragma unroll
@@ -173,10 +210,13 @@ template <> struct HashAlg<kMd5> {
 };
 
 // -------------------------------------------------------------------- SM3 --
-template <> struct HashAlg<kSm3> {
+// Variants: 1 = TT1/TT2/SS1 additions through IMAD/VIADD; 2 = 1 + rotl(b,9) and
+// rotl(f,19) via IMAD/IMAD.HI; 3 = 1 + only rotl(b,9) via IMAD/IMAD.HI.
+template <int V> struct HashAlg<kSm3, V> {
     static constexpr int kStateWords = 8;
     static constexpr int kDigestBytes = 32;
     static constexpr bool kBigEndian = true;
+    static constexpr int kV = V < 0 ? DefaultVariant<kSm3>::value : V;
 
     __device__ __forceinline__ static void init(uint32_t s[8]) {   // sm3.py:5-8
         s[0] = 0x7380166Fu; s[1] = 0x4914B2B9u; s[2] = 0x172442D7u; s[3] = 0xDA8A0600u;
@@ -191,35 +231,56 @@ template <> struct HashAlg<kSm3> {
                                 ((j < 16 ? 0x79CC4519u : 0x7A879D8Au) >> (32 - (j % 32))));
     }
 
-    __device__ __forceinline__ static void compress(uint32_t s[8], const uint32_t raw[16]) {
+    template <int NB>
+    __device__ __forceinline__ static void compress_n(uint32_t (&s)[NB][8], const uint32_t (&raw)[NB][16]) {
         // 16-word circular window: round j needs W[j] and W[j+4]; W[j+4] is
         // expanded (sm3.py:35-40) just in time and overwrites W[j-12].
-        uint32_t w[16];
+        uint32_t w[NB][16], a[NB], b[NB], c[NB], d[NB], e[NB], f[NB], g[NB], h[NB];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) w[t] = bswap(raw[t]);            // sm3.py:34 (">16I")
-        uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
+        for (int q = 0; q < NB; ++q) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t) w[q][t] = bswap(raw[q][t]);  // sm3.py:34 (">16I")
+            a[q] = s[q][0]; b[q] = s[q][1]; c[q] = s[q][2]; d[q] = s[q][3];
+            e[q] = s[q][4]; f[q] = s[q][5]; g[q] = s[q][6]; h[q] = s[q][7];
+        }
 #pragma unroll
         for (int j = 0; j < 64; ++j) {
-            const int k = j + 4;
-            if (k >= 16) {
-                w[k & 15] = p1(xor3(w[(k - 16) & 15], w[(k - 9) & 15], rotl(w[(k - 3) & 15], 15)))
-                            ^ rotl(w[(k - 13) & 15], 7) ^ w[(k - 6) & 15];
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                const int k = j + 4;
+                if (k >= 16) {
+                    w[q][k & 15] = p1(xor3(w[q][(k - 16) & 15], w[q][(k - 9) & 15], rotl(w[q][(k - 3) & 15], 15)))
+                                   ^ rotl(w[q][(k - 13) & 15], 7) ^ w[q][(k - 6) & 15];
+                }
+                const uint32_t wj = w[q][j & 15];
+                const uint32_t wj2 = wj ^ w[q][k & 15];                // W'_j, sm3.py:41
+                const uint32_t a12 = rotl(a[q], 12);
+                uint32_t ss1;                                          // sm3.py:45
+                if (kV >= kVarBal) ss1 = rotl(add_f(a12, e[q]) + tj(j), 7);
+                else ss1 = rotl(a12 + e[q] + tj(j), 7);
+                const uint32_t ss2 = ss1 ^ a12;                        // sm3.py:46
+                uint32_t ff, gg;
+                if (j < 16) { ff = xor3(a[q], b[q], c[q]); gg = xor3(e[q], f[q], g[q]); }   // sm3.py:47-52
+                else        { ff = maj(a[q], b[q], c[q]);  gg = ch(e[q], f[q], g[q]); }
+                uint32_t tt1, tt2;
+                if (kV >= kVarBal) {
+                    tt1 = add_g(ss2, add_f(ff, d[q]) + wj2);           // sm3.py:53
+                    tt2 = add_g(ss1, add_f(gg, h[q]) + wj);            // sm3.py:54
+                } else {
+                    tt1 = ff + d[q] + ss2 + wj2;
+                    tt2 = gg + h[q] + ss1 + wj;
+                }
+                const bool fb = kV == kVarBal2 || kV == kVarBal3;
+                const bool ff19 = kV == kVarBal2;
+                d[q] = c[q]; c[q] = fb ? rotl_f(b[q], 9) : rotl(b[q], 9); b[q] = a[q]; a[q] = tt1;       // sm3.py:55-58
+                h[q] = g[q]; g[q] = ff19 ? rotl_f(f[q], 19) : rotl(f[q], 19); f[q] = e[q]; e[q] = p0(tt2);  // sm3.py:59-62
             }
-            const uint32_t wj = w[j & 15];
-            const uint32_t wj2 = wj ^ w[k & 15];                       // W'_j, sm3.py:41
-            const uint32_t a12 = rotl(a, 12);
-            const uint32_t ss1 = rotl(a12 + e + tj(j), 7);             // sm3.py:45
-            const uint32_t ss2 = ss1 ^ a12;                            // sm3.py:46
-            uint32_t ff, gg;
-            if (j < 16) { ff = xor3(a, b, c); gg = xor3(e, f, g); }    // sm3.py:47-52
-            else        { ff = maj(a, b, c);  gg = ch(e, f, g); }
-            const uint32_t tt1 = ff + d + ss2 + wj2;                   // sm3.py:53
-            const uint32_t tt2 = gg + h + ss1 + wj;                    // sm3.py:54
-            d = c; c = rotl(b, 9); b = a; a = tt1;                     // sm3.py:55-58
-            h = g; g = rotl(f, 19); f = e; e = p0(tt2);                // sm3.py:59-62
         }
-        s[0] ^= a; s[1] ^= b; s[2] ^= c; s[3] ^= d;                    // sm3.py:63 (XOR feed-forward)
-        s[4] ^= e; s[5] ^= f; s[6] ^= g; s[7] ^= h;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {                                 // sm3.py:63 (XOR feed-forward)
+            s[q][0] ^= a[q]; s[q][1] ^= b[q]; s[q][2] ^= c[q]; s[q][3] ^= d[q];
+            s[q][4] ^= e[q]; s[q][5] ^= f[q]; s[q][6] ^= g[q]; s[q][7] ^= h[q];
+        }
     }
 
     __device__ __forceinline__ static void digest_words(const uint32_t s[8], uint32_t o[8]) {
@@ -228,39 +289,75 @@ template <> struct HashAlg<kSm3> {
     }
 };
 
+// Single-message convenience wrapper.
+template <int ALG, int V = -1>
+__device__ __forceinline__ void compress1(uint32_t* st, const uint32_t* raw) {
+    using H = HashAlg<ALG, V>;
+    uint32_t s[1][H::kStateWords];
+    uint32_t r[1][16];
+#pragma unroll
+    for (int i = 0; i < H::kStateWords; ++i) s[0][i] = st[i];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r[0][i] = raw[i];
+    H::template compress_n<1>(s, r);
+#pragma unroll
+    for (int i = 0; i < H::kStateWords; ++i) st[i] = s[0][i];
+}
+
 // ------------------------------------------------- Merkle-Damgard padding --
-// Finish a message whose final r (0 <= r < 64) data bytes sit in raw[] as
-// little-endian words with every byte at position >= r already zero.  Appends
-// 0x80, zero fill and the 64-bit bit length exactly as _pad does
-// (sha1.py:14-18, md5.py:25-29, sm3.py:26-30; batch.py:133-136), compressing
-// one or two blocks.  No dynamic register indexing: the byte position is
-// applied through an unrolled select.
-template <int ALG>
-__device__ __forceinline__ void md_finish(uint32_t st[], uint32_t raw[16], uint32_t r, uint64_t len_bytes) {
-    using H = HashAlg<ALG>;
+// Finish NB messages of the SAME length whose final r (0 <= r < 64) data bytes
+// sit in raw[q][] as little-endian words with every byte at position >= r
+// already zero.  Appends 0x80, zero fill and the 64-bit bit length exactly as
+// _pad does (sha1.py:14-18, md5.py:25-29, sm3.py:26-30; batch.py:133-136),
+// compressing one or two blocks.  No dynamic register indexing: the byte
+// position is applied through an unrolled select.
+template <int ALG, int V, int NB>
+__device__ __forceinline__ void md_finish_n(uint32_t (&st)[NB][HashAlg<ALG, V>::kStateWords], uint32_t (&raw)[NB][16],
+                                            uint32_t r, uint64_t len_bytes) {
+    using H = HashAlg<ALG, V>;
     const uint32_t pad = 0x80u << ((r & 3u) * 8u);
     const uint32_t pw = r >> 2;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) raw[j] |= (pw == (uint32_t)j) ? pad : 0u;
     const uint64_t bits = len_bytes * 8ull;
     const uint32_t lo = (uint32_t)bits, hi = (uint32_t)(bits >> 32);
     const uint32_t l14 = H::kBigEndian ? bswap(hi) : lo;
     const uint32_t l15 = H::kBigEndian ? bswap(lo) : hi;
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) raw[q][j] |= (pw == (uint32_t)j) ? pad : 0u;
+    }
     // One compress call site for the 1- or 2-block tail keeps the kernel's
     // instruction footprint small (SM3's unrolled compress is ~1.7k SASS).
     const int ntail = r < 56u ? 1 : 2;
 #pragma unroll 1
     for (int k = 0; k < ntail; ++k) {
         if (k == ntail - 1) {
-            if (k == 1) {
 #pragma unroll
-                for (int j = 0; j < 14; ++j) raw[j] = 0u;
+            for (int q = 0; q < NB; ++q) {
+                if (k == 1) {
+#pragma unroll
+                    for (int j = 0; j < 14; ++j) raw[q][j] = 0u;
+                }
+                raw[q][14] = l14;
+                raw[q][15] = l15;
             }
-            raw[14] = l14;
-            raw[15] = l15;
         }
-        H::compress(st, raw);
+        H::template compress_n<NB>(st, raw);
     }
+}
+
+template <int ALG, int V = -1>
+__device__ __forceinline__ void md_finish(uint32_t* st, uint32_t* raw, uint32_t r, uint64_t len_bytes) {
+    using H = HashAlg<ALG, V>;
+    uint32_t s[1][H::kStateWords];
+    uint32_t w[1][16];
+#pragma unroll
+    for (int i = 0; i < H::kStateWords; ++i) s[0][i] = st[i];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[0][i] = raw[i];
+    md_finish_n<ALG, V, 1>(s, w, r, len_bytes);
+#pragma unroll
+    for (int i = 0; i < H::kStateWords; ++i) st[i] = s[0][i];
 }
 
 // Keep bytes [0, r) of 16 little-endian words, zero the rest.
@@ -279,7 +376,7 @@ __device__ __forceinline__ void mask_tail(uint32_t raw[16], uint32_t r) {
 // Write a digest (kDigestBytes) with 4-byte stores (20-byte SHA-1 rows are
 // only 4-byte aligned; MD5/SM3 rows are 16-byte aligned and use vector stores).
 template <int ALG>
-__device__ __forceinline__ void store_digest(uint8_t* out, const uint32_t st[]) {
+__device__ __forceinline__ void store_digest(uint8_t* out, const uint32_t* st) {
     using H = HashAlg<ALG>;
     uint32_t o[H::kStateWords];
     H::digest_words(st, o);

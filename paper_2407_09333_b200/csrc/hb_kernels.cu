@@ -12,6 +12,8 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "hb_algos.cuh"
@@ -37,68 +39,90 @@ uint64_t launches_total() { return g_launches.load(std::memory_order_relaxed); }
 // block arrives already masked.
 // =========================================================================
 constexpr int kTmaWarps = 4;
-constexpr int kRowsPerWarp = 32;
-constexpr int kStages = 3;
-constexpr int kStageBytes = 64 * kRowsPerWarp;  // 2 KiB
-constexpr int kTmaSmemBytes = kTmaWarps * kStages * kStageBytes + 1024 /*align slack*/ + kTmaWarps * kStages * 8;
 
-template <int ALG> struct Occupancy { static constexpr int kMinCtas = 8; };   // 1024 threads/SM
-template <> struct Occupancy<kSm3> { static constexpr int kMinCtas = 6; };    // SM3 needs more registers
+// Tunable tile configuration: NB messages per thread (ILP), STAGES-deep ring.
+template <int NB, int STAGES> struct TmaCfg {
+    static constexpr int kRows = 32 * NB;           // rows (messages) per warp
+    static constexpr int kStageBytes = 64 * kRows;  // one 64-byte block of every row
+    static constexpr int kSmem = kTmaWarps * STAGES * kStageBytes + 1024 /*align slack*/ + kTmaWarps * STAGES * 8;
+};
+template <int ALG, int NB, int STAGES> struct TmaOcc {  // CTAs per SM the register/smem budget targets
+    static constexpr int kMinCtas =
+        NB == 1 ? (ALG == kSm3 ? 6 : 8) : (STAGES == 2 && ALG != kSm3 ? 6 : 4);
+};
 
-template <int ALG>
-__global__ void __launch_bounds__(kTmaWarps * 32, Occupancy<ALG>::kMinCtas)
+template <int ALG, int V, int NB, int STAGES>
+__global__ void __launch_bounds__(kTmaWarps * 32, (TmaOcc<ALG, NB, STAGES>::kMinCtas))
 k_fixed_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG>;
+    using H = HashAlg<ALG, V>;
+    using C = TmaCfg<NB, STAGES>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t row0 = (blockIdx.x * kTmaWarps + warp) * kRowsPerWarp;
+    const uint32_t row0 = (blockIdx.x * kTmaWarps + warp) * C::kRows;
     if (row0 >= n) return;  // warp-uniform
 
     // 1024-align the ring (the swizzle pattern is a function of address bits 7:8).
     const uint32_t base_s = smem_u32(smem_raw);
     uint8_t* ring = smem_raw + (((base_s + 1023u) & ~1023u) - base_s);
-    uint8_t* wring = ring + warp * (kStages * kStageBytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kTmaWarps * kStages * kStageBytes) + warp * kStages;
+    uint8_t* wring = ring + warp * (STAGES * C::kStageBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kTmaWarps * STAGES * C::kStageBytes) + warp * STAGES;
 
     const uint32_t nload = (msg_len + 63u) >> 6;  // blocks holding message bytes
     if (lane == 0) {
         prefetch_tmap(&tmap);
 #pragma unroll
-        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
-        const uint32_t pro = nload < (uint32_t)kStages ? nload : (uint32_t)kStages;
+        const uint32_t pro = nload < (uint32_t)STAGES ? nload : (uint32_t)STAGES;
         for (uint32_t b = 0; b < pro; ++b) {
-            mbar_arrive_expect_tx(&bars[b], kStageBytes);
-            tma_load_2d(wring + b * kStageBytes, &tmap, &bars[b], (int)(b * 64u), (int)row0);
+            mbar_arrive_expect_tx(&bars[b], C::kStageBytes);
+            tma_load_2d(wring + b * C::kStageBytes, &tmap, &bars[b], (int)(b * 64u), (int)row0);
         }
     }
     __syncwarp();
 
-    uint32_t st[H::kStateWords];
-    H::init(st);
-    const uint32_t swz = (lane >> 1) & 3u;  // SWIZZLE_64B: 16B-chunk index ^= addr bits 7:8
-    uint32_t stage = 0, phase = 0;
-    uint32_t raw[16];
-    auto read_stage = [&](uint32_t s) {
-        const uint8_t* rowp = wring + s * kStageBytes + lane * 64u;
+    uint32_t st[NB][H::kStateWords];
 #pragma unroll
-        for (uint32_t c = 0; c < 4; ++c) {
-            const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((c ^ swz) << 4));
-            raw[4 * c + 0] = v.x; raw[4 * c + 1] = v.y; raw[4 * c + 2] = v.z; raw[4 * c + 3] = v.w;
+    for (int q = 0; q < NB; ++q) H::init(st[q]);
+    // SWIZZLE_64B: the 16-byte chunk index is XORed with address bits 7:8, i.e.
+    // (row >> 1) & 3; rows lane and lane+32q share it.
+    const uint32_t swz = (lane >> 1) & 3u;
+    uint32_t stage = 0, phase = 0;
+    uint32_t raw[NB][16];
+    // Shared-memory byte offsets of this lane's four 16-byte chunks in stage 0;
+    // a stage adds a warp-uniform base, so each read is LDS.128 [R + UR].
+    uint32_t choff[NB][4];
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+#pragma unroll
+        for (uint32_t c = 0; c < 4; ++c) choff[q][c] = smem_u32(wring) + (lane + 32u * q) * 64u + ((c ^ swz) << 4);
+    auto read_stage = [&](uint32_t s) {
+        const uint32_t sbase = s * C::kStageBytes;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+#pragma unroll
+            for (uint32_t c = 0; c < 4; ++c) {
+                uint32_t x, y, z, w;
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+                             : "r"(choff[q][c] + sbase)
+                             : "memory");
+                raw[q][4 * c + 0] = x; raw[q][4 * c + 1] = y; raw[q][4 * c + 2] = z; raw[q][4 * c + 3] = w;
+            }
         }
     };
     const uint32_t nfull = msg_len >> 6;
     for (uint32_t b = 0; b < nfull; ++b) {
         mbar_wait_parity(&bars[stage], phase);
         read_stage(stage);
-        H::compress(st, raw);
+        H::template compress_n<NB>(st, raw);
         __syncwarp();  // every lane has consumed this stage (its registers fed compress)
-        if (lane == 0 && b + kStages < nload) {
+        if (lane == 0 && b + STAGES < nload) {
             fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&bars[stage], kStageBytes);
-            tma_load_2d(wring + stage * kStageBytes, &tmap, &bars[stage], (int)((b + kStages) * 64u), (int)row0);
+            mbar_arrive_expect_tx(&bars[stage], C::kStageBytes);
+            tma_load_2d(wring + stage * C::kStageBytes, &tmap, &bars[stage], (int)((b + STAGES) * 64u), (int)row0);
         }
-        if (++stage == (uint32_t)kStages) { stage = 0; phase ^= 1u; }
+        if (++stage == (uint32_t)STAGES) { stage = 0; phase ^= 1u; }
     }
     const uint32_t r = msg_len & 63u;
     if (r) {  // partial data block: TMA zero-filled the columns >= msg_len
@@ -106,11 +130,114 @@ k_fixed_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_l
         read_stage(stage);
     } else {  // padding-only final block (0x80, zeros, length)
 #pragma unroll
-        for (int j = 0; j < 16; ++j) raw[j] = 0u;
+        for (int q = 0; q < NB; ++q)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) raw[q][j] = 0u;
     }
-    md_finish<ALG>(st, raw, r, msg_len);
-    const uint32_t row = row0 + lane;
-    if (row < n) store_digest<ALG>(out + (uint64_t)row * H::kDigestBytes, st);
+    md_finish_n<ALG, V, NB>(st, raw, r, msg_len);
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+        const uint32_t row = row0 + lane + 32u * q;
+        if (row < n) store_digest<ALG>(out + (uint64_t)row * H::kDigestBytes, st[q]);
+    }
+}
+
+// -------------------------------------------------------------------------
+// Warp-specialised variant: 4 compute warps + 1 producer warp per CTA.  The
+// producer's lane 0 streams one {64 B, 128 rows} TMA tile per message block
+// into a STAGES-deep CTA ring (full/empty mbarrier pair per stage); compute
+// warps only wait on `full`, read their row (4 x LDS.128) and arrive on
+// `empty` -- no TMA-issue path, fence or lane-0 branch in their loop.
+// -------------------------------------------------------------------------
+constexpr int kWsComputeWarps = 4;
+constexpr int kWsRows = 32 * kWsComputeWarps;  // rows per CTA tile
+constexpr int kWsStageBytes = 64 * kWsRows;    // 8 KiB
+template <int STAGES> struct WsCfg {
+    static constexpr int kSmem = STAGES * kWsStageBytes + 1024 + 2 * STAGES * 8;
+};
+template <int ALG, int STAGES> struct WsOcc {
+    static constexpr int kMinCtas = ALG == kSm3 ? 6 : (STAGES == 2 ? 9 : 8);
+};
+
+template <int ALG, int V, int STAGES>
+__global__ void __launch_bounds__((kWsComputeWarps + 1) * 32, (WsOcc<ALG, STAGES>::kMinCtas))
+k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG, V>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t row0 = blockIdx.x * kWsRows;
+    const uint32_t base_s = smem_u32(smem_raw);
+    uint8_t* ring = smem_raw + (((base_s + 1023u) & ~1023u) - base_s);
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * kWsStageBytes);
+    uint64_t* empty = full + STAGES;
+    const uint32_t nload = (msg_len + 63u) >> 6;
+
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWsComputeWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kWsComputeWarps) {  // ---------------- producer warp
+        if (lane == 0) {
+            prefetch_tmap(&tmap);
+            uint32_t s = 0, ph = 0;
+            for (uint32_t b = 0; b < nload; ++b) {
+                if (b >= (uint32_t)STAGES) mbar_wait_parity(&empty[s], ph ^ 1u);
+                mbar_arrive_expect_tx(&full[s], kWsStageBytes);
+                tma_load_2d(ring + s * kWsStageBytes, &tmap, &full[s], (int)(b * 64u), (int)row0);
+                if (++s == (uint32_t)STAGES) { s = 0; ph ^= 1u; }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------- compute warps
+    uint32_t st[1][H::kStateWords];
+    H::init(st[0]);
+    const uint32_t row = warp * 32u + lane;  // row inside the tile
+    const uint32_t swz = (row >> 1) & 3u;    // SWIZZLE_64B
+    uint32_t choff[4];
+#pragma unroll
+    for (uint32_t c = 0; c < 4; ++c) choff[c] = smem_u32(ring) + row * 64u + ((c ^ swz) << 4);
+    uint32_t raw[1][16];
+    auto read_stage = [&](uint32_t s) {
+        const uint32_t sbase = s * kWsStageBytes;
+#pragma unroll
+        for (uint32_t c = 0; c < 4; ++c) {
+            uint32_t x, y, z, w;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+                         : "r"(choff[c] + sbase)
+                         : "memory");
+            raw[0][4 * c + 0] = x; raw[0][4 * c + 1] = y; raw[0][4 * c + 2] = z; raw[0][4 * c + 3] = w;
+        }
+    };
+    const uint32_t nfull = msg_len >> 6;
+    uint32_t s = 0, ph = 0;
+    for (uint32_t b = 0; b < nfull; ++b) {
+        mbar_wait_parity(&full[s], ph);
+        read_stage(s);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
+        H::template compress_n<1>(st, raw);
+        if (++s == (uint32_t)STAGES) { s = 0; ph ^= 1u; }
+    }
+    const uint32_t r = msg_len & 63u;
+    if (r) {
+        mbar_wait_parity(&full[s], ph);
+        read_stage(s);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) raw[0][j] = 0u;
+    }
+    md_finish_n<ALG, V, 1>(st, raw, r, msg_len);
+    const uint32_t grow = row0 + row;
+    if (grow < n) store_digest<ALG>(out + (uint64_t)grow * H::kDigestBytes, st[0]);
 }
 
 // =========================================================================
@@ -119,7 +246,7 @@ k_fixed_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_l
 // row with 128-bit read-only loads.
 // =========================================================================
 template <int ALG>
-__global__ void __launch_bounds__(128, Occupancy<ALG>::kMinCtas)
+__global__ void __launch_bounds__(128, (TmaOcc<ALG, 1, 3>::kMinCtas))
 k_fixed_direct(const uint8_t* __restrict__ msgs, uint64_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
     using H = HashAlg<ALG>;
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -135,7 +262,7 @@ k_fixed_direct(const uint8_t* __restrict__ msgs, uint64_t n, uint32_t msg_len, u
             const uint4 v = __ldg(p + 4 * b + c);
             raw[4 * c + 0] = v.x; raw[4 * c + 1] = v.y; raw[4 * c + 2] = v.z; raw[4 * c + 3] = v.w;
         }
-        H::compress(st, raw);
+        compress1<ALG>(st, raw);
     }
     const uint32_t r = msg_len & 63u;
     uint32_t raw[16];
@@ -205,7 +332,7 @@ k_generic(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint6
     for (uint64_t b = 0; b < nfull; ++b) {
         uint32_t raw[16];
         load_block_unaligned(p + 64 * b, data_end, raw);
-        H::compress(st, raw);
+        compress1<ALG>(st, raw);
     }
     uint32_t raw[16];
     load_partial_unaligned(p + 64 * nfull, (uint32_t)(len & 63u), raw);
@@ -383,18 +510,21 @@ static PFN_encodeTiled get_encode_tiled() {
 static thread_local char g_tma_err[160];
 const char* tma_error() { return g_tma_err; }
 
-template <int ALG>
+template <int ALG, int V, int NB, int STAGES>
 static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
                                         cudaStream_t stream) {
+    using C = TmaCfg<NB, STAGES>;
     PFN_encodeTiled enc = get_encode_tiled();
     if (!enc) {
         snprintf(g_tma_err, sizeof g_tma_err, "cuTensorMapEncodeTiled unavailable");
         return cudaErrorNotSupported;
     }
+    // The (n, L) byte matrix as a 2-D tensor: dim0 = bytes of a row (contiguous),
+    // dim1 = rows with stride L.  Box = one 64-byte block of kRows rows.
     CUtensorMap map;
     const cuuint64_t dims[2] = {L, n};
     const cuuint64_t strides[1] = {L};
-    const cuuint32_t box[2] = {64, (cuuint32_t)kRowsPerWarp};
+    const cuuint32_t box[2] = {64, (cuuint32_t)C::kRows};
     const cuuint32_t estr[2] = {1, 1};
     CUresult rc = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_msgs), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -406,14 +536,118 @@ static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint3
     static std::once_flag attr_once;
     static cudaError_t attr_rc = cudaSuccess;
     std::call_once(attr_once, [] {
-        attr_rc = cudaFuncSetAttribute(k_fixed_tma<ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemBytes);
+        attr_rc = cudaFuncSetAttribute(k_fixed_tma<ALG, V, NB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       C::kSmem);
     });
     if (attr_rc != cudaSuccess) return attr_rc;
-    const uint32_t rows_per_cta = kTmaWarps * kRowsPerWarp;
+    const uint32_t rows_per_cta = kTmaWarps * C::kRows;
     const uint32_t grid = (n + rows_per_cta - 1) / rows_per_cta;
-    k_fixed_tma<ALG><<<grid, kTmaWarps * 32, kTmaSmemBytes, stream>>>(map, n, L, d_out);
+    k_fixed_tma<ALG, V, NB, STAGES><<<grid, kTmaWarps * 32, C::kSmem, stream>>>(map, n, L, d_out);
     note_launches(1);
     return cudaGetLastError();
+}
+
+template <int ALG, int V, int STAGES>
+static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
+                                       cudaStream_t stream) {
+    PFN_encodeTiled enc = get_encode_tiled();
+    if (!enc) {
+        snprintf(g_tma_err, sizeof g_tma_err, "cuTensorMapEncodeTiled unavailable");
+        return cudaErrorNotSupported;
+    }
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {L, n};
+    const cuuint64_t strides[1] = {L};
+    const cuuint32_t box[2] = {64, (cuuint32_t)kWsRows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult rc = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_msgs), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) {
+        snprintf(g_tma_err, sizeof g_tma_err, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)rc);
+        return cudaErrorInvalidValue;
+    }
+    static std::once_flag attr_once;
+    static cudaError_t attr_rc = cudaSuccess;
+    std::call_once(attr_once, [] {
+        attr_rc = cudaFuncSetAttribute(k_fixed_tma_ws<ALG, V, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       WsCfg<STAGES>::kSmem);
+    });
+    if (attr_rc != cudaSuccess) return attr_rc;
+    const uint32_t grid = (n + kWsRows - 1) / kWsRows;
+    k_fixed_tma_ws<ALG, V, STAGES><<<grid, (kWsComputeWarps + 1) * 32, WsCfg<STAGES>::kSmem, stream>>>(map, n, L,
+                                                                                                       d_out);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+// Tile configuration and round variant.  Defaults are the B200-measured best
+// (profiles/variant_sweep_r1*.txt); $HB_TMA_CFG ("1x3", "2x2", "2x3" =
+// messages-per-thread x ring stages) and $HB_VARIANT (0-3) override them for
+// A/B experiments.
+enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4 };
+template <int ALG> struct DefaultTmaCfg { static constexpr int value = kCfg1x3; };
+
+static int tma_variant(int alg) {
+    const char* v = getenv("HB_VARIANT");
+    if (v && *v >= '0' && *v <= '3' && v[1] == '\0') return *v - '0';
+    switch (alg) {
+    case kSha1: return DefaultVariant<kSha1>::value;
+    case kMd5: return DefaultVariant<kMd5>::value;
+    default: return DefaultVariant<kSm3>::value;
+    }
+}
+
+static int tma_cfg(int alg) {
+    const char* v = getenv("HB_TMA_CFG");
+    if (v && !strcmp(v, "1x3")) return kCfg1x3;
+    if (v && !strcmp(v, "2x2")) return kCfg2x2;
+    if (v && !strcmp(v, "2x3")) return kCfg2x3;
+    if (v && !strcmp(v, "ws2")) return kCfgWs2;
+    if (v && !strcmp(v, "ws3")) return kCfgWs3;
+    switch (alg) {
+    case kSha1: return DefaultTmaCfg<kSha1>::value;
+    case kMd5: return DefaultTmaCfg<kMd5>::value;
+    default: return DefaultTmaCfg<kSm3>::value;
+    }
+}
+
+template <int ALG>
+static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t L, uint8_t* dst, cudaStream_t s) {
+    const int cfg = tma_cfg(ALG);
+    const int v = tma_variant(ALG);
+    if (cfg == kCfgWs2) {
+        switch (v) {
+        case 0: return launch_fixed_tma_ws<ALG, 0, 2>(src, n, L, dst, s);
+        default: return launch_fixed_tma_ws<ALG, 1, 2>(src, n, L, dst, s);
+        }
+    }
+    if (cfg == kCfgWs3) {
+        switch (v) {
+        case 0: return launch_fixed_tma_ws<ALG, 0, 3>(src, n, L, dst, s);
+        default: return launch_fixed_tma_ws<ALG, 1, 3>(src, n, L, dst, s);
+        }
+    }
+    if (cfg == kCfg2x2) {
+        switch (v) {
+        case 0: return launch_fixed_tma_alg<ALG, 0, 2, 2>(src, n, L, dst, s);
+        case 2: return launch_fixed_tma_alg<ALG, 2, 2, 2>(src, n, L, dst, s);
+        default: return launch_fixed_tma_alg<ALG, 1, 2, 2>(src, n, L, dst, s);
+        }
+    }
+    if (cfg == kCfg2x3) {
+        switch (v) {
+        case 0: return launch_fixed_tma_alg<ALG, 0, 2, 3>(src, n, L, dst, s);
+        case 2: return launch_fixed_tma_alg<ALG, 2, 2, 3>(src, n, L, dst, s);
+        default: return launch_fixed_tma_alg<ALG, 1, 2, 3>(src, n, L, dst, s);
+        }
+    }
+    switch (v) {
+    case 0: return launch_fixed_tma_alg<ALG, 0, 1, 3>(src, n, L, dst, s);
+    case 2: return launch_fixed_tma_alg<ALG, 2, 1, 3>(src, n, L, dst, s);
+    case 3: return launch_fixed_tma_alg<ALG, 3, 1, 3>(src, n, L, dst, s);
+    default: return launch_fixed_tma_alg<ALG, 1, 1, 3>(src, n, L, dst, s);
+    }
 }
 
 template <int ALG>
@@ -427,8 +661,9 @@ static cudaError_t launch_fixed_alg(const uint8_t* d_msgs, uint64_t n, uint64_t 
         const uint64_t slab = 1ull << 30;
         for (uint64_t r0 = 0; r0 < n; r0 += slab) {
             const uint64_t rn = (n - r0) < slab ? (n - r0) : slab;
-            cudaError_t e = launch_fixed_tma_alg<ALG>(d_msgs + r0 * L, (uint32_t)rn, (uint32_t)L,
-                                                      d_out + r0 * H::kDigestBytes, stream);
+            const uint8_t* src = d_msgs + r0 * L;
+            uint8_t* dst = d_out + r0 * H::kDigestBytes;
+            const cudaError_t e = launch_tma_dispatch<ALG>(src, (uint32_t)rn, (uint32_t)L, dst, stream);
             if (e != cudaSuccess) return e;
         }
         return cudaSuccess;

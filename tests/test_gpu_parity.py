@@ -178,7 +178,7 @@ def test_decimal_workload(golden):
             assert sha(out) == row[alg]
     for w in list(range(1, 21)) + [25]:
         cnt = min(300, 10**w)
-        start = max(0, min(10**w - cnt, 10**w // 3))
+        start = max(0, min(10**w - cnt, 10**w // 3, 2**63))
         msgs = oracle.gen_decimal(start, cnt, w) if w <= 20 else gen_messages(start, cnt, w).as_array()
         for alg in ALGS:
             assert np.array_equal(hash_decimal(alg, start, cnt, w), oracle.batch_fixed(alg, msgs)), (alg, w)
@@ -256,3 +256,19 @@ def test_full_size_sampled_and_cross_path():
         sample = np.stack([oracle.fill_random(L, 2, int(r) * L) for r in rows])
         assert np.array_equal(got, oracle.batch_fixed(alg, sample, 8))
     del buf
+
+
+@pytest.mark.parametrize("cfg", ["1x3", "2x2", "2x3", "ws2", "ws3"])
+def test_tma_tile_configs_and_variants(cfg, monkeypatch):
+    """Every compiled TMA tile configuration x round variant is bit-exact
+    (the tuned default is only one of them; $HB_TMA_CFG/$HB_VARIANT select)."""
+    variants = ["0", "1", "2", "3"] if cfg == "1x3" else (["0", "1"] if cfg.startswith("ws") else ["0", "1", "2"])
+    monkeypatch.setenv("HB_TMA_CFG", cfg)
+    for L in (16, 48, 64, 112, 128, 1024, 1040):
+        n = 333
+        data = oracle.fill_random(n * L, 7 * L + 1).reshape(n, L)
+        refs = {a: oracle.batch_fixed(a, data, threads=8) for a in ALGS}
+        for v in variants:
+            monkeypatch.setenv("HB_VARIANT", v)
+            for alg in ALGS:
+                assert np.array_equal(batch_digest(alg, data), refs[alg]), (cfg, v, alg, L)

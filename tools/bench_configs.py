@@ -1,0 +1,135 @@
+"""Measure every BASELINE.json config on one B200 (kernel-only, device-resident
+inputs; CUDA events on the launching stream) and write JSON lines.
+
+  C1  SHA-1, 65,536 x 64 B                      (configs[0])
+  C2  MD5, 2^24 x 1 KiB                         (configs[1])
+  C3  SM3, 2^24 x 1 KiB                         (configs[2], 1-GPU point)
+  C4  varlen, 2^22 msgs uniform 1 B-4 KiB, all 3 algorithms (configs[3], 1-GPU point)
+  C5  message-size sweep 16 B-64 KiB x batch count, all 3 algorithms (configs[4], 1-GPU)
+
+Every point's digests are checked against the CPU oracle on a sample of rows.
+usage: python tools/bench_configs.py [out.jsonl] [--quick]
+"""
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+from paper_2407_09333_b200 import _native, device  # noqa: E402
+
+DLEN = {"sha1": 20, "md5": 16, "sm3": 32}
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+# minimal ALU-pipe ops per 64-byte block and the 64 lanes/clk/SM ALU rate
+ALU_OPS = {"md5": 128, "sha1": 448, "sm3": 1084}
+SMS = 148
+
+
+def timed(fn, steps, warmup=3):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / steps
+
+
+def clock_mhz():
+    try:
+        import subprocess
+
+        out = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm", "--format=csv,noheader,nounits", "-i", "0"],
+                             capture_output=True, text=True).stdout.strip()
+        return float(out.splitlines()[0])
+    except Exception:
+        return 1965.0
+
+
+def roof(alg, n_blocks, bytes_hbm, ms, f_mhz):
+    t_hbm = bytes_hbm / (PEAK * 1e9)
+    t_alu = n_blocks * ALU_OPS[alg] / (64 * SMS * f_mhz * 1e6)
+    t_roof = max(t_hbm, t_alu)
+    return {"bound": "hbm" if t_hbm >= t_alu else "alu", "t_roof_ms": round(t_roof * 1e3, 4),
+            "frac": round(t_roof / (ms * 1e-3), 4)}
+
+
+def fixed_point(alg, n, L, seed, steps, out, tag):
+    buf = torch.empty(n * L, dtype=torch.uint8, device="cuda:0")
+    device.fill_random(buf, seed)
+    msgs = buf.view(n, L)
+    dig = torch.empty((n, DLEN[alg]), dtype=torch.uint8, device="cuda:0")
+    ms = timed(lambda: device.hash_fixed(alg, msgs, out=dig), steps)
+    rows = np.unique(np.concatenate([np.random.default_rng(seed).integers(0, n, 256), [0, n - 1]]))
+    sample = np.stack([oracle.fill_random(L, seed, int(r) * L) for r in rows]) if L % 8 == 0 else \
+        buf.cpu().numpy().reshape(n, L)[rows]
+    ok = bool(np.array_equal(dig.cpu().numpy()[rows], oracle.batch_fixed(alg, sample, 8)))
+    blocks = n * ((L + 8) // 64 + 1)
+    f = clock_mhz()
+    rec = {"config": tag, "alg": alg, "n": n, "msg_len": L, "ms": round(ms, 4),
+           "GBps": round(n * L / ms / 1e6, 2), "Mhash_s": round(n / ms / 1e3, 2),
+           "roofline": roof(alg, blocks, n * (L + DLEN[alg]), ms, f), "sm_mhz": f, "bit_exact_sample": ok}
+    print(json.dumps(rec), flush=True)
+    out.write(json.dumps(rec) + "\n")
+    del buf, dig
+
+
+def varlen_point(alg, n, maxlen, seed, steps, out, flags=0):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, maxlen + 1, n).astype(np.int64)
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    total = int(off[-1])
+    data = torch.empty(total + 16, dtype=torch.uint8, device="cuda:0")
+    device.fill_random(data, seed)
+    d_off = torch.from_numpy(off).cuda()
+    dig = torch.empty((n, DLEN[alg]), dtype=torch.uint8, device="cuda:0")
+    scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch.uint8, device="cuda:0")
+    ms = timed(lambda: device.hash_varlen(alg, data, d_off, out=dig, scratch=scratch, flags=flags), steps)
+    k = 512
+    h = data[: int(off[k])].cpu().numpy()
+    ok = bool(np.array_equal(dig[:k].cpu().numpy(), oracle.batch_varlen(alg, h, off[: k + 1].astype(np.uint64), 8)))
+    blocks = int(((lens + 8) // 64 + 1).sum())
+    f = clock_mhz()
+    rec = {"config": "C4 varlen" + (" (no sort)" if flags else ""), "alg": alg, "n": n, "len": f"uniform 1-{maxlen}",
+           "bytes": total, "ms": round(ms, 4), "GBps": round(total / ms / 1e6, 2), "Mhash_s": round(n / ms / 1e3, 2),
+           "roofline": roof(alg, blocks, total + 8 * (n + 1) + n * DLEN[alg], ms, f), "sm_mhz": f,
+           "bit_exact_sample": ok}
+    print(json.dumps(rec), flush=True)
+    out.write(json.dumps(rec) + "\n")
+    del data, d_off, dig, scratch
+
+
+def main():
+    path = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "gpurun_out/configs.jsonl"
+    quick = "--quick" in sys.argv
+    os.makedirs(os.path.dirname(path) or ".", exist_ok=True)
+    t0 = time.time()
+    with open(path, "w") as out:
+        fixed_point("sha1", 65536, 64, 1, 200, out, "C1")
+        fixed_point("md5", 1 << 24, 1024, 2, 20, out, "C2")
+        fixed_point("sm3", 1 << 24, 1024, 3, 10, out, "C3")
+        fixed_point("sha1", 1 << 24, 1024, 2, 10, out, "C5 point")
+        for alg in ("sha1", "md5", "sm3"):
+            varlen_point(alg, 1 << 22, 4096, 4, 5, out)
+        varlen_point("md5", 1 << 22, 4096, 4, 5, out, flags=_native.HB_FLAG_NO_SORT)
+        if not quick:
+            for L in (16, 64, 256, 1024, 4096, 16384, 65536):
+                for n in sorted({1 << 16, (4 << 30) // L}):
+                    for alg in ("sha1", "md5", "sm3"):
+                        fixed_point(alg, n, L, 5000 + L, 5 if n * L > (1 << 30) else 50, out, "C5")
+    print(f"# done in {time.time() - t0:.1f} s", flush=True)
+
+
+if __name__ == "__main__":
+    main()
