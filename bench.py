@@ -34,9 +34,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "SHA-1/MD5/SM3 hashed GB/s and Mhash/s at 1/2/4/8 B200 vs CPU reference"
 DLEN = {"sha1": 20, "md5": 16, "sm3": 32}
-# Algorithmic SASS instructions per 64-byte block of the compiled compression
-# loop (tools/sass_mix.py on libhetoc_b200.so).
-INSTR_PER_BLOCK = {"md5": 258, "sha1": 622, "sm3": 1420}
+# Minimal ALU-pipe operations per 64-byte block (LOP3 boolean functions, SHF
+# rotates, LEA.HI rotate+add, PRMT byte swaps -- the work with no full-rate
+# FMA-pipe equivalent; every addition can be issued as IMAD/VIADD instead).
+# The ALU pipe retires 64 lanes/clk/SM on sm_100 (tools/pipe_bench.cu,
+# profiles/pipe_bench_r1.txt).  DESIGN.md §4 derives these counts.
+ALU_OPS_PER_BLOCK = {"md5": 128, "sha1": 448, "sm3": 1084}
 
 WORKLOADS = {
     # name: (alg, n per GPU, msg_len, seed, BASELINE config)
@@ -301,17 +304,24 @@ def run_ours(args):
     achieved = alg_bytes / (ms_local * 1e-3) / 1e9
     blocks = n * ((L + 8) // 64 + 1)
     clk = sampler.summary()
-    f_mhz = clk["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    f_max = peaks.get("sm_max_mhz", 1965.0)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
-    int_peak = sms * 128 * f_mhz * 1e6  # thread-instructions/s (4 SMSP x 32 lanes issue)
-    int_ach = blocks * INSTR_PER_BLOCK[alg] / (ms_local * 1e-3)
-    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": load_ncu_traffic(alg, n, L),
-            "kernel": f"k_fixed_tma<{alg}>", "bytes_per_launch": alg_bytes, "peak_source": peak_src,
-            "int_issue": {"achieved_tinstr_s": round(int_ach / 1e12, 2),
-                          "peak_tinstr_s": round(int_peak / 1e12, 2), "frac": round(int_ach / int_peak, 4),
-                          "instr_per_block": INSTR_PER_BLOCK[alg], "blocks_per_launch": blocks,
-                          "clock_mhz": f_mhz}}
+    alu_peak = sms * 64 * f_max * 1e6  # ALU-pipe lane-ops/s at max clock
+    alu_ach = blocks * ALU_OPS_PER_BLOCK[alg] / (ms_local * 1e-3)
+    t_hbm = alg_bytes / (peaks["hbm_gbs"] * 1e9)
+    t_alu = blocks * ALU_OPS_PER_BLOCK[alg] / alu_peak
+    alu = {"achieved": round(alu_ach / 1e12, 3), "peak": round(alu_peak / 1e12, 3), "unit": "Tops/s",
+           "frac": round(alu_ach / alu_peak, 4), "alu_ops_per_block": ALU_OPS_PER_BLOCK[alg],
+           "blocks_per_launch": blocks, "clock_mhz": f_max}
+    if t_hbm >= t_alu:
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved / peaks["hbm_gbs"], 4)}
+    else:  # integer (ALU-pipe) bound: report against the ALU-pipe roofline, HBM alongside
+        roof = {"bound": "alu", "achieved": alu["achieved"], "peak": alu["peak"], "unit": "Tops/s",
+                "frac": alu["frac"], "hbm_achieved_gbs": round(achieved, 1), "hbm_peak_gbs": peaks["hbm_gbs"]}
+    roof.update({"traffic": load_ncu_traffic(alg, n, L), "kernel": f"k_fixed_tma_ws<{alg}>",
+                 "bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                 "t_roof_ms": round(max(t_hbm, t_alu) * 1e3, 4), "alu_pipe": alu})
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),

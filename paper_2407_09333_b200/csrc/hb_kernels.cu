@@ -48,7 +48,8 @@ template <int NB, int STAGES> struct TmaCfg {
 };
 template <int ALG, int NB, int STAGES> struct TmaOcc {  // CTAs per SM the register/smem budget targets
     static constexpr int kMinCtas =
-        NB == 1 ? (ALG == kSm3 ? 6 : 8) : (STAGES == 2 && ALG != kSm3 ? 6 : 4);
+        NB == 1 ? (STAGES == 2 ? (ALG == kMd5 ? 12 : ALG == kSha1 ? 9 : 8) : (ALG == kSm3 ? 6 : 8))
+                : (STAGES == 2 && ALG != kSm3 ? 6 : 4);
 };
 
 template <int ALG, int V, int NB, int STAGES>
@@ -156,7 +157,7 @@ template <int STAGES> struct WsCfg {
     static constexpr int kSmem = STAGES * kWsStageBytes + 1024 + 2 * STAGES * 8;
 };
 template <int ALG, int STAGES> struct WsOcc {
-    static constexpr int kMinCtas = ALG == kSm3 ? 6 : (STAGES == 2 ? 9 : 8);
+    static constexpr int kMinCtas = ALG == kSm3 ? 6 : (STAGES == 2 ? (ALG == kMd5 ? 10 : 8) : 8);
 };
 
 template <int ALG, int V, int STAGES>
@@ -585,8 +586,10 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
 // (profiles/variant_sweep_r1*.txt); $HB_TMA_CFG ("1x3", "2x2", "2x3" =
 // messages-per-thread x ring stages) and $HB_VARIANT (0-3) override them for
 // A/B experiments.
-enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4 };
-template <int ALG> struct DefaultTmaCfg { static constexpr int value = kCfg1x3; };
+enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4, kCfg1x2 = 5 };
+// B200-measured (profiles/variant_sweep_r1d.txt, interleaved rounds): the
+// warp-specialised 3-stage ring is best for MD5 and SM3, 2-stage for SHA-1.
+template <int ALG> struct DefaultTmaCfg { static constexpr int value = ALG == kSha1 ? kCfgWs2 : kCfgWs3; };
 
 static int tma_variant(int alg) {
     const char* v = getenv("HB_VARIANT");
@@ -604,6 +607,7 @@ static int tma_cfg(int alg) {
     if (v && !strcmp(v, "2x2")) return kCfg2x2;
     if (v && !strcmp(v, "2x3")) return kCfg2x3;
     if (v && !strcmp(v, "ws2")) return kCfgWs2;
+    if (v && !strcmp(v, "1x2")) return kCfg1x2;
     if (v && !strcmp(v, "ws3")) return kCfgWs3;
     switch (alg) {
     case kSha1: return DefaultTmaCfg<kSha1>::value;
@@ -616,6 +620,12 @@ template <int ALG>
 static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t L, uint8_t* dst, cudaStream_t s) {
     const int cfg = tma_cfg(ALG);
     const int v = tma_variant(ALG);
+    if (cfg == kCfg1x2) {
+        switch (v) {
+        case 0: return launch_fixed_tma_alg<ALG, 0, 1, 2>(src, n, L, dst, s);
+        default: return launch_fixed_tma_alg<ALG, 1, 1, 2>(src, n, L, dst, s);
+        }
+    }
     if (cfg == kCfgWs2) {
         switch (v) {
         case 0: return launch_fixed_tma_ws<ALG, 0, 2>(src, n, L, dst, s);
