@@ -391,7 +391,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override messages per GPU")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=3.0)
-    ap.add_argument("--ref-step-seconds", type=float, default=2.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=1.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

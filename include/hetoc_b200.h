@@ -26,6 +26,8 @@
  *                     pkg/src/hetoc/runtime/executor.py:562-599
  *   hb_hash_decimal   hash_batch(alg, gen_messages(start, count, width))
  *                     pkg/src/hetoc/crypto/batch.py:86-99, :293-316
+ *   hb_hash_fixed_split hash_batch lowered with hyper.for duty ratios over GPUs
+ *                     (lower_loop pkg/src/hetoc/passes/lower_hyper_for.py:207-254)
  *   hb_partition_range partition_range  pkg/src/hetoc/passes/partition.py:17-31
  *   hb_device_count / hb_device_info   detect_hardware
  *                     pkg/src/hetoc/runtime/devices.py:169-184
@@ -57,6 +59,7 @@ typedef enum { HB_SHA1 = 0, HB_MD5 = 1, HB_SM3 = 2 } hb_alg;
 #define HB_FLAG_NO_TMA   0x1u  /* fixed width: direct-load kernel instead of TMA staging */
 #define HB_FLAG_NO_SORT  0x2u  /* varlen: skip the length-bucket sort                    */
 #define HB_FLAG_SYNC_H2D 0x4u  /* engine: no copy/compute overlap (diagnostics)          */
+#define HB_FLAG_VARLEN_WORDS 0x8u /* varlen: 32-bit-load kernel instead of 128-bit (A/B) */
 
 typedef struct {
     double total_ms;       /* host wall time of the call                              */
@@ -99,6 +102,14 @@ uint64_t hb_launch_count(void);           /* kernels launched by this process so
 int hb_hash_fixed(int alg, const uint8_t *msgs, uint64_t n, uint64_t msg_len, uint8_t *out,
                   const int *gpus, int n_gpus, uint32_t flags, hb_timing *t);
 
+/* Same with explicit duty ratios per GPU -- the hyper.for device bindings
+ * (lower_loop + partition_range, pkg/src/hetoc/passes/lower_hyper_for.py:207-254):
+ * ratios[i] in [0,1] summing to 1 (+-1e-9, pkg/src/hetoc/hir/verify.py:245-260);
+ * gpu i gets messages [b_i, b_{i+1}) by the cumulative round-half-up rule.
+ * Output is bit-identical for every ratio vector.             */
+int hb_hash_fixed_split(int alg, const uint8_t *msgs, uint64_t n, uint64_t msg_len, uint8_t *out,
+                        const int *gpus, const double *ratios, int n_gpus, uint32_t flags, hb_timing *t);
+
 /* Variable-length: message i = data[offsets[i], offsets[i+1]); offsets has n+1
  * non-decreasing entries, offsets[0] may be non-zero.                        */
 int hb_hash_varlen(int alg, const uint8_t *data, const uint64_t *offsets, uint64_t n, uint8_t *out,
@@ -114,7 +125,8 @@ int hb_hash_decimal(int alg, uint64_t start, uint64_t count, int width, uint8_t 
  * (NULL = legacy default stream) and NOT synchronised.                       */
 int hb_hash_fixed_dev(int alg, int gpu, const void *d_msgs, uint64_t n, uint64_t msg_len, void *d_out,
                       void *stream, uint32_t flags);
-/* d_data must be readable up to round_up(d_offsets[n] - offset_base, 4).
+/* d_data must be readable up to round_up(address of the last byte + 1, 16)
+ * (16-byte granular loads; cudaMalloc / torch allocations satisfy this).
  * d_scratch: hb_varlen_scratch_bytes(n) bytes, or NULL (unsorted).          */
 int hb_hash_varlen_dev(int alg, int gpu, const void *d_data, uint64_t data_bytes, const uint64_t *d_offsets,
                        uint64_t offset_base, uint64_t n, void *d_out, void *d_scratch, void *stream,

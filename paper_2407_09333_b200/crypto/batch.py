@@ -115,23 +115,33 @@ def _ptr(a: np.ndarray) -> int | None:
     return a.ctypes.data if a.size else None
 
 
-def batch_digest(alg: str, data, accel: bool = False, *, gpus=None, flags: int = 0,
+def batch_digest(alg: str, data, accel: bool = False, *, gpus=None, ratios=None, flags: int = 0,
                  timing: dict | None = None) -> np.ndarray:
     """Hash each row of an (n, width) uint8 array; returns a new (n, digest_len) uint8 array.
 
     Reference: batch.py:274-290.  ``accel`` is accepted for API compatibility.
+    ``ratios`` (with ``gpus``) are hyper.for duty ratios: GPU i hashes the
+    message range partition_range gives it (lower_hyper_for.py:207-254).
     If ``timing`` is a dict it receives the engine's hb_timing fields.
     """
     _check_alg(alg)
     rows = _as_rows(data)
     n, width = rows.shape
     out = np.empty((n, DIGEST_LEN[alg]), np.uint8)
-    if n == 0:
+    if ratios is not None:
+        if gpus is None or len(gpus) != len(ratios):
+            raise ValueError("ratios need a gpus list of the same length")
+    if n == 0 and ratios is None:
         return out
     garr, ng = _native.gpu_array(gpus)
     t = _native.HbTiming()
-    rc = _native.lib().hb_hash_fixed(_native.ALG_ID[alg], _ptr(rows), n, width, out.ctypes.data, garr, ng,
-                                     int(flags), ctypes.byref(t))
+    if ratios is not None:
+        r = (ctypes.c_double * len(ratios))(*[float(x) for x in ratios])
+        rc = _native.lib().hb_hash_fixed_split(_native.ALG_ID[alg], _ptr(rows), n, width, out.ctypes.data, garr,
+                                               r, ng, int(flags), ctypes.byref(t))
+    else:
+        rc = _native.lib().hb_hash_fixed(_native.ALG_ID[alg], _ptr(rows), n, width, out.ctypes.data, garr, ng,
+                                         int(flags), ctypes.byref(t))
     _native.check(rc, "hb_hash_fixed")
     if timing is not None:
         timing.update(t.as_dict())

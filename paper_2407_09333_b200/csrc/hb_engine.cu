@@ -433,11 +433,26 @@ static int resolve_gpus(const int* gpus, int n_gpus, std::vector<int>& out) {
     return HB_OK;
 }
 
-// Split [0, n) over the GPUs, run one host thread per shard, merge stats.
-static int run_sharded(ShardJob proto, uint64_t n, const std::vector<int>& devs, hb_timing* t) {
+// Duty-ratio validation as the reference verifier does for hyper.for device
+// bindings (pkg/src/hetoc/hir/verify.py:245-260, RATIO_SUM_TOL core.py:21).
+static int check_ratios(const double* r, int k) {
+    double total = 0.0;
+    for (int i = 0; i < k; ++i) {
+        if (!(r[i] >= 0.0 && r[i] <= 1.0)) return fail(HB_ERR_INVAL, "duty ratio %g outside [0, 1]", r[i]);
+        total += r[i];
+    }
+    if (std::fabs(total - 1.0) > 1e-9) return fail(HB_ERR_INVAL, "duty ratios sum to %.10g", total);
+    return HB_OK;
+}
+
+// Split [0, n) over the GPUs (equal ratios unless given), run one host thread
+// per shard, merge stats.
+static int run_sharded(ShardJob proto, uint64_t n, const std::vector<int>& devs, hb_timing* t,
+                       const double* user_ratios = nullptr) {
     const auto t0 = std::chrono::steady_clock::now();
     const int k = (int)devs.size();
     std::vector<double> ratios(k, 1.0 / k);
+    if (user_ratios) ratios.assign(user_ratios, user_ratios + k);
     std::vector<int64_t> bounds(k + 1);
     int rc = partition(0, (int64_t)n, ratios.data(), k, bounds.data());
     if (rc) return rc;
@@ -551,6 +566,32 @@ int hb_hash_fixed(int alg, const uint8_t* msgs, uint64_t n, uint64_t msg_len, ui
     j.in_pinned = is_pinned(msgs, n * msg_len);
     j.out_pinned = is_pinned(out, n * (uint64_t)dlen);
     return run_sharded(j, n, devs, t);
+}
+
+int hb_hash_fixed_split(int alg, const uint8_t* msgs, uint64_t n, uint64_t msg_len, uint8_t* out, const int* gpus,
+                        const double* ratios, int n_gpus, uint32_t flags, hb_timing* t) {
+    const int dlen = digest_len(alg);
+    if (dlen < 0) return fail(HB_ERR_ALG, "unknown hash algorithm id %d", alg);
+    if (t) memset(t, 0, sizeof *t);
+    if (!gpus || !ratios || n_gpus < 1) return fail(HB_ERR_INVAL, "need at least one (gpu, ratio) binding");
+    int rc = check_ratios(ratios, n_gpus);
+    if (rc) return rc;
+    if (n == 0) return HB_OK;
+    if (!out || (!msgs && msg_len)) return fail(HB_ERR_INVAL, "null buffer");
+    if (msg_len && n > UINT64_MAX / msg_len) return fail(HB_ERR_INVAL, "n*msg_len overflows");
+    std::vector<int> devs;
+    rc = resolve_gpus(gpus, n_gpus, devs);
+    if (rc) return rc;
+    ShardJob j;
+    j.kind = 0;
+    j.alg = alg;
+    j.msgs = msgs;
+    j.msg_len = msg_len;
+    j.out = out;
+    j.flags = flags;
+    j.in_pinned = is_pinned(msgs, n * msg_len);
+    j.out_pinned = is_pinned(out, n * (uint64_t)dlen);
+    return run_sharded(j, n, devs, t, ratios);
 }
 
 int hb_hash_varlen(int alg, const uint8_t* data, const uint64_t* offsets, uint64_t n, uint8_t* out,

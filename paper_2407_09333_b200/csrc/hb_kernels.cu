@@ -341,24 +341,96 @@ k_generic(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint6
     store_digest<ALG>(out + i * H::kDigestBytes, st);
 }
 
+// -------------------------------------------------------------------------
+// Variable-length kernel: per message, 128-bit read-only loads of the 16-byte
+// aligned window around each block (4-5 LDG.128 instead of 17 LDG.32), then a
+// realignment by the message's byte offset a%16: a word select by q=(a>>2)&3
+// (a switch that is warp-uniform because the length sort also groups messages
+// by q) and one funnel shift per word by (a%4)*8.
+// -------------------------------------------------------------------------
+__device__ __forceinline__ void realign16(const uint32_t (&c)[20], uint32_t q, uint32_t sh, uint32_t (&raw)[16]) {
+#define HB_RA(Q)                                                                    \
+    _Pragma("unroll") for (int j = 0; j < 16; ++j) raw[j] = __funnelshift_r(c[j + Q], c[j + Q + 1], sh);
+    switch (q) {
+    case 0: HB_RA(0) break;
+    case 1: HB_RA(1) break;
+    case 2: HB_RA(2) break;
+    default: HB_RA(3) break;
+    }
+#undef HB_RA
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(128)
+k_varlen16(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offsets, uint64_t offset_base,
+           const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = perm ? (uint64_t)perm[t] : t;
+    const uint64_t start = offsets[i] - offset_base;
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
+    const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
+    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
+    const bool misaligned = (a & 15u) != 0;
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    uint32_t c[20];
+    uint32_t raw[16];
+    const uint64_t nfull = len >> 6;
+    for (uint64_t b = 0; b < nfull; ++b) {
+        const uint4* src = w16 + 4 * b;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint4 v = __ldg(src + k);
+            c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+        }
+        uint4 v4 = make_uint4(0, 0, 0, 0);
+        if (misaligned) v4 = __ldg(src + 4);
+        c[16] = v4.x; c[17] = v4.y; c[18] = v4.z; c[19] = v4.w;
+        realign16(c, q, sh, raw);
+        compress1<ALG>(st, raw);
+    }
+    // tail: the r = len % 64 remaining bytes (chunks that overlap [p, p+r) only)
+    const uint32_t r = (uint32_t)(len & 63u);
+    const uintptr_t tail_end = a + len;
+    const uint4* src = w16 + 4 * nfull;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (reinterpret_cast<uintptr_t>(src + k) < tail_end) v = __ldg(src + k);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+    realign16(c, q, sh, raw);
+    mask_tail(raw, r);
+    md_finish<ALG>(st, raw, r, len);
+    store_digest<ALG>(out + i * H::kDigestBytes, st);
+}
+
 // ---------------------------------------------------- length-bucket sort --
 // Counting sort of message indices by block count, longest first.  Three
 // small kernels: per-CTA shared-memory histograms -> global histogram, one
 // exclusive scan, per-CTA reservation + scatter.  Order inside a bucket is
 // irrelevant (digests are written to out[i]).
-constexpr int kSortBuckets = 2048;
+// 1024 block-count classes (longest first; >= 1023 blocks share the first)
+// x 4 word-alignment classes q = (address >> 2) & 3, so a warp's messages
+// have similar lengths AND the same realignment path in k_varlen16.
+constexpr int kSortNbClasses = 1024;
+constexpr int kSortBuckets = kSortNbClasses * 4;
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 16;  // per thread
 
-__device__ __forceinline__ uint32_t sort_bucket(const uint64_t* offsets, uint64_t i) {
+__device__ __forceinline__ uint32_t sort_bucket(const uint64_t* offsets, uint64_t i, uint64_t addr_bias) {
     const uint64_t len = offsets[i + 1] - offsets[i];
     const uint64_t nb = (len + 8u) / 64u + 1u;
-    const uint64_t c = nb < (uint64_t)(kSortBuckets - 1) ? nb : (uint64_t)(kSortBuckets - 1);
-    return (uint32_t)(kSortBuckets - 1) - (uint32_t)c;
+    const uint64_t c = nb < (uint64_t)(kSortNbClasses - 1) ? nb : (uint64_t)(kSortNbClasses - 1);
+    const uint32_t q = (uint32_t)((offsets[i] + addr_bias) >> 2) & 3u;
+    return ((uint32_t)(kSortNbClasses - 1) - (uint32_t)c) * 4u + q;
 }
 
 __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __restrict__ offsets, uint64_t n,
-                                                            uint32_t* __restrict__ hist) {
+                                                            uint64_t addr_bias, uint32_t* __restrict__ hist) {
     __shared__ uint32_t h[kSortBuckets];
     for (int k = threadIdx.x; k < kSortBuckets; k += kSortThreads) h[k] = 0;
     __syncthreads();
@@ -366,7 +438,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __re
 #pragma unroll 4
     for (int it = 0; it < kSortItems; ++it) {
         const uint64_t i = base + (uint64_t)it * kSortThreads + threadIdx.x;
-        if (i < n) atomicAdd(&h[sort_bucket(offsets, i)], 1u);
+        if (i < n) atomicAdd(&h[sort_bucket(offsets, i, addr_bias)], 1u);
     }
     __syncthreads();
     for (int k = threadIdx.x; k < kSortBuckets; k += kSortThreads)
@@ -374,15 +446,19 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __re
 }
 
 __global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* __restrict__ hist) {
-    // exclusive scan of kSortBuckets (2 per thread) in place
+    // exclusive scan of kSortBuckets in place; thread t owns kPer consecutive buckets
+    constexpr int kPer = kSortBuckets / 1024;
     __shared__ uint32_t warp_sums[32];
     const int t = threadIdx.x;
-    const uint32_t a = hist[2 * t], b = hist[2 * t + 1];
-    uint32_t s = a + b, incl = s;
+    uint32_t v[kPer];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) { v[k] = hist[kPer * t + k]; s += v[k]; }
+    uint32_t incl = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if ((t & 31) >= o) incl += v;
+        const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if ((t & 31) >= o) incl += x;
     }
     if ((t & 31) == 31) warp_sums[t >> 5] = incl;
     __syncthreads();
@@ -390,19 +466,19 @@ __global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* __restrict__ hist)
         uint32_t w = warp_sums[t], wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, wi, o);
-            if (t >= o) wi += v;
+            const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (t >= o) wi += x;
         }
         warp_sums[t] = wi - w;  // exclusive warp prefix
     }
     __syncthreads();
-    const uint32_t excl = warp_sums[t >> 5] + incl - s;
-    hist[2 * t] = excl;
-    hist[2 * t + 1] = excl + a;
+    uint32_t run = warp_sums[t >> 5] + incl - s;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) { hist[kPer * t + k] = run; run += v[k]; }
 }
 
 __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const uint64_t* __restrict__ offsets, uint64_t n,
-                                                               uint32_t* __restrict__ cursor,
+                                                               uint64_t addr_bias, uint32_t* __restrict__ cursor,
                                                                uint32_t* __restrict__ perm) {
     __shared__ uint32_t h[kSortBuckets];
     __shared__ uint32_t base[kSortBuckets];
@@ -413,7 +489,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const uint64_t* _
 #pragma unroll
     for (int it = 0; it < kSortItems; ++it) {
         const uint64_t i = b0 + (uint64_t)it * kSortThreads + threadIdx.x;
-        bucket[it] = (i < n) ? sort_bucket(offsets, i) : 0xFFFFFFFFu;
+        bucket[it] = (i < n) ? sort_bucket(offsets, i, addr_bias) : 0xFFFFFFFFu;
         if (i < n) atomicAdd(&h[bucket[it]], 1u);
     }
     __syncthreads();
@@ -714,15 +790,20 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
         if (e != cudaSuccess) return e;
         const uint64_t per_cta = (uint64_t)kSortThreads * kSortItems;
         const unsigned g = (unsigned)((n + per_cta - 1) / per_cta);
-        k_sort_hist<<<g, kSortThreads, 0, stream>>>(d_offsets, n, hist);
+        const uint64_t bias = reinterpret_cast<uintptr_t>(d_data) - offset_base;  // address = offsets[i] + bias
+        k_sort_hist<<<g, kSortThreads, 0, stream>>>(d_offsets, n, bias, hist);
         k_sort_scan<<<1, 1024, 0, stream>>>(hist);
-        k_sort_scatter<<<g, kSortThreads, 0, stream>>>(d_offsets, n, hist, p);
+        k_sort_scatter<<<g, kSortThreads, 0, stream>>>(d_offsets, n, bias, hist, p);
         note_launches(3);
         perm = p;
     }
     const uint64_t grid = (n + 127) / 128;
-    k_generic<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets, offset_base,
-                                                             perm, 0, n, d_out);
+    if (flags & HB_FLAG_VARLEN_WORDS) {  // A/B baseline: 32-bit loads
+        k_generic<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets,
+                                                                 offset_base, perm, 0, n, d_out);
+    } else {
+        k_varlen16<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
+    }
     note_launches(1);
     return cudaGetLastError();
 }

@@ -152,3 +152,16 @@ def test_no_cpu_fallback_without_gpu():
         batch_digest("md5", np.zeros((4, 16), np.uint8))
     lib = _native.lib()
     assert lib.hb_hash_fixed_dev(1, 0, ctypes.c_void_p(16), 1, 16, ctypes.c_void_p(16), None, 0) == _native.HB_ERR_NODEV
+
+
+def test_ratio_validation_matches_reference_verifier():
+    # pkg/src/hetoc/hir/verify.py:245-260: ratios in [0,1], sum within 1e-9 (checked before any device work)
+    from paper_2407_09333_b200.crypto import batch_digest as bd
+
+    rows = np.zeros((4, 8), np.uint8)
+    with pytest.raises(ValueError, match="outside"):
+        bd("md5", rows, gpus=[0, 0], ratios=[1.5, -0.5])
+    with pytest.raises(ValueError, match="sum"):
+        bd("md5", rows, gpus=[0, 0], ratios=[0.5, 0.4])
+    with pytest.raises(ValueError):
+        bd("md5", rows, gpus=[0], ratios=[0.5, 0.5])

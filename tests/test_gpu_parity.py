@@ -119,8 +119,9 @@ def test_varlen_random_sorted_and_unsorted(alg):
     off[0] = 5
     data = oracle.fill_random(int(off[-1]) + 3, 99)
     ref = oracle.batch_varlen(alg, data, off, threads=8)
-    for fl in (0, _native.HB_FLAG_NO_SORT):
-        assert np.array_equal(batch_digest_varlen(alg, data, off, flags=fl), ref)
+    for fl in (0, _native.HB_FLAG_NO_SORT, _native.HB_FLAG_VARLEN_WORDS,
+               _native.HB_FLAG_VARLEN_WORDS | _native.HB_FLAG_NO_SORT):
+        assert np.array_equal(batch_digest_varlen(alg, data, off, flags=fl), ref), fl
 
 
 def test_engine_chunking_and_pinned(monkeypatch):
@@ -272,3 +273,18 @@ def test_tma_tile_configs_and_variants(cfg, monkeypatch):
             monkeypatch.setenv("HB_VARIANT", v)
             for alg in ALGS:
                 assert np.array_equal(batch_digest(alg, data), refs[alg]), (cfg, v, alg, L)
+
+
+def test_duty_ratio_invariance():
+    """SPEC.md:505 on the GPU: 10^5 x 9-byte generated messages give bit-identical
+    digests for every duty-ratio split on the 0.02 grid (two bindings here map to
+    GPU 0 and, when present, GPU 1; on one GPU both bindings share it)."""
+    n_dev = _native.device_count()
+    gpus = [0, 1 if n_dev > 1 else 0]
+    msgs = gen_messages(0, 10**5).as_array()
+    for alg in ALGS:
+        ref = oracle.batch_fixed(alg, msgs, threads=8)
+        for k in range(0, 51):
+            x = k / 50
+            got = batch_digest(alg, msgs, gpus=gpus, ratios=[x, 1.0 - x])
+            assert np.array_equal(got, ref), (alg, x)

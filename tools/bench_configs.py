@@ -101,7 +101,8 @@ def varlen_point(alg, n, maxlen, seed, steps, out, flags=0):
     ok = bool(np.array_equal(dig[:k].cpu().numpy(), oracle.batch_varlen(alg, h, off[: k + 1].astype(np.uint64), 8)))
     blocks = int(((lens + 8) // 64 + 1).sum())
     f = clock_mhz()
-    rec = {"config": "C4 varlen" + (" (no sort)" if flags else ""), "alg": alg, "n": n, "len": f"uniform 1-{maxlen}",
+    tagf = {0: "", _native.HB_FLAG_NO_SORT: " (no sort)", _native.HB_FLAG_VARLEN_WORDS: " (32-bit loads)"}[flags]
+    rec = {"config": "C4 varlen" + tagf, "alg": alg, "n": n, "len": f"uniform 1-{maxlen}",
            "bytes": total, "ms": round(ms, 4), "GBps": round(total / ms / 1e6, 2), "Mhash_s": round(n / ms / 1e3, 2),
            "roofline": roof(alg, blocks, total + 8 * (n + 1) + n * DLEN[alg], ms, f), "sm_mhz": f,
            "bit_exact_sample": ok}
@@ -123,6 +124,8 @@ def main():
         for alg in ("sha1", "md5", "sm3"):
             varlen_point(alg, 1 << 22, 4096, 4, 5, out)
         varlen_point("md5", 1 << 22, 4096, 4, 5, out, flags=_native.HB_FLAG_NO_SORT)
+        for alg in ("sha1", "md5", "sm3"):
+            varlen_point(alg, 1 << 22, 4096, 4, 5, out, flags=_native.HB_FLAG_VARLEN_WORDS)
         if not quick:
             for L in (16, 64, 256, 1024, 4096, 16384, 65536):
                 for n in sorted({1 << 16, (4 << 30) // L}):

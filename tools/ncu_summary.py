@@ -41,7 +41,10 @@ UNIT = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "byte": 1.0}
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # a `--page raw --csv` export made on the GPU box
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         return []
@@ -84,7 +87,8 @@ def launches(path):
 
 def main():
     tag = sys.argv[1]
-    reps = [a for a in sys.argv[2:] if a.endswith(".ncu-rep")]
+    args = sys.argv[2:sys.argv.index("--launches")] if "--launches" in sys.argv else sys.argv[2:]
+    reps = [a for a in args if a.endswith(".ncu-rep") or a.endswith(".csv")]
     lcs = []
     if "--launches" in sys.argv:
         lcs = sys.argv[sys.argv.index("--launches") + 1:]
@@ -106,7 +110,8 @@ def main():
             md.append("")
             rd = to_bytes(*d["dram__bytes_read.sum"]) if "dram__bytes_read.sum" in d else None
             wr = to_bytes(*d["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in d else None
-            wl = os.path.basename(rep).replace("prof_", "").replace(".ncu-rep", "")
+            wl = re.sub(r"_r\d+\w*$", "", os.path.basename(rep).replace("prof_", "").replace("raw_", "")
+                        .replace(".ncu-rep", "").replace(".csv", ""))
             key = {"md5_1k": "md5_16777216x1024", "sha1_1k": "sha1_16777216x1024",
                    "sm3_1k": "sm3_16777216x1024"}.get(wl, wl)
             summ[key] = {
