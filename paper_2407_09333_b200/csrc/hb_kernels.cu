@@ -41,32 +41,36 @@ uint64_t launches_total() { return g_launches.load(std::memory_order_relaxed); }
 constexpr int kTmaWarps = 4;
 
 // Tunable tile configuration: NB messages per thread (ILP), STAGES-deep ring.
-template <int NB, int STAGES> struct TmaCfg {
+// W warps per CTA.  W = 1 is the small-batch shape: a batch of n messages
+// becomes n/32 single-warp CTAs spread evenly over all 148 SMs (with 4-warp
+// CTAs a 65,536-message batch fills only 512 CTAs, 3-4 per SM, unevenly).
+template <int NB, int STAGES, int W = kTmaWarps> struct TmaCfg {
     static constexpr int kRows = 32 * NB;           // rows (messages) per warp
     static constexpr int kStageBytes = 64 * kRows;  // one 64-byte block of every row
-    static constexpr int kSmem = kTmaWarps * STAGES * kStageBytes + 1024 /*align slack*/ + kTmaWarps * STAGES * 8;
+    static constexpr int kSmem = W * STAGES * kStageBytes + 1024 /*align slack*/ + W * STAGES * 8;
 };
-template <int ALG, int NB, int STAGES> struct TmaOcc {  // CTAs per SM the register/smem budget targets
+template <int ALG, int NB, int STAGES, int W = kTmaWarps> struct TmaOcc {  // CTAs per SM the budget targets
     static constexpr int kMinCtas =
-        NB == 1 ? (STAGES == 2 ? (ALG == kMd5 ? 12 : ALG == kSha1 ? 9 : 8) : (ALG == kSm3 ? 6 : 8))
-                : (STAGES == 2 && ALG != kSm3 ? 6 : 4);
+        W == 1 ? 16
+        : NB == 1 ? (STAGES == 2 ? (ALG == kMd5 ? 12 : ALG == kSha1 ? 9 : 8) : (ALG == kSm3 ? 6 : 8))
+                  : (STAGES == 2 && ALG != kSm3 ? 6 : 4);
 };
 
-template <int ALG, int V, int NB, int STAGES>
-__global__ void __launch_bounds__(kTmaWarps * 32, (TmaOcc<ALG, NB, STAGES>::kMinCtas))
+template <int ALG, int V, int NB, int STAGES, int W = kTmaWarps>
+__global__ void __launch_bounds__(W * 32, (TmaOcc<ALG, NB, STAGES, W>::kMinCtas))
 k_fixed_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
     using H = HashAlg<ALG, V>;
-    using C = TmaCfg<NB, STAGES>;
+    using C = TmaCfg<NB, STAGES, W>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t row0 = (blockIdx.x * kTmaWarps + warp) * C::kRows;
+    const uint32_t row0 = (blockIdx.x * W + warp) * C::kRows;
     if (row0 >= n) return;  // warp-uniform
 
     // 1024-align the ring (the swizzle pattern is a function of address bits 7:8).
     const uint32_t base_s = smem_u32(smem_raw);
     uint8_t* ring = smem_raw + (((base_s + 1023u) & ~1023u) - base_s);
     uint8_t* wring = ring + warp * (STAGES * C::kStageBytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kTmaWarps * STAGES * C::kStageBytes) + warp * STAGES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + W * STAGES * C::kStageBytes) + warp * STAGES;
 
     const uint32_t nload = (msg_len + 63u) >> 6;  // blocks holding message bytes
     if (lane == 0) {
@@ -151,25 +155,27 @@ k_fixed_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_l
 // `empty` -- no TMA-issue path, fence or lane-0 branch in their loop.
 // -------------------------------------------------------------------------
 constexpr int kWsComputeWarps = 4;
-constexpr int kWsRows = 32 * kWsComputeWarps;  // rows per CTA tile
-constexpr int kWsStageBytes = 64 * kWsRows;    // 8 KiB
-template <int STAGES> struct WsCfg {
-    static constexpr int kSmem = STAGES * kWsStageBytes + 1024 + 2 * STAGES * 8;
+template <int NB, int STAGES> struct WsCfg {
+    static constexpr int kRows = 32 * kWsComputeWarps * NB;  // rows per CTA tile (TMA box height <= 256)
+    static constexpr int kStageBytes = 64 * kRows;            // 8 KiB per message slot
+    static constexpr int kSmem = STAGES * kStageBytes + 1024 + 2 * STAGES * 8;
 };
-template <int ALG, int STAGES> struct WsOcc {
-    static constexpr int kMinCtas = ALG == kSm3 ? 6 : (STAGES == 2 ? (ALG == kMd5 ? 10 : 8) : 8);
+template <int ALG, int NB, int STAGES> struct WsOcc {
+    static constexpr int kMinCtas =
+        NB == 2 ? (STAGES == 2 ? 6 : 4) : ALG == kSm3 ? 6 : (STAGES == 2 ? (ALG == kMd5 ? 10 : 8) : 8);
 };
 
-template <int ALG, int V, int STAGES>
-__global__ void __launch_bounds__((kWsComputeWarps + 1) * 32, (WsOcc<ALG, STAGES>::kMinCtas))
+template <int ALG, int V, int NB, int STAGES>
+__global__ void __launch_bounds__((kWsComputeWarps + 1) * 32, (WsOcc<ALG, NB, STAGES>::kMinCtas))
 k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
     using H = HashAlg<ALG, V>;
+    using C = WsCfg<NB, STAGES>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t row0 = blockIdx.x * kWsRows;
+    const uint32_t row0 = blockIdx.x * C::kRows;
     const uint32_t base_s = smem_u32(smem_raw);
     uint8_t* ring = smem_raw + (((base_s + 1023u) & ~1023u) - base_s);
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * kWsStageBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * C::kStageBytes);
     uint64_t* empty = full + STAGES;
     const uint32_t nload = (msg_len + 63u) >> 6;
 
@@ -189,8 +195,8 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
             uint32_t s = 0, ph = 0;
             for (uint32_t b = 0; b < nload; ++b) {
                 if (b >= (uint32_t)STAGES) mbar_wait_parity(&empty[s], ph ^ 1u);
-                mbar_arrive_expect_tx(&full[s], kWsStageBytes);
-                tma_load_2d(ring + s * kWsStageBytes, &tmap, &full[s], (int)(b * 64u), (int)row0);
+                mbar_arrive_expect_tx(&full[s], C::kStageBytes);
+                tma_load_2d(ring + s * C::kStageBytes, &tmap, &full[s], (int)(b * 64u), (int)row0);
                 if (++s == (uint32_t)STAGES) { s = 0; ph ^= 1u; }
             }
         }
@@ -198,24 +204,31 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
     }
 
     // ------------------------------------------------- compute warps
-    uint32_t st[1][H::kStateWords];
-    H::init(st[0]);
-    const uint32_t row = warp * 32u + lane;  // row inside the tile
-    const uint32_t swz = (row >> 1) & 3u;    // SWIZZLE_64B
-    uint32_t choff[4];
+    // Thread (warp, lane) owns tile rows warp*32 + lane + 128*q, q < NB.
+    uint32_t st[NB][H::kStateWords];
 #pragma unroll
-    for (uint32_t c = 0; c < 4; ++c) choff[c] = smem_u32(ring) + row * 64u + ((c ^ swz) << 4);
-    uint32_t raw[1][16];
+    for (int q = 0; q < NB; ++q) H::init(st[q]);
+    const uint32_t row = warp * 32u + lane;  // row inside the tile (q = 0)
+    const uint32_t swz = (row >> 1) & 3u;    // SWIZZLE_64B (same for row + 128q)
+    uint32_t choff[NB][4];
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+#pragma unroll
+        for (uint32_t c = 0; c < 4; ++c) choff[q][c] = smem_u32(ring) + (row + 128u * q) * 64u + ((c ^ swz) << 4);
+    uint32_t raw[NB][16];
     auto read_stage = [&](uint32_t s) {
-        const uint32_t sbase = s * kWsStageBytes;
+        const uint32_t sbase = s * C::kStageBytes;
 #pragma unroll
-        for (uint32_t c = 0; c < 4; ++c) {
-            uint32_t x, y, z, w;
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
-                         : "r"(choff[c] + sbase)
-                         : "memory");
-            raw[0][4 * c + 0] = x; raw[0][4 * c + 1] = y; raw[0][4 * c + 2] = z; raw[0][4 * c + 3] = w;
+        for (int q = 0; q < NB; ++q) {
+#pragma unroll
+            for (uint32_t c = 0; c < 4; ++c) {
+                uint32_t x, y, z, w;
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+                             : "r"(choff[q][c] + sbase)
+                             : "memory");
+                raw[q][4 * c + 0] = x; raw[q][4 * c + 1] = y; raw[q][4 * c + 2] = z; raw[q][4 * c + 3] = w;
+            }
         }
     };
     const uint32_t nfull = msg_len >> 6;
@@ -225,7 +238,7 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
         read_stage(s);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
-        H::template compress_n<1>(st, raw);
+        H::template compress_n<NB>(st, raw);
         if (++s == (uint32_t)STAGES) { s = 0; ph ^= 1u; }
     }
     const uint32_t r = msg_len & 63u;
@@ -234,11 +247,16 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
         read_stage(s);
     } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) raw[0][j] = 0u;
+        for (int q = 0; q < NB; ++q)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) raw[q][j] = 0u;
     }
-    md_finish_n<ALG, V, 1>(st, raw, r, msg_len);
-    const uint32_t grow = row0 + row;
-    if (grow < n) store_digest<ALG>(out + (uint64_t)grow * H::kDigestBytes, st[0]);
+    md_finish_n<ALG, V, NB>(st, raw, r, msg_len);
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+        const uint32_t grow = row0 + row + 128u * q;
+        if (grow < n) store_digest<ALG>(out + (uint64_t)grow * H::kDigestBytes, st[q]);
+    }
 }
 
 // =========================================================================
@@ -587,10 +605,10 @@ static PFN_encodeTiled get_encode_tiled() {
 static thread_local char g_tma_err[160];
 const char* tma_error() { return g_tma_err; }
 
-template <int ALG, int V, int NB, int STAGES>
+template <int ALG, int V, int NB, int STAGES, int W = kTmaWarps>
 static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
                                         cudaStream_t stream) {
-    using C = TmaCfg<NB, STAGES>;
+    using C = TmaCfg<NB, STAGES, W>;
     PFN_encodeTiled enc = get_encode_tiled();
     if (!enc) {
         snprintf(g_tma_err, sizeof g_tma_err, "cuTensorMapEncodeTiled unavailable");
@@ -613,20 +631,21 @@ static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint3
     static std::once_flag attr_once;
     static cudaError_t attr_rc = cudaSuccess;
     std::call_once(attr_once, [] {
-        attr_rc = cudaFuncSetAttribute(k_fixed_tma<ALG, V, NB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       C::kSmem);
+        attr_rc = cudaFuncSetAttribute(k_fixed_tma<ALG, V, NB, STAGES, W>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     });
     if (attr_rc != cudaSuccess) return attr_rc;
-    const uint32_t rows_per_cta = kTmaWarps * C::kRows;
+    const uint32_t rows_per_cta = W * C::kRows;
     const uint32_t grid = (n + rows_per_cta - 1) / rows_per_cta;
-    k_fixed_tma<ALG, V, NB, STAGES><<<grid, kTmaWarps * 32, C::kSmem, stream>>>(map, n, L, d_out);
+    k_fixed_tma<ALG, V, NB, STAGES, W><<<grid, W * 32, C::kSmem, stream>>>(map, n, L, d_out);
     note_launches(1);
     return cudaGetLastError();
 }
 
-template <int ALG, int V, int STAGES>
+template <int ALG, int V, int NB, int STAGES>
 static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
                                        cudaStream_t stream) {
+    using C = WsCfg<NB, STAGES>;
     PFN_encodeTiled enc = get_encode_tiled();
     if (!enc) {
         snprintf(g_tma_err, sizeof g_tma_err, "cuTensorMapEncodeTiled unavailable");
@@ -635,7 +654,7 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     CUtensorMap map;
     const cuuint64_t dims[2] = {L, n};
     const cuuint64_t strides[1] = {L};
-    const cuuint32_t box[2] = {64, (cuuint32_t)kWsRows};
+    const cuuint32_t box[2] = {64, (cuuint32_t)C::kRows};
     const cuuint32_t estr[2] = {1, 1};
     CUresult rc = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_msgs), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -647,13 +666,12 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     static std::once_flag attr_once;
     static cudaError_t attr_rc = cudaSuccess;
     std::call_once(attr_once, [] {
-        attr_rc = cudaFuncSetAttribute(k_fixed_tma_ws<ALG, V, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       WsCfg<STAGES>::kSmem);
+        attr_rc = cudaFuncSetAttribute(k_fixed_tma_ws<ALG, V, NB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       C::kSmem);
     });
     if (attr_rc != cudaSuccess) return attr_rc;
-    const uint32_t grid = (n + kWsRows - 1) / kWsRows;
-    k_fixed_tma_ws<ALG, V, STAGES><<<grid, (kWsComputeWarps + 1) * 32, WsCfg<STAGES>::kSmem, stream>>>(map, n, L,
-                                                                                                       d_out);
+    const uint32_t grid = (n + C::kRows - 1) / C::kRows;
+    k_fixed_tma_ws<ALG, V, NB, STAGES><<<grid, (kWsComputeWarps + 1) * 32, C::kSmem, stream>>>(map, n, L, d_out);
     note_launches(1);
     return cudaGetLastError();
 }
@@ -662,10 +680,12 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
 // (profiles/variant_sweep_r1*.txt); $HB_TMA_CFG ("1x3", "2x2", "2x3" =
 // messages-per-thread x ring stages) and $HB_VARIANT (0-3) override them for
 // A/B experiments.
-enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4, kCfg1x2 = 5 };
-// B200-measured (profiles/variant_sweep_r1d.txt, interleaved rounds): the
-// warp-specialised 3-stage ring is best for MD5 and SM3, 2-stage for SHA-1.
-template <int ALG> struct DefaultTmaCfg { static constexpr int value = ALG == kSha1 ? kCfgWs2 : kCfgWs3; };
+enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4, kCfg1x2 = 5, kCfgWs2x2 = 6, kCfgWs3x2 = 7 };
+// B200-measured (profiles/variant_sweep_r1d.txt and _r1e.txt, interleaved
+// rounds): the warp-specialised 3-stage ring is best for MD5 and SM3 (SM3's
+// 61 registers make two messages per thread lose occupancy); SHA-1 gains 4 %
+// from two messages per thread (ws3x2: 7.38 vs 7.69 ms at 2^24 x 1 KiB).
+template <int ALG> struct DefaultTmaCfg { static constexpr int value = ALG == kSha1 ? kCfgWs3x2 : kCfgWs3; };
 
 static int tma_variant(int alg) {
     const char* v = getenv("HB_VARIANT");
@@ -685,6 +705,8 @@ static int tma_cfg(int alg) {
     if (v && !strcmp(v, "ws2")) return kCfgWs2;
     if (v && !strcmp(v, "1x2")) return kCfg1x2;
     if (v && !strcmp(v, "ws3")) return kCfgWs3;
+    if (v && !strcmp(v, "ws2x2")) return kCfgWs2x2;
+    if (v && !strcmp(v, "ws3x2")) return kCfgWs3x2;
     switch (alg) {
     case kSha1: return DefaultTmaCfg<kSha1>::value;
     case kMd5: return DefaultTmaCfg<kMd5>::value;
@@ -692,10 +714,19 @@ static int tma_cfg(int alg) {
     }
 }
 
+// Below this many messages the 4-warp tiles cannot fill the GPU evenly and
+// the single-warp-CTA kernel is used ($HB_SMALL_N overrides; 0 disables).
+static uint64_t small_n_threshold() {
+    const char* v = getenv("HB_SMALL_N");
+    return v ? strtoull(v, nullptr, 10) : (1ull << 18);
+}
+
 template <int ALG>
 static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t L, uint8_t* dst, cudaStream_t s) {
     const int cfg = tma_cfg(ALG);
     const int v = tma_variant(ALG);
+    if (!getenv("HB_TMA_CFG") && (uint64_t)n < small_n_threshold())
+        return launch_fixed_tma_alg<ALG, DefaultVariant<ALG>::value, 1, 3, 1>(src, n, L, dst, s);
     if (cfg == kCfg1x2) {
         switch (v) {
         case 0: return launch_fixed_tma_alg<ALG, 0, 1, 2>(src, n, L, dst, s);
@@ -704,14 +735,26 @@ static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t 
     }
     if (cfg == kCfgWs2) {
         switch (v) {
-        case 0: return launch_fixed_tma_ws<ALG, 0, 2>(src, n, L, dst, s);
-        default: return launch_fixed_tma_ws<ALG, 1, 2>(src, n, L, dst, s);
+        case 0: return launch_fixed_tma_ws<ALG, 0, 1, 2>(src, n, L, dst, s);
+        default: return launch_fixed_tma_ws<ALG, 1, 1, 2>(src, n, L, dst, s);
         }
     }
     if (cfg == kCfgWs3) {
         switch (v) {
-        case 0: return launch_fixed_tma_ws<ALG, 0, 3>(src, n, L, dst, s);
-        default: return launch_fixed_tma_ws<ALG, 1, 3>(src, n, L, dst, s);
+        case 0: return launch_fixed_tma_ws<ALG, 0, 1, 3>(src, n, L, dst, s);
+        default: return launch_fixed_tma_ws<ALG, 1, 1, 3>(src, n, L, dst, s);
+        }
+    }
+    if (cfg == kCfgWs2x2) {
+        switch (v) {
+        case 3: return launch_fixed_tma_ws<ALG, 3, 2, 2>(src, n, L, dst, s);
+        default: return launch_fixed_tma_ws<ALG, 1, 2, 2>(src, n, L, dst, s);
+        }
+    }
+    if (cfg == kCfgWs3x2) {
+        switch (v) {
+        case 3: return launch_fixed_tma_ws<ALG, 3, 2, 3>(src, n, L, dst, s);
+        default: return launch_fixed_tma_ws<ALG, 1, 2, 3>(src, n, L, dst, s);
         }
     }
     if (cfg == kCfg2x2) {

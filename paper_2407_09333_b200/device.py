@@ -36,8 +36,11 @@ def hash_fixed(alg: str, msgs, out=None, flags: int = 0):
     return out
 
 
-def hash_varlen(alg: str, data, offsets, out=None, scratch=None, flags: int = 0):
-    """Digest message i = data[offsets[i]-offsets[0] : offsets[i+1]-offsets[0]] (CUDA tensors)."""
+def hash_varlen(alg: str, data, offsets, out=None, scratch=None, flags: int = 0, offset_base=None):
+    """Digest message i = data[offsets[i]-base : offsets[i+1]-base] (CUDA tensors).
+
+    ``offset_base`` defaults to ``offsets[0]`` (read back from the device, a
+    synchronising copy); pass it when known to keep the call asynchronous."""
     import torch
 
     _check_alg(alg)
@@ -51,7 +54,7 @@ def hash_varlen(alg: str, data, offsets, out=None, scratch=None, flags: int = 0)
         return out
     if scratch is None and not (flags & _native.HB_FLAG_NO_SORT):
         scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch.uint8, device=data.device)
-    base = int(offsets[0].item())
+    base = int(offsets[0].item()) if offset_base is None else int(offset_base)
     rc = _native.lib().hb_hash_varlen_dev(_native.ALG_ID[alg], dev, data.data_ptr(), data.numel(),
                                           offsets.data_ptr(), base, n, out.data_ptr(),
                                           scratch.data_ptr() if scratch is not None else None,

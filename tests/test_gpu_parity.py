@@ -259,11 +259,12 @@ def test_full_size_sampled_and_cross_path():
     del buf
 
 
-@pytest.mark.parametrize("cfg", ["1x3", "2x2", "2x3", "ws2", "ws3"])
+@pytest.mark.parametrize("cfg", ["1x3", "2x2", "2x3", "ws2", "ws3", "ws2x2", "ws3x2"])
 def test_tma_tile_configs_and_variants(cfg, monkeypatch):
     """Every compiled TMA tile configuration x round variant is bit-exact
     (the tuned default is only one of them; $HB_TMA_CFG/$HB_VARIANT select)."""
-    variants = ["0", "1", "2", "3"] if cfg == "1x3" else (["0", "1"] if cfg.startswith("ws") else ["0", "1", "2"])
+    variants = (["0", "1", "2", "3"] if cfg == "1x3" else ["1", "3"] if cfg.endswith("x2") and cfg.startswith("ws")
+                else ["0", "1"] if cfg.startswith("ws") else ["0", "1", "2"])
     monkeypatch.setenv("HB_TMA_CFG", cfg)
     for L in (16, 48, 64, 112, 128, 1024, 1040):
         n = 333
@@ -288,3 +289,17 @@ def test_duty_ratio_invariance():
             x = k / 50
             got = batch_digest(alg, msgs, gpus=gpus, ratios=[x, 1.0 - x])
             assert np.array_equal(got, ref), (alg, x)
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_small_batch_kernel_matches(alg, monkeypatch):
+    """Batches below $HB_SMALL_N run the single-warp-CTA TMA kernel; it must
+    agree with the 4-warp warp-specialised kernel and the oracle."""
+    for L in (16, 64, 96, 1024):
+        n = 3001
+        data = oracle.fill_random(n * L, 5 * L + 3).reshape(n, L)
+        ref = oracle.batch_fixed(alg, data, threads=8)
+        monkeypatch.delenv("HB_SMALL_N", raising=False)
+        assert np.array_equal(batch_digest(alg, data), ref), (alg, L, "small")
+        monkeypatch.setenv("HB_SMALL_N", "0")
+        assert np.array_equal(batch_digest(alg, data), ref), (alg, L, "ws")

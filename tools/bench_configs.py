@@ -95,7 +95,7 @@ def varlen_point(alg, n, maxlen, seed, steps, out, flags=0):
     d_off = torch.from_numpy(off).cuda()
     dig = torch.empty((n, DLEN[alg]), dtype=torch.uint8, device="cuda:0")
     scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch.uint8, device="cuda:0")
-    ms = timed(lambda: device.hash_varlen(alg, data, d_off, out=dig, scratch=scratch, flags=flags), steps)
+    ms = timed(lambda: device.hash_varlen(alg, data, d_off, out=dig, scratch=scratch, flags=flags, offset_base=0), steps)
     k = 512
     h = data[: int(off[k])].cpu().numpy()
     ok = bool(np.array_equal(dig[:k].cpu().numpy(), oracle.batch_varlen(alg, h, off[: k + 1].astype(np.uint64), 8)))
@@ -111,9 +111,25 @@ def varlen_point(alg, n, maxlen, seed, steps, out, flags=0):
     del data, d_off, dig, scratch
 
 
+def sweep(out):
+    """configs[4]: message size 16 B .. 64 KiB (13 powers of two) x batch count
+    2^12 / 2^16 / 2^20 / the largest power of two with n*L <= 16 GiB (cap 2^24)."""
+    for k in range(13):
+        L = 16 << k
+        nmax = min(1 << 24, (16 << 30) // L)
+        for n in sorted({x for x in (1 << 12, 1 << 16, 1 << 20, nmax) if x <= nmax}):
+            for alg in ("sha1", "md5", "sm3"):
+                fixed_point(alg, n, L, 5000 + k, 5 if n * L > (1 << 30) else 30, out, "C5")
+                torch.cuda.empty_cache()
+
+
 def main():
     path = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "gpurun_out/configs.jsonl"
     quick = "--quick" in sys.argv
+    if "--sweep-only" in sys.argv:
+        with open(path, "w") as out:
+            sweep(out)
+        return
     os.makedirs(os.path.dirname(path) or ".", exist_ok=True)
     t0 = time.time()
     with open(path, "w") as out:
@@ -127,10 +143,7 @@ def main():
         for alg in ("sha1", "md5", "sm3"):
             varlen_point(alg, 1 << 22, 4096, 4, 5, out, flags=_native.HB_FLAG_VARLEN_WORDS)
         if not quick:
-            for L in (16, 64, 256, 1024, 4096, 16384, 65536):
-                for n in sorted({1 << 16, (4 << 30) // L}):
-                    for alg in ("sha1", "md5", "sm3"):
-                        fixed_point(alg, n, L, 5000 + L, 5 if n * L > (1 << 30) else 50, out, "C5")
+            sweep(out)
     print(f"# done in {time.time() - t0:.1f} s", flush=True)
 
 
