@@ -426,6 +426,122 @@ k_varlen16(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offset
     store_digest<ALG>(out + i * H::kDigestBytes, st);
 }
 
+// -------------------------------------------------------------------------
+// Variable-length kernel, warp-cooperative staging (the default).
+//
+// A warp owns 32 messages (after the length sort: equal block counts and the
+// same word alignment).  Per 64-byte step every message needs the 80-byte
+// 16-aligned window around its block: 32 x 5 = 160 16-byte chunks.  Lane l
+// copies chunks c = l + 32j (j < 5) -- message c/5, chunk c%5 -- with
+// cp.async (zero-filled past the message end), so five consecutive lanes
+// fetch one message's 80 contiguous bytes: each warp instruction touches ~7
+// messages instead of 32 (per-thread LDG.128 touches 32 lines per
+// instruction and the L1 tag stage, not HBM, was the limit for MD5).  Chunks
+// land in a STAGES-deep per-warp ring (slot m at m*80: conflict-free
+// LDS.128 reads); the owner lane realigns its window (word select + funnel
+// shift) and compresses.  Padding is applied in registers on the last one
+// or two blocks (bytes past the end arrive as zeros), so there is one
+// compress call site and the loop runs to the warp's largest block count.
+// -------------------------------------------------------------------------
+constexpr int kVcWarps = 4;
+constexpr int kVcSlot = 80;                   // bytes per message per stage
+constexpr int kVcWarpStage = 32 * kVcSlot;    // 2,560 bytes
+constexpr int kVcStages = 4;
+
+template <int ALG>
+__global__ void __launch_bounds__(kVcWarps * 32)
+k_varlen_coop(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offsets, uint64_t offset_base,
+              const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    __shared__ __align__(128) uint8_t ring[kVcWarps][kVcStages][kVcWarpStage];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t wbase = ((uint64_t)blockIdx.x * kVcWarps + warp) * 32u;
+    if (wbase >= n) return;  // warp-uniform
+    const uint64_t t = wbase + lane;
+    const bool live = t < n;
+    uint64_t i = 0, len = 0;
+    uintptr_t a = reinterpret_cast<uintptr_t>(data);
+    if (live) {
+        i = perm ? (uint64_t)perm[t] : t;
+        a = reinterpret_cast<uintptr_t>(data + (offsets[i] - offset_base));
+        len = offsets[i + 1] - offsets[i];
+    }
+    const uint32_t nb = live ? (uint32_t)((len + 8u) / 64u + 1u) : 0u;   // blocks incl. padding
+    const uint32_t nfull = (uint32_t)(len >> 6);
+    const uint32_t nbmax = __reduce_max_sync(0xFFFFFFFFu, nb);
+
+    // This lane's five copy slots: source message m = c/5, chunk k = c%5.
+    uintptr_t src0[5];
+    int64_t avail0[5];  // bytes of the chunk inside the message at step 0 (minus 64 per step)
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const uint32_t c = lane + 32u * j, m = c / 5u, k = c % 5u;
+        const uintptr_t am = __shfl_sync(0xFFFFFFFFu, a, m);
+        const uint64_t lm = __shfl_sync(0xFFFFFFFFu, len, m);
+        src0[j] = (am & ~uintptr_t(15)) + 16u * k;
+        const bool need = (k < 4u) || (am & 15u);  // chunk 4 only for a misaligned window
+        avail0[j] = (need && lm) ? (int64_t)lm + (int64_t)(am & 15u) - 16 * (int64_t)k : INT64_MIN / 2;
+    }
+    uint8_t* wring = &ring[warp][0][0];
+    const uint32_t sring = smem_u32(wring);
+    auto issue = [&](uint32_t b) {
+        const uint32_t sdst = sring + (b % kVcStages) * kVcWarpStage;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            const int64_t av = avail0[j] - 64 * (int64_t)b;
+            const uint32_t sz = av <= 0 ? 0u : av >= 16 ? 16u : (uint32_t)av;
+            const uintptr_t src = sz ? src0[j] + 64u * (uintptr_t)b : reinterpret_cast<uintptr_t>(data);
+            cp_async16_zfill(sdst + 16u * (lane + 32u * j), reinterpret_cast<const void*>(src), sz);
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < kVcStages - 1; ++s) {
+        if ((uint32_t)s < nbmax) issue(s);
+        cp_async_commit();
+    }
+
+    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
+    const uint32_t r = (uint32_t)(len & 63u);
+    const uint64_t bits = len * 8ull;
+    const uint32_t l14 = H::kBigEndian ? bswap((uint32_t)(bits >> 32)) : (uint32_t)bits;
+    const uint32_t l15 = H::kBigEndian ? bswap((uint32_t)bits) : (uint32_t)(bits >> 32);
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    const uint32_t slot = smem_u32(wring) + lane * kVcSlot;
+    for (uint32_t b = 0; b < nbmax; ++b) {
+        if (b + kVcStages - 1 < nbmax) issue(b + kVcStages - 1);
+        cp_async_commit();
+        cp_async_wait<kVcStages - 1>();  // this lane's copies of step b have landed
+        __syncwarp();                    // ... and every other lane's
+        uint32_t c[20];
+        const uint32_t sbase = slot + (b % kVcStages) * kVcWarpStage;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            uint32_t x, y, z, w;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+                         : "r"(sbase + 16u * k)
+                         : "memory");
+            c[4 * k] = x; c[4 * k + 1] = y; c[4 * k + 2] = z; c[4 * k + 3] = w;
+        }
+        __syncwarp();  // the stage may be refilled from the next iteration on
+        if (b < nb) {
+            uint32_t raw[16];
+            realign16(c, q, sh, raw);
+            if (b >= nfull) {  // the final one or two blocks: 0x80, zero fill, bit length
+                if (b == nfull) {
+                    const uint32_t pad = 0x80u << ((r & 3u) * 8u), pw = r >> 2;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) raw[j] |= (pw == (uint32_t)j) ? pad : 0u;
+                }
+                if (b == nb - 1u) { raw[14] = l14; raw[15] = l15; }
+            }
+            compress1<ALG>(st, raw);
+        }
+    }
+    if (live) store_digest<ALG>(out + i * H::kDigestBytes, st);
+}
+
 // ---------------------------------------------------- length-bucket sort --
 // Counting sort of message indices by block count, longest first.  Three
 // small kernels: per-CTA shared-memory histograms -> global histogram, one
@@ -714,19 +830,26 @@ static int tma_cfg(int alg) {
     }
 }
 
-// Below this many messages the 4-warp tiles cannot fill the GPU evenly and
-// the single-warp-CTA kernel is used ($HB_SMALL_N overrides; 0 disables).
-static uint64_t small_n_threshold() {
-    const char* v = getenv("HB_SMALL_N");
-    return v ? strtoull(v, nullptr, 10) : (1ull << 18);
+// Shape selection by batch geometry (B200-measured, profiles/ab_small_r1.txt):
+//  * fewer than $HB_SMALL_N (default 2^18) messages: one message per thread
+//    (NB=1) so the grid still covers all SMs -- SHA-1's tuned NB=2 tiles
+//    halve the CTA count (4096 x 64 KiB: 251 vs 428 GB/s);
+//  * messages of <= $HB_DIRECT_MAX_L (default 128) bytes: the direct
+//    per-thread-load kernel (one or two blocks per message, the 8 KiB TMA
+//    stage would be mostly padding: MD5 2^24 x 16 B 1121 vs 683 GB/s).
+static uint64_t env_u64(const char* name, uint64_t dflt) {
+    const char* v = getenv(name);
+    return v ? strtoull(v, nullptr, 10) : dflt;
 }
+static uint64_t small_n_threshold() { return env_u64("HB_SMALL_N", 1ull << 18); }
+static uint64_t direct_max_len() { return env_u64("HB_DIRECT_MAX_L", 128); }
 
 template <int ALG>
 static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t L, uint8_t* dst, cudaStream_t s) {
     const int cfg = tma_cfg(ALG);
     const int v = tma_variant(ALG);
     if (!getenv("HB_TMA_CFG") && (uint64_t)n < small_n_threshold())
-        return launch_fixed_tma_alg<ALG, DefaultVariant<ALG>::value, 1, 3, 1>(src, n, L, dst, s);
+        return launch_fixed_tma_ws<ALG, DefaultVariant<ALG>::value, 1, 3>(src, n, L, dst, s);
     if (cfg == kCfg1x2) {
         switch (v) {
         case 0: return launch_fixed_tma_alg<ALG, 0, 1, 2>(src, n, L, dst, s);
@@ -785,7 +908,8 @@ static cudaError_t launch_fixed_alg(const uint8_t* d_msgs, uint64_t n, uint64_t 
     using H = HashAlg<ALG>;
     const bool aligned = L > 0 && (L % 16) == 0 && (reinterpret_cast<uintptr_t>(d_msgs) % 16) == 0 &&
                          L < (1ull << 31);
-    if (aligned && !(flags & HB_FLAG_NO_TMA)) {
+    const bool direct = (flags & HB_FLAG_NO_TMA) || (!getenv("HB_TMA_CFG") && L <= direct_max_len());
+    if (aligned && !direct) {
         // TMA coordinates are int32: split very large batches into row slabs.
         const uint64_t slab = 1ull << 30;
         for (uint64_t r0 = 0; r0 < n; r0 += slab) {
@@ -841,10 +965,17 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
         perm = p;
     }
     const uint64_t grid = (n + 127) / 128;
-    if (flags & HB_FLAG_VARLEN_WORDS) {  // A/B baseline: 32-bit loads
+    if (flags & HB_FLAG_VARLEN_WORDS) {  // A/B baseline: per-thread 32-bit loads
         k_generic<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets,
                                                                  offset_base, perm, 0, n, d_out);
-    } else {
+    } else if (((flags & HB_FLAG_VARLEN_COOP) || (ALG == kMd5 && !(flags & HB_FLAG_VARLEN_COOP_OFF))) &&
+               data_bytes < (1ull << 37)) {  // block counts fit u32
+        // Default for MD5 only (B200, 2^22 msgs of 1-4096 B: 2.38 vs 4.36 ms);
+        // SHA-1/SM3 are ALU-bound and lose more to the cooperative kernel's
+        // 92-96 registers than they gain (4.30 vs 3.96, 10.5 vs 8.95 ms).
+        const uint64_t g = (n + kVcWarps * 32 - 1) / (kVcWarps * 32);
+        k_varlen_coop<ALG><<<(unsigned)g, kVcWarps * 32, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
+    } else {  // A/B baseline: per-thread 128-bit loads
         k_varlen16<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
     }
     note_launches(1);

@@ -1,0 +1,21 @@
+"""B200 runtime for lowered *hyper* hash programs.
+
+``program``  lowered-program records, the reference printer's text form, and
+             an adapter for reference ``HirModule`` objects;
+``lowering`` ``crypto.hash_batch`` -> per-GPU launch groups (partition +
+             staging contract of ``lower_hyper_for``);
+``devices``  host + ``cuda`` device table (``detect_hardware``);
+``executor`` ``execute`` / ``execute_batched`` on real GPUs;
+``sweep``    ``Workload`` / ``run_point`` over GPU splits.
+"""
+
+from .devices import DeviceConfigError, DeviceSpec, DeviceTable, HOST_ID, detect_hardware, from_reference
+from .executor import ExecError, ExecReport, execute, execute_batched
+from .lowering import LoweringError, lower_hash_batch
+from .program import BufType, DigestLoop, Op, Program, ProgramError, from_hir, parse
+from .sweep import RunRecord, Workload, run_point
+
+__all__ = ["DeviceConfigError", "DeviceSpec", "DeviceTable", "HOST_ID", "detect_hardware", "from_reference",
+           "ExecError", "ExecReport", "execute", "execute_batched", "LoweringError", "lower_hash_batch",
+           "BufType", "DigestLoop", "Op", "Program", "ProgramError", "from_hir", "parse", "RunRecord", "Workload",
+           "run_point"]

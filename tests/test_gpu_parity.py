@@ -120,7 +120,9 @@ def test_varlen_random_sorted_and_unsorted(alg):
     data = oracle.fill_random(int(off[-1]) + 3, 99)
     ref = oracle.batch_varlen(alg, data, off, threads=8)
     for fl in (0, _native.HB_FLAG_NO_SORT, _native.HB_FLAG_VARLEN_WORDS,
-               _native.HB_FLAG_VARLEN_WORDS | _native.HB_FLAG_NO_SORT):
+               _native.HB_FLAG_VARLEN_WORDS | _native.HB_FLAG_NO_SORT, _native.HB_FLAG_VARLEN_COOP_OFF,
+               _native.HB_FLAG_VARLEN_COOP_OFF | _native.HB_FLAG_NO_SORT, _native.HB_FLAG_VARLEN_COOP,
+               _native.HB_FLAG_VARLEN_COOP | _native.HB_FLAG_NO_SORT):
         assert np.array_equal(batch_digest_varlen(alg, data, off, flags=fl), ref), fl
 
 
@@ -292,14 +294,37 @@ def test_duty_ratio_invariance():
 
 
 @pytest.mark.parametrize("alg", ALGS)
-def test_small_batch_kernel_matches(alg, monkeypatch):
-    """Batches below $HB_SMALL_N run the single-warp-CTA TMA kernel; it must
-    agree with the 4-warp warp-specialised kernel and the oracle."""
-    for L in (16, 64, 96, 1024):
+def test_batch_geometry_dispatch_matches(alg, monkeypatch):
+    """The fixed-width dispatch picks a kernel shape by batch geometry (direct
+    loads for short rows, one message per thread below $HB_SMALL_N, the tuned
+    tiles otherwise); every shape must give the oracle's digests."""
+    arms = [{}, {"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"}, {"HB_SMALL_N": str(1 << 40), "HB_DIRECT_MAX_L": "0"}]
+    for L in (16, 64, 96, 128, 144, 1024):
         n = 3001
         data = oracle.fill_random(n * L, 5 * L + 3).reshape(n, L)
         ref = oracle.batch_fixed(alg, data, threads=8)
-        monkeypatch.delenv("HB_SMALL_N", raising=False)
-        assert np.array_equal(batch_digest(alg, data), ref), (alg, L, "small")
-        monkeypatch.setenv("HB_SMALL_N", "0")
-        assert np.array_equal(batch_digest(alg, data), ref), (alg, L, "ws")
+        for env in arms:
+            for k in ("HB_SMALL_N", "HB_DIRECT_MAX_L"):
+                monkeypatch.delenv(k, raising=False)
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            assert np.array_equal(batch_digest(alg, data), ref), (alg, L, env)
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_varlen_every_length_and_alignment(alg):
+    """Every length 0..260 (x3, shuffled, so message starts take every
+    alignment mod 16) in one batch and in partial warps (n not a multiple of
+    32), with several leading offsets, sorted and unsorted, every kernel."""
+    lens = np.array([L for L in range(261) for _ in range(3)], np.uint64)
+    np.random.default_rng(5).shuffle(lens)
+    for shift in (0, 1, 3, 7, 13):
+        off = np.zeros(len(lens) + 1, np.uint64)
+        off[1:] = np.cumsum(lens)
+        off += np.uint64(shift)
+        buf = oracle.fill_random(int(off[-1]) + 5, 17 + shift)
+        ref = oracle.batch_varlen(alg, buf, off, threads=8)
+        for k in (len(lens), 31, 33, 1):
+            for fl in (0, _native.HB_FLAG_NO_SORT, _native.HB_FLAG_VARLEN_COOP_OFF, _native.HB_FLAG_VARLEN_COOP):
+                got = batch_digest_varlen(alg, buf, off[: k + 1], flags=fl)
+                assert np.array_equal(got, ref[:k]), (alg, shift, k, fl)

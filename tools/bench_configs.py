@@ -101,7 +101,9 @@ def varlen_point(alg, n, maxlen, seed, steps, out, flags=0):
     ok = bool(np.array_equal(dig[:k].cpu().numpy(), oracle.batch_varlen(alg, h, off[: k + 1].astype(np.uint64), 8)))
     blocks = int(((lens + 8) // 64 + 1).sum())
     f = clock_mhz()
-    tagf = {0: "", _native.HB_FLAG_NO_SORT: " (no sort)", _native.HB_FLAG_VARLEN_WORDS: " (32-bit loads)"}[flags]
+    tagf = {0: "", _native.HB_FLAG_NO_SORT: " (no sort)", _native.HB_FLAG_VARLEN_WORDS: " (32-bit loads)",
+            _native.HB_FLAG_VARLEN_COOP_OFF: " (per-thread 128-bit loads)",
+            _native.HB_FLAG_VARLEN_COOP: " (warp-cooperative cp.async)"}[flags]
     rec = {"config": "C4 varlen" + tagf, "alg": alg, "n": n, "len": f"uniform 1-{maxlen}",
            "bytes": total, "ms": round(ms, 4), "GBps": round(total / ms / 1e6, 2), "Mhash_s": round(n / ms / 1e3, 2),
            "roofline": roof(alg, blocks, total + 8 * (n + 1) + n * DLEN[alg], ms, f), "sm_mhz": f,
@@ -141,7 +143,8 @@ def main():
             varlen_point(alg, 1 << 22, 4096, 4, 5, out)
         varlen_point("md5", 1 << 22, 4096, 4, 5, out, flags=_native.HB_FLAG_NO_SORT)
         for alg in ("sha1", "md5", "sm3"):
-            varlen_point(alg, 1 << 22, 4096, 4, 5, out, flags=_native.HB_FLAG_VARLEN_WORDS)
+            varlen_point(alg, 1 << 22, 4096, 4, 5, out, flags=_native.HB_FLAG_VARLEN_COOP_OFF)
+            varlen_point(alg, 1 << 22, 4096, 4, 5, out, flags=_native.HB_FLAG_VARLEN_COOP)
         if not quick:
             sweep(out)
     print(f"# done in {time.time() - t0:.1f} s", flush=True)
