@@ -410,11 +410,11 @@ def _chunk_ranges(n: int, k: int) -> list[tuple[int, int]]:  # executor.py:702-7
     return [(int(bounds[i]), int(bounds[i + 1])) for i in range(k)]
 
 
-def _as_program(program) -> Program:
+def _as_program(program, param_names=None) -> Program:
     if isinstance(program, Program):
         return program
     if isinstance(program, str):
-        return parse(program)
+        return parse(program, param_names)
     from .program import from_hir
 
     try:
@@ -425,12 +425,15 @@ def _as_program(program) -> Program:
         raise ProgramError(f"cannot execute {type(program).__name__}: {e}") from None
 
 
-def execute(program, devices: DeviceTable, inputs: dict | None = None, *, batched: bool = False) -> ExecReport:
-    """Run a lowered hash program (a :class:`Program`, its printed text, or a
+def execute(program, devices: DeviceTable, inputs: dict | None = None, *, batched: bool = False,
+            param_names: list[str] | None = None) -> ExecReport:
+    """Run a lowered hash program (a :class:`Program`, its printed text -- whose
+    parameters are ``arg0, arg1, ...`` unless ``param_names`` is given -- or a
     reference ``HirModule``) on the GPUs of ``devices``."""
-    return _Executor(_as_program(program), devices, inputs, batched).run()
+    return _Executor(_as_program(program, param_names), devices, inputs, batched).run()
 
 
-def execute_batched(program, devices: DeviceTable, inputs: dict | None = None) -> ExecReport:
+def execute_batched(program, devices: DeviceTable, inputs: dict | None = None, *,
+                    param_names: list[str] | None = None) -> ExecReport:
     """Like :func:`execute`, but launch groups too large for their device run in sub-batches."""
-    return execute(program, devices, inputs, batched=True)
+    return execute(program, devices, inputs, batched=True, param_names=param_names)

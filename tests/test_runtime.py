@@ -118,10 +118,11 @@ def test_host_share_and_capacity_errors(golden):
     by = {c["name"]: c for c in cases(golden)}
     c = by["md5_host_share"]
     with pytest.raises(ExecError, match="no CPU hash path"):
-        execute_batched(c["text"], _gpu_table(c), {"msgs": gen_messages(0, c["count"], c["width"]).data})
+        execute_batched(c["text"], _gpu_table(c), {"msgs": gen_messages(0, c["count"], c["width"]).data},
+                        param_names=["msgs", "out"])
     c = by["sha1_many_batches_accel"]  # over capacity without batching: the arena refuses (arena.py:40-44)
     with pytest.raises(ExecError, match="over capacity"):
-        execute(c["text"], _gpu_table(c), {"msgs": gen_messages(0, c["count"], c["width"]).data})
+        execute(c["text"], _gpu_table(c), {"arg0": gen_messages(0, c["count"], c["width"]).data})
 
 
 @pytest.mark.gpu
