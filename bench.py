@@ -15,7 +15,7 @@ messages per GPU (weak scaling under torchrun: rank r hashes global messages
                compared bit-for-bit with the GPU's for that sample
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload md5_1k|sha1_1k|sm3_1k|sha1_64|varlen|decimal|sweep]
+                  [--workload md5_1k|sha1_1k|sm3_1k|sha1_64|varlen_md5|varlen_sha1|varlen_sm3]
 """
 
 from __future__ import annotations
@@ -28,6 +28,8 @@ import subprocess
 import sys
 import threading
 import time
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -42,11 +44,14 @@ DLEN = {"sha1": 20, "md5": 16, "sm3": 32}
 ALU_OPS_PER_BLOCK = {"md5": 128, "sha1": 448, "sm3": 1084}
 
 WORKLOADS = {
-    # name: (alg, n per GPU, msg_len, seed, BASELINE config)
+    # name: (alg | "varlen:"alg, n per GPU, msg_len | max varlen length, seed, BASELINE config)
     "md5_1k": ("md5", 1 << 24, 1024, 2, "configs[1]: MD5 over 2^24 random 1 KiB messages per B200"),
     "sha1_1k": ("sha1", 1 << 24, 1024, 2, "SHA-1 over 2^24 random 1 KiB messages per B200 (configs[4] point)"),
     "sm3_1k": ("sm3", 1 << 24, 1024, 3, "configs[2]: SM3 over 2^24 random 1 KiB messages per B200"),
     "sha1_64": ("sha1", 65536, 64, 1, "configs[0]: SHA-1 over 65,536 random 64-byte messages"),
+    "varlen_md5": ("varlen:md5", 1 << 22, 4096, 4, "configs[3]: mixed variable-length batch, uniform 1 B-4 KiB"),
+    "varlen_sha1": ("varlen:sha1", 1 << 22, 4096, 4, "configs[3]: mixed variable-length batch, uniform 1 B-4 KiB"),
+    "varlen_sm3": ("varlen:sm3", 1 << 22, 4096, 4, "configs[3]: mixed variable-length batch, uniform 1 B-4 KiB"),
 }
 
 
@@ -159,67 +164,220 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
-def load_ncu_traffic(alg: str, n: int, L: int):
+def load_ncu_traffic(workload: str):
     """dram bytes per launch of the dominant kernel from the committed ncu summary."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    k = d.get(f"{alg}_{n}x{L}")
+    k = d.get(workload)
     return k.get("dram_bytes") if k else None
 
 
 # ------------------------------------------------------------ CPU oracle --
-def cpu_oracle_run(alg: str, rows, threads: int):
-    import oracle
-
-    t0 = time.perf_counter()
-    out = oracle.batch_fixed(alg, rows, threads=threads)
-    return out, time.perf_counter() - t0
-
-
 def cpu_sample_rows(alg: str, L: int, n: int, threads: int, target_s: float):
     """Pick a sample size giving ~target_s seconds of wall time on `threads` threads."""
     import oracle
 
     probe = oracle.fill_random(min(n, 2048) * L, 123).reshape(-1, L)
-    _, t = cpu_oracle_run(alg, probe, 1)
+    t0 = time.perf_counter()
+    oracle.batch_fixed(alg, probe, threads=1)
+    t = time.perf_counter() - t0
     per_row = max(t / probe.shape[0], 1e-9)
     rows = int(target_s * threads / per_row)
     rows = max(threads * 16, min(n, rows))
     return rows
 
 
-# ---------------------------------------------------------------- our arm --
-def run_ours(args):
-    import numpy as np
+# -------------------------------------------------------------- workloads --
+class FixedWorkload:
+    """n messages of L bytes per GPU, (n, L) row-major (configs[0..2], [4])."""
+
+    kind = "fixed"
+
+    def __init__(self, name, alg, n, L, seed, desc, rank, local):
+        import torch
+
+        from paper_2407_09333_b200 import device
+
+        self.name, self.alg, self.n, self.L, self.seed, self.desc = name, alg, n, L, seed, desc
+        self.dlen = DLEN[alg]
+        self.buf = torch.empty(n * L, dtype=torch.uint8, device=f"cuda:{local}")
+        device.fill_random(self.buf, seed, byte_offset=rank * n * L)  # global messages [rank*n, (rank+1)*n)
+        self.msgs = self.buf.view(n, L)
+        self.out = torch.empty((n, self.dlen), dtype=torch.uint8, device=f"cuda:{local}")
+        self.msg_bytes = n * L
+        self.alg_bytes = n * (L + self.dlen)  # message bytes read once + digests written once
+        self.blocks = n * ((L + 8) // 64 + 1)
+        self.h2d_bytes, self.d2h_bytes = n * L, n * self.dlen
+
+    def step(self):
+        from paper_2407_09333_b200 import device
+
+        device.hash_fixed(self.alg, self.msgs, out=self.out)
+
+    def host_inputs(self, lib):
+        import ctypes
+
+        import numpy as np
+
+        hp = lib.hb_alloc_pinned(self.n * self.L)
+        if not hp:
+            return None
+        host = np.ctypeslib.as_array(ctypes.cast(hp, ctypes.POINTER(ctypes.c_uint8)),
+                                     shape=(self.n * self.L,)).reshape(self.n, self.L)
+        import torch
+
+        torch.from_numpy(host.reshape(-1)).copy_(self.buf)  # same bytes as the device-resident run
+        self._host = host
+        return hp
+
+    def e2e_step(self, local, tim):
+        from paper_2407_09333_b200.crypto import batch_digest
+
+        return batch_digest(self.alg, self._host, gpus=[local], timing=tim)
+
+    def config(self, world):
+        return {"workload": f"{self.alg} {self.n} x {self.L} B fixed-width per GPU ({self.desc})", "alg": self.alg,
+                "msgs_per_gpu": self.n, "msg_len": self.L, "global_batch_msgs": world * self.n,
+                "parallelism": f"message-range shards over {world} GPU(s), no collective",
+                "l2": "inputs are %.1f GiB per GPU >> 126 MB L2; no flush needed" % (self.n * self.L / 2**30)}
+
+    def kernel_name(self):
+        return "k_fixed_tma_ws<%s>" % self.alg
+
+    def cpu_sample(self, threads, target_s):
+        import oracle
+
+        rows = cpu_sample_rows(self.alg, self.L, self.n, threads, target_s)
+        sample = self.buf[: rows * self.L].cpu().numpy().reshape(rows, self.L)
+        t0 = time.perf_counter()
+        ref = oracle.batch_fixed(self.alg, sample, threads=threads)
+        t = time.perf_counter() - t0
+        ok = bool(np.array_equal(ref, self.out[:rows].cpu().numpy()))
+        return rows, rows * self.L, t, ok, f"first {rows} of the {self.n} x {self.L} B messages (same bytes)"
+
+
+class VarlenWorkload:
+    """configs[3]: n messages per GPU, lengths uniform 1..maxlen B, offsets
+    layout (data bytes + u64 offsets[n+1])."""
+
+    kind = "varlen"
+
+    def __init__(self, name, alg, n, maxlen, seed, desc, rank, local):
+        import numpy as np
+        import torch
+
+        from paper_2407_09333_b200 import _native, device
+
+        self.name, self.alg, self.n, self.maxlen, self.seed, self.desc = name, alg, n, maxlen, seed, desc
+        self.dlen = DLEN[alg]
+        lens = np.random.default_rng(seed + 1000 * rank).integers(1, maxlen + 1, n).astype(np.uint64)
+        self.off = np.zeros(n + 1, np.uint64)
+        self.off[1:] = np.cumsum(lens)
+        total = int(self.off[-1])
+        self.total = total
+        self.buf = torch.empty(total, dtype=torch.uint8, device=f"cuda:{local}")
+        device.fill_random(self.buf, seed, byte_offset=8 * ((rank * total + 7) // 8))
+        self.d_off = torch.from_numpy(self.off.view(np.int64)).to(f"cuda:{local}")
+        self.out = torch.empty((n, self.dlen), dtype=torch.uint8, device=f"cuda:{local}")
+        self.scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch.uint8,
+                                   device=f"cuda:{local}")
+        self.msg_bytes = total
+        self.alg_bytes = total + 8 * (n + 1) + n * self.dlen
+        self.blocks = int(((lens + 8) // 64 + 1).sum())
+        self.h2d_bytes, self.d2h_bytes = total + 8 * (n + 1), n * self.dlen
+
+    def step(self):
+        from paper_2407_09333_b200 import device
+
+        device.hash_varlen(self.alg, self.buf, self.d_off, out=self.out, scratch=self.scratch, offset_base=0)
+
+    def host_inputs(self, lib):
+        import ctypes
+
+        import numpy as np
+        import torch
+
+        hp = lib.hb_alloc_pinned(self.total)
+        if not hp:
+            return None
+        self._host = np.ctypeslib.as_array(ctypes.cast(hp, ctypes.POINTER(ctypes.c_uint8)), shape=(self.total,))
+        torch.from_numpy(self._host).copy_(self.buf)
+        return hp
+
+    def e2e_step(self, local, tim):
+        from paper_2407_09333_b200.crypto import batch_digest_varlen
+
+        return batch_digest_varlen(self.alg, self._host, self.off, gpus=[local], timing=tim)
+
+    def config(self, world):
+        return {"workload": f"{self.alg} {self.n} messages of uniform 1-{self.maxlen} B per GPU, offsets layout "
+                            f"({self.desc})", "alg": self.alg, "msgs_per_gpu": self.n,
+                "msg_len": f"uniform 1-{self.maxlen}", "bytes_per_gpu": self.total,
+                "global_batch_msgs": world * self.n,
+                "parallelism": f"message-range shards over {world} GPU(s), no collective",
+                "l2": "inputs are %.1f GiB per GPU >> 126 MB L2; no flush needed" % (self.total / 2**30)}
+
+    def kernel_name(self):
+        return ("k_varlen_coop<%s>" if self.alg == "md5" else "k_varlen16<%s>") % self.alg
+
+    def cpu_sample(self, threads, target_s):
+        import oracle
+
+        k = min(self.n, max(threads * 16, int(self.n * min(1.0, target_s / 8.0))))
+        data = self.buf[: int(self.off[k])].cpu().numpy()
+        t0 = time.perf_counter()
+        ref = oracle.batch_varlen(self.alg, data, self.off[: k + 1], threads=threads)
+        t = time.perf_counter() - t0
+        ok = bool(np.array_equal(ref, self.out[:k].cpu().numpy()))
+        return k, int(self.off[k]), t, ok, f"first {k} of the {self.n} messages (same bytes)"
+
+
+def make_workload(name, rank, local, n_override=0):
+    spec = WORKLOADS[name]
+    cls = VarlenWorkload if spec[0].startswith("varlen:") else FixedWorkload
+    alg = spec[0].split(":")[-1]
+    n = n_override or spec[1]
+    return cls(name, alg, n, spec[2], spec[3], spec[4], rank, local)
+
+
+def h2d_peak(buf_bytes: int, local: int) -> float:
+    """Pinned host -> device copy bandwidth (GB/s) on this GPU's link, same size class."""
     import torch
 
-    from paper_2407_09333_b200 import _native, device
-    from paper_2407_09333_b200.crypto import batch_digest
+    nbytes = min(buf_bytes, 1 << 30)
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{local}")
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(3):
+        d.copy_(h, non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    return 3 * nbytes / (s.elapsed_time(e) * 1e-3) / 1e9
+
+
+# ---------------------------------------------------------------- our arm --
+def run_ours(args):
+    import numpy as np  # noqa: F401
+    import torch
+
+    from paper_2407_09333_b200 import _native
 
     world, rank, local = dist_setup(args)
-    alg, n, L, seed, cfg_desc = WORKLOADS[args.workload]
-    if args.n:
-        n = args.n
-    dlen = DLEN[alg]
+    w = make_workload(args.workload, rank, local, args.n)
+    alg = w.alg
     stream = torch.cuda.current_stream(local)
     sampler = ClockSampler(local)
     sampler.start()
-
-    # ---- inputs resident in HBM: global messages [rank*n, (rank+1)*n)
-    buf = torch.empty(n * L, dtype=torch.uint8, device=f"cuda:{local}")
-    device.fill_random(buf, seed, byte_offset=rank * n * L)
-    msgs = buf.view(n, L)
-    out = torch.empty((n, dlen), dtype=torch.uint8, device=f"cuda:{local}")
     torch.cuda.synchronize()
 
-    def step():
-        device.hash_fixed(alg, msgs, out=out)
-
     for _ in range(args.warmup):
-        step()
+        w.step()
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
@@ -229,7 +387,7 @@ def run_ours(args):
     t_wall0 = time.perf_counter()
     for s, e in evs:
         s.record(stream)
-        step()
+        w.step()
         e.record(stream)
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall0
@@ -239,48 +397,51 @@ def run_ours(args):
     per_step = [s.elapsed_time(e) for s, e in evs]
     ms_local = sum(per_step) / len(per_step)
     ms = reduce_max(ms_local, world, local)
-    total_bytes = world * n * L
+    total_bytes = world * w.msg_bytes
     value = total_bytes / (ms * 1e-3) / 1e9
-    mhash = world * n / (ms * 1e-3) / 1e6
-    log(f"[rank {rank}] kernel-only {alg} {n}x{L}: {ms_local:.3f} ms/step (min {min(per_step):.3f}, "
-        f"max {max(per_step):.3f}); wall {t_wall * 1e3 / args.steps:.3f} ms/step")
+    mhash = world * w.n / (ms * 1e-3) / 1e6
+    log(f"[rank {rank}] kernel-only {w.name}: {ms_local:.3f} ms/step (min {min(per_step):.3f}, "
+        f"max {max(per_step):.3f}); wall {t_wall * 1e3 / args.steps:.3f} ms/step; {launches} launches")
 
-    # ---- end to end through the public API: pinned host input -> hb_hash_fixed
+    # ---- end to end through the public API: pinned host input -> hb_hash_fixed / hb_hash_varlen
     e2e = None
     lib = _native.lib()
-    hp = lib.hb_alloc_pinned(n * L) if not args.no_e2e else None
+    hp = w.host_inputs(lib) if not args.no_e2e else None
     if hp:
-        import ctypes
-
-        host = np.ctypeslib.as_array(ctypes.cast(hp, ctypes.POINTER(ctypes.c_uint8)), shape=(n * L,)).reshape(n, L)
-        host_t = torch.from_numpy(host.reshape(-1))
-        host_t.copy_(buf, non_blocking=False)  # same bytes as the device-resident run
         e2e_steps = args.e2e_steps or min(args.steps, 10)
         tim = {}
         for _ in range(max(1, min(args.warmup, 2))):
-            batch_digest(alg, host, gpus=[local])
+            w.e2e_step(local, tim)
         barrier(world)
         torch.cuda.synchronize()
         sampler.active = True
         l1 = _native.launch_count()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            res = batch_digest(alg, host, gpus=[local], timing=tim)
+            res = w.e2e_step(local, tim)
         t1 = time.perf_counter()
         sampler.active = False
         e2e_launches = _native.launch_count() - l1
         barrier(world)
         e2e_ms = reduce_max((t1 - t0) * 1e3 / e2e_steps, world, local)
-        ok = bool(np.array_equal(res, out.cpu().numpy()))
-        e2e = {"value": round(total_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
-               "h2d_bytes_per_step": world * n * L, "d2h_bytes_per_step": world * n * dlen,
-               "ms_per_step": round(e2e_ms, 3), "mhash_per_s": round(world * n / (e2e_ms * 1e-3) / 1e6, 2),
-               "api": "paper_2407_09333_b200.crypto.batch_digest(pinned host array) -> hb_hash_fixed",
-               "steps": e2e_steps, "engine_timing_last_step": {k: (round(v, 3) if isinstance(v, float) else v)
-                                                               for k, v in tim.items()},
+        ok = bool(np.array_equal(res, w.out.cpu().numpy()))
+        bw = h2d_peak(w.h2d_bytes, local)
+        e2e_gbs = total_bytes / (e2e_ms * 1e-3) / 1e9
+        h2d_gbs = world * w.h2d_bytes / (e2e_ms * 1e-3) / 1e9
+        e2e = {"value": round(e2e_gbs, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": world * w.h2d_bytes, "d2h_bytes_per_step": world * w.d2h_bytes,
+               "ms_per_step": round(e2e_ms, 3), "mhash_per_s": round(world * w.n / (e2e_ms * 1e-3) / 1e6, 2),
+               "api": ("paper_2407_09333_b200.crypto.batch_digest(pinned host array) -> hb_hash_fixed"
+                       if w.kind == "fixed" else
+                       "paper_2407_09333_b200.crypto.batch_digest_varlen(pinned host data, offsets) -> hb_hash_varlen"),
+               "steps": e2e_steps,
+               "roofline": {"bound": "pcie_h2d", "achieved": round(h2d_gbs / world, 2), "peak": round(bw, 2),
+                            "unit": "GB/s per GPU", "frac": round(h2d_gbs / world / bw, 4),
+                            "peak_source": "pinned host->device copy of 1 GiB on the same GPU, this run"},
+               "engine_timing_last_step": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in tim.items()},
                "gpu_launches": e2e_launches, "matches_device_run": ok}
-        log(f"[rank {rank}] e2e {e2e_ms:.1f} ms/step, engine {tim}")
-        del host_t, host
+        log(f"[rank {rank}] e2e {e2e_ms:.1f} ms/step, H2D peak {bw:.1f} GB/s, engine {tim}")
+        w._host = None
         lib.hb_free_pinned(hp)
     sampler.stop()
 
@@ -289,50 +450,42 @@ def run_ours(args):
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        rows = cpu_sample_rows(alg, L, n, threads, args.cpu_seconds)
-        sample = buf[: rows * L].cpu().numpy().reshape(rows, L)
-        ref, t = cpu_oracle_run(alg, sample, threads)
-        parity = {"rows_checked": rows, "bit_exact": bool(np.array_equal(ref, out[:rows].cpu().numpy()))}
-        cpu = {"value": round(rows * L / t / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": f"first {rows} of the {n} x {L} B messages (same bytes), oracle/hetoc_oracle.c "
-                         f"batch_fixed on {threads} threads, {t:.2f} s",
+        rows, nbytes, t, ok, what = w.cpu_sample(threads, args.cpu_seconds)
+        parity = {"rows_checked": rows, "bit_exact": ok}
+        fn = "batch_fixed" if w.kind == "fixed" else "batch_varlen"
+        cpu = {"value": round(nbytes / t / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+               "sample": f"{what}, oracle/hetoc_oracle.c {fn} on {threads} threads, {t:.2f} s",
                "mhash_per_s": round(rows / t / 1e6, 4)}
 
-    # ---- roofline of the dominant kernel (k_fixed_tma<alg>)
+    # ---- roofline of the dominant kernel
     peaks, peak_src = load_peaks()
-    alg_bytes = n * (L + dlen)  # per launch: message bytes read + digests written
-    achieved = alg_bytes / (ms_local * 1e-3) / 1e9
-    blocks = n * ((L + 8) // 64 + 1)
+    achieved = w.alg_bytes / (ms_local * 1e-3) / 1e9
     clk = sampler.summary()
     f_max = peaks.get("sm_max_mhz", 1965.0)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     alu_peak = sms * 64 * f_max * 1e6  # ALU-pipe lane-ops/s at max clock
-    alu_ach = blocks * ALU_OPS_PER_BLOCK[alg] / (ms_local * 1e-3)
-    t_hbm = alg_bytes / (peaks["hbm_gbs"] * 1e9)
-    t_alu = blocks * ALU_OPS_PER_BLOCK[alg] / alu_peak
+    alu_ach = w.blocks * ALU_OPS_PER_BLOCK[alg] / (ms_local * 1e-3)
+    t_hbm = w.alg_bytes / (peaks["hbm_gbs"] * 1e9)
+    t_alu = w.blocks * ALU_OPS_PER_BLOCK[alg] / alu_peak
     alu = {"achieved": round(alu_ach / 1e12, 3), "peak": round(alu_peak / 1e12, 3), "unit": "Tops/s",
            "frac": round(alu_ach / alu_peak, 4), "alu_ops_per_block": ALU_OPS_PER_BLOCK[alg],
-           "blocks_per_launch": blocks, "clock_mhz": f_max}
+           "blocks_per_launch": w.blocks, "clock_mhz": f_max}
     if t_hbm >= t_alu:
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved / peaks["hbm_gbs"], 4)}
     else:  # integer (ALU-pipe) bound: report against the ALU-pipe roofline, HBM alongside
         roof = {"bound": "alu", "achieved": alu["achieved"], "peak": alu["peak"], "unit": "Tops/s",
                 "frac": alu["frac"], "hbm_achieved_gbs": round(achieved, 1), "hbm_peak_gbs": peaks["hbm_gbs"]}
-    roof.update({"traffic": load_ncu_traffic(alg, n, L), "kernel": f"k_fixed_tma_ws<{alg}>",
-                 "bytes_per_launch": alg_bytes, "peak_source": peak_src,
+    roof.update({"traffic": load_ncu_traffic(w.name), "kernel": w.kernel_name(),
+                 "bytes_per_launch": w.alg_bytes, "peak_source": peak_src,
                  "t_roof_ms": round(max(t_hbm, t_alu) * 1e3, 4), "alu_pipe": alu})
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-                "data": f"synthetic: counter-based splitmix64 bytes (seed {seed}), generated on device",
-                "config": {"workload": f"{alg} {n} x {L} B fixed-width per GPU ({cfg_desc})", "alg": alg,
-                           "msgs_per_gpu": n, "msg_len": L, "global_batch_msgs": world * n,
-                           "parallelism": f"message-range shards over {world} GPU(s), no collective",
-                           "l2": "inputs are %.1f GiB per GPU >> 126 MB L2; no flush needed" % (n * L / 2**30)},
-                "mhash_per_s": round(mhash, 2), "clocks": clk, "e2e": e2e, "gpu_launches": launches,
-                "roofline": roof, "cpu_baseline": cpu, "parity": parity}
+                "data": f"synthetic: counter-based splitmix64 bytes (seed {w.seed}), generated on device",
+                "config": w.config(world), "mhash_per_s": round(mhash, 2), "clocks": clk, "e2e": e2e,
+                "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "parity": parity}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -345,37 +498,59 @@ def run_reference(args):
     """The reference algorithm's CPU implementation (oracle port of hetoc.crypto;
     the reference itself is pure Python/numpy and is not installed on the box)
     on all host threads, each step a bounded sample of the same workload."""
-    import numpy as np
-
     import oracle
 
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    alg, n, L, seed, cfg_desc = WORKLOADS[args.workload]
-    if args.n:
-        n = args.n
+    spec = WORKLOADS[args.workload]
+    alg = spec[0].split(":")[-1]
+    n = args.n or spec[1]
+    seed, cfg_desc = spec[3], spec[4]
     threads = os.cpu_count() or 1
-    rows = cpu_sample_rows(alg, L, n, threads, args.ref_step_seconds)
-    data = oracle.fill_random(rows * L, seed).reshape(rows, L)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if spec[0].startswith("varlen:"):
+        maxlen = spec[2]
+        lens = np.random.default_rng(seed).integers(1, maxlen + 1, n).astype(np.uint64)
+        probe_k = min(n, 2048)
+        off = np.zeros(n + 1, np.uint64)
+        off[1:] = np.cumsum(lens)
+        probe = oracle.fill_random(int(off[probe_k]), seed)
+        t0 = time.perf_counter()
+        oracle.batch_varlen(alg, probe, off[: probe_k + 1], threads=1)
+        per_msg = max((time.perf_counter() - t0) / probe_k, 1e-9)
+        k = max(threads * 16, min(n, int(args.ref_step_seconds * threads / per_msg)))
+        data = oracle.fill_random(int(off[k]), seed)
+        run = lambda: oracle.batch_varlen(alg, data, off[: k + 1], threads=threads)  # noqa: E731
+        nbytes, rows = int(off[k]), k
+        sample = f"first {k} of the {n} messages (uniform 1-{maxlen} B) per step"
+        config = {"workload": f"{alg} {n} messages of uniform 1-{maxlen} B per GPU, offsets layout ({cfg_desc})",
+                  "alg": alg, "msgs_per_gpu": n, "msg_len": f"uniform 1-{maxlen}"}
+    else:
+        L = spec[2]
+        rows = cpu_sample_rows(alg, L, n, threads, args.ref_step_seconds)
+        data = oracle.fill_random(rows * L, seed).reshape(rows, L)
+        run = lambda: oracle.batch_fixed(alg, data, threads=threads)  # noqa: E731
+        nbytes = rows * L
+        sample = f"{rows} of the {n} x {L} B messages per step"
+        config = {"workload": f"{alg} {n} x {L} B fixed-width per GPU ({cfg_desc})", "alg": alg,
+                  "msgs_per_gpu": n, "msg_len": L}
     for _ in range(args.warmup):
-        cpu_oracle_run(alg, data[: max(threads, rows // 8)], threads)
+        run()
     times = []
     for _ in range(args.steps):
-        _, t = cpu_oracle_run(alg, data, threads)
-        times.append(t)
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    value = rows * L / t / 1e9
+    value = nbytes / t / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": f"synthetic: counter-based splitmix64 bytes (seed {seed})",
-            "config": {"workload": f"{alg} {n} x {L} B fixed-width per GPU ({cfg_desc})", "alg": alg,
-                       "msgs_per_gpu": n, "msg_len": L},
+            "data": f"synthetic: counter-based splitmix64 bytes (seed {seed})", "config": config,
             "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-                             "sample": f"{rows} of the {n} x {L} B messages per step, oracle/hetoc_oracle.c "
-                                       f"(C restatement of hetoc.crypto) on {threads} threads"},
+                             "sample": f"{sample}, oracle/hetoc_oracle.c (C restatement of hetoc.crypto) "
+                                       f"on {threads} threads"},
             "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "mhash_per_s": round(rows / t / 1e6, 4)}
     print(json.dumps(line), flush=True)

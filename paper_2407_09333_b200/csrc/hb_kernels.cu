@@ -295,6 +295,52 @@ k_fixed_direct(const uint8_t* __restrict__ msgs, uint64_t n, uint32_t msg_len, u
     store_digest<ALG>(out + i * H::kDigestBytes, st);
 }
 
+// -------------------------------------------------------------------------
+// Short fixed-width messages, width known at compile time (L in {16, 32, 48,
+// 64, 128}: the powers of two of the configs[4] sweep below 256 B, plus 48).
+// One message per thread, L/16 LDG.128 loads; the padding words (0x80, zero
+// fill, bit length) are immediates, so the last block costs nothing beyond
+// its compression (the generic direct kernel places them with select chains,
+// a visible share of a single-block MD5 message).
+// -------------------------------------------------------------------------
+__host__ __device__ constexpr uint32_t bswap_c(uint32_t x) {
+    return (x >> 24) | ((x >> 8) & 0xFF00u) | ((x << 8) & 0xFF0000u) | (x << 24);
+}
+
+template <int ALG, int L>
+__global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__ msgs, uint64_t n,
+                                                     uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    static_assert(L % 16 == 0 && L >= 16 && L <= 128, "width");
+    constexpr int kNb = (L + 8) / 64 + 1;  // blocks including padding
+    constexpr uint64_t kBits = (uint64_t)L * 8u;
+    constexpr uint32_t kL14 = H::kBigEndian ? bswap_c((uint32_t)(kBits >> 32)) : (uint32_t)kBits;
+    constexpr uint32_t kL15 = H::kBigEndian ? bswap_c((uint32_t)kBits) : (uint32_t)(kBits >> 32);
+    const uint64_t i = (uint64_t)blockIdx.x * 128u + threadIdx.x;
+    if (i >= n) return;
+    const uint4* p = reinterpret_cast<const uint4*>(msgs + i * L);
+    uint32_t w[L / 4];
+#pragma unroll
+    for (int c = 0; c < L / 16; ++c) {
+        const uint4 v = __ldg(p + c);
+        w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
+    }
+    uint32_t st[H::kStateWords];
+    H::init(st);
+#pragma unroll
+    for (int b = 0; b < kNb; ++b) {
+        uint32_t raw[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int pos = 64 * b + 4 * j;  // _pad: data, 0x80, zeros, 64-bit bit length
+            raw[j] = pos < L ? w[pos / 4] : pos == L ? 0x80u : 0u;
+        }
+        if (b == kNb - 1) { raw[14] = kL14; raw[15] = kL15; }
+        compress1<ALG>(st, raw);
+    }
+    store_digest<ALG>(out + i * H::kDigestBytes, st);
+}
+
 // =========================================================================
 // Generic kernel: any width / alignment, and variable length.
 // Message bytes are fetched as aligned 32-bit words and realigned with one
@@ -446,14 +492,15 @@ k_varlen16(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offset
 constexpr int kVcWarps = 4;
 constexpr int kVcSlot = 80;                   // bytes per message per stage
 constexpr int kVcWarpStage = 32 * kVcSlot;    // 2,560 bytes
-constexpr int kVcStages = 4;
 
-template <int ALG>
-__global__ void __launch_bounds__(kVcWarps * 32)
+// STAGES-deep ring (smem 10 KiB per stage per CTA), MINB CTAs/SM register
+// target, PF = L2 prefetch size of the cp.async copies.
+template <int ALG, int STAGES = 4, int MINB = 5, int PF = 256>
+__global__ void __launch_bounds__(kVcWarps * 32, MINB)
 k_varlen_coop(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offsets, uint64_t offset_base,
               const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
     using H = HashAlg<ALG>;
-    __shared__ __align__(128) uint8_t ring[kVcWarps][kVcStages][kVcWarpStage];
+    __shared__ __align__(128) uint8_t ring[kVcWarps][STAGES][kVcWarpStage];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t wbase = ((uint64_t)blockIdx.x * kVcWarps + warp) * 32u;
     if (wbase >= n) return;  // warp-uniform
@@ -485,17 +532,17 @@ k_varlen_coop(const uint8_t* __restrict__ data, const uint64_t* __restrict__ off
     uint8_t* wring = &ring[warp][0][0];
     const uint32_t sring = smem_u32(wring);
     auto issue = [&](uint32_t b) {
-        const uint32_t sdst = sring + (b % kVcStages) * kVcWarpStage;
+        const uint32_t sdst = sring + (b % STAGES) * kVcWarpStage;
 #pragma unroll
         for (int j = 0; j < 5; ++j) {
             const int64_t av = avail0[j] - 64 * (int64_t)b;
             const uint32_t sz = av <= 0 ? 0u : av >= 16 ? 16u : (uint32_t)av;
             const uintptr_t src = sz ? src0[j] + 64u * (uintptr_t)b : reinterpret_cast<uintptr_t>(data);
-            cp_async16_zfill(sdst + 16u * (lane + 32u * j), reinterpret_cast<const void*>(src), sz);
+            cp_async16_zfill<PF>(sdst + 16u * (lane + 32u * j), reinterpret_cast<const void*>(src), sz);
         }
     };
 #pragma unroll
-    for (int s = 0; s < kVcStages - 1; ++s) {
+    for (int s = 0; s < STAGES - 1; ++s) {
         if ((uint32_t)s < nbmax) issue(s);
         cp_async_commit();
     }
@@ -509,12 +556,12 @@ k_varlen_coop(const uint8_t* __restrict__ data, const uint64_t* __restrict__ off
     H::init(st);
     const uint32_t slot = smem_u32(wring) + lane * kVcSlot;
     for (uint32_t b = 0; b < nbmax; ++b) {
-        if (b + kVcStages - 1 < nbmax) issue(b + kVcStages - 1);
+        if (b + STAGES - 1 < nbmax) issue(b + STAGES - 1);
         cp_async_commit();
-        cp_async_wait<kVcStages - 1>();  // this lane's copies of step b have landed
+        cp_async_wait<STAGES - 1>();  // this lane's copies of step b have landed
         __syncwarp();                    // ... and every other lane's
         uint32_t c[20];
-        const uint32_t sbase = slot + (b % kVcStages) * kVcWarpStage;
+        const uint32_t sbase = slot + (b % STAGES) * kVcWarpStage;
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
             uint32_t x, y, z, w;
@@ -922,7 +969,18 @@ static cudaError_t launch_fixed_alg(const uint8_t* d_msgs, uint64_t n, uint64_t 
         return cudaSuccess;
     }
     const uint64_t grid = (n + 127) / 128;
-    if (aligned) {
+    const bool small_ok = aligned && !getenv("HB_NO_SMALL_KERNEL");
+    if (small_ok && L == 16) {
+        k_fixed_small<ALG, 16><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+    } else if (small_ok && L == 32) {
+        k_fixed_small<ALG, 32><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+    } else if (small_ok && L == 48) {
+        k_fixed_small<ALG, 48><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+    } else if (small_ok && L == 64) {
+        k_fixed_small<ALG, 64><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+    } else if (small_ok && L == 128) {
+        k_fixed_small<ALG, 128><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+    } else if (aligned) {
         k_fixed_direct<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, (uint32_t)L, d_out);
     } else {
         k_generic<ALG, false><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, d_msgs + n * L, nullptr, 0, nullptr, L, n,
@@ -974,7 +1032,20 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
         // SHA-1/SM3 are ALU-bound and lose more to the cooperative kernel's
         // 92-96 registers than they gain (4.30 vs 3.96, 10.5 vs 8.95 ms).
         const uint64_t g = (n + kVcWarps * 32 - 1) / (kVcWarps * 32);
-        k_varlen_coop<ALG><<<(unsigned)g, kVcWarps * 32, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
+        // A/B knobs: $HB_VC_STAGES (ring depth; 4 -> 5 CTAs/SM by smem, 3 -> 7), $HB_VC_PF (L2 prefetch)
+        const int stages = (int)env_u64("HB_VC_STAGES", 4), pf = (int)env_u64("HB_VC_PF", 256);
+        const unsigned gg = (unsigned)g;
+        constexpr int T = kVcWarps * 32;
+        if (stages == 3)
+            k_varlen_coop<ALG, 3, 7, 256><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
+        else if (stages == 2)
+            k_varlen_coop<ALG, 2, 8, 256><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
+        else if (pf == 128)
+            k_varlen_coop<ALG, 4, 5, 128><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
+        else if (pf == 0)
+            k_varlen_coop<ALG, 4, 5, 0><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
+        else
+            k_varlen_coop<ALG, 4, 5, 256><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
     } else {  // A/B baseline: per-thread 128-bit loads
         k_varlen16<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
     }

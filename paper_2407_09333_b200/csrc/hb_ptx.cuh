@@ -63,9 +63,17 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 // `src_bytes` (0..16) bytes are read, the rest of the 16 written as zero.
 // The L2::256B hint lets L2 fetch a whole 256-byte line per miss (a message
 // is read 64 bytes per step; the next steps then hit L2).
+template <int PF = 256>
 __device__ __forceinline__ void cp_async16_zfill(uint32_t dst_smem, const void* src, uint32_t src_bytes) {
-    asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(src_bytes)
-                 : "memory");
+    if constexpr (PF == 256)
+        asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src),
+                     "r"(src_bytes) : "memory");
+    else if constexpr (PF == 128)
+        asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src),
+                     "r"(src_bytes) : "memory");
+    else
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(src_bytes)
+                     : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N> __device__ __forceinline__ void cp_async_wait() {

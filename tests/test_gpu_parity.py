@@ -298,13 +298,14 @@ def test_batch_geometry_dispatch_matches(alg, monkeypatch):
     """The fixed-width dispatch picks a kernel shape by batch geometry (direct
     loads for short rows, one message per thread below $HB_SMALL_N, the tuned
     tiles otherwise); every shape must give the oracle's digests."""
-    arms = [{}, {"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"}, {"HB_SMALL_N": str(1 << 40), "HB_DIRECT_MAX_L": "0"}]
-    for L in (16, 64, 96, 128, 144, 1024):
+    arms = [{}, {"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"}, {"HB_SMALL_N": str(1 << 40), "HB_DIRECT_MAX_L": "0"},
+            {"HB_NO_SMALL_KERNEL": "1"}]
+    for L in (16, 32, 48, 64, 96, 128, 144, 1024):
         n = 3001
         data = oracle.fill_random(n * L, 5 * L + 3).reshape(n, L)
         ref = oracle.batch_fixed(alg, data, threads=8)
         for env in arms:
-            for k in ("HB_SMALL_N", "HB_DIRECT_MAX_L"):
+            for k in ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL"):
                 monkeypatch.delenv(k, raising=False)
             for k, v in env.items():
                 monkeypatch.setenv(k, v)
@@ -312,7 +313,7 @@ def test_batch_geometry_dispatch_matches(alg, monkeypatch):
 
 
 @pytest.mark.parametrize("alg", ALGS)
-def test_varlen_every_length_and_alignment(alg):
+def test_varlen_every_length_and_alignment(alg, monkeypatch):
     """Every length 0..260 (x3, shuffled, so message starts take every
     alignment mod 16) in one batch and in partial warps (n not a multiple of
     32), with several leading offsets, sorted and unsorted, every kernel."""
@@ -328,3 +329,10 @@ def test_varlen_every_length_and_alignment(alg):
             for fl in (0, _native.HB_FLAG_NO_SORT, _native.HB_FLAG_VARLEN_COOP_OFF, _native.HB_FLAG_VARLEN_COOP):
                 got = batch_digest_varlen(alg, buf, off[: k + 1], flags=fl)
                 assert np.array_equal(got, ref[:k]), (alg, shift, k, fl)
+        for env in ({"HB_VC_STAGES": "3"}, {"HB_VC_STAGES": "2"}, {"HB_VC_PF": "128"}, {"HB_VC_PF": "0"}):
+            for key, v in env.items():
+                monkeypatch.setenv(key, v)
+            got = batch_digest_varlen(alg, buf, off, flags=_native.HB_FLAG_VARLEN_COOP)
+            assert np.array_equal(got, ref), (alg, shift, env)
+            for key in env:
+                monkeypatch.delenv(key)

@@ -1,0 +1,53 @@
+"""A/B of the varlen kernels on configs[3] (2^22 messages, uniform 1-4096 B):
+cooperative-staging knobs ($HB_VC_STAGES, $HB_VC_PF) and the per-thread
+kernel, interleaved rounds, digests cross-checked.  One JSON line per arm."""
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2407_09333_b200 import _native, device  # noqa: E402
+
+DLEN = {"md5": 16, "sha1": 20, "sm3": 32}
+n, maxlen = 1 << 22, 4096
+lens = np.random.default_rng(4).integers(1, maxlen + 1, n).astype(np.int64)
+off = np.zeros(n + 1, np.int64)
+off[1:] = np.cumsum(lens)
+data = torch.empty(int(off[-1]), dtype=torch.uint8, device="cuda:0")
+device.fill_random(data, 4)
+d_off = torch.from_numpy(off).cuda()
+scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch.uint8, device="cuda:0")
+C = _native.HB_FLAG_VARLEN_COOP
+ARMS = {"coop_s4_pf256": ({}, C), "coop_s3": ({"HB_VC_STAGES": "3"}, C), "coop_s2": ({"HB_VC_STAGES": "2"}, C),
+        "coop_s4_pf128": ({"HB_VC_PF": "128"}, C), "coop_s4_pf0": ({"HB_VC_PF": "0"}, C),
+        "per_thread": ({}, _native.HB_FLAG_VARLEN_COOP_OFF)}
+for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
+    ref, times = None, {}
+    for _ in range(3):
+        for arm, (env, flags) in ARMS.items():
+            for k in ("HB_VC_STAGES", "HB_VC_PF"):
+                os.environ.pop(k, None)
+            os.environ.update(env)
+            out = torch.empty((n, DLEN[alg]), dtype=torch.uint8, device="cuda:0")
+            f = lambda: device.hash_varlen(alg, data, d_off, out=out, scratch=scratch, flags=flags,  # noqa: E731
+                                           offset_base=0)
+            f()
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(5):
+                f()
+            e.record()
+            torch.cuda.synchronize()
+            if ref is None:
+                ref = out.clone()
+            assert torch.equal(out, ref), (alg, arm)
+            times.setdefault(arm, []).append(s.elapsed_time(e) / 5)
+    for arm, ts in times.items():
+        ms = statistics.median(ts)
+        print(json.dumps({"alg": alg, "arm": arm, "ms": round(ms, 4), "GBps": round(int(off[-1]) / ms / 1e6, 1)}),
+              flush=True)

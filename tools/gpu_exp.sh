@@ -1,5 +1,6 @@
 set -u
 mkdir -p gpurun_out
-T=${T:-exp4}
-timeout 900 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pytest_$T.log
-timeout 600 python tools/bench_configs.py gpurun_out/configs_$T.jsonl --quick > /dev/null 2>gpurun_out/configs_$T.err; echo "configs rc=$?"; cut -c1-250 gpurun_out/configs_$T.jsonl
+T=${T:-exp6}
+timeout 900 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_$T.log
+timeout 600 python tools/ab_varlen.py > gpurun_out/ab_varlen_$T.txt 2>&1; echo "abv rc=$?"; cat gpurun_out/ab_varlen_$T.txt
+timeout 600 python tools/ab_small.py > gpurun_out/ab_small_$T.txt 2>&1; echo "abs rc=$?"

@@ -112,8 +112,7 @@ def main():
             wr = to_bytes(*d["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in d else None
             wl = re.sub(r"_r\d+\w*$", "", os.path.basename(rep).replace("prof_", "").replace("raw_", "")
                         .replace(".ncu-rep", "").replace(".csv", ""))
-            key = {"md5_1k": "md5_16777216x1024", "sha1_1k": "sha1_16777216x1024",
-                   "sm3_1k": "sm3_16777216x1024"}.get(wl, wl)
+            key = wl  # bench.py workload name
             summ[key] = {
                 "kernel": name,
                 "dram_bytes": (rd + wr) if rd is not None and wr is not None else None,
