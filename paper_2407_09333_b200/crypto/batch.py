@@ -84,6 +84,48 @@ class MessageBatch:
         return np.frombuffer(self.data, np.uint8).reshape(self.count, self.msg_len)
 
 
+@dataclass(frozen=True)
+class VarMessageBatch:
+    """Variable-length layout (configs[3]): message i
+    lives at bytes [offsets[i], offsets[i+1]) of ``data``.  The reference's
+    ``MessageBatch`` is fixed-width by design and its only
+    variable-length path is the scalar ``digest``; this type lets
+    ``hash_batch`` take a whole mixed-length batch in one engine call.
+    Zero-length messages are allowed (their digest is the empty-message one)."""
+
+    data: bytes
+    offsets: tuple
+
+    def __post_init__(self):
+        off = np.asarray(self.offsets, dtype=np.int64)
+        if off.ndim != 1 or off.shape[0] < 1:
+            raise ValueError("offsets must be a 1-D sequence of count+1 entries")
+        if off[0] < 0 or np.any(np.diff(off) < 0):
+            raise ValueError("offsets must be non-negative and non-decreasing")
+        if int(off[-1]) > len(self.data):
+            raise ValueError(f"offsets[-1]={int(off[-1])} exceeds the data length {len(self.data)}")
+        object.__setattr__(self, "offsets", tuple(int(x) for x in off))
+
+    @classmethod
+    def from_messages(cls, messages) -> "VarMessageBatch":
+        msgs = [bytes(m) for m in messages]
+        off = np.zeros(len(msgs) + 1, np.int64)
+        off[1:] = np.cumsum([len(m) for m in msgs])
+        return cls(b"".join(msgs), tuple(int(x) for x in off))
+
+    @property
+    def count(self) -> int:
+        return len(self.offsets) - 1
+
+    def message(self, i: int) -> bytes:
+        if not 0 <= i < self.count:
+            raise IndexError(i)
+        return self.data[self.offsets[i] : self.offsets[i + 1]]
+
+    def offsets_array(self) -> np.ndarray:
+        return np.asarray(self.offsets, dtype=np.uint64)
+
+
 def gen_messages(start_index: int, count: int, width: int = 9) -> MessageBatch:
     """Zero-padded decimal messages for indices [start_index, start_index+count) (batch.py:86-99)."""
     if width <= 0:
@@ -217,15 +259,20 @@ def digest_sha1_accel(message: bytes) -> Digest:
     return digest("sha1", message)
 
 
-def hash_batch(alg: str, batch: MessageBatch, threads: int = 1, accel: bool = False, *,
+def hash_batch(alg: str, batch, threads: int = 1, accel: bool = False, *,
                gpus=None) -> list[Digest]:
-    """Digest every message of a batch; output is independent of ``threads`` (batch.py:293-316)."""
+    """Digest every message of a batch; output is independent of ``threads`` (batch.py:293-316).
+    ``batch`` is a ``MessageBatch`` (fixed width) or a ``VarMessageBatch``."""
     _check_alg(alg)
     if threads < 1:
         raise ValueError("threads must be >= 1")
     if batch.count == 0:
         return []
-    out = batch_digest(alg, batch.as_array(), accel=accel, gpus=gpus)
+    if isinstance(batch, VarMessageBatch):
+        out = batch_digest_varlen(alg, np.frombuffer(batch.data, np.uint8) if batch.data else np.zeros(0, np.uint8),
+                                  batch.offsets_array(), gpus=gpus)
+    else:
+        out = batch_digest(alg, batch.as_array(), accel=accel, gpus=gpus)
     dlen = DIGEST_LEN[alg]
     raw = out.tobytes()
     return [Digest(alg, raw[i * dlen : (i + 1) * dlen]) for i in range(batch.count)]

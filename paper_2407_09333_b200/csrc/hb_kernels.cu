@@ -1032,8 +1032,9 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
         // SHA-1/SM3 are ALU-bound and lose more to the cooperative kernel's
         // 92-96 registers than they gain (4.30 vs 3.96, 10.5 vs 8.95 ms).
         const uint64_t g = (n + kVcWarps * 32 - 1) / (kVcWarps * 32);
-        // A/B knobs: $HB_VC_STAGES (ring depth; 4 -> 5 CTAs/SM by smem, 3 -> 7), $HB_VC_PF (L2 prefetch)
-        const int stages = (int)env_u64("HB_VC_STAGES", 4), pf = (int)env_u64("HB_VC_PF", 256);
+        // A/B knobs: $HB_VC_STAGES (ring depth; 4 -> 5 CTAs/SM by smem, 3 -> 7), $HB_VC_PF (L2 prefetch).
+        // B200 (profiles/ab_varlen_r1.txt): MD5 best at 3 stages (2.52 vs 2.62 ms for 4), 256 B prefetch.
+        const int stages = (int)env_u64("HB_VC_STAGES", ALG == kMd5 ? 3 : 4), pf = (int)env_u64("HB_VC_PF", 256);
         const unsigned gg = (unsigned)g;
         constexpr int T = kVcWarps * 32;
         if (stages == 3)

@@ -165,3 +165,17 @@ def test_ratio_validation_matches_reference_verifier():
         bd("md5", rows, gpus=[0, 0], ratios=[0.5, 0.4])
     with pytest.raises(ValueError):
         bd("md5", rows, gpus=[0], ratios=[0.5, 0.5])
+
+
+def test_var_message_batch_layout():
+    from paper_2407_09333_b200.crypto import VarMessageBatch
+
+    b = VarMessageBatch.from_messages([b"", b"abc", b"x" * 70])
+    assert b.count == 3 and b.message(0) == b"" and b.message(1) == b"abc" and b.message(2) == b"x" * 70
+    assert list(b.offsets_array()) == [0, 0, 3, 73]
+    with pytest.raises(ValueError):
+        VarMessageBatch(b"abc", (0, 2, 1))
+    with pytest.raises(ValueError):
+        VarMessageBatch(b"abc", (0, 4))
+    with pytest.raises(IndexError):
+        b.message(3)

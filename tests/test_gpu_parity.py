@@ -336,3 +336,18 @@ def test_varlen_every_length_and_alignment(alg, monkeypatch):
             assert np.array_equal(got, ref), (alg, shift, env)
             for key in env:
                 monkeypatch.delenv(key)
+
+
+def test_hash_batch_var_message_batch():
+    """§8(f) row 3: a mixed-length batch through hash_batch is the scalar
+    digest of every message (the reference's only variable-length path)."""
+    from paper_2407_09333_b200.crypto import VarMessageBatch
+
+    rng = np.random.default_rng(3)
+    msgs = [bytes(rng.integers(0, 256, int(L), dtype=np.uint8)) for L in rng.integers(0, 300, 2500)]
+    b = VarMessageBatch.from_messages(msgs)
+    for alg in ALGS:
+        got = hash_batch(alg, b, threads=4)
+        ref = oracle.batch_varlen(alg, np.frombuffer(b.data, np.uint8), b.offsets_array(), threads=8)
+        assert [d.data for d in got] == [bytes(r) for r in ref]
+        assert all(d.alg == alg for d in got)
