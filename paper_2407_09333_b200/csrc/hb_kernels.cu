@@ -686,6 +686,69 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const uint64_t* _
     }
 }
 
+// Windowed variant (the default): the same (block count, alignment) key, but
+// sorted only inside windows of kSortWindow consecutive messages, one CTA per
+// window, in shared memory.  Warps still see near-equal lengths (a window of
+// 4,096 messages has ~60 per block-count class at U(1, 4096)) while the
+// messages a window's warps read concurrently stay within a few MB of each
+// other: L2 lines fetched for one message (256 B promotion) are still
+// resident when its neighbours are hashed, instead of being re-fetched from
+// HBM after a global sort scattered the neighbours across the whole batch.
+constexpr int kSortWindow = 4096;
+
+__global__ void __launch_bounds__(1024) k_sort_window(const uint64_t* __restrict__ offsets, uint64_t n,
+                                                      uint64_t addr_bias, uint32_t* __restrict__ perm) {
+    __shared__ uint32_t h[kSortBuckets];
+    __shared__ uint32_t wsum[32];
+    const uint32_t t = threadIdx.x;
+    const uint64_t w0 = (uint64_t)blockIdx.x * kSortWindow;
+    for (int k = t; k < kSortBuckets; k += 1024) h[k] = 0;
+    __syncthreads();
+    constexpr int kItems = kSortWindow / 1024;
+    uint32_t key[kItems], rank[kItems];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+        const uint64_t i = w0 + (uint64_t)it * 1024u + t;
+        key[it] = 0xFFFFFFFFu;
+        if (i < n) {
+            key[it] = sort_bucket(offsets, i, addr_bias);
+            rank[it] = atomicAdd(&h[key[it]], 1u);
+        }
+    }
+    __syncthreads();
+    // exclusive scan of the 4,096 bucket counts; thread t owns buckets 4t..4t+3
+    constexpr int kPer = kSortBuckets / 1024;
+    uint32_t v[kPer], sum = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) { v[k] = h[kPer * t + k]; sum += v[k]; }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if ((t & 31) >= (uint32_t)o) incl += x;
+    }
+    if ((t & 31) == 31) wsum[t >> 5] = incl;
+    __syncthreads();
+    if (t < 32) {
+        const uint32_t w = wsum[t];
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (t >= (uint32_t)o) wi += x;
+        }
+        wsum[t] = wi - w;
+    }
+    __syncthreads();
+    uint32_t run = wsum[t >> 5] + incl - sum;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) { h[kPer * t + k] = run; run += v[k]; }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < kItems; ++it)
+        if (key[it] != 0xFFFFFFFFu) perm[w0 + h[key[it]] + rank[it]] = (uint32_t)(w0 + (uint64_t)it * 1024u + t);
+}
+
 // ------------------------------------------------------- synthetic bytes --
 __device__ __forceinline__ uint64_t mix64(uint64_t seed, uint64_t idx) {  // == oracle mix64
     uint64_t z = (idx + 1ull) * 0x9E3779B97F4A7C15ull + seed * 0xD1B54A32D192ED03ull;
@@ -1008,7 +1071,13 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
                                      uint64_t offset_base, uint64_t n, uint8_t* d_out, void* d_scratch,
                                      cudaStream_t stream, uint32_t flags) {
     const uint32_t* perm = nullptr;
-    if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch) {
+    const uint64_t bias0 = reinterpret_cast<uintptr_t>(d_data) - offset_base;  // address = offsets[i] + bias
+    if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch && !getenv("HB_VARLEN_GLOBAL_SORT")) {
+        uint32_t* p = static_cast<uint32_t*>(d_scratch) + kSortBuckets;
+        k_sort_window<<<(unsigned)((n + kSortWindow - 1) / kSortWindow), 1024, 0, stream>>>(d_offsets, n, bias0, p);
+        note_launches(1);
+        perm = p;
+    } else if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch) {
         uint32_t* hist = static_cast<uint32_t*>(d_scratch);
         uint32_t* p = hist + kSortBuckets;
         cudaError_t e = cudaMemsetAsync(hist, 0, kSortBuckets * sizeof(uint32_t), stream);

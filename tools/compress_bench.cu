@@ -56,6 +56,23 @@ static void run(const char* name, int ctas_per_sm, int sms, uint32_t* out, int c
            ns_blk_sm * clk_mhz / 1000.0, clk_mhz);
 }
 
+template <int ALG>
+static void run_lat(const char* name, int sms, uint32_t* out, int clk_mhz) {
+    kern<ALG, -1, 1><<<sms, 32>>>(3u, out);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    kern<ALG, -1, 1><<<sms, 32>>>(5u, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    const double ns = ms * 1e6 / kR;
+    printf("%-8s chain latency (1 warp/SM): %.1f ns = %.0f cycles per compression @%d MHz\n", name, ns,
+           ns * clk_mhz / 1000.0, clk_mhz);
+}
+
 int main(int argc, char** argv) {
     int sms = 0, clk_khz = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -77,6 +94,13 @@ int main(int argc, char** argv) {
     run<kSm3, 1, 1>("sm3", 6, sms, out, clk);
     run<kSm3, 2, 1>("sm3", 6, sms, out, clk);
     run<kSm3, 3, 1>("sm3", 6, sms, out, clk);
+    // Dependent-chain latency: ONE warp per SM (32 threads per CTA, one CTA
+    // per SM), so nothing hides the round-to-round dependency -- cycles per
+    // compression of a single message = the latency bound of a batch with
+    // fewer messages than the GPU can overlap (configs[4] small-n points).
+    run_lat<kMd5>("md5", sms, out, clk);
+    run_lat<kSha1>("sha1", sms, out, clk);
+    run_lat<kSm3>("sm3", sms, out, clk);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
     return 0;
