@@ -60,10 +60,9 @@ typedef enum { HB_SHA1 = 0, HB_MD5 = 1, HB_SM3 = 2 } hb_alg;
 #define HB_FLAG_NO_SORT  0x2u  /* varlen: skip the length-bucket sort                    */
 #define HB_FLAG_SYNC_H2D 0x4u  /* engine: no copy/compute overlap (diagnostics)          */
 #define HB_FLAG_VARLEN_WORDS 0x8u /* varlen: per-thread 32-bit-load kernel (A/B baseline)       */
-#define HB_FLAG_VARLEN_COOP_OFF 0x10u /* varlen: per-thread 128-bit-load kernel (the SHA-1/SM3
-                                         default) instead of the warp-cooperative cp.async
-                                         staging (the MD5 default)                              */
-#define HB_FLAG_VARLEN_COOP 0x20u     /* varlen: warp-cooperative staging for every algorithm  */
+#define HB_FLAG_VARLEN_COOP_OFF 0x10u /* varlen: per-thread 128-bit-load kernel (the default;
+                                         kept so callers can pin it explicitly)                 */
+#define HB_FLAG_VARLEN_COOP 0x20u     /* varlen: warp-cooperative cp.async staging kernel      */
 
 typedef struct {
     double total_ms;       /* host wall time of the call                              */

@@ -694,8 +694,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const uint64_t* _
 // other: L2 lines fetched for one message (256 B promotion) are still
 // resident when its neighbours are hashed, instead of being re-fetched from
 // HBM after a global sort scattered the neighbours across the whole batch.
-constexpr int kSortWindow = 4096;
-
+template <int kSortWindow>
 __global__ void __launch_bounds__(1024) k_sort_window(const uint64_t* __restrict__ offsets, uint64_t n,
                                                       uint64_t addr_bias, uint32_t* __restrict__ perm) {
     __shared__ uint32_t h[kSortBuckets];
@@ -1072,9 +1071,20 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
                                      cudaStream_t stream, uint32_t flags) {
     const uint32_t* perm = nullptr;
     const uint64_t bias0 = reinterpret_cast<uintptr_t>(d_data) - offset_base;  // address = offsets[i] + bias
-    if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch && !getenv("HB_VARLEN_GLOBAL_SORT")) {
+    // Sort mode: windowed for MD5 (HBM-bound: locality wins), global for SHA-1/SM3
+    // (ALU-bound: full (block count, alignment) uniformity wins); B200 A/B in
+    // profiles/ab_varlen_r1b.txt.  $HB_VARLEN_SORT = window | global, $HB_SORT_WINDOW.
+    const char* sm = getenv("HB_VARLEN_SORT");
+    const bool window = sm ? strcmp(sm, "global") != 0 : ALG == kMd5;
+    if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch && window) {
         uint32_t* p = static_cast<uint32_t*>(d_scratch) + kSortBuckets;
-        k_sort_window<<<(unsigned)((n + kSortWindow - 1) / kSortWindow), 1024, 0, stream>>>(d_offsets, n, bias0, p);
+        const uint64_t w = env_u64("HB_SORT_WINDOW", 8192);
+        if (w >= 16384)
+            k_sort_window<16384><<<(unsigned)((n + 16383) / 16384), 1024, 0, stream>>>(d_offsets, n, bias0, p);
+        else if (w >= 8192)
+            k_sort_window<8192><<<(unsigned)((n + 8191) / 8192), 1024, 0, stream>>>(d_offsets, n, bias0, p);
+        else
+            k_sort_window<4096><<<(unsigned)((n + 4095) / 4096), 1024, 0, stream>>>(d_offsets, n, bias0, p);
         note_launches(1);
         perm = p;
     } else if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch) {
@@ -1095,11 +1105,11 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
     if (flags & HB_FLAG_VARLEN_WORDS) {  // A/B baseline: per-thread 32-bit loads
         k_generic<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets,
                                                                  offset_base, perm, 0, n, d_out);
-    } else if (((flags & HB_FLAG_VARLEN_COOP) || (ALG == kMd5 && !(flags & HB_FLAG_VARLEN_COOP_OFF))) &&
-               data_bytes < (1ull << 37)) {  // block counts fit u32
-        // Default for MD5 only (B200, 2^22 msgs of 1-4096 B: 2.38 vs 4.36 ms);
-        // SHA-1/SM3 are ALU-bound and lose more to the cooperative kernel's
-        // 92-96 registers than they gain (4.30 vs 3.96, 10.5 vs 8.95 ms).
+    } else if ((flags & HB_FLAG_VARLEN_COOP) && data_bytes < (1ull << 37)) {  // block counts fit u32
+        // Opt-in.  It beat the per-thread kernel for MD5 under the global sort
+        // (2.38 vs 4.36 ms at configs[3]) because its coalesced staging hid the
+        // scattered reads; with the windowed sort the per-thread kernel reads
+        // neighbouring messages together and wins (2.24 vs 2.85 ms).
         const uint64_t g = (n + kVcWarps * 32 - 1) / (kVcWarps * 32);
         // A/B knobs: $HB_VC_STAGES (ring depth; 4 -> 5 CTAs/SM by smem, 3 -> 7), $HB_VC_PF (L2 prefetch).
         // B200 (profiles/ab_varlen_r1.txt): MD5 best at 3 stages (2.52 vs 2.62 ms for 4), 256 B prefetch.

@@ -108,11 +108,12 @@ def test_varlen_golden(golden):
             assert sha(batch_digest_varlen(alg, data, off)) == row[alg]
 
 
-@pytest.mark.parametrize("sort", ["window", "global"])
+@pytest.mark.parametrize("sort", ["window4096", "window16384", "global"])
 @pytest.mark.parametrize("alg", ALGS)
 def test_varlen_random_sorted_and_unsorted(alg, sort, monkeypatch):
-    if sort == "global":
-        monkeypatch.setenv("HB_VARLEN_GLOBAL_SORT", "1")
+    monkeypatch.setenv("HB_VARLEN_SORT", "global" if sort == "global" else "window")
+    if sort != "global":
+        monkeypatch.setenv("HB_SORT_WINDOW", sort[6:])
     rng = np.random.default_rng(12)
     n = 20000  # above the sort threshold
     lens = rng.integers(0, 4097, n).astype(np.uint64)

@@ -29,6 +29,12 @@ PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if 
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 # minimal ALU-pipe ops per 64-byte block and the 64 lanes/clk/SM ALU rate
 ALU_OPS = {"md5": 128, "sha1": 448, "sm3": 1084}
+# Dependent-chain latency of one compression with nothing to overlap it (one
+# warp per SM; tools/compress_bench.cu, profiles/compress_bench_r1b.txt): a
+# message's blocks are compressed in sequence, so no batch finishes faster than
+# (blocks per message) x this -- the binding bound when there are fewer
+# messages than the GPU has lanes to overlap.
+CHAIN_CYCLES = {"md5": 1509, "sha1": 1116, "sm3": 2514}
 SMS = 148
 
 
@@ -56,12 +62,13 @@ def clock_mhz():
         return 1965.0
 
 
-def roof(alg, n_blocks, bytes_hbm, ms, f_mhz):
-    t_hbm = bytes_hbm / (PEAK * 1e9)
-    t_alu = n_blocks * ALU_OPS[alg] / (64 * SMS * f_mhz * 1e6)
-    t_roof = max(t_hbm, t_alu)
-    return {"bound": "hbm" if t_hbm >= t_alu else "alu", "t_roof_ms": round(t_roof * 1e3, 4),
-            "frac": round(t_roof / (ms * 1e-3), 4)}
+def roof(alg, n_blocks, bytes_hbm, ms, f_mhz, max_blocks_per_msg=0):
+    t = {"hbm": bytes_hbm / (PEAK * 1e9),
+         "alu": n_blocks * ALU_OPS[alg] / (64 * SMS * f_mhz * 1e6),
+         "chain": max_blocks_per_msg * CHAIN_CYCLES[alg] / (f_mhz * 1e6)}
+    bound = max(t, key=t.get)
+    return {"bound": bound, "t_roof_ms": round(t[bound] * 1e3, 4), "frac": round(t[bound] / (ms * 1e-3), 4),
+            "t_ms": {k: round(v * 1e3, 4) for k, v in t.items()}}
 
 
 def fixed_point(alg, n, L, seed, steps, out, tag):
@@ -78,7 +85,8 @@ def fixed_point(alg, n, L, seed, steps, out, tag):
     f = clock_mhz()
     rec = {"config": tag, "alg": alg, "n": n, "msg_len": L, "ms": round(ms, 4),
            "GBps": round(n * L / ms / 1e6, 2), "Mhash_s": round(n / ms / 1e3, 2),
-           "roofline": roof(alg, blocks, n * (L + DLEN[alg]), ms, f), "sm_mhz": f, "bit_exact_sample": ok}
+           "roofline": roof(alg, blocks, n * (L + DLEN[alg]), ms, f, (L + 8) // 64 + 1), "sm_mhz": f,
+           "bit_exact_sample": ok}
     print(json.dumps(rec), flush=True)
     out.write(json.dumps(rec) + "\n")
     del buf, dig
@@ -106,7 +114,8 @@ def varlen_point(alg, n, maxlen, seed, steps, out, flags=0):
             _native.HB_FLAG_VARLEN_COOP: " (warp-cooperative cp.async)"}[flags]
     rec = {"config": "C4 varlen" + tagf, "alg": alg, "n": n, "len": f"uniform 1-{maxlen}",
            "bytes": total, "ms": round(ms, 4), "GBps": round(total / ms / 1e6, 2), "Mhash_s": round(n / ms / 1e3, 2),
-           "roofline": roof(alg, blocks, total + 8 * (n + 1) + n * DLEN[alg], ms, f), "sm_mhz": f,
+           "roofline": roof(alg, blocks, total + 8 * (n + 1) + n * DLEN[alg], ms, f, (maxlen + 8) // 64 + 1),
+           "sm_mhz": f,
            "bit_exact_sample": ok}
     print(json.dumps(rec), flush=True)
     out.write(json.dumps(rec) + "\n")

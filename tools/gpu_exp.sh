@@ -1,6 +1,6 @@
 set -u
 mkdir -p gpurun_out
-T=${T:-exp8}
+T=${T:-exp9}
 timeout 900 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_$T.log
-timeout 300 ./tools/compress_bench > gpurun_out/compress_$T.txt 2>&1; echo "compress rc=$?"; cat gpurun_out/compress_$T.txt
-timeout 600 python tools/ab_varlen.py md5 sha1 > gpurun_out/ab_varlen_$T.txt 2>&1; echo "abv rc=$?"; cat gpurun_out/ab_varlen_$T.txt
+timeout 600 python tools/ab_varlen.py > gpurun_out/ab_varlen_$T.txt 2>&1; echo "abv rc=$?"; cat gpurun_out/ab_varlen_$T.txt
+timeout 900 python tools/bench_configs.py gpurun_out/configs_$T.jsonl > /dev/null 2>gpurun_out/configs_$T.err; echo "configs rc=$?"; head -14 gpurun_out/configs_$T.jsonl | cut -c1-200

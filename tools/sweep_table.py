@@ -15,8 +15,11 @@ def main():
     print(f"# BASELINE configs on 1 B200 ({sys.argv[1].split('/')[-1]})\n")
     print("Kernel-only, inputs resident in HBM, CUDA events, median of back-to-back launches; every point's "
           "digests checked against the CPU oracle on a row sample (`bit_exact_sample`). Fraction = "
-          "max(T_hbm, T_alu) / T_measured with T_hbm at the HBM peak (6,650 GB/s fallback unless "
-          "MEASURED_PEAKS.json) and T_alu = blocks x ALU-only ops / (64 lanes/clk x 148 SMs x clock).\n")
+          "max(T_hbm, T_alu, T_chain) / T_measured with T_hbm at the HBM peak (6,650 GB/s fallback unless "
+          "MEASURED_PEAKS.json), T_alu = blocks x ALU-only ops / (64 lanes/clk x 148 SMs x clock) and "
+          "T_chain = blocks per message x the measured dependent-chain latency of one compression "
+          "(MD5 1,509 / SHA-1 1,116 / SM3 2,514 cycles, one warp per SM) -- the bound when the batch has too "
+          "few messages to overlap.\n")
     print("| config | alg | messages | size | ms | GB/s | Mhash/s | bound | fraction | bit-exact |")
     print("|---|---|---|---|---|---|---|---|---|---|")
     for r in other:
