@@ -16,6 +16,12 @@ void note_launches(uint64_t k);
 cudaError_t launch_fixed(int alg, const uint8_t* d_msgs, uint64_t n, uint64_t msg_len, uint8_t* d_out,
                          cudaStream_t stream, uint32_t flags);
 
+// Length/alignment-bucket permutation used by launch_varlen (*perm_out = null
+// when not sorting: HB_FLAG_NO_SORT, small n or no scratch).
+cudaError_t launch_varlen_sort(int alg, const uint8_t* d_data, const uint64_t* d_offsets, uint64_t offset_base,
+                               uint64_t n, void* d_scratch, cudaStream_t stream, uint32_t flags,
+                               const uint32_t** perm_out);
+
 // Scratch bytes launch_varlen needs for n messages (length-bucket sort).
 uint64_t varlen_scratch_bytes(uint64_t n);
 

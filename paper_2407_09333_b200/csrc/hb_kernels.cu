@@ -20,595 +20,13 @@
 #include "hb_internal.h"
 #include "hb_ptx.cuh"
 #include "../../include/hetoc_b200.h"
+#include "hb_kernels.cuh"
 
 namespace hb {
 
 static std::atomic<uint64_t> g_launches{0};
 void note_launches(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 uint64_t launches_total() { return g_launches.load(std::memory_order_relaxed); }
-
-// =========================================================================
-// Fixed-width, TMA-staged kernel (the hot path).
-//
-// CTA = 4 warps; warp w owns 32 consecutive messages (rows).  Each warp runs
-// its own kStages-deep ring of 2 KiB stages: lane 0 issues one 2-D TMA load
-// per 64-byte message block ({64 B, 32 rows} box over the (n, msg_len) byte
-// matrix, SWIZZLE_64B), completion lands on the stage's mbarrier, all lanes
-// wait on the phase and read their row with four conflict-free 16-byte
-// shared loads.  TMA zero-fills columns >= msg_len, so the final partial
-// block arrives already masked.
-// =========================================================================
-constexpr int kTmaWarps = 4;
-
-// Tunable tile configuration: NB messages per thread (ILP), STAGES-deep ring.
-// W warps per CTA.  W = 1 is the small-batch shape: a batch of n messages
-// becomes n/32 single-warp CTAs spread evenly over all 148 SMs (with 4-warp
-// CTAs a 65,536-message batch fills only 512 CTAs, 3-4 per SM, unevenly).
-template <int NB, int STAGES, int W = kTmaWarps> struct TmaCfg {
-    static constexpr int kRows = 32 * NB;           // rows (messages) per warp
-    static constexpr int kStageBytes = 64 * kRows;  // one 64-byte block of every row
-    static constexpr int kSmem = W * STAGES * kStageBytes + 1024 /*align slack*/ + W * STAGES * 8;
-};
-template <int ALG, int NB, int STAGES, int W = kTmaWarps> struct TmaOcc {  // CTAs per SM the budget targets
-    static constexpr int kMinCtas =
-        W == 1 ? 16
-        : NB == 1 ? (STAGES == 2 ? (ALG == kMd5 ? 12 : ALG == kSha1 ? 9 : 8) : (ALG == kSm3 ? 6 : 8))
-                  : (STAGES == 2 && ALG != kSm3 ? 6 : 4);
-};
-
-template <int ALG, int V, int NB, int STAGES, int W = kTmaWarps>
-__global__ void __launch_bounds__(W * 32, (TmaOcc<ALG, NB, STAGES, W>::kMinCtas))
-k_fixed_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG, V>;
-    using C = TmaCfg<NB, STAGES, W>;
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t row0 = (blockIdx.x * W + warp) * C::kRows;
-    if (row0 >= n) return;  // warp-uniform
-
-    // 1024-align the ring (the swizzle pattern is a function of address bits 7:8).
-    const uint32_t base_s = smem_u32(smem_raw);
-    uint8_t* ring = smem_raw + (((base_s + 1023u) & ~1023u) - base_s);
-    uint8_t* wring = ring + warp * (STAGES * C::kStageBytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + W * STAGES * C::kStageBytes) + warp * STAGES;
-
-    const uint32_t nload = (msg_len + 63u) >> 6;  // blocks holding message bytes
-    if (lane == 0) {
-        prefetch_tmap(&tmap);
-#pragma unroll
-        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
-        fence_mbar_init();
-        const uint32_t pro = nload < (uint32_t)STAGES ? nload : (uint32_t)STAGES;
-        for (uint32_t b = 0; b < pro; ++b) {
-            mbar_arrive_expect_tx(&bars[b], C::kStageBytes);
-            tma_load_2d(wring + b * C::kStageBytes, &tmap, &bars[b], (int)(b * 64u), (int)row0);
-        }
-    }
-    __syncwarp();
-
-    uint32_t st[NB][H::kStateWords];
-#pragma unroll
-    for (int q = 0; q < NB; ++q) H::init(st[q]);
-    // SWIZZLE_64B: the 16-byte chunk index is XORed with address bits 7:8, i.e.
-    // (row >> 1) & 3; rows lane and lane+32q share it.
-    const uint32_t swz = (lane >> 1) & 3u;
-    uint32_t stage = 0, phase = 0;
-    uint32_t raw[NB][16];
-    // Shared-memory byte offsets of this lane's four 16-byte chunks in stage 0;
-    // a stage adds a warp-uniform base, so each read is LDS.128 [R + UR].
-    uint32_t choff[NB][4];
-#pragma unroll
-    for (int q = 0; q < NB; ++q)
-#pragma unroll
-        for (uint32_t c = 0; c < 4; ++c) choff[q][c] = smem_u32(wring) + (lane + 32u * q) * 64u + ((c ^ swz) << 4);
-    auto read_stage = [&](uint32_t s) {
-        const uint32_t sbase = s * C::kStageBytes;
-#pragma unroll
-        for (int q = 0; q < NB; ++q) {
-#pragma unroll
-            for (uint32_t c = 0; c < 4; ++c) {
-                uint32_t x, y, z, w;
-                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
-                             : "r"(choff[q][c] + sbase)
-                             : "memory");
-                raw[q][4 * c + 0] = x; raw[q][4 * c + 1] = y; raw[q][4 * c + 2] = z; raw[q][4 * c + 3] = w;
-            }
-        }
-    };
-    const uint32_t nfull = msg_len >> 6;
-    for (uint32_t b = 0; b < nfull; ++b) {
-        mbar_wait_parity(&bars[stage], phase);
-        read_stage(stage);
-        H::template compress_n<NB>(st, raw);
-        __syncwarp();  // every lane has consumed this stage (its registers fed compress)
-        if (lane == 0 && b + STAGES < nload) {
-            fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&bars[stage], C::kStageBytes);
-            tma_load_2d(wring + stage * C::kStageBytes, &tmap, &bars[stage], (int)((b + STAGES) * 64u), (int)row0);
-        }
-        if (++stage == (uint32_t)STAGES) { stage = 0; phase ^= 1u; }
-    }
-    const uint32_t r = msg_len & 63u;
-    if (r) {  // partial data block: TMA zero-filled the columns >= msg_len
-        mbar_wait_parity(&bars[stage], phase);
-        read_stage(stage);
-    } else {  // padding-only final block (0x80, zeros, length)
-#pragma unroll
-        for (int q = 0; q < NB; ++q)
-#pragma unroll
-            for (int j = 0; j < 16; ++j) raw[q][j] = 0u;
-    }
-    md_finish_n<ALG, V, NB>(st, raw, r, msg_len);
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-        const uint32_t row = row0 + lane + 32u * q;
-        if (row < n) store_digest<ALG>(out + (uint64_t)row * H::kDigestBytes, st[q]);
-    }
-}
-
-// -------------------------------------------------------------------------
-// Warp-specialised variant: 4 compute warps + 1 producer warp per CTA.  The
-// producer's lane 0 streams one {64 B, 128 rows} TMA tile per message block
-// into a STAGES-deep CTA ring (full/empty mbarrier pair per stage); compute
-// warps only wait on `full`, read their row (4 x LDS.128) and arrive on
-// `empty` -- no TMA-issue path, fence or lane-0 branch in their loop.
-// -------------------------------------------------------------------------
-constexpr int kWsComputeWarps = 4;
-template <int NB, int STAGES> struct WsCfg {
-    static constexpr int kRows = 32 * kWsComputeWarps * NB;  // rows per CTA tile (TMA box height <= 256)
-    static constexpr int kStageBytes = 64 * kRows;            // 8 KiB per message slot
-    static constexpr int kSmem = STAGES * kStageBytes + 1024 + 2 * STAGES * 8;
-};
-template <int ALG, int NB, int STAGES> struct WsOcc {
-    static constexpr int kMinCtas =
-        NB == 2 ? (STAGES == 2 ? 6 : 4) : ALG == kSm3 ? 6 : (STAGES == 2 ? (ALG == kMd5 ? 10 : 8) : 8);
-};
-
-template <int ALG, int V, int NB, int STAGES>
-__global__ void __launch_bounds__((kWsComputeWarps + 1) * 32, (WsOcc<ALG, NB, STAGES>::kMinCtas))
-k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG, V>;
-    using C = WsCfg<NB, STAGES>;
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t row0 = blockIdx.x * C::kRows;
-    const uint32_t base_s = smem_u32(smem_raw);
-    uint8_t* ring = smem_raw + (((base_s + 1023u) & ~1023u) - base_s);
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * C::kStageBytes);
-    uint64_t* empty = full + STAGES;
-    const uint32_t nload = (msg_len + 63u) >> 6;
-
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kWsComputeWarps);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    if (warp == kWsComputeWarps) {  // ---------------- producer warp
-        if (lane == 0) {
-            prefetch_tmap(&tmap);
-            uint32_t s = 0, ph = 0;
-            for (uint32_t b = 0; b < nload; ++b) {
-                if (b >= (uint32_t)STAGES) mbar_wait_parity(&empty[s], ph ^ 1u);
-                mbar_arrive_expect_tx(&full[s], C::kStageBytes);
-                tma_load_2d(ring + s * C::kStageBytes, &tmap, &full[s], (int)(b * 64u), (int)row0);
-                if (++s == (uint32_t)STAGES) { s = 0; ph ^= 1u; }
-            }
-        }
-        return;
-    }
-
-    // ------------------------------------------------- compute warps
-    // Thread (warp, lane) owns tile rows warp*32 + lane + 128*q, q < NB.
-    uint32_t st[NB][H::kStateWords];
-#pragma unroll
-    for (int q = 0; q < NB; ++q) H::init(st[q]);
-    const uint32_t row = warp * 32u + lane;  // row inside the tile (q = 0)
-    const uint32_t swz = (row >> 1) & 3u;    // SWIZZLE_64B (same for row + 128q)
-    uint32_t choff[NB][4];
-#pragma unroll
-    for (int q = 0; q < NB; ++q)
-#pragma unroll
-        for (uint32_t c = 0; c < 4; ++c) choff[q][c] = smem_u32(ring) + (row + 128u * q) * 64u + ((c ^ swz) << 4);
-    uint32_t raw[NB][16];
-    auto read_stage = [&](uint32_t s) {
-        const uint32_t sbase = s * C::kStageBytes;
-#pragma unroll
-        for (int q = 0; q < NB; ++q) {
-#pragma unroll
-            for (uint32_t c = 0; c < 4; ++c) {
-                uint32_t x, y, z, w;
-                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
-                             : "r"(choff[q][c] + sbase)
-                             : "memory");
-                raw[q][4 * c + 0] = x; raw[q][4 * c + 1] = y; raw[q][4 * c + 2] = z; raw[q][4 * c + 3] = w;
-            }
-        }
-    };
-    const uint32_t nfull = msg_len >> 6;
-    uint32_t s = 0, ph = 0;
-    for (uint32_t b = 0; b < nfull; ++b) {
-        mbar_wait_parity(&full[s], ph);
-        read_stage(s);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
-        H::template compress_n<NB>(st, raw);
-        if (++s == (uint32_t)STAGES) { s = 0; ph ^= 1u; }
-    }
-    const uint32_t r = msg_len & 63u;
-    if (r) {
-        mbar_wait_parity(&full[s], ph);
-        read_stage(s);
-    } else {
-#pragma unroll
-        for (int q = 0; q < NB; ++q)
-#pragma unroll
-            for (int j = 0; j < 16; ++j) raw[q][j] = 0u;
-    }
-    md_finish_n<ALG, V, NB>(st, raw, r, msg_len);
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-        const uint32_t grow = row0 + row + 128u * q;
-        if (grow < n) store_digest<ALG>(out + (uint64_t)grow * H::kDigestBytes, st[q]);
-    }
-}
-
-// =========================================================================
-// Fixed-width direct-load kernel (HB_FLAG_NO_TMA; 16B-aligned rows only).
-// Kept as the A/B baseline for the TMA staging: each thread streams its own
-// row with 128-bit read-only loads.
-// =========================================================================
-template <int ALG>
-__global__ void __launch_bounds__(128, (TmaOcc<ALG, 1, 3>::kMinCtas))
-k_fixed_direct(const uint8_t* __restrict__ msgs, uint64_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG>;
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint4* p = reinterpret_cast<const uint4*>(msgs + i * msg_len);
-    uint32_t st[H::kStateWords];
-    H::init(st);
-    const uint32_t nfull = msg_len >> 6;
-    for (uint32_t b = 0; b < nfull; ++b) {
-        uint32_t raw[16];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const uint4 v = __ldg(p + 4 * b + c);
-            raw[4 * c + 0] = v.x; raw[4 * c + 1] = v.y; raw[4 * c + 2] = v.z; raw[4 * c + 3] = v.w;
-        }
-        compress1<ALG>(st, raw);
-    }
-    const uint32_t r = msg_len & 63u;
-    uint32_t raw[16];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if ((uint32_t)(16 * c) < r) v = __ldg(p + 4 * nfull + c);  // r is a multiple of 16 here
-        raw[4 * c + 0] = v.x; raw[4 * c + 1] = v.y; raw[4 * c + 2] = v.z; raw[4 * c + 3] = v.w;
-    }
-    md_finish<ALG>(st, raw, r, msg_len);
-    store_digest<ALG>(out + i * H::kDigestBytes, st);
-}
-
-// -------------------------------------------------------------------------
-// Short fixed-width messages, width known at compile time (L in {16, 32, 48,
-// 64, 128}: the powers of two of the configs[4] sweep below 256 B, plus 48).
-// One message per thread, L/16 LDG.128 loads; the padding words (0x80, zero
-// fill, bit length) are immediates, so the last block costs nothing beyond
-// its compression (the generic direct kernel places them with select chains,
-// a visible share of a single-block MD5 message).
-// -------------------------------------------------------------------------
-__host__ __device__ constexpr uint32_t bswap_c(uint32_t x) {
-    return (x >> 24) | ((x >> 8) & 0xFF00u) | ((x << 8) & 0xFF0000u) | (x << 24);
-}
-
-template <int ALG, int L>
-__global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__ msgs, uint64_t n,
-                                                     uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG>;
-    static_assert(L % 16 == 0 && L >= 16 && L <= 128, "width");
-    constexpr int kNb = (L + 8) / 64 + 1;  // blocks including padding
-    constexpr uint64_t kBits = (uint64_t)L * 8u;
-    constexpr uint32_t kL14 = H::kBigEndian ? bswap_c((uint32_t)(kBits >> 32)) : (uint32_t)kBits;
-    constexpr uint32_t kL15 = H::kBigEndian ? bswap_c((uint32_t)kBits) : (uint32_t)(kBits >> 32);
-    const uint64_t i = (uint64_t)blockIdx.x * 128u + threadIdx.x;
-    if (i >= n) return;
-    const uint4* p = reinterpret_cast<const uint4*>(msgs + i * L);
-    uint32_t w[L / 4];
-#pragma unroll
-    for (int c = 0; c < L / 16; ++c) {
-        const uint4 v = __ldg(p + c);
-        w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
-    }
-    uint32_t st[H::kStateWords];
-    H::init(st);
-#pragma unroll
-    for (int b = 0; b < kNb; ++b) {
-        uint32_t raw[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int pos = 64 * b + 4 * j;  // _pad: data, 0x80, zeros, 64-bit bit length
-            raw[j] = pos < L ? w[pos / 4] : pos == L ? 0x80u : 0u;
-        }
-        if (b == kNb - 1) { raw[14] = kL14; raw[15] = kL15; }
-        compress1<ALG>(st, raw);
-    }
-    store_digest<ALG>(out + i * H::kDigestBytes, st);
-}
-
-// =========================================================================
-// Generic kernel: any width / alignment, and variable length.
-// Message bytes are fetched as aligned 32-bit words and realigned with one
-// funnel shift per word; the tail is masked and padded in registers.
-// For variable length, `perm` (optional) is a length-descending permutation
-// so the 32 lanes of a warp run (nearly) the same number of blocks.
-// =========================================================================
-__device__ __forceinline__ void load_block_unaligned(const uint8_t* p, const uint8_t* end, uint32_t raw[16]) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    const uint32_t* q = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
-    const uint32_t sh = (uint32_t)(a & 3u) * 8u;
-    uint32_t c[17];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) c[k] = __ldg(q + k);
-    c[16] = (sh != 0u && reinterpret_cast<const uint8_t*>(q + 16) < end) ? __ldg(q + 16) : 0u;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) raw[j] = __funnelshift_r(c[j], c[j + 1], sh);
-}
-
-__device__ __forceinline__ void load_partial_unaligned(const uint8_t* p, uint32_t r, uint32_t raw[16]) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    const uint32_t* q = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
-    const uint32_t sh = (uint32_t)(a & 3u) * 8u;
-    const uint8_t* e = p + r;
-    uint32_t c[17];
-#pragma unroll
-    for (int k = 0; k < 17; ++k) c[k] = (reinterpret_cast<const uint8_t*>(q + k) < e) ? __ldg(q + k) : 0u;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) raw[j] = __funnelshift_r(c[j], c[j + 1], sh);
-    mask_tail(raw, r);
-}
-
-template <int ALG, bool VARLEN>
-__global__ void __launch_bounds__(128)
-k_generic(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
-          uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t msg_len, uint64_t n,
-          uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG>;
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const uint64_t i = (VARLEN && perm) ? (uint64_t)perm[t] : t;
-    uint64_t start, len;
-    if (VARLEN) {
-        start = offsets[i] - offset_base;
-        len = offsets[i + 1] - offsets[i];
-    } else {
-        start = i * msg_len;
-        len = msg_len;
-    }
-    const uint8_t* p = data + start;
-    uint32_t st[H::kStateWords];
-    H::init(st);
-    const uint64_t nfull = len >> 6;
-    for (uint64_t b = 0; b < nfull; ++b) {
-        uint32_t raw[16];
-        load_block_unaligned(p + 64 * b, data_end, raw);
-        compress1<ALG>(st, raw);
-    }
-    uint32_t raw[16];
-    load_partial_unaligned(p + 64 * nfull, (uint32_t)(len & 63u), raw);
-    md_finish<ALG>(st, raw, (uint32_t)(len & 63u), len);
-    store_digest<ALG>(out + i * H::kDigestBytes, st);
-}
-
-// -------------------------------------------------------------------------
-// Variable-length kernel: per message, 128-bit read-only loads of the 16-byte
-// aligned window around each block (4-5 LDG.128 instead of 17 LDG.32), then a
-// realignment by the message's byte offset a%16: a word select by q=(a>>2)&3
-// (a switch that is warp-uniform because the length sort also groups messages
-// by q) and one funnel shift per word by (a%4)*8.
-// -------------------------------------------------------------------------
-__device__ __forceinline__ void realign16(const uint32_t (&c)[20], uint32_t q, uint32_t sh, uint32_t (&raw)[16]) {
-#define HB_RA(Q)                                                                    \
-    _Pragma("unroll") for (int j = 0; j < 16; ++j) raw[j] = __funnelshift_r(c[j + Q], c[j + Q + 1], sh);
-    switch (q) {
-    case 0: HB_RA(0) break;
-    case 1: HB_RA(1) break;
-    case 2: HB_RA(2) break;
-    default: HB_RA(3) break;
-    }
-#undef HB_RA
-}
-
-template <int ALG>
-__global__ void __launch_bounds__(128)
-k_varlen16(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offsets, uint64_t offset_base,
-           const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG>;
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const uint64_t i = perm ? (uint64_t)perm[t] : t;
-    const uint64_t start = offsets[i] - offset_base;
-    const uint64_t len = offsets[i + 1] - offsets[i];
-    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
-    const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
-    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
-    const bool misaligned = (a & 15u) != 0;
-    uint32_t st[H::kStateWords];
-    H::init(st);
-    uint32_t c[20];
-    uint32_t raw[16];
-    const uint64_t nfull = len >> 6;
-    for (uint64_t b = 0; b < nfull; ++b) {
-        const uint4* src = w16 + 4 * b;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint4 v = __ldg(src + k);
-            c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
-        }
-        uint4 v4 = make_uint4(0, 0, 0, 0);
-        if (misaligned) v4 = __ldg(src + 4);
-        c[16] = v4.x; c[17] = v4.y; c[18] = v4.z; c[19] = v4.w;
-        realign16(c, q, sh, raw);
-        compress1<ALG>(st, raw);
-    }
-    // tail: the r = len % 64 remaining bytes (chunks that overlap [p, p+r) only)
-    const uint32_t r = (uint32_t)(len & 63u);
-    const uintptr_t tail_end = a + len;
-    const uint4* src = w16 + 4 * nfull;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (reinterpret_cast<uintptr_t>(src + k) < tail_end) v = __ldg(src + k);
-        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
-    }
-    realign16(c, q, sh, raw);
-    mask_tail(raw, r);
-    md_finish<ALG>(st, raw, r, len);
-    store_digest<ALG>(out + i * H::kDigestBytes, st);
-}
-
-// -------------------------------------------------------------------------
-// Variable-length kernel, warp-cooperative staging (the default).
-//
-// A warp owns 32 messages (after the length sort: equal block counts and the
-// same word alignment).  Per 64-byte step every message needs the 80-byte
-// 16-aligned window around its block: 32 x 5 = 160 16-byte chunks.  Lane l
-// copies chunks c = l + 32j (j < 5) -- message c/5, chunk c%5 -- with
-// cp.async (zero-filled past the message end), so five consecutive lanes
-// fetch one message's 80 contiguous bytes: each warp instruction touches ~7
-// messages instead of 32 (per-thread LDG.128 touches 32 lines per
-// instruction and the L1 tag stage, not HBM, was the limit for MD5).  Chunks
-// land in a STAGES-deep per-warp ring (slot m at m*80: conflict-free
-// LDS.128 reads); the owner lane realigns its window (word select + funnel
-// shift) and compresses.  Padding is applied in registers on the last one
-// or two blocks (bytes past the end arrive as zeros), so there is one
-// compress call site and the loop runs to the warp's largest block count.
-// -------------------------------------------------------------------------
-constexpr int kVcWarps = 4;
-constexpr int kVcSlot = 80;                   // bytes per message per stage
-constexpr int kVcWarpStage = 32 * kVcSlot;    // 2,560 bytes
-
-// STAGES-deep ring (smem 10 KiB per stage per CTA), MINB CTAs/SM register
-// target, PF = L2 prefetch size of the cp.async copies.
-template <int ALG, int STAGES = 4, int MINB = 5, int PF = 256>
-__global__ void __launch_bounds__(kVcWarps * 32, MINB)
-k_varlen_coop(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offsets, uint64_t offset_base,
-              const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG>;
-    __shared__ __align__(128) uint8_t ring[kVcWarps][STAGES][kVcWarpStage];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t wbase = ((uint64_t)blockIdx.x * kVcWarps + warp) * 32u;
-    if (wbase >= n) return;  // warp-uniform
-    const uint64_t t = wbase + lane;
-    const bool live = t < n;
-    uint64_t i = 0, len = 0;
-    uintptr_t a = reinterpret_cast<uintptr_t>(data);
-    if (live) {
-        i = perm ? (uint64_t)perm[t] : t;
-        a = reinterpret_cast<uintptr_t>(data + (offsets[i] - offset_base));
-        len = offsets[i + 1] - offsets[i];
-    }
-    const uint32_t nb = live ? (uint32_t)((len + 8u) / 64u + 1u) : 0u;   // blocks incl. padding
-    const uint32_t nfull = (uint32_t)(len >> 6);
-    const uint32_t nbmax = __reduce_max_sync(0xFFFFFFFFu, nb);
-
-    // This lane's five copy slots: source message m = c/5, chunk k = c%5.
-    uintptr_t src0[5];
-    int64_t avail0[5];  // bytes of the chunk inside the message at step 0 (minus 64 per step)
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-        const uint32_t c = lane + 32u * j, m = c / 5u, k = c % 5u;
-        const uintptr_t am = __shfl_sync(0xFFFFFFFFu, a, m);
-        const uint64_t lm = __shfl_sync(0xFFFFFFFFu, len, m);
-        src0[j] = (am & ~uintptr_t(15)) + 16u * k;
-        const bool need = (k < 4u) || (am & 15u);  // chunk 4 only for a misaligned window
-        avail0[j] = (need && lm) ? (int64_t)lm + (int64_t)(am & 15u) - 16 * (int64_t)k : INT64_MIN / 2;
-    }
-    uint8_t* wring = &ring[warp][0][0];
-    const uint32_t sring = smem_u32(wring);
-    auto issue = [&](uint32_t b) {
-        const uint32_t sdst = sring + (b % STAGES) * kVcWarpStage;
-#pragma unroll
-        for (int j = 0; j < 5; ++j) {
-            const int64_t av = avail0[j] - 64 * (int64_t)b;
-            const uint32_t sz = av <= 0 ? 0u : av >= 16 ? 16u : (uint32_t)av;
-            const uintptr_t src = sz ? src0[j] + 64u * (uintptr_t)b : reinterpret_cast<uintptr_t>(data);
-            cp_async16_zfill<PF>(sdst + 16u * (lane + 32u * j), reinterpret_cast<const void*>(src), sz);
-        }
-    };
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if ((uint32_t)s < nbmax) issue(s);
-        cp_async_commit();
-    }
-
-    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
-    const uint32_t r = (uint32_t)(len & 63u);
-    const uint64_t bits = len * 8ull;
-    const uint32_t l14 = H::kBigEndian ? bswap((uint32_t)(bits >> 32)) : (uint32_t)bits;
-    const uint32_t l15 = H::kBigEndian ? bswap((uint32_t)bits) : (uint32_t)(bits >> 32);
-    uint32_t st[H::kStateWords];
-    H::init(st);
-    const uint32_t slot = smem_u32(wring) + lane * kVcSlot;
-    for (uint32_t b = 0; b < nbmax; ++b) {
-        if (b + STAGES - 1 < nbmax) issue(b + STAGES - 1);
-        cp_async_commit();
-        cp_async_wait<STAGES - 1>();  // this lane's copies of step b have landed
-        __syncwarp();                    // ... and every other lane's
-        uint32_t c[20];
-        const uint32_t sbase = slot + (b % STAGES) * kVcWarpStage;
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            uint32_t x, y, z, w;
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
-                         : "r"(sbase + 16u * k)
-                         : "memory");
-            c[4 * k] = x; c[4 * k + 1] = y; c[4 * k + 2] = z; c[4 * k + 3] = w;
-        }
-        __syncwarp();  // the stage may be refilled from the next iteration on
-        if (b < nb) {
-            uint32_t raw[16];
-            realign16(c, q, sh, raw);
-            if (b >= nfull) {  // the final one or two blocks: 0x80, zero fill, bit length
-                if (b == nfull) {
-                    const uint32_t pad = 0x80u << ((r & 3u) * 8u), pw = r >> 2;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) raw[j] |= (pw == (uint32_t)j) ? pad : 0u;
-                }
-                if (b == nb - 1u) { raw[14] = l14; raw[15] = l15; }
-            }
-            compress1<ALG>(st, raw);
-        }
-    }
-    if (live) store_digest<ALG>(out + i * H::kDigestBytes, st);
-}
-
-// ---------------------------------------------------- length-bucket sort --
-// Counting sort of message indices by block count, longest first.  Three
-// small kernels: per-CTA shared-memory histograms -> global histogram, one
-// exclusive scan, per-CTA reservation + scatter.  Order inside a bucket is
-// irrelevant (digests are written to out[i]).
-// 1024 block-count classes (longest first; >= 1023 blocks share the first)
-// x 4 word-alignment classes q = (address >> 2) & 3, so a warp's messages
-// have similar lengths AND the same realignment path in k_varlen16.
-constexpr int kSortNbClasses = 1024;
-constexpr int kSortBuckets = kSortNbClasses * 4;
-constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;  // per thread
-
-__device__ __forceinline__ uint32_t sort_bucket(const uint64_t* offsets, uint64_t i, uint64_t addr_bias) {
-    const uint64_t len = offsets[i + 1] - offsets[i];
-    const uint64_t nb = (len + 8u) / 64u + 1u;
-    const uint64_t c = nb < (uint64_t)(kSortNbClasses - 1) ? nb : (uint64_t)(kSortNbClasses - 1);
-    const uint32_t q = (uint32_t)((offsets[i] + addr_bias) >> 2) & 3u;
-    return ((uint32_t)(kSortNbClasses - 1) - (uint32_t)c) * 4u + q;
-}
 
 __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __restrict__ offsets, uint64_t n,
                                                             uint64_t addr_bias, uint32_t* __restrict__ hist) {
@@ -748,334 +166,18 @@ __global__ void __launch_bounds__(1024) k_sort_window(const uint64_t* __restrict
         if (key[it] != 0xFFFFFFFFu) perm[w0 + h[key[it]] + rank[it]] = (uint32_t)(w0 + (uint64_t)it * 1024u + t);
 }
 
-// ------------------------------------------------------- synthetic bytes --
-__device__ __forceinline__ uint64_t mix64(uint64_t seed, uint64_t idx) {  // == oracle mix64
-    uint64_t z = (idx + 1ull) * 0x9E3779B97F4A7C15ull + seed * 0xD1B54A32D192ED03ull;
-    z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
-    z ^= z >> 27; z *= 0x94D049BB133111EBull;
-    z ^= z >> 31;
-    return z;
-}
-
-__global__ void k_fill_random(uint8_t* __restrict__ buf, uint64_t nbytes, uint64_t seed, uint64_t w0) {
-    const uint64_t nwords = (nbytes + 7) / 8;
-    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
-         w += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t v = mix64(seed, w0 + w);
-        if (8 * w + 8 <= nbytes) {
-            reinterpret_cast<uint64_t*>(buf)[w] = v;
-        } else {
-            for (uint64_t k = 0; 8 * w + k < nbytes; ++k) buf[8 * w + k] = (uint8_t)(v >> (8 * k));
-        }
-    }
-}
-
-// -------------------------------------------- decimal messages in-register --
-// gen_messages (batch.py:86-99): message i is the zero-padded decimal
-// rendering of start+i, WIDTH bytes.  The bytes are built in registers and
-// hashed directly; only digests touch HBM.
-template <int ALG, int WIDTH>
-__global__ void __launch_bounds__(128) k_decimal(uint64_t start, uint64_t count, uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG>;
-    static_assert(WIDTH >= 1 && WIDTH <= 20, "width");
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= count) return;
-    uint64_t v = start + i;
-    uint32_t raw[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) raw[j] = 0u;
-#pragma unroll
-    for (int pos = WIDTH - 1; pos >= 0; --pos) {  // batch.py:96-98
-        const uint32_t d = (uint32_t)(v % 10u);
-        v /= 10u;
-        raw[pos >> 2] |= (0x30u + d) << ((pos & 3) * 8);
-    }
-    uint32_t st[H::kStateWords];
-    H::init(st);
-    md_finish<ALG>(st, raw, (uint32_t)WIDTH, (uint64_t)WIDTH);
-    store_digest<ALG>(out + i * H::kDigestBytes, st);
-}
-
-__global__ void k_gen_decimal(uint64_t start, uint64_t count, int width, uint8_t* __restrict__ out) {
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= count) return;
-    uint64_t v = start + i;
-    for (int pos = width - 1; pos >= 0; --pos) {
-        out[i * (uint64_t)width + pos] = (uint8_t)('0' + v % 10u);
-        v /= 10u;
-    }
-}
-
-// =========================================================================
-// Host-side launchers
-// =========================================================================
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static PFN_encodeTiled get_encode_tiled() {
-    static PFN_encodeTiled fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_encodeTiled>(p);
-    });
-    return fn;
-}
-
-static thread_local char g_tma_err[160];
-const char* tma_error() { return g_tma_err; }
-
-template <int ALG, int V, int NB, int STAGES, int W = kTmaWarps>
-static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
-                                        cudaStream_t stream) {
-    using C = TmaCfg<NB, STAGES, W>;
-    PFN_encodeTiled enc = get_encode_tiled();
-    if (!enc) {
-        snprintf(g_tma_err, sizeof g_tma_err, "cuTensorMapEncodeTiled unavailable");
-        return cudaErrorNotSupported;
-    }
-    // The (n, L) byte matrix as a 2-D tensor: dim0 = bytes of a row (contiguous),
-    // dim1 = rows with stride L.  Box = one 64-byte block of kRows rows.
-    CUtensorMap map;
-    const cuuint64_t dims[2] = {L, n};
-    const cuuint64_t strides[1] = {L};
-    const cuuint32_t box[2] = {64, (cuuint32_t)C::kRows};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult rc = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_msgs), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (rc != CUDA_SUCCESS) {
-        snprintf(g_tma_err, sizeof g_tma_err, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)rc);
-        return cudaErrorInvalidValue;
-    }
-    static std::once_flag attr_once;
-    static cudaError_t attr_rc = cudaSuccess;
-    std::call_once(attr_once, [] {
-        attr_rc = cudaFuncSetAttribute(k_fixed_tma<ALG, V, NB, STAGES, W>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    });
-    if (attr_rc != cudaSuccess) return attr_rc;
-    const uint32_t rows_per_cta = W * C::kRows;
-    const uint32_t grid = (n + rows_per_cta - 1) / rows_per_cta;
-    k_fixed_tma<ALG, V, NB, STAGES, W><<<grid, W * 32, C::kSmem, stream>>>(map, n, L, d_out);
-    note_launches(1);
-    return cudaGetLastError();
-}
-
-template <int ALG, int V, int NB, int STAGES>
-static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
-                                       cudaStream_t stream) {
-    using C = WsCfg<NB, STAGES>;
-    PFN_encodeTiled enc = get_encode_tiled();
-    if (!enc) {
-        snprintf(g_tma_err, sizeof g_tma_err, "cuTensorMapEncodeTiled unavailable");
-        return cudaErrorNotSupported;
-    }
-    CUtensorMap map;
-    const cuuint64_t dims[2] = {L, n};
-    const cuuint64_t strides[1] = {L};
-    const cuuint32_t box[2] = {64, (cuuint32_t)C::kRows};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult rc = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_msgs), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (rc != CUDA_SUCCESS) {
-        snprintf(g_tma_err, sizeof g_tma_err, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)rc);
-        return cudaErrorInvalidValue;
-    }
-    static std::once_flag attr_once;
-    static cudaError_t attr_rc = cudaSuccess;
-    std::call_once(attr_once, [] {
-        attr_rc = cudaFuncSetAttribute(k_fixed_tma_ws<ALG, V, NB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       C::kSmem);
-    });
-    if (attr_rc != cudaSuccess) return attr_rc;
-    const uint32_t grid = (n + C::kRows - 1) / C::kRows;
-    k_fixed_tma_ws<ALG, V, NB, STAGES><<<grid, (kWsComputeWarps + 1) * 32, C::kSmem, stream>>>(map, n, L, d_out);
-    note_launches(1);
-    return cudaGetLastError();
-}
-
-// Tile configuration and round variant.  Defaults are the B200-measured best
-// (profiles/variant_sweep_r1*.txt); $HB_TMA_CFG ("1x3", "2x2", "2x3" =
-// messages-per-thread x ring stages) and $HB_VARIANT (0-3) override them for
-// A/B experiments.
-enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4, kCfg1x2 = 5, kCfgWs2x2 = 6, kCfgWs3x2 = 7 };
-// B200-measured (profiles/variant_sweep_r1d.txt and _r1e.txt, interleaved
-// rounds): the warp-specialised 3-stage ring is best for MD5 and SM3 (SM3's
-// 61 registers make two messages per thread lose occupancy); SHA-1 gains 4 %
-// from two messages per thread (ws3x2: 7.38 vs 7.69 ms at 2^24 x 1 KiB).
-template <int ALG> struct DefaultTmaCfg { static constexpr int value = ALG == kSha1 ? kCfgWs3x2 : kCfgWs3; };
-
-static int tma_variant(int alg) {
-    const char* v = getenv("HB_VARIANT");
-    if (v && *v >= '0' && *v <= '3' && v[1] == '\0') return *v - '0';
-    switch (alg) {
-    case kSha1: return DefaultVariant<kSha1>::value;
-    case kMd5: return DefaultVariant<kMd5>::value;
-    default: return DefaultVariant<kSm3>::value;
-    }
-}
-
-static int tma_cfg(int alg) {
-    const char* v = getenv("HB_TMA_CFG");
-    if (v && !strcmp(v, "1x3")) return kCfg1x3;
-    if (v && !strcmp(v, "2x2")) return kCfg2x2;
-    if (v && !strcmp(v, "2x3")) return kCfg2x3;
-    if (v && !strcmp(v, "ws2")) return kCfgWs2;
-    if (v && !strcmp(v, "1x2")) return kCfg1x2;
-    if (v && !strcmp(v, "ws3")) return kCfgWs3;
-    if (v && !strcmp(v, "ws2x2")) return kCfgWs2x2;
-    if (v && !strcmp(v, "ws3x2")) return kCfgWs3x2;
-    switch (alg) {
-    case kSha1: return DefaultTmaCfg<kSha1>::value;
-    case kMd5: return DefaultTmaCfg<kMd5>::value;
-    default: return DefaultTmaCfg<kSm3>::value;
-    }
-}
-
-// Shape selection by batch geometry (B200-measured, profiles/ab_small_r1.txt):
-//  * fewer than $HB_SMALL_N (default 2^18) messages: one message per thread
-//    (NB=1) so the grid still covers all SMs -- SHA-1's tuned NB=2 tiles
-//    halve the CTA count (4096 x 64 KiB: 251 vs 428 GB/s);
-//  * messages of <= $HB_DIRECT_MAX_L (default 128) bytes: the direct
-//    per-thread-load kernel (one or two blocks per message, the 8 KiB TMA
-//    stage would be mostly padding: MD5 2^24 x 16 B 1121 vs 683 GB/s).
-static uint64_t env_u64(const char* name, uint64_t dflt) {
-    const char* v = getenv(name);
-    return v ? strtoull(v, nullptr, 10) : dflt;
-}
-static uint64_t small_n_threshold() { return env_u64("HB_SMALL_N", 1ull << 18); }
-static uint64_t direct_max_len() { return env_u64("HB_DIRECT_MAX_L", 128); }
-
-template <int ALG>
-static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t L, uint8_t* dst, cudaStream_t s) {
-    const int cfg = tma_cfg(ALG);
-    const int v = tma_variant(ALG);
-    if (!getenv("HB_TMA_CFG") && (uint64_t)n < small_n_threshold())
-        return launch_fixed_tma_ws<ALG, DefaultVariant<ALG>::value, 1, 3>(src, n, L, dst, s);
-    if (cfg == kCfg1x2) {
-        switch (v) {
-        case 0: return launch_fixed_tma_alg<ALG, 0, 1, 2>(src, n, L, dst, s);
-        default: return launch_fixed_tma_alg<ALG, 1, 1, 2>(src, n, L, dst, s);
-        }
-    }
-    if (cfg == kCfgWs2) {
-        switch (v) {
-        case 0: return launch_fixed_tma_ws<ALG, 0, 1, 2>(src, n, L, dst, s);
-        default: return launch_fixed_tma_ws<ALG, 1, 1, 2>(src, n, L, dst, s);
-        }
-    }
-    if (cfg == kCfgWs3) {
-        switch (v) {
-        case 0: return launch_fixed_tma_ws<ALG, 0, 1, 3>(src, n, L, dst, s);
-        default: return launch_fixed_tma_ws<ALG, 1, 1, 3>(src, n, L, dst, s);
-        }
-    }
-    if (cfg == kCfgWs2x2) {
-        switch (v) {
-        case 3: return launch_fixed_tma_ws<ALG, 3, 2, 2>(src, n, L, dst, s);
-        default: return launch_fixed_tma_ws<ALG, 1, 2, 2>(src, n, L, dst, s);
-        }
-    }
-    if (cfg == kCfgWs3x2) {
-        switch (v) {
-        case 3: return launch_fixed_tma_ws<ALG, 3, 2, 3>(src, n, L, dst, s);
-        default: return launch_fixed_tma_ws<ALG, 1, 2, 3>(src, n, L, dst, s);
-        }
-    }
-    if (cfg == kCfg2x2) {
-        switch (v) {
-        case 0: return launch_fixed_tma_alg<ALG, 0, 2, 2>(src, n, L, dst, s);
-        case 2: return launch_fixed_tma_alg<ALG, 2, 2, 2>(src, n, L, dst, s);
-        default: return launch_fixed_tma_alg<ALG, 1, 2, 2>(src, n, L, dst, s);
-        }
-    }
-    if (cfg == kCfg2x3) {
-        switch (v) {
-        case 0: return launch_fixed_tma_alg<ALG, 0, 2, 3>(src, n, L, dst, s);
-        case 2: return launch_fixed_tma_alg<ALG, 2, 2, 3>(src, n, L, dst, s);
-        default: return launch_fixed_tma_alg<ALG, 1, 2, 3>(src, n, L, dst, s);
-        }
-    }
-    switch (v) {
-    case 0: return launch_fixed_tma_alg<ALG, 0, 1, 3>(src, n, L, dst, s);
-    case 2: return launch_fixed_tma_alg<ALG, 2, 1, 3>(src, n, L, dst, s);
-    case 3: return launch_fixed_tma_alg<ALG, 3, 1, 3>(src, n, L, dst, s);
-    default: return launch_fixed_tma_alg<ALG, 1, 1, 3>(src, n, L, dst, s);
-    }
-}
-
-template <int ALG>
-static cudaError_t launch_fixed_alg(const uint8_t* d_msgs, uint64_t n, uint64_t L, uint8_t* d_out,
-                                    cudaStream_t stream, uint32_t flags) {
-    using H = HashAlg<ALG>;
-    const bool aligned = L > 0 && (L % 16) == 0 && (reinterpret_cast<uintptr_t>(d_msgs) % 16) == 0 &&
-                         L < (1ull << 31);
-    const bool direct = (flags & HB_FLAG_NO_TMA) || (!getenv("HB_TMA_CFG") && L <= direct_max_len());
-    if (aligned && !direct) {
-        // TMA coordinates are int32: split very large batches into row slabs.
-        const uint64_t slab = 1ull << 30;
-        for (uint64_t r0 = 0; r0 < n; r0 += slab) {
-            const uint64_t rn = (n - r0) < slab ? (n - r0) : slab;
-            const uint8_t* src = d_msgs + r0 * L;
-            uint8_t* dst = d_out + r0 * H::kDigestBytes;
-            const cudaError_t e = launch_tma_dispatch<ALG>(src, (uint32_t)rn, (uint32_t)L, dst, stream);
-            if (e != cudaSuccess) return e;
-        }
-        return cudaSuccess;
-    }
-    const uint64_t grid = (n + 127) / 128;
-    const bool small_ok = aligned && !getenv("HB_NO_SMALL_KERNEL");
-    if (small_ok && L == 16) {
-        k_fixed_small<ALG, 16><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
-    } else if (small_ok && L == 32) {
-        k_fixed_small<ALG, 32><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
-    } else if (small_ok && L == 48) {
-        k_fixed_small<ALG, 48><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
-    } else if (small_ok && L == 64) {
-        k_fixed_small<ALG, 64><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
-    } else if (small_ok && L == 128) {
-        k_fixed_small<ALG, 128><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
-    } else if (aligned) {
-        k_fixed_direct<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, (uint32_t)L, d_out);
-    } else {
-        k_generic<ALG, false><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, d_msgs + n * L, nullptr, 0, nullptr, L, n,
-                                                                  d_out);
-    }
-    note_launches(1);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_fixed(int alg, const uint8_t* d_msgs, uint64_t n, uint64_t msg_len, uint8_t* d_out,
-                         cudaStream_t stream, uint32_t flags) {
-    if (n == 0) return cudaSuccess;
-    switch (alg) {
-    case kSha1: return launch_fixed_alg<kSha1>(d_msgs, n, msg_len, d_out, stream, flags);
-    case kMd5: return launch_fixed_alg<kMd5>(d_msgs, n, msg_len, d_out, stream, flags);
-    case kSm3: return launch_fixed_alg<kSm3>(d_msgs, n, msg_len, d_out, stream, flags);
-    default: return cudaErrorInvalidValue;
-    }
-}
-
-uint64_t varlen_scratch_bytes(uint64_t n) { return (uint64_t)kSortBuckets * 4u + n * 4u + 256u; }
-
-template <int ALG>
-static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes, const uint64_t* d_offsets,
-                                     uint64_t offset_base, uint64_t n, uint8_t* d_out, void* d_scratch,
-                                     cudaStream_t stream, uint32_t flags) {
+// Length/alignment-bucket permutation for the varlen kernels (null when not
+// sorting).  Shared by the per-algorithm translation units.
+cudaError_t launch_varlen_sort(int alg, const uint8_t* d_data, const uint64_t* d_offsets, uint64_t offset_base,
+                               uint64_t n, void* d_scratch, cudaStream_t stream, uint32_t flags,
+                               const uint32_t** perm_out) {
     const uint32_t* perm = nullptr;
     const uint64_t bias0 = reinterpret_cast<uintptr_t>(d_data) - offset_base;  // address = offsets[i] + bias
     // Sort mode: windowed for MD5 (HBM-bound: locality wins), global for SHA-1/SM3
     // (ALU-bound: full (block count, alignment) uniformity wins); B200 A/B in
     // profiles/ab_varlen_r1b.txt.  $HB_VARLEN_SORT = window | global, $HB_SORT_WINDOW.
     const char* sm = getenv("HB_VARLEN_SORT");
-    const bool window = sm ? strcmp(sm, "global") != 0 : ALG == kMd5;
+    const bool window = sm ? strcmp(sm, "global") != 0 : alg == kMd5;
     if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch && window) {
         uint32_t* p = static_cast<uint32_t*>(d_scratch) + kSortBuckets;
         const uint64_t w = env_u64("HB_SORT_WINDOW", 8192);
@@ -1101,37 +203,87 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
         note_launches(3);
         perm = p;
     }
-    const uint64_t grid = (n + 127) / 128;
-    if (flags & HB_FLAG_VARLEN_WORDS) {  // A/B baseline: per-thread 32-bit loads
-        k_generic<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets,
-                                                                 offset_base, perm, 0, n, d_out);
-    } else if ((flags & HB_FLAG_VARLEN_COOP) && data_bytes < (1ull << 37)) {  // block counts fit u32
-        // Opt-in.  It beat the per-thread kernel for MD5 under the global sort
-        // (2.38 vs 4.36 ms at configs[3]) because its coalesced staging hid the
-        // scattered reads; with the windowed sort the per-thread kernel reads
-        // neighbouring messages together and wins (2.24 vs 2.85 ms).
-        const uint64_t g = (n + kVcWarps * 32 - 1) / (kVcWarps * 32);
-        // A/B knobs: $HB_VC_STAGES (ring depth; 4 -> 5 CTAs/SM by smem, 3 -> 7), $HB_VC_PF (L2 prefetch).
-        // B200 (profiles/ab_varlen_r1.txt): MD5 best at 3 stages (2.52 vs 2.62 ms for 4), 256 B prefetch.
-        const int stages = (int)env_u64("HB_VC_STAGES", ALG == kMd5 ? 3 : 4), pf = (int)env_u64("HB_VC_PF", 256);
-        const unsigned gg = (unsigned)g;
-        constexpr int T = kVcWarps * 32;
-        if (stages == 3)
-            k_varlen_coop<ALG, 3, 7, 256><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
-        else if (stages == 2)
-            k_varlen_coop<ALG, 2, 8, 256><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
-        else if (pf == 128)
-            k_varlen_coop<ALG, 4, 5, 128><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
-        else if (pf == 0)
-            k_varlen_coop<ALG, 4, 5, 0><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
-        else
-            k_varlen_coop<ALG, 4, 5, 256><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
-    } else {  // A/B baseline: per-thread 128-bit loads
-        k_varlen16<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
-    }
-    note_launches(1);
+    *perm_out = perm;
     return cudaGetLastError();
 }
+
+// ------------------------------------------------------- synthetic bytes --
+__device__ __forceinline__ uint64_t mix64(uint64_t seed, uint64_t idx) {  // == oracle mix64
+    uint64_t z = (idx + 1ull) * 0x9E3779B97F4A7C15ull + seed * 0xD1B54A32D192ED03ull;
+    z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27; z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+__global__ void k_fill_random(uint8_t* __restrict__ buf, uint64_t nbytes, uint64_t seed, uint64_t w0) {
+    const uint64_t nwords = (nbytes + 7) / 8;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = mix64(seed, w0 + w);
+        if (8 * w + 8 <= nbytes) {
+            reinterpret_cast<uint64_t*>(buf)[w] = v;
+        } else {
+            for (uint64_t k = 0; 8 * w + k < nbytes; ++k) buf[8 * w + k] = (uint8_t)(v >> (8 * k));
+        }
+    }
+}
+
+__global__ void k_gen_decimal(uint64_t start, uint64_t count, int width, uint8_t* __restrict__ out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    uint64_t v = start + i;
+    for (int pos = width - 1; pos >= 0; --pos) {
+        out[i * (uint64_t)width + pos] = (uint8_t)('0' + v % 10u);
+        v /= 10u;
+    }
+}
+
+// =========================================================================
+// Host-side launchers
+// =========================================================================
+
+PFN_encodeTiled get_encode_tiled() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    });
+    return fn;
+}
+
+static thread_local char g_tma_err[kTmaErrLen];
+const char* tma_error() { return g_tma_err; }
+char* tma_error_buf() { return g_tma_err; }
+
+// Per-algorithm launchers (hb_alg_*.cu).
+#define HB_DECL(A)                                                                                               \
+    cudaError_t launch_fixed_##A(const uint8_t*, uint64_t, uint64_t, uint8_t*, cudaStream_t, uint32_t);          \
+    cudaError_t launch_varlen_##A(const uint8_t*, uint64_t, const uint64_t*, uint64_t, uint64_t, uint8_t*, void*, \
+                                  cudaStream_t, uint32_t);                                                      \
+    cudaError_t launch_decimal_##A(uint64_t, uint64_t, int, uint8_t*, cudaStream_t);
+HB_DECL(sha1)
+HB_DECL(md5)
+HB_DECL(sm3)
+#undef HB_DECL
+
+cudaError_t launch_fixed(int alg, const uint8_t* d_msgs, uint64_t n, uint64_t msg_len, uint8_t* d_out,
+                         cudaStream_t stream, uint32_t flags) {
+    if (n == 0) return cudaSuccess;
+    switch (alg) {
+    case kSha1: return launch_fixed_sha1(d_msgs, n, msg_len, d_out, stream, flags);
+    case kMd5: return launch_fixed_md5(d_msgs, n, msg_len, d_out, stream, flags);
+    case kSm3: return launch_fixed_sm3(d_msgs, n, msg_len, d_out, stream, flags);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+uint64_t varlen_scratch_bytes(uint64_t n) { return (uint64_t)kSortBuckets * 4u + n * 4u + 256u; }
 
 cudaError_t launch_varlen(int alg, const uint8_t* d_data, uint64_t data_bytes, const uint64_t* d_offsets,
                           uint64_t offset_base, uint64_t n, uint8_t* d_out, void* d_scratch, cudaStream_t stream,
@@ -1139,9 +291,9 @@ cudaError_t launch_varlen(int alg, const uint8_t* d_data, uint64_t data_bytes, c
     if (n == 0) return cudaSuccess;
     if (n >= (1ull << 32)) return cudaErrorInvalidValue;
     switch (alg) {
-    case kSha1: return launch_varlen_alg<kSha1>(d_data, data_bytes, d_offsets, offset_base, n, d_out, d_scratch, stream, flags);
-    case kMd5: return launch_varlen_alg<kMd5>(d_data, data_bytes, d_offsets, offset_base, n, d_out, d_scratch, stream, flags);
-    case kSm3: return launch_varlen_alg<kSm3>(d_data, data_bytes, d_offsets, offset_base, n, d_out, d_scratch, stream, flags);
+    case kSha1: return launch_varlen_sha1(d_data, data_bytes, d_offsets, offset_base, n, d_out, d_scratch, stream, flags);
+    case kMd5: return launch_varlen_md5(d_data, data_bytes, d_offsets, offset_base, n, d_out, d_scratch, stream, flags);
+    case kSm3: return launch_varlen_sm3(d_data, data_bytes, d_offsets, offset_base, n, d_out, d_scratch, stream, flags);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -1157,33 +309,13 @@ cudaError_t launch_fill_random(uint8_t* d_buf, uint64_t nbytes, uint64_t seed, u
     return cudaGetLastError();
 }
 
-template <int ALG, int W>
-static void dec_launch(uint64_t start, uint64_t count, uint8_t* d_out, cudaStream_t s) {
-    k_decimal<ALG, W><<<(unsigned)((count + 127) / 128), 128, 0, s>>>(start, count, d_out);
-}
-
-template <int ALG>
-static cudaError_t launch_decimal_alg(uint64_t start, uint64_t count, int width, uint8_t* d_out, cudaStream_t s) {
-    switch (width) {
-#define HB_DEC_CASE(W) case W: dec_launch<ALG, W>(start, count, d_out, s); break;
-    HB_DEC_CASE(1) HB_DEC_CASE(2) HB_DEC_CASE(3) HB_DEC_CASE(4) HB_DEC_CASE(5) HB_DEC_CASE(6) HB_DEC_CASE(7)
-    HB_DEC_CASE(8) HB_DEC_CASE(9) HB_DEC_CASE(10) HB_DEC_CASE(11) HB_DEC_CASE(12) HB_DEC_CASE(13)
-    HB_DEC_CASE(14) HB_DEC_CASE(15) HB_DEC_CASE(16) HB_DEC_CASE(17) HB_DEC_CASE(18) HB_DEC_CASE(19)
-    HB_DEC_CASE(20)
-#undef HB_DEC_CASE
-    default: return cudaErrorInvalidValue;
-    }
-    note_launches(1);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_decimal(int alg, uint64_t start, uint64_t count, int width, uint8_t* d_out, cudaStream_t stream) {
     if (count == 0) return cudaSuccess;
     if (count >= (1ull << 40)) return cudaErrorInvalidValue;
     switch (alg) {
-    case kSha1: return launch_decimal_alg<kSha1>(start, count, width, d_out, stream);
-    case kMd5: return launch_decimal_alg<kMd5>(start, count, width, d_out, stream);
-    case kSm3: return launch_decimal_alg<kSm3>(start, count, width, d_out, stream);
+    case kSha1: return launch_decimal_sha1(start, count, width, d_out, stream);
+    case kMd5: return launch_decimal_md5(start, count, width, d_out, stream);
+    case kSm3: return launch_decimal_sm3(start, count, width, d_out, stream);
     default: return cudaErrorInvalidValue;
     }
 }
