@@ -157,8 +157,21 @@ def _ptr(a: np.ndarray) -> int | None:
     return a.ctypes.data if a.size else None
 
 
+def _out_array(out, n: int, alg: str) -> np.ndarray:
+    """The digest array: a new (n, dlen) uint8 array, or the caller's ``out=``
+    (keyword-only extension: a reused -- e.g. page-locked -- buffer lets the
+    engine DMA digests straight into it)."""
+    shape = (n, DIGEST_LEN[alg])
+    if out is None:
+        return np.empty(shape, np.uint8)
+    if not isinstance(out, np.ndarray) or out.dtype != np.uint8 or out.shape != shape or \
+            not out.flags.c_contiguous or not out.flags.writeable:
+        raise ValueError(f"out must be a writable C-contiguous uint8 array of shape {shape}")
+    return out
+
+
 def batch_digest(alg: str, data, accel: bool = False, *, gpus=None, ratios=None, flags: int = 0,
-                 timing: dict | None = None) -> np.ndarray:
+                 timing: dict | None = None, out=None) -> np.ndarray:
     """Hash each row of an (n, width) uint8 array; returns a new (n, digest_len) uint8 array.
 
     Reference: batch.py:274-290.  ``accel`` is accepted for API compatibility.
@@ -169,7 +182,7 @@ def batch_digest(alg: str, data, accel: bool = False, *, gpus=None, ratios=None,
     _check_alg(alg)
     rows = _as_rows(data)
     n, width = rows.shape
-    out = np.empty((n, DIGEST_LEN[alg]), np.uint8)
+    out = _out_array(out, n, alg)
     if ratios is not None:
         if gpus is None or len(gpus) != len(ratios):
             raise ValueError("ratios need a gpus list of the same length")
@@ -191,7 +204,7 @@ def batch_digest(alg: str, data, accel: bool = False, *, gpus=None, ratios=None,
 
 
 def batch_digest_varlen(alg: str, data, offsets, *, gpus=None, flags: int = 0,
-                        timing: dict | None = None) -> np.ndarray:
+                        timing: dict | None = None, out=None) -> np.ndarray:
     """Hash message i = data[offsets[i]:offsets[i+1]] for i < len(offsets)-1.
 
     The reference has no variable-length batch; this is
@@ -204,7 +217,7 @@ def batch_digest_varlen(alg: str, data, offsets, *, gpus=None, flags: int = 0,
     if off.ndim != 1 or off.shape[0] < 1:
         raise ValueError("offsets must be a 1-D array of n+1 entries")
     n = off.shape[0] - 1
-    out = np.empty((n, DIGEST_LEN[alg]), np.uint8)
+    out = _out_array(out, n, alg)
     if n == 0:
         return out
     if int(off[-1]) > buf.shape[0]:
@@ -220,7 +233,7 @@ def batch_digest_varlen(alg: str, data, offsets, *, gpus=None, flags: int = 0,
 
 
 def hash_decimal(alg: str, start_index: int, count: int, width: int = 9, *, gpus=None,
-                 timing: dict | None = None) -> np.ndarray:
+                 timing: dict | None = None, out=None) -> np.ndarray:
     """Digests of ``gen_messages(start_index, count, width)`` with the messages
     generated in registers on the GPU (the paper's 10^9 x 9-digit workload,
     PAPER.md:206); returns (count, digest_len) uint8."""
@@ -231,11 +244,12 @@ def hash_decimal(alg: str, start_index: int, count: int, width: int = 9, *, gpus
         raise ValueError(
             f"index range [{start_index}, {start_index + count}) does not fit in {width} digits"
         )
-    out = np.empty((count, DIGEST_LEN[alg]), np.uint8)
+    out = _out_array(out, count, alg)
     if count == 0:
         return out
     if width > 20:  # leading zeros beyond 64-bit indices: hash the materialised bytes
-        return batch_digest(alg, gen_messages(start_index, count, width).as_array(), gpus=gpus, timing=timing)
+        return batch_digest(alg, gen_messages(start_index, count, width).as_array(), gpus=gpus, timing=timing,
+                            out=out)
     garr, ng = _native.gpu_array(gpus)
     t = _native.HbTiming()
     rc = _native.lib().hb_hash_decimal(_native.ALG_ID[alg], start_index, count, width, out.ctypes.data, garr, ng,

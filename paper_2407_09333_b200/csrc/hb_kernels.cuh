@@ -320,10 +320,10 @@ __host__ __device__ constexpr uint32_t bswap_c(uint32_t x) {
     return (x >> 24) | ((x >> 8) & 0xFF00u) | ((x << 8) & 0xFF0000u) | (x << 24);
 }
 
-template <int ALG, int L>
+template <int ALG, int L, int V = -1>
 __global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__ msgs, uint64_t n,
                                                      uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG>;
+    using H = HashAlg<ALG, V>;
     static_assert(L % 16 == 0 && L >= 16 && L <= 128, "width");
     constexpr int kNb = (L + 8) / 64 + 1;  // blocks including padding
     constexpr uint64_t kBits = (uint64_t)L * 8u;
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__
             raw[j] = pos < L ? w[pos / 4] : pos == L ? 0x80u : 0u;
         }
         if (b == kNb - 1) { raw[14] = kL14; raw[15] = kL15; }
-        compress1<ALG>(st, raw);
+        compress1<ALG, V>(st, raw);
     }
     store_digest<ALG>(out + i * H::kDigestBytes, st);
 }
@@ -627,10 +627,12 @@ __device__ __forceinline__ uint32_t sort_bucket(const uint64_t* offsets, uint64_
 // gen_messages (batch.py:86-99): message i is the zero-padded decimal
 // rendering of start+i, WIDTH bytes.  The bytes are built in registers and
 // hashed directly; only digests touch HBM.
-template <int ALG, int WIDTH>
+template <int ALG, int WIDTH, int V = -1>
 __global__ void __launch_bounds__(128) k_decimal(uint64_t start, uint64_t count, uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG>;
+    using H = HashAlg<ALG, V>;
     static_assert(WIDTH >= 1 && WIDTH <= 20, "width");
+    // One message per thread, one-shot CTAs: a grid-stride loop measured 4-8 %
+    // slower (profiles/ab_decimal_r1.txt).
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
     uint64_t v = start + i;
@@ -655,7 +657,7 @@ __global__ void __launch_bounds__(128) k_decimal(uint64_t start, uint64_t count,
     }
     uint32_t st[H::kStateWords];
     H::init(st);
-    md_finish<ALG>(st, raw, (uint32_t)WIDTH, (uint64_t)WIDTH);
+    md_finish<ALG, V>(st, raw, (uint32_t)WIDTH, (uint64_t)WIDTH);
     store_digest<ALG>(out + i * H::kDigestBytes, st);
 }
 
@@ -857,16 +859,25 @@ static cudaError_t launch_fixed_alg(const uint8_t* d_msgs, uint64_t n, uint64_t 
     }
     const uint64_t grid = (n + 127) / 128;
     const bool small_ok = aligned && !getenv("HB_NO_SMALL_KERNEL");
+    // Pipe-balanced rounds (default) or the plain ones ($HB_CONST_VARIANT=0):
+    // folding the constant padding words does not pay for the lost ALU/FMA
+    // balance (B200: MD5 16 B 1366 vs 1262 GB/s, profiles/ab_small_r1c.txt).
+    const bool small_v1 = env_u64("HB_CONST_VARIANT", 1) == 1;
     if (small_ok && L == 16) {
-        k_fixed_small<ALG, 16><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? k_fixed_small<ALG, 16, kVarBal><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out)
+                 : k_fixed_small<ALG, 16, kVarPlain><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
     } else if (small_ok && L == 32) {
-        k_fixed_small<ALG, 32><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? k_fixed_small<ALG, 32, kVarBal><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out)
+                 : k_fixed_small<ALG, 32, kVarPlain><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
     } else if (small_ok && L == 48) {
-        k_fixed_small<ALG, 48><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? k_fixed_small<ALG, 48, kVarBal><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out)
+                 : k_fixed_small<ALG, 48, kVarPlain><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
     } else if (small_ok && L == 64) {
-        k_fixed_small<ALG, 64><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? k_fixed_small<ALG, 64, kVarBal><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out)
+                 : k_fixed_small<ALG, 64, kVarPlain><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
     } else if (small_ok && L == 128) {
-        k_fixed_small<ALG, 128><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? k_fixed_small<ALG, 128, kVarBal><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out)
+                 : k_fixed_small<ALG, 128, kVarPlain><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
     } else if (aligned) {
         k_fixed_direct<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, (uint32_t)L, d_out);
     } else {
@@ -920,7 +931,11 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
 
 template <int ALG, int W>
 static void dec_launch(uint64_t start, uint64_t count, uint8_t* d_out, cudaStream_t s) {
-    k_decimal<ALG, W><<<(unsigned)((count + 127) / 128), 128, 0, s>>>(start, count, d_out);
+    const unsigned grid = (unsigned)((count + 127) / 128);
+    if (env_u64("HB_CONST_VARIANT", 1) == 0)  // A/B: plain rounds
+        k_decimal<ALG, W, kVarPlain><<<grid, 128, 0, s>>>(start, count, d_out);
+    else
+        k_decimal<ALG, W, kVarBal><<<grid, 128, 0, s>>>(start, count, d_out);
 }
 
 template <int ALG>

@@ -179,3 +179,18 @@ def test_var_message_batch_layout():
         VarMessageBatch(b"abc", (0, 4))
     with pytest.raises(IndexError):
         b.message(3)
+
+
+def test_out_argument_validation():
+    """``out=`` (keyword-only extension) is checked before any device work."""
+    from paper_2407_09333_b200.crypto import batch_digest, batch_digest_varlen, hash_decimal
+
+    data = np.zeros((4, 8), np.uint8)
+    for bad in (np.zeros((4, 20), np.uint8), np.zeros((4, 16), np.int32), np.zeros((16, 4), np.uint8).T,
+                [[0] * 16] * 4):
+        with pytest.raises(ValueError):
+            batch_digest("md5", data, out=bad)
+    with pytest.raises(ValueError):
+        batch_digest_varlen("sha1", np.zeros(8, np.uint8), np.array([0, 8], np.uint64), out=np.zeros((2, 20), np.uint8))
+    with pytest.raises(ValueError):
+        hash_decimal("sm3", 0, 3, out=np.zeros((3, 20), np.uint8))

@@ -178,7 +178,13 @@ def test_ratio_invariance_style_sharding():
         assert np.array_equal(batch_digest(alg, data, gpus=list(range(n)) + [0]), ref)  # uneven split, repeated dev
 
 
-def test_decimal_workload(golden):
+@pytest.mark.parametrize("variant", ["0", "1"])
+def test_decimal_workload(golden, variant, monkeypatch):
+    monkeypatch.setenv("HB_CONST_VARIANT", variant)
+    # the 32-bit digit path ends exactly at index 2^32 - 1; straddle it
+    start, cnt = 2**32 - 150, 300
+    for alg in ALGS:
+        assert np.array_equal(hash_decimal(alg, start, cnt, 10), oracle.batch_fixed(alg, oracle.gen_decimal(start, cnt, 10)))
     for row in golden("decimal_batches.json"):
         for alg in ALGS:
             out = hash_decimal(alg, row["start"], row["count"], row["width"])
@@ -303,13 +309,13 @@ def test_batch_geometry_dispatch_matches(alg, monkeypatch):
     loads for short rows, one message per thread below $HB_SMALL_N, the tuned
     tiles otherwise); every shape must give the oracle's digests."""
     arms = [{}, {"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"}, {"HB_SMALL_N": str(1 << 40), "HB_DIRECT_MAX_L": "0"},
-            {"HB_NO_SMALL_KERNEL": "1"}]
+            {"HB_NO_SMALL_KERNEL": "1"}, {"HB_CONST_VARIANT": "0"}]
     for L in (16, 32, 48, 64, 96, 128, 144, 1024):
         n = 3001
         data = oracle.fill_random(n * L, 5 * L + 3).reshape(n, L)
         ref = oracle.batch_fixed(alg, data, threads=8)
         for env in arms:
-            for k in ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL"):
+            for k in ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_CONST_VARIANT"):
                 monkeypatch.delenv(k, raising=False)
             for k, v in env.items():
                 monkeypatch.setenv(k, v)
@@ -378,3 +384,25 @@ def test_fixed_hash_graph_replay():
             rows = np.array([0, 1, 777, n - 1])
             sample = np.stack([oracle.fill_random(L, seed, int(r) * L) for r in rows])
             assert np.array_equal(out.cpu().numpy()[rows], oracle.batch_fixed(alg, sample)), (alg, seed)
+
+
+def test_out_argument_reuse_and_pinned():
+    """Digests written into a caller buffer (pageable or page-locked) equal a fresh result."""
+    import ctypes
+
+    n, L = 3000, 100
+    data = oracle.fill_random(n * L, 77).reshape(n, L)
+    lib = _native.lib()
+    hp = lib.hb_alloc_pinned(n * 32)
+    try:
+        pinned = np.ctypeslib.as_array(ctypes.cast(hp, ctypes.POINTER(ctypes.c_uint8)), shape=(n * 32,))
+        for alg in ALGS:
+            d = {"sha1": 20, "md5": 16, "sm3": 32}[alg]
+            ref = oracle.batch_fixed(alg, data, threads=8)
+            for out in (np.empty((n, d), np.uint8), pinned[: n * d].reshape(n, d)):
+                got = batch_digest(alg, data, out=out)
+                assert got is out and np.array_equal(out, ref)
+            dec = hash_decimal(alg, 5, n, 9, out=np.empty((n, d), np.uint8))
+            assert np.array_equal(dec, oracle.batch_fixed(alg, gen_messages(5, n, 9).as_array(), threads=8))
+    finally:
+        lib.hb_free_pinned(hp)

@@ -1,0 +1,37 @@
+"""A/B of the in-kernel decimal workload (paper: 10^9 x 9 digits) across round
+variants ($HB_CONST_VARIANT), kernel-only, digests cross-checked."""
+import json
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2407_09333_b200 import device  # noqa: E402
+
+n = int(os.environ.get("AB_N", 10**9))
+for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
+    out = torch.empty((n, {"md5": 16, "sha1": 20, "sm3": 32}[alg]), dtype=torch.uint8, device="cuda:0")
+    ref, times = None, {}
+    for _ in range(3):
+        for arm in ("plain", "balanced"):
+            os.environ["HB_CONST_VARIANT"] = "1" if arm == "balanced" else "0"
+            device.hash_decimal(alg, 0, n, 9, out=out)
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(3):
+                device.hash_decimal(alg, 0, n, 9, out=out)
+            e.record()
+            torch.cuda.synchronize()
+            h = out[:: 997].clone()
+            if ref is None:
+                ref = h
+            assert torch.equal(h, ref), (alg, arm)
+            times.setdefault(arm, []).append(s.elapsed_time(e) / 3)
+    for arm, ts in times.items():
+        ms = statistics.median(ts)
+        print(json.dumps({"alg": alg, "arm": arm, "ms": round(ms, 3), "Mhash_s": round(n / ms / 1e3, 1)}), flush=True)
+    del out
+    torch.cuda.empty_cache()

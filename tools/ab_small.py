@@ -13,9 +13,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2407_09333_b200 import _native, device  # noqa: E402
 
 DLEN = {"md5": 16, "sha1": 20, "sm3": 32}
-POINTS = [(1 << 24, 16), (1 << 24, 32), (1 << 24, 64), (1 << 24, 128), (1 << 22, 256),
-          (1 << 16, 1024), (1 << 16, 65536), (1 << 12, 65536), (1 << 14, 16384), (1 << 17, 4096)]
-ARMS = {"default": ({}, 0), "direct": ({"HB_NO_SMALL_KERNEL": "1"}, _native.HB_FLAG_NO_TMA), "ws_forced": ({"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"}, 0),
+POINTS = [(1 << 24, 16), (1 << 24, 32), (1 << 24, 64), (1 << 24, 128)] if os.environ.get("AB_SHORT_ONLY") else \
+    [(1 << 24, 16), (1 << 24, 32), (1 << 24, 64), (1 << 24, 128), (1 << 22, 256),
+     (1 << 16, 1024), (1 << 16, 65536), (1 << 12, 65536), (1 << 14, 16384), (1 << 17, 4096)]
+ARMS = {"default": ({}, 0), "const_v1": ({"HB_CONST_VARIANT": "1"}, 0), "direct": ({"HB_NO_SMALL_KERNEL": "1"}, _native.HB_FLAG_NO_TMA), "ws_forced": ({"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"}, 0),
         "small_forced": ({"HB_SMALL_N": str(1 << 40), "HB_DIRECT_MAX_L": "0"}, 0)}
 rounds = int(os.environ.get("AB_ROUNDS", 3))
 for n, L in POINTS:
@@ -27,7 +28,7 @@ for n, L in POINTS:
         ref, times = None, {}
         for _ in range(rounds):
             for arm, (env, flags) in ARMS.items():
-                for k in ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL"):
+                for k in ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_CONST_VARIANT"):
                     os.environ.pop(k, None)
                 os.environ.update(env)
                 out = torch.empty((n, DLEN[alg]), dtype=torch.uint8, device="cuda:0")
@@ -43,7 +44,7 @@ for n, L in POINTS:
                     ref = out.clone()
                 assert torch.equal(out, ref), (alg, n, L, arm)
                 times.setdefault(arm, []).append(s.elapsed_time(e) / steps)
-        for k in ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL"):
+        for k in ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_CONST_VARIANT"):
             os.environ.pop(k, None)
         for arm, ts in times.items():
             ms = statistics.median(ts)
