@@ -178,7 +178,10 @@ template <int ALG, int NB, int STAGES> struct WsOcc {
         NB == 2 ? (STAGES == 2 ? 6 : 4) : ALG == kSm3 ? 6 : (STAGES == 2 ? (ALG == kMd5 ? 10 : 8) : 8);
 };
 
-template <int ALG, int V, int NB, int STAGES>
+// UNR: the compute warps' main loop is unrolled by STAGES so every ring
+// index is a compile-time constant (no stage/phase bookkeeping, immediate
+// shared-memory offsets); the remainder blocks take the generic loop.
+template <int ALG, int V, int NB, int STAGES, bool UNR = false>
 __global__ void __launch_bounds__((kWsComputeWarps + 1) * 32, (WsOcc<ALG, NB, STAGES>::kMinCtas))
 k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
     using H = HashAlg<ALG, V>;
@@ -246,7 +249,21 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
     };
     const uint32_t nfull = msg_len >> 6;
     uint32_t s = 0, ph = 0;
-    for (uint32_t b = 0; b < nfull; ++b) {
+    uint32_t b = 0;
+    if (UNR) {
+        for (; b + STAGES <= nfull; b += STAGES) {
+#pragma unroll
+            for (int k = 0; k < STAGES; ++k) {
+                mbar_wait_parity(&full[k], ph);
+                read_stage(k);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[k]);
+                H::template compress_n<NB>(st, raw);
+            }
+            ph ^= 1u;
+        }
+    }
+    for (; b < nfull; ++b) {
         mbar_wait_parity(&full[s], ph);
         read_stage(s);
         __syncwarp();
@@ -437,7 +454,22 @@ __device__ __forceinline__ void realign16(const uint32_t (&c)[20], uint32_t q, u
 #undef HB_RA
 }
 
-template <int ALG>
+// PF: software pipelining -- block b+1's loads are issued right after block b
+// is realigned out of c[], so they are in flight during b's compression
+// (+20 registers; pays off once the windowed sort makes a warp's loads L2-
+// friendly, see profiles/ab_varlen_r1d.txt).
+__device__ __forceinline__ void load_full_window(const uint4* src, bool misaligned, uint32_t (&c)[20]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint4 v = __ldg(src + k);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+    uint4 v4 = make_uint4(0, 0, 0, 0);
+    if (misaligned) v4 = __ldg(src + 4);
+    c[16] = v4.x; c[17] = v4.y; c[18] = v4.z; c[19] = v4.w;
+}
+
+template <int ALG, bool PF = false>
 __global__ void __launch_bounds__(128)
 k_varlen16(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offsets, uint64_t offset_base,
            const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
@@ -456,18 +488,19 @@ k_varlen16(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offset
     uint32_t c[20];
     uint32_t raw[16];
     const uint64_t nfull = len >> 6;
-    for (uint64_t b = 0; b < nfull; ++b) {
-        const uint4* src = w16 + 4 * b;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint4 v = __ldg(src + k);
-            c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    if (PF) {
+        if (nfull) load_full_window(w16, misaligned, c);
+        for (uint64_t b = 0; b < nfull; ++b) {
+            realign16(c, q, sh, raw);
+            if (b + 1 < nfull) load_full_window(w16 + 4 * (b + 1), misaligned, c);
+            compress1<ALG>(st, raw);
         }
-        uint4 v4 = make_uint4(0, 0, 0, 0);
-        if (misaligned) v4 = __ldg(src + 4);
-        c[16] = v4.x; c[17] = v4.y; c[18] = v4.z; c[19] = v4.w;
-        realign16(c, q, sh, raw);
-        compress1<ALG>(st, raw);
+    } else {
+        for (uint64_t b = 0; b < nfull; ++b) {
+            load_full_window(w16 + 4 * b, misaligned, c);
+            realign16(c, q, sh, raw);
+            compress1<ALG>(st, raw);
+        }
     }
     // tail: the r = len % 64 remaining bytes (chunks that overlap [p, p+r) only)
     const uint32_t r = (uint32_t)(len & 63u);
@@ -698,7 +731,7 @@ static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint3
     return cudaGetLastError();
 }
 
-template <int ALG, int V, int NB, int STAGES>
+template <int ALG, int V, int NB, int STAGES, bool UNR = false>
 static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
                                        cudaStream_t stream) {
     using C = WsCfg<NB, STAGES>;
@@ -722,12 +755,12 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     static std::once_flag attr_once;
     static cudaError_t attr_rc = cudaSuccess;
     std::call_once(attr_once, [] {
-        attr_rc = cudaFuncSetAttribute(k_fixed_tma_ws<ALG, V, NB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       C::kSmem);
+        attr_rc = cudaFuncSetAttribute(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     });
     if (attr_rc != cudaSuccess) return attr_rc;
     const uint32_t grid = (n + C::kRows - 1) / C::kRows;
-    k_fixed_tma_ws<ALG, V, NB, STAGES><<<grid, (kWsComputeWarps + 1) * 32, C::kSmem, stream>>>(map, n, L, d_out);
+    k_fixed_tma_ws<ALG, V, NB, STAGES, UNR><<<grid, (kWsComputeWarps + 1) * 32, C::kSmem, stream>>>(map, n, L, d_out);
     note_launches(1);
     return cudaGetLastError();
 }
@@ -736,7 +769,8 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
 // (profiles/variant_sweep_r1*.txt); $HB_TMA_CFG ("1x3", "2x2", "2x3" =
 // messages-per-thread x ring stages) and $HB_VARIANT (0-3) override them for
 // A/B experiments.
-enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4, kCfg1x2 = 5, kCfgWs2x2 = 6, kCfgWs3x2 = 7 };
+enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4, kCfg1x2 = 5, kCfgWs2x2 = 6, kCfgWs3x2 = 7,
+                kCfgWs3u = 8, kCfgWs3x2u = 9 };
 // B200-measured (profiles/variant_sweep_r1d.txt and _r1e.txt, interleaved
 // rounds): the warp-specialised 3-stage ring is best for MD5 and SM3 (SM3's
 // 61 registers make two messages per thread lose occupancy); SHA-1 gains 4 %
@@ -763,6 +797,8 @@ static int tma_cfg(int alg) {
     if (v && !strcmp(v, "ws3")) return kCfgWs3;
     if (v && !strcmp(v, "ws2x2")) return kCfgWs2x2;
     if (v && !strcmp(v, "ws3x2")) return kCfgWs3x2;
+    if (v && !strcmp(v, "ws3u")) return kCfgWs3u;
+    if (v && !strcmp(v, "ws3x2u")) return kCfgWs3x2u;
     switch (alg) {
     case kSha1: return DefaultTmaCfg<kSha1>::value;
     case kMd5: return DefaultTmaCfg<kMd5>::value;
@@ -804,6 +840,8 @@ static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t 
         default: return launch_fixed_tma_ws<ALG, 1, 1, 3>(src, n, L, dst, s);
         }
     }
+    if (cfg == kCfgWs3u) return launch_fixed_tma_ws<ALG, DefaultVariant<ALG>::value, 1, 3, true>(src, n, L, dst, s);
+    if (cfg == kCfgWs3x2u) return launch_fixed_tma_ws<ALG, DefaultVariant<ALG>::value, 2, 3, true>(src, n, L, dst, s);
     if (cfg == kCfgWs2x2) {
         switch (v) {
         case 3: return launch_fixed_tma_ws<ALG, 3, 2, 2>(src, n, L, dst, s);
@@ -922,8 +960,10 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
             k_varlen_coop<ALG, 4, 5, 0><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
         else
             k_varlen_coop<ALG, 4, 5, 256><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
-    } else {  // A/B baseline: per-thread 128-bit loads
-        k_varlen16<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
+    } else if (env_u64("HB_VARLEN_PREFETCH", 0)) {  // per-thread 128-bit loads, software-pipelined
+        k_varlen16<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
+    } else {  // per-thread 128-bit loads
+        k_varlen16<ALG, false><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
     }
     note_launches(1);
     return cudaGetLastError();
@@ -932,10 +972,12 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
 template <int ALG, int W>
 static void dec_launch(uint64_t start, uint64_t count, uint8_t* d_out, cudaStream_t s) {
     const unsigned grid = (unsigned)((count + 127) / 128);
-    if (env_u64("HB_CONST_VARIANT", 1) == 0)  // A/B: plain rounds
-        k_decimal<ALG, W, kVarPlain><<<grid, 128, 0, s>>>(start, count, d_out);
-    else
-        k_decimal<ALG, W, kVarBal><<<grid, 128, 0, s>>>(start, count, d_out);
+    switch (env_u64("HB_CONST_VARIANT", 1)) {  // round variant (A/B; 1 = tuned default)
+    case 0: k_decimal<ALG, W, kVarPlain><<<grid, 128, 0, s>>>(start, count, d_out); break;
+    case 2: k_decimal<ALG, W, kVarBal2><<<grid, 128, 0, s>>>(start, count, d_out); break;
+    case 3: k_decimal<ALG, W, kVarBal3><<<grid, 128, 0, s>>>(start, count, d_out); break;
+    default: k_decimal<ALG, W, kVarBal><<<grid, 128, 0, s>>>(start, count, d_out); break;
+    }
 }
 
 template <int ALG>

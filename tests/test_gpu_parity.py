@@ -108,12 +108,14 @@ def test_varlen_golden(golden):
             assert sha(batch_digest_varlen(alg, data, off)) == row[alg]
 
 
-@pytest.mark.parametrize("sort", ["window4096", "window16384", "global"])
+@pytest.mark.parametrize("sort", ["window4096", "window16384", "global", "prefetch"])
 @pytest.mark.parametrize("alg", ALGS)
 def test_varlen_random_sorted_and_unsorted(alg, sort, monkeypatch):
     monkeypatch.setenv("HB_VARLEN_SORT", "global" if sort == "global" else "window")
-    if sort != "global":
+    if sort.startswith("window"):
         monkeypatch.setenv("HB_SORT_WINDOW", sort[6:])
+    if sort == "prefetch":
+        monkeypatch.setenv("HB_VARLEN_PREFETCH", "1")
     rng = np.random.default_rng(12)
     n = 20000  # above the sort threshold
     lens = rng.integers(0, 4097, n).astype(np.uint64)
@@ -178,7 +180,7 @@ def test_ratio_invariance_style_sharding():
         assert np.array_equal(batch_digest(alg, data, gpus=list(range(n)) + [0]), ref)  # uneven split, repeated dev
 
 
-@pytest.mark.parametrize("variant", ["0", "1"])
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3"])
 def test_decimal_workload(golden, variant, monkeypatch):
     monkeypatch.setenv("HB_CONST_VARIANT", variant)
     # the 32-bit digit path ends exactly at index 2^32 - 1; straddle it
@@ -271,7 +273,7 @@ def test_full_size_sampled_and_cross_path():
     del buf
 
 
-@pytest.mark.parametrize("cfg", ["1x3", "2x2", "2x3", "ws2", "ws3", "ws2x2", "ws3x2"])
+@pytest.mark.parametrize("cfg", ["1x3", "2x2", "2x3", "ws2", "ws3", "ws2x2", "ws3x2", "ws3u", "ws3x2u"])
 def test_tma_tile_configs_and_variants(cfg, monkeypatch):
     """Every compiled TMA tile configuration x round variant is bit-exact
     (the tuned default is only one of them; $HB_TMA_CFG/$HB_VARIANT select)."""
@@ -339,10 +341,12 @@ def test_varlen_every_length_and_alignment(alg, monkeypatch):
             for fl in (0, _native.HB_FLAG_NO_SORT, _native.HB_FLAG_VARLEN_COOP_OFF, _native.HB_FLAG_VARLEN_COOP):
                 got = batch_digest_varlen(alg, buf, off[: k + 1], flags=fl)
                 assert np.array_equal(got, ref[:k]), (alg, shift, k, fl)
-        for env in ({"HB_VC_STAGES": "3"}, {"HB_VC_STAGES": "2"}, {"HB_VC_PF": "128"}, {"HB_VC_PF": "0"}):
+        C = _native.HB_FLAG_VARLEN_COOP
+        for env, fl in (({"HB_VC_STAGES": "3"}, C), ({"HB_VC_STAGES": "2"}, C), ({"HB_VC_PF": "128"}, C),
+                        ({"HB_VC_PF": "0"}, C), ({"HB_VARLEN_PREFETCH": "1"}, 0)):
             for key, v in env.items():
                 monkeypatch.setenv(key, v)
-            got = batch_digest_varlen(alg, buf, off, flags=_native.HB_FLAG_VARLEN_COOP)
+            got = batch_digest_varlen(alg, buf, off, flags=fl)
             assert np.array_equal(got, ref), (alg, shift, env)
             for key in env:
                 monkeypatch.delenv(key)

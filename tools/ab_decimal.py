@@ -15,8 +15,8 @@ for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
     out = torch.empty((n, {"md5": 16, "sha1": 20, "sm3": 32}[alg]), dtype=torch.uint8, device="cuda:0")
     ref, times = None, {}
     for _ in range(3):
-        for arm in ("plain", "balanced"):
-            os.environ["HB_CONST_VARIANT"] = "1" if arm == "balanced" else "0"
+        for arm in ("v0_plain", "v1", "v2", "v3"):
+            os.environ["HB_CONST_VARIANT"] = arm[1]
             device.hash_decimal(alg, 0, n, 9, out=out)
             torch.cuda.synchronize()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

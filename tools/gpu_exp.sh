@@ -1,6 +1,5 @@
 set -u
 mkdir -p gpurun_out
-T=${T:-exp12}
+T=${T:-exp14}
 timeout 900 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_$T.log
-timeout 600 python tools/ab_decimal.py > gpurun_out/ab_decimal_$T.txt 2>&1; echo "abd rc=$?"; cat gpurun_out/ab_decimal_$T.txt
-AB_SHORT_ONLY=1 timeout 600 python tools/ab_small.py > gpurun_out/ab_small_$T.txt 2>&1; echo "abs rc=$?"; cat gpurun_out/ab_small_$T.txt
+timeout 600 python tools/ab_varlen.py > gpurun_out/ab_varlen_$T.txt 2>&1; echo "abv rc=$?"; cat gpurun_out/ab_varlen_$T.txt
