@@ -519,6 +519,104 @@ k_varlen16(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offset
 }
 
 // -------------------------------------------------------------------------
+// Variable-length kernel, per-lane bulk copies (TMA engine).
+//
+// The per-thread kernel is bound by the L1 data pipe (ncu: LSU wavefronts at
+// 85 % of peak): every LDG.128 of a warp touches 32 scattered lines.  Here
+// each lane asks the TMA engine for its own message's 16-aligned window of
+// block b (<= 80 bytes, clipped at the message's last 16-byte chunk) with one
+// cp.async.bulk into its slot of a per-warp STAGES-deep ring; completion is
+// counted on the stage's mbarrier (32 arrivals + tx bytes).  Lanes then read
+// their slot with LDS.128 (conflict-free at an 80-byte stride), realign,
+// apply padding in registers and compress.
+// -------------------------------------------------------------------------
+template <int ALG, int STAGES, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB)
+k_varlen_bulk(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offsets, uint64_t offset_base,
+              const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    constexpr int kWarps = 4, kSlot = 80, kStage = 32 * kSlot;
+    __shared__ __align__(128) uint8_t ring[kWarps][STAGES][kStage];
+    __shared__ __align__(8) uint64_t bars[kWarps][STAGES];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t wbase = ((uint64_t)blockIdx.x * kWarps + warp) * 32u;
+    if (wbase >= n) return;  // warp-uniform
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < STAGES; ++k) mbar_init(&bars[warp][k], 32);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const uint64_t t = wbase + lane;
+    const bool live = t < n;
+    uint64_t i = 0, len = 0;
+    uintptr_t a = reinterpret_cast<uintptr_t>(data);
+    if (live) {
+        i = perm ? (uint64_t)perm[t] : t;
+        a = reinterpret_cast<uintptr_t>(data + (offsets[i] - offset_base));
+        len = offsets[i + 1] - offsets[i];
+    }
+    const uint32_t nb = live ? (uint32_t)((len + 8u) / 64u + 1u) : 0u;  // blocks incl. padding
+    const uint32_t nfull = (uint32_t)(len >> 6);
+    const uint32_t nbmax = __reduce_max_sync(0xFFFFFFFFu, nb);
+    const uintptr_t w16 = a & ~uintptr_t(15);
+    const uintptr_t end16 = (a + len + 15u) & ~uintptr_t(15);  // message bytes live in [w16, end16)
+    const uint32_t slot = smem_u32(&ring[warp][0][0]) + lane * kSlot;
+    auto issue = [&](uint32_t b) {
+        const uint32_t s = b % STAGES;
+        const uintptr_t ws = w16 + 64u * (uintptr_t)b;
+        // only blocks holding message bytes are fetched (b <= nfull); at most 80 bytes
+        const uint32_t bytes = (b > nfull || ws >= end16) ? 0u
+                               : (end16 - ws >= 80u ? 80u : (uint32_t)(end16 - ws));
+        mbar_arrive_expect_tx(&bars[warp][s], bytes);
+        if (bytes) bulk_copy_g2s(slot + s * kStage, reinterpret_cast<const void*>(ws), bytes, &bars[warp][s]);
+    };
+#pragma unroll
+    for (int k = 0; k < STAGES - 1; ++k)
+        if ((uint32_t)k < nbmax) issue(k);
+
+    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
+    const uint32_t r = (uint32_t)(len & 63u);
+    const uint64_t bits = len * 8ull;
+    const uint32_t l14 = H::kBigEndian ? bswap((uint32_t)(bits >> 32)) : (uint32_t)bits;
+    const uint32_t l15 = H::kBigEndian ? bswap((uint32_t)bits) : (uint32_t)(bits >> 32);
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    for (uint32_t b = 0; b < nbmax; ++b) {
+        if (b + STAGES - 1 < nbmax) {
+            fence_proxy_async_smem();  // this lane's generic reads of the stage happened before (syncwarp below)
+            issue(b + STAGES - 1);
+        }
+        const uint32_t s = b % STAGES;
+        mbar_wait_parity(&bars[warp][s], (b / STAGES) & 1u);
+        uint32_t c[20];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            uint32_t x, y, z, w;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+                         : "r"(slot + s * kStage + 16u * k)
+                         : "memory");
+            c[4 * k] = x; c[4 * k + 1] = y; c[4 * k + 2] = z; c[4 * k + 3] = w;
+        }
+        __syncwarp();  // every lane has read stage s before it is refilled
+        if (b < nb) {
+            uint32_t raw[16];
+            realign16(c, q, sh, raw);
+            if (b >= nfull) {  // the last one or two blocks: keep bytes [0, r) (none after), 0x80, length
+                mask_tail(raw, b == nfull ? r : 0u);
+                const uint32_t pad = b == nfull ? 0x80u << ((r & 3u) * 8u) : 0u, pw = r >> 2;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) raw[j] |= (pw == (uint32_t)j) ? pad : 0u;
+                if (b == nb - 1u) { raw[14] = l14; raw[15] = l15; }
+            }
+            compress1<ALG>(st, raw);
+        }
+    }
+    if (live) store_digest<ALG>(out + i * H::kDigestBytes, st);
+}
+
+// -------------------------------------------------------------------------
 // Variable-length kernel, warp-cooperative staging (the default).
 //
 // A warp owns 32 messages (after the length sort: equal block counts and the
@@ -960,6 +1058,14 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
             k_varlen_coop<ALG, 4, 5, 0><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
         else
             k_varlen_coop<ALG, 4, 5, 256><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
+    } else if (env_u64("HB_VARLEN_BULK", 0)) {  // per-lane TMA bulk copies (A/B)
+        const unsigned g = (unsigned)((n + 127) / 128);
+        switch (env_u64("HB_VARLEN_BULK", 0)) {  // ring depth x register cap
+        case 2: k_varlen_bulk<ALG, 2, 1><<<g, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out); break;
+        case 4: k_varlen_bulk<ALG, 3, 6><<<g, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out); break;
+        case 5: k_varlen_bulk<ALG, 2, 8><<<g, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out); break;
+        default: k_varlen_bulk<ALG, 3, 1><<<g, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out); break;
+        }
     } else if (env_u64("HB_VARLEN_PREFETCH", 0)) {  // per-thread 128-bit loads, software-pipelined
         k_varlen16<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
     } else {  // per-thread 128-bit loads

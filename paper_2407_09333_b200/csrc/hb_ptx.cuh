@@ -63,6 +63,16 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 // `src_bytes` (0..16) bytes are read, the rest of the 16 written as zero.
 // The L2::256B hint lets L2 fetch a whole 256-byte line per miss (a message
 // is read 64 bytes per step; the next steps then hit L2).
+// 1-D bulk async copy (TMA engine, no tensor map) global -> shared; `bytes` a
+// multiple of 16, both addresses 16-byte aligned; completion as tx bytes on
+// `bar`.  The copy bypasses the LSU/L1 data pipe entirely.
+__device__ __forceinline__ void bulk_copy_g2s(uint32_t dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_smem),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <int PF = 256>
 __device__ __forceinline__ void cp_async16_zfill(uint32_t dst_smem, const void* src, uint32_t src_bytes) {
     if constexpr (PF == 256)

@@ -108,7 +108,7 @@ def test_varlen_golden(golden):
             assert sha(batch_digest_varlen(alg, data, off)) == row[alg]
 
 
-@pytest.mark.parametrize("sort", ["window4096", "window16384", "global", "prefetch"])
+@pytest.mark.parametrize("sort", ["window4096", "window16384", "global", "prefetch", "bulk"])
 @pytest.mark.parametrize("alg", ALGS)
 def test_varlen_random_sorted_and_unsorted(alg, sort, monkeypatch):
     monkeypatch.setenv("HB_VARLEN_SORT", "global" if sort == "global" else "window")
@@ -116,6 +116,8 @@ def test_varlen_random_sorted_and_unsorted(alg, sort, monkeypatch):
         monkeypatch.setenv("HB_SORT_WINDOW", sort[6:])
     if sort == "prefetch":
         monkeypatch.setenv("HB_VARLEN_PREFETCH", "1")
+    if sort == "bulk":
+        monkeypatch.setenv("HB_VARLEN_BULK", "2")
     rng = np.random.default_rng(12)
     n = 20000  # above the sort threshold
     lens = rng.integers(0, 4097, n).astype(np.uint64)
@@ -343,7 +345,8 @@ def test_varlen_every_length_and_alignment(alg, monkeypatch):
                 assert np.array_equal(got, ref[:k]), (alg, shift, k, fl)
         C = _native.HB_FLAG_VARLEN_COOP
         for env, fl in (({"HB_VC_STAGES": "3"}, C), ({"HB_VC_STAGES": "2"}, C), ({"HB_VC_PF": "128"}, C),
-                        ({"HB_VC_PF": "0"}, C), ({"HB_VARLEN_PREFETCH": "1"}, 0)):
+                        ({"HB_VC_PF": "0"}, C), ({"HB_VARLEN_PREFETCH": "1"}, 0), ({"HB_VARLEN_BULK": "3"}, 0),
+                        ({"HB_VARLEN_BULK": "5"}, 0)):
             for key, v in env.items():
                 monkeypatch.setenv(key, v)
             got = batch_digest_varlen(alg, buf, off, flags=fl)
@@ -410,3 +413,31 @@ def test_out_argument_reuse_and_pinned():
             assert np.array_equal(dec, oracle.batch_fixed(alg, gen_messages(5, n, 9).as_array(), threads=8))
     finally:
         lib.hb_free_pinned(hp)
+
+
+def test_concurrent_callers_thread_safe():
+    """The reference calls the boundary from pool threads (_fast_digest,
+    executor.py:596-599; hash_batch's ThreadPool, batch.py:310-313): concurrent
+    engine calls from many threads (GIL released in ctypes) must each get
+    their own correct digests."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    jobs = []
+    for k in range(24):
+        alg = ALGS[k % 3]
+        n, L = 500 + 37 * k, [64, 100, 1024, 9, 200][k % 5]
+        data = oracle.fill_random(n * L, 1000 + k).reshape(n, L)
+        jobs.append((alg, data, oracle.batch_fixed(alg, data, threads=4)))
+    lens = np.random.default_rng(9).integers(0, 3000, 1500).astype(np.uint64)
+    off = np.zeros(len(lens) + 1, np.uint64)
+    off[1:] = np.cumsum(lens)
+    vdata = oracle.fill_random(int(off[-1]), 55)
+    vref = {a: oracle.batch_varlen(a, vdata, off, threads=4) for a in ALGS}
+
+    def run(j):
+        alg, data, ref = jobs[j]
+        ok = np.array_equal(batch_digest(alg, data), ref)
+        return ok and np.array_equal(batch_digest_varlen(alg, vdata, off), vref[alg])
+
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        assert all(ex.map(run, range(len(jobs))))

@@ -23,19 +23,19 @@ d_off = torch.from_numpy(off).cuda()
 scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch.uint8, device="cuda:0")
 C = _native.HB_FLAG_VARLEN_COOP
 P = _native.HB_FLAG_VARLEN_COOP_OFF
-ARMS = {"default": ({}, 0), "prefetch": ({"HB_VARLEN_PREFETCH": "1"}, 0),
-        "prefetch_win4k": ({"HB_VARLEN_PREFETCH": "1", "HB_SORT_WINDOW": "4096"}, 0),
-        "prefetch_global": ({"HB_VARLEN_PREFETCH": "1", "HB_VARLEN_SORT": "global"}, 0),
-        "thread_win4k": ({"HB_VARLEN_SORT": "window", "HB_SORT_WINDOW": "4096"}, P),
-        "thread_win8k": ({"HB_VARLEN_SORT": "window", "HB_SORT_WINDOW": "8192"}, P),
-        "thread_win16k": ({"HB_VARLEN_SORT": "window", "HB_SORT_WINDOW": "16384"}, P),
+ARMS = {"default": ({}, 0),
+        "bulk_s3": ({"HB_VARLEN_BULK": "3"}, 0), "bulk_s2": ({"HB_VARLEN_BULK": "2"}, 0),
+        "bulk_s3_minb6": ({"HB_VARLEN_BULK": "4"}, 0), "bulk_s2_minb8": ({"HB_VARLEN_BULK": "5"}, 0),
+        "bulk_s3_global": ({"HB_VARLEN_BULK": "3", "HB_VARLEN_SORT": "global"}, 0),
+        "bulk_s3_win4k": ({"HB_VARLEN_BULK": "3", "HB_SORT_WINDOW": "4096"}, 0),
         "thread_global": ({"HB_VARLEN_SORT": "global"}, P),
         "coop_s4_global": ({"HB_VARLEN_SORT": "global"}, C)}
 for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
     ref, times = None, {}
     for _ in range(3):
         for arm, (env, flags) in ARMS.items():
-            for k in ("HB_VC_STAGES", "HB_VC_PF", "HB_VARLEN_SORT", "HB_SORT_WINDOW", "HB_VARLEN_PREFETCH"):
+            for k in ("HB_VC_STAGES", "HB_VC_PF", "HB_VARLEN_SORT", "HB_SORT_WINDOW", "HB_VARLEN_PREFETCH",
+                      "HB_VARLEN_BULK"):
                 os.environ.pop(k, None)
             os.environ.update(env)
             out = torch.empty((n, DLEN[alg]), dtype=torch.uint8, device="cuda:0")
