@@ -528,7 +528,9 @@ k_varlen16(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offset
 // cp.async.bulk into its slot of a per-warp STAGES-deep ring; completion is
 // counted on the stage's mbarrier (32 arrivals + tx bytes).  Lanes then read
 // their slot with LDS.128 (conflict-free at an 80-byte stride), realign,
-// apply padding in registers and compress.
+// apply padding in registers and compress.  Opt-in ($HB_VARLEN_BULK): on the
+// B200 the TMA engine does not keep up with 32 tiny (<= 80 B) copies per warp
+// step -- 3.9-4.2 vs 2.06 ms for MD5 at configs[3] (profiles/ab_varlen_r1e.txt).
 // -------------------------------------------------------------------------
 template <int ALG, int STAGES, int MINB = 1>
 __global__ void __launch_bounds__(128, MINB)
