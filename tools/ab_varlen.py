@@ -24,12 +24,10 @@ scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch
 C = _native.HB_FLAG_VARLEN_COOP
 P = _native.HB_FLAG_VARLEN_COOP_OFF
 ARMS = {"default": ({}, 0),
-        "bulk_s3": ({"HB_VARLEN_BULK": "3"}, 0), "bulk_s2": ({"HB_VARLEN_BULK": "2"}, 0),
-        "bulk_s3_minb6": ({"HB_VARLEN_BULK": "4"}, 0), "bulk_s2_minb8": ({"HB_VARLEN_BULK": "5"}, 0),
-        "bulk_s3_global": ({"HB_VARLEN_BULK": "3", "HB_VARLEN_SORT": "global"}, 0),
-        "bulk_s3_win4k": ({"HB_VARLEN_BULK": "3", "HB_SORT_WINDOW": "4096"}, 0),
-        "thread_global": ({"HB_VARLEN_SORT": "global"}, P),
-        "coop_s4_global": ({"HB_VARLEN_SORT": "global"}, C)}
+        "coop_s3_win8k": ({"HB_VC_STAGES": "3"}, C), "coop_s3_win16k": ({"HB_VC_STAGES": "3", "HB_SORT_WINDOW": "16384"}, C),
+        "coop_s4_win16k": ({"HB_SORT_WINDOW": "16384"}, C),
+        "coop_s3_global": ({"HB_VC_STAGES": "3", "HB_VARLEN_SORT": "global"}, C),
+        "thread_win16k": ({"HB_SORT_WINDOW": "16384"}, P)}
 for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
     ref, times = None, {}
     for _ in range(3):
