@@ -141,3 +141,24 @@ def test_run_point_gpu_splits():
             assert r.digests == ref, (mem, ratios)
             if mem == 100000 and ratios == (0.5, 0.5):
                 assert all(b > 1 for b in r.batches.values())
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference package not present (authoring container only)")
+def test_from_reference_device_table():
+    """A reference DeviceTable maps onto GPUs with its capacities kept; a
+    host-mapped accelerator is refused (no CPU hash path)."""
+    from paper_2407_09333_b200.runtime import DeviceConfigError, from_reference
+
+    sys.path.insert(0, REF_SRC)
+    try:
+        from hetoc.runtime.devices import DeviceSpec as RSpec, DeviceTable as RTable
+    finally:
+        sys.path.remove(REF_SRC)
+    ref = RTable(RSpec("host", kind="host", threads=8, sha_accel=True),
+                 (RSpec("gpu0", mem_bytes=5000), RSpec("gpu1", mem_bytes=1 << 20, sha_accel=True)))
+    t = from_reference(ref, {"gpu1": 3})
+    assert [(a.id, a.kind, a.ordinal, a.mem_bytes, a.sha_accel) for a in t.accels] == \
+        [("gpu0", "cuda", 0, 5000, False), ("gpu1", "cuda", 3, 1 << 20, True)]
+    assert t.host.sha_accel and t.host.threads == 8
+    with pytest.raises(DeviceConfigError):
+        from_reference(RTable(RSpec("host", kind="host"), (RSpec("acc", host_mapped=True),)))
