@@ -760,7 +760,12 @@ __device__ __forceinline__ uint32_t sort_bucket(const uint64_t* offsets, uint64_
 // gen_messages (batch.py:86-99): message i is the zero-padded decimal
 // rendering of start+i, WIDTH bytes.  The bytes are built in registers and
 // hashed directly; only digests touch HBM.
-template <int ALG, int WIDTH, int V = -1>
+// FMA_DIGITS: below 2^30 the digits are produced entirely on the FMA pipe --
+// q = umulhi(v, 0x1999999A) is exactly v / 10 for v < 2^30 (the reciprocal's
+// excess 0.4 * v / 2^32 stays under 0.1), d = v - 10 q, and each digit is
+// placed with a multiply by an opaque 2^(8k) -- leaving the ALU pipe (the
+// bottleneck: booleans, rotates) to the compression.
+template <int ALG, int WIDTH, int V = -1, bool FMA_DIGITS = false>
 __global__ void __launch_bounds__(128) k_decimal(uint64_t start, uint64_t count, uint8_t* __restrict__ out) {
     using H = HashAlg<ALG, V>;
     static_assert(WIDTH >= 1 && WIDTH <= 20, "width");
@@ -772,7 +777,25 @@ __global__ void __launch_bounds__(128) k_decimal(uint64_t start, uint64_t count,
     uint32_t raw[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) raw[j] = 0u;
-    if (start + count <= 0xFFFFFFFFull) {  // grid-uniform: 32-bit digit extraction (IMAD.HI, not 64-bit division)
+    if (FMA_DIGITS && WIDTH <= 9 && start + count <= (1ull << 30)) {  // grid-uniform
+        uint32_t v32 = (uint32_t)v;
+#pragma unroll
+        for (int pos = WIDTH - 1; pos >= 0; --pos) {  // batch.py:96-98
+            const uint32_t q = __umulhi(v32, 0x1999999Au);
+            const uint32_t d = v32 - q * 10u;
+            raw[pos >> 2] = d * c_opaque[8 * (pos & 3)] + raw[pos >> 2];  // IMAD: d << 8(pos%4)
+            v32 = q;
+        }
+        // the '0' (0x30) of every digit byte, as one add per word (compile-time constants)
+#pragma unroll
+        for (int w = 0; w < (WIDTH + 3) / 4; ++w) {
+            uint32_t ascii = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (4 * w + k < WIDTH) ascii |= 0x30u << (8 * k);
+            raw[w] += ascii;
+        }
+    } else if (start + count <= 0xFFFFFFFFull) {  // grid-uniform: 32-bit digit extraction (IMAD.HI, not 64-bit division)
         uint32_t v32 = (uint32_t)v;
 #pragma unroll
         for (int pos = WIDTH - 1; pos >= 0; --pos) {  // batch.py:96-98
@@ -1080,7 +1103,17 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
 template <int ALG, int W>
 static void dec_launch(uint64_t start, uint64_t count, uint8_t* d_out, cudaStream_t s) {
     const unsigned grid = (unsigned)((count + 127) / 128);
-    switch (env_u64("HB_CONST_VARIANT", 1)) {  // round variant (A/B; 1 = tuned default)
+    // Defaults (B200, profiles/ab_decimal_r1c.txt): FMA-pipe digits, round
+    // variant 1 (SHA-1: 3).  $HB_FMA_DIGITS=0 / $HB_CONST_VARIANT select A/B arms.
+    const uint64_t v = env_u64("HB_CONST_VARIANT", ALG == kSha1 ? 3 : 1);
+    if (env_u64("HB_FMA_DIGITS", 1) && (v == 1 || v == 3)) {
+        if (v == 3)
+            k_decimal<ALG, W, kVarBal3, true><<<grid, 128, 0, s>>>(start, count, d_out);
+        else
+            k_decimal<ALG, W, kVarBal, true><<<grid, 128, 0, s>>>(start, count, d_out);
+        return;
+    }
+    switch (v) {  // round variant (A/B)
     case 0: k_decimal<ALG, W, kVarPlain><<<grid, 128, 0, s>>>(start, count, d_out); break;
     case 2: k_decimal<ALG, W, kVarBal2><<<grid, 128, 0, s>>>(start, count, d_out); break;
     case 3: k_decimal<ALG, W, kVarBal3><<<grid, 128, 0, s>>>(start, count, d_out); break;

@@ -182,9 +182,21 @@ def test_ratio_invariance_style_sharding():
         assert np.array_equal(batch_digest(alg, data, gpus=list(range(n)) + [0]), ref)  # uneven split, repeated dev
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "fma_digits"])
 def test_decimal_workload(golden, variant, monkeypatch):
-    monkeypatch.setenv("HB_CONST_VARIANT", variant)
+    monkeypatch.setenv("HB_FMA_DIGITS", "0")
+    if variant == "fma_digits":
+        monkeypatch.setenv("HB_FMA_DIGITS", "1")
+        # the FMA digit path ends at index 2^30; straddle it and check every width it serves
+        for w in range(1, 10):
+            for start, cnt in ((max(0, 10**w - 300), min(300, 10**w)), (2**30 - 150, 300)):
+                if start + cnt > 10**w:
+                    continue
+                for alg in ALGS:
+                    assert np.array_equal(hash_decimal(alg, start, cnt, w),
+                                          oracle.batch_fixed(alg, oracle.gen_decimal(start, cnt, w))), (alg, w, start)
+    else:
+        monkeypatch.setenv("HB_CONST_VARIANT", variant)
     # the 32-bit digit path ends exactly at index 2^32 - 1; straddle it
     start, cnt = 2**32 - 150, 300
     for alg in ALGS:
