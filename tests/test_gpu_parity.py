@@ -188,7 +188,8 @@ def test_decimal_workload(golden, variant, monkeypatch):
     if variant == "fma_digits":
         monkeypatch.setenv("HB_FMA_DIGITS", "1")
         # the FMA digit path ends at index 2^30; straddle it and check every width it serves
-        for w in range(1, 10):
+        for w, v in [(w, v) for w in range(1, 10) for v in ("1", "3")]:
+            monkeypatch.setenv("HB_CONST_VARIANT", v)
             for start, cnt in ((max(0, 10**w - 300), min(300, 10**w)), (2**30 - 150, 300)):
                 if start + cnt > 10**w:
                     continue
