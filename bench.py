@@ -47,7 +47,8 @@ WORKLOADS = {
     # name: (alg | "varlen:"alg, n per GPU, msg_len | max varlen length, seed, BASELINE config)
     "md5_1k": ("md5", 1 << 24, 1024, 2, "configs[1]: MD5 over 2^24 random 1 KiB messages per B200"),
     "sha1_1k": ("sha1", 1 << 24, 1024, 2, "SHA-1 over 2^24 random 1 KiB messages per B200 (configs[4] point)"),
-    "sm3_1k": ("sm3", 1 << 24, 1024, 3, "configs[2]: SM3 over 2^24 random 1 KiB messages per B200"),
+    "sm3_1k": ("strong:sm3", 1 << 24, 1024, 3,
+               "configs[2]: SM3 over 2^24 random 1 KiB messages sharded by message range across the GPUs"),
     "sha1_64": ("sha1", 65536, 64, 1, "configs[0]: SHA-1 over 65,536 random 64-byte messages"),
     "varlen_md5": ("varlen:md5", 1 << 22, 4096, 4, "configs[3]: mixed variable-length batch, uniform 1 B-4 KiB"),
     "varlen_sha1": ("varlen:sha1", 1 << 22, 4096, 4, "configs[3]: mixed variable-length batch, uniform 1 B-4 KiB"),
@@ -199,15 +200,25 @@ class FixedWorkload:
 
     kind = "fixed"
 
-    def __init__(self, name, alg, n, L, seed, desc, rank, local):
+    def __init__(self, name, alg, n, L, seed, desc, rank, local, world=1, strong=False):
         import torch
 
         from paper_2407_09333_b200 import device
+        from paper_2407_09333_b200.passes import partition_range
 
-        self.name, self.alg, self.n, self.L, self.seed, self.desc = name, alg, n, L, seed, desc
+        self.name, self.alg, self.L, self.seed, self.desc = name, alg, L, seed, desc
+        self.scaling = "strong" if strong else "weak"
+        if strong:  # configs[2]: the SAME 2^24 messages split over the GPUs by message range
+            lo, hi = partition_range(0, n, [1.0 / world] * world)[rank]
+            self.total = n
+        else:  # n messages per GPU: rank r hashes global messages [r*n, (r+1)*n)
+            lo, hi = rank * n, (rank + 1) * n
+            self.total = world * n
+        n = hi - lo
+        self.n, self.lo = n, lo
         self.dlen = DLEN[alg]
         self.buf = torch.empty(n * L, dtype=torch.uint8, device=f"cuda:{local}")
-        device.fill_random(self.buf, seed, byte_offset=rank * n * L)  # global messages [rank*n, (rank+1)*n)
+        device.fill_random(self.buf, seed, byte_offset=lo * L)
         self.msgs = self.buf.view(n, L)
         self.out = torch.empty((n, self.dlen), dtype=torch.uint8, device=f"cuda:{local}")
         self.msg_bytes = n * L
@@ -253,8 +264,10 @@ class FixedWorkload:
         return batch_digest(self.alg, self._host, gpus=[local], timing=tim, out=self._out_host)
 
     def config(self, world):
-        return {"workload": f"{self.alg} {self.n} x {self.L} B fixed-width per GPU ({self.desc})", "alg": self.alg,
-                "msgs_per_gpu": self.n, "msg_len": self.L, "global_batch_msgs": world * self.n,
+        what = (f"{self.alg} {self.total} x {self.L} B fixed-width, split over the GPUs" if self.scaling == "strong"
+                else f"{self.alg} {self.n} x {self.L} B fixed-width per GPU")
+        return {"workload": f"{what} ({self.desc})", "alg": self.alg,
+                "msgs_per_gpu": self.n, "msg_len": self.L, "global_batch_msgs": self.total,
                 "parallelism": f"message-range shards over {world} GPU(s), no collective",
                 "l2": "inputs are %.1f GiB per GPU >> 126 MB L2; no flush needed" % (self.n * self.L / 2**30)}
 
@@ -279,13 +292,14 @@ class VarlenWorkload:
 
     kind = "varlen"
 
-    def __init__(self, name, alg, n, maxlen, seed, desc, rank, local):
+    def __init__(self, name, alg, n, maxlen, seed, desc, rank, local, world=1):
         import numpy as np
         import torch
 
         from paper_2407_09333_b200 import _native, device
 
         self.name, self.alg, self.n, self.maxlen, self.seed, self.desc = name, alg, n, maxlen, seed, desc
+        self.total = world * n
         self.dlen = DLEN[alg]
         lens = np.random.default_rng(seed + 1000 * rank).integers(1, maxlen + 1, n).astype(np.uint64)
         self.off = np.zeros(n + 1, np.uint64)
@@ -424,8 +438,10 @@ def make_workload(name, rank, local, n_override=0, world=1):
     n = n_override or spec[1]
     if spec[0].startswith("decimal:"):
         return DecimalWorkload(name, alg, n, spec[2], spec[3], spec[4], rank, local, world)
-    cls = VarlenWorkload if spec[0].startswith("varlen:") else FixedWorkload
-    return cls(name, alg, n, spec[2], spec[3], spec[4], rank, local)
+    if spec[0].startswith("varlen:"):
+        return VarlenWorkload(name, alg, n, spec[2], spec[3], spec[4], rank, local, world)
+    return FixedWorkload(name, alg, n, spec[2], spec[3], spec[4], rank, local, world,
+                         strong=spec[0].startswith("strong:"))
 
 
 def h2d_peak(buf_bytes: int, local: int, d2h: bool = False) -> float:
@@ -485,8 +501,8 @@ def run_ours(args):
     per_step = [s.elapsed_time(e) for s, e in evs]
     ms_local = sum(per_step) / len(per_step)
     ms = reduce_max(ms_local, world, local)
-    total_msgs = getattr(w, "total", None) if w.kind == "decimal" else world * w.n
-    total_bytes = total_msgs * w.msg_bytes // max(w.n, 1) if w.kind == "decimal" else world * w.msg_bytes
+    total_msgs = w.total  # messages hashed by all ranks in one step
+    total_bytes = w.msg_bytes * world if w.kind == "varlen" else total_msgs * (w.L if w.kind == "fixed" else w.width)
     value = total_bytes / (ms * 1e-3) / 1e9
     mhash = total_msgs / (ms * 1e-3) / 1e6
     log(f"[rank {rank}] kernel-only {w.name}: {ms_local:.3f} ms/step (min {min(per_step):.3f}, "
@@ -528,9 +544,15 @@ def run_ours(args):
             ok = bool(np.array_equal(res[idx], w.out[torch.from_numpy(idx).to(w.out.device)].cpu().numpy()))
         bw = h2d_peak(max(w.h2d_bytes, w.d2h_bytes), local, d2h=w.h2d_bytes < w.d2h_bytes)
         e2e_gbs = total_bytes / (e2e_ms * 1e-3) / 1e9
-        h2d_gbs = world * max(w.h2d_bytes, w.d2h_bytes) / (e2e_ms * 1e-3) / 1e9
+        # per-step bytes over all ranks (fixed/decimal: exact from the global message count)
+        if w.kind == "varlen":
+            h2d_tot, d2h_tot = world * w.h2d_bytes, world * w.d2h_bytes
+        else:
+            h2d_tot = w.total * w.L if w.kind == "fixed" else 0
+            d2h_tot = w.total * w.dlen
+        h2d_gbs = max(h2d_tot, d2h_tot) / (e2e_ms * 1e-3) / 1e9
         e2e = {"value": round(e2e_gbs, 3), "unit": "GB/s",
-               "h2d_bytes_per_step": world * w.h2d_bytes, "d2h_bytes_per_step": world * w.d2h_bytes,
+               "h2d_bytes_per_step": h2d_tot, "d2h_bytes_per_step": d2h_tot,
                "ms_per_step": round(e2e_ms, 3), "mhash_per_s": round(total_msgs / (e2e_ms * 1e-3) / 1e6, 2),
                "api": ("paper_2407_09333_b200.crypto.batch_digest(pinned host array, out=pinned) -> hb_hash_fixed"
                        if w.kind == "fixed" else
@@ -655,8 +677,11 @@ def run_reference(args):
         run = lambda: oracle.batch_fixed(alg, data, threads=threads)  # noqa: E731
         nbytes = rows * L
         sample = f"{rows} of the {n} x {L} B messages per step"
-        config = {"workload": f"{alg} {n} x {L} B fixed-width per GPU ({cfg_desc})", "alg": alg,
-                  "msgs_per_gpu": n, "msg_len": L}
+        strong = spec[0].startswith("strong:")
+        what = (f"{alg} {n} x {L} B fixed-width, split over the GPUs" if strong
+                else f"{alg} {n} x {L} B fixed-width per GPU")
+        config = {"workload": f"{what} ({cfg_desc})", "alg": alg, "msgs_per_gpu": n // world if strong else n,
+                  "msg_len": L}
     for _ in range(args.warmup):
         run()
     times = []
@@ -666,11 +691,11 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
     value = nbytes / t / 1e9
-    dec = spec[0].startswith("decimal:")
+    dec = spec[0].startswith("decimal:") or spec[0].startswith("strong:")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
             "scaling": "strong" if dec else "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "paper workload: decimal messages (gen_messages)" if dec else
+            "data": "paper workload: decimal messages (gen_messages)" if spec[0].startswith("decimal:") else
                     f"synthetic: counter-based splitmix64 bytes (seed {seed})", "config": config,
             "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "port",
                              "sample": f"{sample}, oracle/hetoc_oracle.c (C restatement of hetoc.crypto) "
