@@ -210,10 +210,10 @@ class FixedWorkload:
         self.scaling = "strong" if strong else "weak"
         if strong:  # configs[2]: the SAME 2^24 messages split over the GPUs by message range
             lo, hi = partition_range(0, n, [1.0 / world] * world)[rank]
-            self.total = n
+            self.total_msgs = n
         else:  # n messages per GPU: rank r hashes global messages [r*n, (r+1)*n)
             lo, hi = rank * n, (rank + 1) * n
-            self.total = world * n
+            self.total_msgs = world * n
         n = hi - lo
         self.n, self.lo = n, lo
         self.dlen = DLEN[alg]
@@ -264,10 +264,10 @@ class FixedWorkload:
         return batch_digest(self.alg, self._host, gpus=[local], timing=tim, out=self._out_host)
 
     def config(self, world):
-        what = (f"{self.alg} {self.total} x {self.L} B fixed-width, split over the GPUs" if self.scaling == "strong"
+        what = (f"{self.alg} {self.total_msgs} x {self.L} B fixed-width, split over the GPUs" if self.scaling == "strong"
                 else f"{self.alg} {self.n} x {self.L} B fixed-width per GPU")
         return {"workload": f"{what} ({self.desc})", "alg": self.alg,
-                "msgs_per_gpu": self.n, "msg_len": self.L, "global_batch_msgs": self.total,
+                "msgs_per_gpu": self.n, "msg_len": self.L, "global_batch_msgs": self.total_msgs,
                 "parallelism": f"message-range shards over {world} GPU(s), no collective",
                 "l2": "inputs are %.1f GiB per GPU >> 126 MB L2; no flush needed" % (self.n * self.L / 2**30)}
 
@@ -299,7 +299,7 @@ class VarlenWorkload:
         from paper_2407_09333_b200 import _native, device
 
         self.name, self.alg, self.n, self.maxlen, self.seed, self.desc = name, alg, n, maxlen, seed, desc
-        self.total = world * n
+        self.total_msgs = world * n
         self.dlen = DLEN[alg]
         lens = np.random.default_rng(seed + 1000 * rank).integers(1, maxlen + 1, n).astype(np.uint64)
         self.off = np.zeros(n + 1, np.uint64)
@@ -382,7 +382,7 @@ class DecimalWorkload:
         from paper_2407_09333_b200.passes import partition_range
 
         self.name, self.alg, self.width, self.seed, self.desc, self.local = name, alg, width, seed, desc, local
-        self.total = n
+        self.total = self.total_msgs = n
         self.start, end = partition_range(0, n, [1.0 / world] * world)[rank]
         self.n = end - self.start
         self.dlen = DLEN[alg]
@@ -501,7 +501,7 @@ def run_ours(args):
     per_step = [s.elapsed_time(e) for s, e in evs]
     ms_local = sum(per_step) / len(per_step)
     ms = reduce_max(ms_local, world, local)
-    total_msgs = w.total  # messages hashed by all ranks in one step
+    total_msgs = w.total_msgs  # messages hashed by all ranks in one step
     total_bytes = w.msg_bytes * world if w.kind == "varlen" else total_msgs * (w.L if w.kind == "fixed" else w.width)
     value = total_bytes / (ms * 1e-3) / 1e9
     mhash = total_msgs / (ms * 1e-3) / 1e6
@@ -548,8 +548,8 @@ def run_ours(args):
         if w.kind == "varlen":
             h2d_tot, d2h_tot = world * w.h2d_bytes, world * w.d2h_bytes
         else:
-            h2d_tot = w.total * w.L if w.kind == "fixed" else 0
-            d2h_tot = w.total * w.dlen
+            h2d_tot = w.total_msgs * w.L if w.kind == "fixed" else 0
+            d2h_tot = w.total_msgs * w.dlen
         h2d_gbs = max(h2d_tot, d2h_tot) / (e2e_ms * 1e-3) / 1e9
         e2e = {"value": round(e2e_gbs, 3), "unit": "GB/s",
                "h2d_bytes_per_step": h2d_tot, "d2h_bytes_per_step": d2h_tot,
