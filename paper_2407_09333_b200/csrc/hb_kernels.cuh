@@ -960,6 +960,8 @@ static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t 
     if (cfg == kCfgWs3) {
         switch (v) {
         case 0: return launch_fixed_tma_ws<ALG, 0, 1, 3>(src, n, L, dst, s);
+        case 2: return launch_fixed_tma_ws<ALG, 2, 1, 3>(src, n, L, dst, s);
+        case 3: return launch_fixed_tma_ws<ALG, 3, 1, 3>(src, n, L, dst, s);
         default: return launch_fixed_tma_ws<ALG, 1, 1, 3>(src, n, L, dst, s);
         }
     }

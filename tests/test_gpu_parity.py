@@ -293,7 +293,7 @@ def test_tma_tile_configs_and_variants(cfg, monkeypatch):
     """Every compiled TMA tile configuration x round variant is bit-exact
     (the tuned default is only one of them; $HB_TMA_CFG/$HB_VARIANT select)."""
     variants = (["0", "1", "2", "3"] if cfg == "1x3" else ["1", "3"] if cfg.endswith("x2") and cfg.startswith("ws")
-                else ["0", "1"] if cfg.startswith("ws") else ["0", "1", "2"])
+                else ["0", "1", "2", "3"] if cfg == "ws3" else ["0", "1"] if cfg.startswith("ws") else ["0", "1", "2"])
     monkeypatch.setenv("HB_TMA_CFG", cfg)
     for L in (16, 48, 64, 112, 128, 1024, 1040):
         n = 333

@@ -22,7 +22,7 @@ from paper_2407_09333_b200 import device  # noqa: E402
 
 n = int(os.environ.get("SWEEP_N", 1 << 24))
 L = int(os.environ.get("SWEEP_L", 1024))
-steps = 10
+steps = int(os.environ.get("SWEEP_STEPS", 10))
 rounds = int(os.environ.get("SWEEP_ROUNDS", 3))
 cfgs = os.environ.get("SWEEP_CFGS", "1x3,1x2,ws2,ws3").split(",")
 vars_ = list(os.environ.get("SWEEP_VARS", "01"))
