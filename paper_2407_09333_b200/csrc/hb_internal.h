@@ -20,7 +20,7 @@ cudaError_t launch_fixed(int alg, const uint8_t* d_msgs, uint64_t n, uint64_t ms
 // when not sorting: HB_FLAG_NO_SORT, small n or no scratch).
 cudaError_t launch_varlen_sort(int alg, const uint8_t* d_data, const uint64_t* d_offsets, uint64_t offset_base,
                                uint64_t n, void* d_scratch, cudaStream_t stream, uint32_t flags,
-                               const uint32_t** perm_out);
+                               const uint32_t** perm_out, int qclasses = 4);
 
 // Scratch bytes launch_varlen needs for n messages (length-bucket sort).
 uint64_t varlen_scratch_bytes(uint64_t n);

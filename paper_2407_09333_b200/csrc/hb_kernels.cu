@@ -112,14 +112,15 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const uint64_t* _
 // other: L2 lines fetched for one message (256 B promotion) are still
 // resident when its neighbours are hashed, instead of being re-fetched from
 // HBM after a global sort scattered the neighbours across the whole batch.
-template <int kSortWindow>
+template <int kSortWindow, int Q>
 __global__ void __launch_bounds__(1024) k_sort_window(const uint64_t* __restrict__ offsets, uint64_t n,
                                                       uint64_t addr_bias, uint32_t* __restrict__ perm) {
-    __shared__ uint32_t h[kSortBuckets];
+    constexpr int kBuckets = kSortNbClasses * Q;
+    __shared__ uint32_t h[kBuckets];
     __shared__ uint32_t wsum[32];
     const uint32_t t = threadIdx.x;
     const uint64_t w0 = (uint64_t)blockIdx.x * kSortWindow;
-    for (int k = t; k < kSortBuckets; k += 1024) h[k] = 0;
+    for (int k = t; k < kBuckets; k += 1024) h[k] = 0;
     __syncthreads();
     constexpr int kItems = kSortWindow / 1024;
     uint32_t key[kItems], rank[kItems];
@@ -128,13 +129,13 @@ __global__ void __launch_bounds__(1024) k_sort_window(const uint64_t* __restrict
         const uint64_t i = w0 + (uint64_t)it * 1024u + t;
         key[it] = 0xFFFFFFFFu;
         if (i < n) {
-            key[it] = sort_bucket(offsets, i, addr_bias);
+            key[it] = sort_bucket_q<Q>(offsets, i, addr_bias);
             rank[it] = atomicAdd(&h[key[it]], 1u);
         }
     }
     __syncthreads();
-    // exclusive scan of the 4,096 bucket counts; thread t owns buckets 4t..4t+3
-    constexpr int kPer = kSortBuckets / 1024;
+    // exclusive scan of the bucket counts; thread t owns buckets kPer*t .. kPer*t + kPer-1
+    constexpr int kPer = kBuckets / 1024;
     uint32_t v[kPer], sum = 0;
 #pragma unroll
     for (int k = 0; k < kPer; ++k) { v[k] = h[kPer * t + k]; sum += v[k]; }
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(1024) k_sort_window(const uint64_t* __restrict
 // sorting).  Shared by the per-algorithm translation units.
 cudaError_t launch_varlen_sort(int alg, const uint8_t* d_data, const uint64_t* d_offsets, uint64_t offset_base,
                                uint64_t n, void* d_scratch, cudaStream_t stream, uint32_t flags,
-                               const uint32_t** perm_out) {
+                               const uint32_t** perm_out, int qclasses) {
     const uint32_t* perm = nullptr;
     const uint64_t bias0 = reinterpret_cast<uintptr_t>(d_data) - offset_base;  // address = offsets[i] + bias
     // Sort mode: windowed for MD5 (HBM-bound: locality wins), global for SHA-1/SM3
@@ -181,12 +182,17 @@ cudaError_t launch_varlen_sort(int alg, const uint8_t* d_data, const uint64_t* d
     if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch && window) {
         uint32_t* p = static_cast<uint32_t*>(d_scratch) + kSortBuckets;
         const uint64_t w = env_u64("HB_SORT_WINDOW", 8192);
+        const bool q8 = qclasses == 8;
+#define HB_WIN(W)                                                                                            \
+    q8 ? k_sort_window<W, 8><<<(unsigned)((n + W - 1) / W), 1024, 0, stream>>>(d_offsets, n, bias0, p)     \
+       : k_sort_window<W, 4><<<(unsigned)((n + W - 1) / W), 1024, 0, stream>>>(d_offsets, n, bias0, p)
         if (w >= 16384)
-            k_sort_window<16384><<<(unsigned)((n + 16383) / 16384), 1024, 0, stream>>>(d_offsets, n, bias0, p);
+            HB_WIN(16384);
         else if (w >= 8192)
-            k_sort_window<8192><<<(unsigned)((n + 8191) / 8192), 1024, 0, stream>>>(d_offsets, n, bias0, p);
+            HB_WIN(8192);
         else
-            k_sort_window<4096><<<(unsigned)((n + 4095) / 4096), 1024, 0, stream>>>(d_offsets, n, bias0, p);
+            HB_WIN(4096);
+#undef HB_WIN
         note_launches(1);
         perm = p;
     } else if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch) {

@@ -519,6 +519,107 @@ k_varlen16(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offset
 }
 
 // -------------------------------------------------------------------------
+// Variable-length kernel, 256-bit loads (LDG.E.ENL2.256, sm_100).
+//
+// The 16-byte kernel is bound by the L1 data pipe: each LDG.128 of a warp
+// touches 32 scattered lines (one wavefront each), 4-5 per block.  A 256-bit
+// load moves the same line traffic in half the instructions, so each block
+// costs 2-3 wavefronts per lane instead of 4-5.  The message's 32-aligned
+// 96-byte window around block b is realigned by a word select over
+// q = (address >> 2) mod 8 (warp-uniform: the sort key uses 8 alignment
+// classes) and one funnel shift.  Loads never cross `data_end`: a chunk that
+// would (only possible for the batch's last message) is read word by word.
+// -------------------------------------------------------------------------
+__device__ __forceinline__ void ld256_nc(const uint32_t* p, uint32_t* w) {
+    asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                 : "l"(p));
+}
+
+// 32-byte chunk at p (32-aligned): bytes < lim are read, the rest are zero
+// (lim = min(message end, data_end) is only binding in the tail; full blocks
+// pass lim = data_end).
+__device__ __forceinline__ void load_chunk32(const uint8_t* p, uintptr_t lim, uint32_t* w) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    if (a + 32u <= lim) {
+        ld256_nc(reinterpret_cast<const uint32_t*>(p), w);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            w[k] = (a + 4u * k < lim) ? __ldg(reinterpret_cast<const uint32_t*>(p) + k) : 0u;
+    }
+}
+
+__device__ __forceinline__ void realign32(const uint32_t (&c)[24], uint32_t q, uint32_t sh, uint32_t (&raw)[16]) {
+#define HB_RA(Q)                                                                    \
+    _Pragma("unroll") for (int j = 0; j < 16; ++j) raw[j] = __funnelshift_r(c[j + Q], c[j + Q + 1], sh);
+    switch (q) {
+    case 0: HB_RA(0) break;
+    case 1: HB_RA(1) break;
+    case 2: HB_RA(2) break;
+    case 3: HB_RA(3) break;
+    case 4: HB_RA(4) break;
+    case 5: HB_RA(5) break;
+    case 6: HB_RA(6) break;
+    default: HB_RA(7) break;
+    }
+#undef HB_RA
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(128)
+k_varlen32(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+           uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = perm ? (uint64_t)perm[t] : t;
+    const uint64_t start = offsets[i] - offset_base;
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
+    const uint8_t* w32 = reinterpret_cast<const uint8_t*>(a & ~uintptr_t(31));
+    const uint32_t q = (uint32_t)(a >> 2) & 7u, sh = (uint32_t)(a & 3u) * 8u;
+    const bool misaligned = (a & 31u) != 0;
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    uint32_t c[24];
+    uint32_t raw[16];
+    const uint64_t nfull = len >> 6;
+    for (uint64_t b = 0; b < nfull; ++b) {
+        const uint8_t* src = w32 + 64 * b;
+        load_chunk32(src, dend, c);
+        load_chunk32(src + 32, dend, c + 8);
+        if (misaligned) {
+            load_chunk32(src + 64, dend, c + 16);
+        } else {
+#pragma unroll
+            for (int k = 16; k < 24; ++k) c[k] = 0u;
+        }
+        realign32(c, q, sh, raw);
+        compress1<ALG>(st, raw);
+    }
+    // tail: the r = len % 64 remaining bytes (chunks overlapping [p, p + r) only)
+    const uint32_t r = (uint32_t)(len & 63u);
+    const uintptr_t mend = a + len;
+    const uintptr_t lim = mend < dend ? mend : dend;
+    const uint8_t* src = w32 + 64 * nfull;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (reinterpret_cast<uintptr_t>(src + 32 * k) < mend) {
+            load_chunk32(src + 32 * k, lim, c + 8 * k);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) c[8 * k + j] = 0u;
+        }
+    }
+    realign32(c, q, sh, raw);
+    mask_tail(raw, r);
+    md_finish<ALG>(st, raw, r, len);
+    store_digest<ALG>(out + i * H::kDigestBytes, st);
+}
+
+// -------------------------------------------------------------------------
 // Variable-length kernel, per-lane bulk copies (TMA engine).
 //
 // The per-thread kernel is bound by the L1 data pipe (ncu: LSU wavefronts at
@@ -748,12 +849,19 @@ constexpr int kSortBuckets = kSortNbClasses * 4;
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 16;  // per thread
 
-__device__ __forceinline__ uint32_t sort_bucket(const uint64_t* offsets, uint64_t i, uint64_t addr_bias) {
+// Sort key: block-count class (longest first) x Q word-alignment classes
+// q = (address >> 2) mod Q -- Q = 4 for the 16-byte-window kernels, 8 for the
+// 32-byte-window one -- so a warp's messages take the same realignment path.
+template <int Q>
+__device__ __forceinline__ uint32_t sort_bucket_q(const uint64_t* offsets, uint64_t i, uint64_t addr_bias) {
     const uint64_t len = offsets[i + 1] - offsets[i];
     const uint64_t nb = (len + 8u) / 64u + 1u;
     const uint64_t c = nb < (uint64_t)(kSortNbClasses - 1) ? nb : (uint64_t)(kSortNbClasses - 1);
-    const uint32_t q = (uint32_t)((offsets[i] + addr_bias) >> 2) & 3u;
-    return ((uint32_t)(kSortNbClasses - 1) - (uint32_t)c) * 4u + q;
+    const uint32_t q = (uint32_t)((offsets[i] + addr_bias) >> 2) & (uint32_t)(Q - 1);
+    return ((uint32_t)(kSortNbClasses - 1) - (uint32_t)c) * (uint32_t)Q + q;
+}
+__device__ __forceinline__ uint32_t sort_bucket(const uint64_t* offsets, uint64_t i, uint64_t addr_bias) {
+    return sort_bucket_q<4>(offsets, i, addr_bias);
 }
 
 // -------------------------------------------- decimal messages in-register --
@@ -1055,13 +1163,24 @@ template <int ALG>
 static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes, const uint64_t* d_offsets,
                                      uint64_t offset_base, uint64_t n, uint8_t* d_out, void* d_scratch,
                                      cudaStream_t stream, uint32_t flags) {
+    // 256-bit-load kernel: opt-in ($HB_VARLEN_LD=32; its sort uses 8 alignment
+    // classes).  It relieves the L1 data pipe but the 8-class sort splits a
+    // window's warps over more (block count, alignment) buckets: MD5 at
+    // configs[3] 2.24-2.28 vs 2.03 ms for the 16-byte kernel (ab_varlen_r1g.txt).
+    const bool special = (flags & (HB_FLAG_VARLEN_WORDS | HB_FLAG_VARLEN_COOP | HB_FLAG_VARLEN_COOP_OFF)) ||
+                         env_u64("HB_VARLEN_BULK", 0) || env_u64("HB_VARLEN_PREFETCH", 0);
+    const bool wide = !special && env_u64("HB_VARLEN_LD", 16) == 32;
     const uint32_t* perm = nullptr;
     {
-        const cudaError_t e = launch_varlen_sort(ALG, d_data, d_offsets, offset_base, n, d_scratch, stream, flags, &perm);
+        const cudaError_t e = launch_varlen_sort(ALG, d_data, d_offsets, offset_base, n, d_scratch, stream, flags,
+                                                 &perm, wide ? 8 : 4);
         if (e != cudaSuccess) return e;
     }
     const uint64_t grid = (n + 127) / 128;
-    if (flags & HB_FLAG_VARLEN_WORDS) {  // A/B baseline: per-thread 32-bit loads
+    if (wide) {
+        k_varlen32<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets, offset_base, perm,
+                                                            n, d_out);
+    } else if (flags & HB_FLAG_VARLEN_WORDS) {  // A/B baseline: per-thread 32-bit loads
         k_generic<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets,
                                                                  offset_base, perm, 0, n, d_out);
     } else if ((flags & HB_FLAG_VARLEN_COOP) && data_bytes < (1ull << 37)) {  // block counts fit u32

@@ -108,7 +108,7 @@ def test_varlen_golden(golden):
             assert sha(batch_digest_varlen(alg, data, off)) == row[alg]
 
 
-@pytest.mark.parametrize("sort", ["window4096", "window16384", "global", "prefetch", "bulk"])
+@pytest.mark.parametrize("sort", ["window4096", "window16384", "global", "prefetch", "bulk", "ld32", "ld16"])
 @pytest.mark.parametrize("alg", ALGS)
 def test_varlen_random_sorted_and_unsorted(alg, sort, monkeypatch):
     monkeypatch.setenv("HB_VARLEN_SORT", "global" if sort == "global" else "window")
@@ -118,6 +118,8 @@ def test_varlen_random_sorted_and_unsorted(alg, sort, monkeypatch):
         monkeypatch.setenv("HB_VARLEN_PREFETCH", "1")
     if sort == "bulk":
         monkeypatch.setenv("HB_VARLEN_BULK", "2")
+    if sort.startswith("ld"):
+        monkeypatch.setenv("HB_VARLEN_LD", sort[2:])
     rng = np.random.default_rng(12)
     n = 20000  # above the sort threshold
     lens = rng.integers(0, 4097, n).astype(np.uint64)
@@ -359,7 +361,7 @@ def test_varlen_every_length_and_alignment(alg, monkeypatch):
         C = _native.HB_FLAG_VARLEN_COOP
         for env, fl in (({"HB_VC_STAGES": "3"}, C), ({"HB_VC_STAGES": "2"}, C), ({"HB_VC_PF": "128"}, C),
                         ({"HB_VC_PF": "0"}, C), ({"HB_VARLEN_PREFETCH": "1"}, 0), ({"HB_VARLEN_BULK": "3"}, 0),
-                        ({"HB_VARLEN_BULK": "5"}, 0)):
+                        ({"HB_VARLEN_BULK": "5"}, 0), ({"HB_VARLEN_LD": "32"}, 0), ({"HB_VARLEN_LD": "16"}, 0)):
             for key, v in env.items():
                 monkeypatch.setenv(key, v)
             got = batch_digest_varlen(alg, buf, off, flags=fl)
@@ -454,3 +456,26 @@ def test_concurrent_callers_thread_safe():
 
     with ThreadPoolExecutor(max_workers=8) as ex:
         assert all(ex.map(run, range(len(jobs))))
+
+
+@pytest.mark.parametrize("ld", ["16", "32"])
+def test_varlen_last_message_at_buffer_end(ld, monkeypatch):
+    """The wide loads never read past the data buffer: the batch's last message
+    ends exactly at the end of a device allocation whose size is not a
+    multiple of 32 (checked with every tail length 0..95)."""
+    import torch
+
+    from paper_2407_09333_b200 import device
+
+    monkeypatch.setenv("HB_VARLEN_LD", ld)
+    for tail in range(0, 96):
+        lens = np.array([100, 37, 64 + tail], np.int64)
+        off = np.zeros(4, np.int64)
+        off[1:] = np.cumsum(lens)
+        total = int(off[-1])
+        host = oracle.fill_random(total, 400 + tail)
+        data = torch.from_numpy(host).cuda()  # exactly `total` bytes
+        d_off = torch.from_numpy(off).cuda()
+        for alg in ALGS:
+            got = device.hash_varlen(alg, data, d_off, offset_base=0).cpu().numpy()
+            assert np.array_equal(got, oracle.batch_varlen(alg, host, off.astype(np.uint64))), (alg, tail, ld)

@@ -24,16 +24,18 @@ scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch
 C = _native.HB_FLAG_VARLEN_COOP
 P = _native.HB_FLAG_VARLEN_COOP_OFF
 ARMS = {"default": ({}, 0),
-        "coop_s3_win8k": ({"HB_VC_STAGES": "3"}, C), "coop_s3_win16k": ({"HB_VC_STAGES": "3", "HB_SORT_WINDOW": "16384"}, C),
-        "coop_s4_win16k": ({"HB_SORT_WINDOW": "16384"}, C),
-        "coop_s3_global": ({"HB_VC_STAGES": "3", "HB_VARLEN_SORT": "global"}, C),
-        "thread_win16k": ({"HB_SORT_WINDOW": "16384"}, P)}
+        "ld16_win8k": ({"HB_VARLEN_LD": "16", "HB_VARLEN_SORT": "window"}, 0),
+        "ld32_win8k": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "window"}, 0),
+        "ld32_win16k": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "window", "HB_SORT_WINDOW": "16384"}, 0),
+        "ld32_win4k": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "window", "HB_SORT_WINDOW": "4096"}, 0),
+        "ld32_global": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "global"}, 0),
+        "ld16_global": ({"HB_VARLEN_LD": "16", "HB_VARLEN_SORT": "global"}, 0)}
 for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
     ref, times = None, {}
     for _ in range(3):
         for arm, (env, flags) in ARMS.items():
             for k in ("HB_VC_STAGES", "HB_VC_PF", "HB_VARLEN_SORT", "HB_SORT_WINDOW", "HB_VARLEN_PREFETCH",
-                      "HB_VARLEN_BULK"):
+                      "HB_VARLEN_BULK", "HB_VARLEN_LD"):
                 os.environ.pop(k, None)
             os.environ.update(env)
             out = torch.empty((n, DLEN[alg]), dtype=torch.uint8, device="cuda:0")
