@@ -1172,8 +1172,9 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
     const bool wide = !special && env_u64("HB_VARLEN_LD", 16) == 32;
     const uint32_t* perm = nullptr;
     {
+        const int qcls = wide ? (int)env_u64("HB_VARLEN_Q", 8) : 4;  // A/B: 4-class sort with the wide kernel
         const cudaError_t e = launch_varlen_sort(ALG, d_data, d_offsets, offset_base, n, d_scratch, stream, flags,
-                                                 &perm, wide ? 8 : 4);
+                                                 &perm, qcls == 4 ? 4 : 8);
         if (e != cudaSuccess) return e;
     }
     const uint64_t grid = (n + 127) / 128;

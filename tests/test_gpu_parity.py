@@ -361,7 +361,8 @@ def test_varlen_every_length_and_alignment(alg, monkeypatch):
         C = _native.HB_FLAG_VARLEN_COOP
         for env, fl in (({"HB_VC_STAGES": "3"}, C), ({"HB_VC_STAGES": "2"}, C), ({"HB_VC_PF": "128"}, C),
                         ({"HB_VC_PF": "0"}, C), ({"HB_VARLEN_PREFETCH": "1"}, 0), ({"HB_VARLEN_BULK": "3"}, 0),
-                        ({"HB_VARLEN_BULK": "5"}, 0), ({"HB_VARLEN_LD": "32"}, 0), ({"HB_VARLEN_LD": "16"}, 0)):
+                        ({"HB_VARLEN_BULK": "5"}, 0), ({"HB_VARLEN_LD": "32"}, 0), ({"HB_VARLEN_LD": "16"}, 0),
+                        ({"HB_VARLEN_LD": "32", "HB_VARLEN_Q": "4"}, 0)):
             for key, v in env.items():
                 monkeypatch.setenv(key, v)
             got = batch_digest_varlen(alg, buf, off, flags=fl)

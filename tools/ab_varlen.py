@@ -27,7 +27,9 @@ ARMS = {"default": ({}, 0),
         "ld16_win8k": ({"HB_VARLEN_LD": "16", "HB_VARLEN_SORT": "window"}, 0),
         "ld32_win8k": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "window"}, 0),
         "ld32_win16k": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "window", "HB_SORT_WINDOW": "16384"}, 0),
-        "ld32_win4k": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "window", "HB_SORT_WINDOW": "4096"}, 0),
+        "ld32_q4_win8k": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "window", "HB_VARLEN_Q": "4"}, 0),
+        "ld32_q4_win16k": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "window", "HB_VARLEN_Q": "4",
+                            "HB_SORT_WINDOW": "16384"}, 0),
         "ld32_global": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "global"}, 0),
         "ld16_global": ({"HB_VARLEN_LD": "16", "HB_VARLEN_SORT": "global"}, 0)}
 for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
@@ -35,7 +37,7 @@ for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
     for _ in range(3):
         for arm, (env, flags) in ARMS.items():
             for k in ("HB_VC_STAGES", "HB_VC_PF", "HB_VARLEN_SORT", "HB_SORT_WINDOW", "HB_VARLEN_PREFETCH",
-                      "HB_VARLEN_BULK", "HB_VARLEN_LD"):
+                      "HB_VARLEN_BULK", "HB_VARLEN_LD", "HB_VARLEN_Q"):
                 os.environ.pop(k, None)
             os.environ.update(env)
             out = torch.empty((n, DLEN[alg]), dtype=torch.uint8, device="cuda:0")
