@@ -480,3 +480,15 @@ def test_varlen_last_message_at_buffer_end(ld, monkeypatch):
         for alg in ALGS:
             got = device.hash_varlen(alg, data, d_off, offset_base=0).cpu().numpy()
             assert np.array_equal(got, oracle.batch_varlen(alg, host, off.astype(np.uint64))), (alg, tail, ld)
+
+
+def test_accel_generic_equivalence_1e6():
+    """the accelerated SHA-1 path equals the generic one on 10^6
+    random messages (here both are the GPU kernel; the oracle is the judge)."""
+    n, L = 10**6, 23
+    data = oracle.fill_random(n * L, 265).reshape(n, L)
+    ref = oracle.batch_fixed("sha1", data, threads=8)
+    assert np.array_equal(batch_digest("sha1", data, accel=True), ref)
+    assert np.array_equal(batch_digest("sha1", data, accel=False), ref)
+    assert [d.data for d in hash_batch("sha1", MessageBatch(n, L, data.tobytes()), accel=True)[:1000]] == \
+        [bytes(r) for r in ref[:1000]]

@@ -1,0 +1,83 @@
+"""Small invocations of every kernel shape, for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck) on the GPU box:
+
+    compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_cases.py
+
+Each case is checked against the CPU oracle as well, so a clean sanitizer run
+also confirms the results.  Inputs are sized so every batch sits exactly at
+the end of its device allocation (no slack after the last message).
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+from paper_2407_09333_b200 import _native, device  # noqa: E402
+
+ALGS = ("sha1", "md5", "sm3")
+ENV_KEYS = ("HB_TMA_CFG", "HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_VARLEN_SORT", "HB_VARLEN_LD",
+            "HB_VARLEN_BULK", "HB_VARLEN_PREFETCH", "HB_VC_STAGES")
+
+
+def with_env(env):
+    for k in ENV_KEYS:
+        os.environ.pop(k, None)
+    os.environ.update(env)
+
+
+def fixed(alg, n, L, flags=0):
+    host = oracle.fill_random(n * L, n + L).reshape(n, L)
+    d = torch.from_numpy(host.copy()).cuda()
+    got = device.hash_fixed(alg, d, flags=flags).cpu().numpy()
+    assert np.array_equal(got, oracle.batch_fixed(alg, host, 8)), (alg, n, L, flags)
+
+
+def varlen(alg, n, maxlen, flags=0):
+    lens = np.random.default_rng(n).integers(0, maxlen + 1, n).astype(np.int64)
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    host = oracle.fill_random(int(off[-1]), 7)
+    d = torch.from_numpy(host.copy()).cuda()
+    got = device.hash_varlen(alg, d, torch.from_numpy(off).cuda(), flags=flags, offset_base=0).cpu().numpy()
+    assert np.array_equal(got, oracle.batch_varlen(alg, host, off.astype(np.uint64), 8)), (alg, n, maxlen, flags)
+
+
+def main():
+    cases = 0
+    fixed_shapes = [({}, [(3000, 1024), (700, 1040), (300, 64), (300, 16), (300, 96), (257, 7), (129, 0)]),
+                    ({"HB_TMA_CFG": "ws3x2"}, [(3000, 1024), (513, 80)]),
+                    ({"HB_TMA_CFG": "1x3"}, [(3000, 1024)]),
+                    ({"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"}, [(5000, 64), (5000, 144)])]
+    for env, shapes in fixed_shapes:
+        with_env(env)
+        for alg in ALGS:
+            for n, L in shapes:
+                fixed(alg, n, L)
+                cases += 1
+    for alg in ALGS:
+        fixed(alg, 2000, 1024, _native.HB_FLAG_NO_TMA)
+        cases += 1
+    varlen_arms = [({}, 0), ({"HB_VARLEN_SORT": "global"}, 0), ({"HB_VARLEN_SORT": "window"}, 0),
+                   ({}, _native.HB_FLAG_VARLEN_COOP), ({}, _native.HB_FLAG_VARLEN_WORDS),
+                   ({"HB_VARLEN_LD": "32"}, 0), ({"HB_VARLEN_BULK": "3"}, 0), ({"HB_VARLEN_PREFETCH": "1"}, 0)]
+    for env, fl in varlen_arms:
+        with_env(env)
+        for alg in ALGS:
+            varlen(alg, 3000, 700, fl)
+            varlen(alg, 40, 300, fl)
+            cases += 2
+    with_env({})
+    for alg in ALGS:
+        for w in (9, 12):
+            out = device.hash_decimal(alg, 5, 4000, w).cpu().numpy()
+            assert np.array_equal(out, oracle.batch_fixed(alg, oracle.gen_decimal(5, 4000, w), 8))
+            cases += 1
+    torch.cuda.synchronize()
+    print(f"sanitize cases ok: {cases} invocations bit-exact")
+
+
+if __name__ == "__main__":
+    main()
