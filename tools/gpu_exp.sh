@@ -1,5 +1,8 @@
 set -u
 mkdir -p gpurun_out
-T=${T:-exp22}
-timeout 900 python -m pytest tests -q -m gpu --timeout 600 -k "varlen" > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_$T.log
-timeout 600 python tools/ab_varlen.py md5 > gpurun_out/ab_varlen_$T.txt 2>&1; echo "abv rc=$?"; cat gpurun_out/ab_varlen_$T.txt
+T=${T:-san1}
+timeout 300 python tools/sanitize_cases.py > gpurun_out/sanitize_plain_$T.log 2>&1; echo "plain rc=$?"; tail -2 gpurun_out/sanitize_plain_$T.log
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 1800 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 python tools/sanitize_cases.py > gpurun_out/sanitize_${tool}_$T.log 2>&1
+  echo "$tool rc=$?"; tail -3 gpurun_out/sanitize_${tool}_$T.log
+done
