@@ -168,28 +168,34 @@ k_fixed_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_l
 // `empty` -- no TMA-issue path, fence or lane-0 branch in their loop.
 // -------------------------------------------------------------------------
 constexpr int kWsComputeWarps = 4;
-template <int NB, int STAGES> struct WsCfg {
+// SLACK: reserve 1 KiB to align the ring to 1024 B at run time.  Without it
+// (the dynamic window of a kernel with no static shared memory starts 1 KiB
+// aligned -- checked in-kernel) a 3-stage CTA needs 24 KiB and 9 CTAs fit an
+// SM instead of 8.
+template <int NB, int STAGES, bool SLACK = true> struct WsCfg {
     static constexpr int kRows = 32 * kWsComputeWarps * NB;  // rows per CTA tile (TMA box height <= 256)
     static constexpr int kStageBytes = 64 * kRows;            // 8 KiB per message slot
-    static constexpr int kSmem = STAGES * kStageBytes + 1024 + 2 * STAGES * 8;
+    static constexpr int kSmem = STAGES * kStageBytes + (SLACK ? 1024 : 0) + 2 * STAGES * 8;
 };
-template <int ALG, int NB, int STAGES> struct WsOcc {
+template <int ALG, int NB, int STAGES, bool SLACK = true> struct WsOcc {
     static constexpr int kMinCtas =
-        NB == 2 ? (STAGES == 2 ? 6 : 4) : ALG == kSm3 ? 6 : (STAGES == 2 ? (ALG == kMd5 ? 10 : 8) : 8);
+        !SLACK && NB == 1 && STAGES == 3 && ALG != kSm3 ? 9
+        : NB == 2 ? (STAGES == 2 ? 6 : 4) : ALG == kSm3 ? 6 : (STAGES == 2 ? (ALG == kMd5 ? 10 : 8) : 8);
 };
 
 // UNR: the compute warps' main loop is unrolled by STAGES so every ring
 // index is a compile-time constant (no stage/phase bookkeeping, immediate
 // shared-memory offsets); the remainder blocks take the generic loop.
-template <int ALG, int V, int NB, int STAGES, bool UNR = false>
-__global__ void __launch_bounds__((kWsComputeWarps + 1) * 32, (WsOcc<ALG, NB, STAGES>::kMinCtas))
+template <int ALG, int V, int NB, int STAGES, bool UNR = false, bool SLACK = true>
+__global__ void __launch_bounds__((kWsComputeWarps + 1) * 32, (WsOcc<ALG, NB, STAGES, SLACK>::kMinCtas))
 k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
     using H = HashAlg<ALG, V>;
-    using C = WsCfg<NB, STAGES>;
-    extern __shared__ uint8_t smem_raw[];
+    using C = WsCfg<NB, STAGES, SLACK>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t row0 = blockIdx.x * C::kRows;
     const uint32_t base_s = smem_u32(smem_raw);
+    if (!SLACK && (base_s & 1023u)) __trap();  // the swizzled ring needs 1 KiB alignment
     uint8_t* ring = smem_raw + (((base_s + 1023u) & ~1023u) - base_s);
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * C::kStageBytes);
     uint64_t* empty = full + STAGES;
@@ -962,10 +968,10 @@ static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint3
     return cudaGetLastError();
 }
 
-template <int ALG, int V, int NB, int STAGES, bool UNR = false>
+template <int ALG, int V, int NB, int STAGES, bool UNR = false, bool SLACK = true>
 static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
                                        cudaStream_t stream) {
-    using C = WsCfg<NB, STAGES>;
+    using C = WsCfg<NB, STAGES, SLACK>;
     PFN_encodeTiled enc = get_encode_tiled();
     if (!enc) {
         snprintf(tma_error_buf(), kTmaErrLen, "cuTensorMapEncodeTiled unavailable");
@@ -986,12 +992,13 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     static std::once_flag attr_once;
     static cudaError_t attr_rc = cudaSuccess;
     std::call_once(attr_once, [] {
-        attr_rc = cudaFuncSetAttribute(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR>,
+        attr_rc = cudaFuncSetAttribute(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     });
     if (attr_rc != cudaSuccess) return attr_rc;
     const uint32_t grid = (n + C::kRows - 1) / C::kRows;
-    k_fixed_tma_ws<ALG, V, NB, STAGES, UNR><<<grid, (kWsComputeWarps + 1) * 32, C::kSmem, stream>>>(map, n, L, d_out);
+    k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK><<<grid, (kWsComputeWarps + 1) * 32, C::kSmem, stream>>>(map, n, L,
+                                                                                                       d_out);
     note_launches(1);
     return cudaGetLastError();
 }
@@ -1001,7 +1008,7 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
 // messages-per-thread x ring stages) and $HB_VARIANT (0-3) override them for
 // A/B experiments.
 enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4, kCfg1x2 = 5, kCfgWs2x2 = 6, kCfgWs3x2 = 7,
-                kCfgWs3u = 8, kCfgWs3x2u = 9 };
+                kCfgWs3u = 8, kCfgWs3x2u = 9, kCfgWs3n = 10 };
 // B200-measured (profiles/variant_sweep_r1d.txt and _r1e.txt, interleaved
 // rounds): the warp-specialised 3-stage ring is best for MD5 and SM3 (SM3's
 // 61 registers make two messages per thread lose occupancy); SHA-1 gains 4 %
@@ -1030,6 +1037,7 @@ static int tma_cfg(int alg) {
     if (v && !strcmp(v, "ws3x2")) return kCfgWs3x2;
     if (v && !strcmp(v, "ws3u")) return kCfgWs3u;
     if (v && !strcmp(v, "ws3x2u")) return kCfgWs3x2u;
+    if (v && !strcmp(v, "ws3n")) return kCfgWs3n;
     switch (alg) {
     case kSha1: return DefaultTmaCfg<kSha1>::value;
     case kMd5: return DefaultTmaCfg<kMd5>::value;
@@ -1074,6 +1082,8 @@ static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t 
         }
     }
     if (cfg == kCfgWs3u) return launch_fixed_tma_ws<ALG, DefaultVariant<ALG>::value, 1, 3, true>(src, n, L, dst, s);
+    if (cfg == kCfgWs3n)
+        return launch_fixed_tma_ws<ALG, DefaultVariant<ALG>::value, 1, 3, false, false>(src, n, L, dst, s);
     if (cfg == kCfgWs3x2u) return launch_fixed_tma_ws<ALG, DefaultVariant<ALG>::value, 2, 3, true>(src, n, L, dst, s);
     if (cfg == kCfgWs2x2) {
         switch (v) {

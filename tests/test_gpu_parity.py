@@ -290,7 +290,7 @@ def test_full_size_sampled_and_cross_path():
     del buf
 
 
-@pytest.mark.parametrize("cfg", ["1x3", "2x2", "2x3", "ws2", "ws3", "ws2x2", "ws3x2", "ws3u", "ws3x2u"])
+@pytest.mark.parametrize("cfg", ["1x3", "2x2", "2x3", "ws2", "ws3", "ws2x2", "ws3x2", "ws3u", "ws3x2u", "ws3n"])
 def test_tma_tile_configs_and_variants(cfg, monkeypatch):
     """Every compiled TMA tile configuration x round variant is bit-exact
     (the tuned default is only one of them; $HB_TMA_CFG/$HB_VARIANT select)."""
