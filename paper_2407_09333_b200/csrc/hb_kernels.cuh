@@ -1236,20 +1236,15 @@ template <int ALG, int W>
 static void dec_launch(uint64_t start, uint64_t count, uint8_t* d_out, cudaStream_t s) {
     const unsigned grid = (unsigned)((count + 127) / 128);
     // Defaults (B200, profiles/ab_decimal_r1c.txt): FMA-pipe digits, round
-    // variant 1 (SHA-1: 3).  $HB_FMA_DIGITS=0 / $HB_CONST_VARIANT select A/B arms.
-    const uint64_t v = env_u64("HB_CONST_VARIANT", ALG == kSha1 ? 3 : 1);
-    if (env_u64("HB_FMA_DIGITS", 1) && (v == 1 || v == 3)) {
-        if (v == 3)
-            k_decimal<ALG, W, kVarBal3, true><<<grid, 128, 0, s>>>(start, count, d_out);
-        else
-            k_decimal<ALG, W, kVarBal, true><<<grid, 128, 0, s>>>(start, count, d_out);
-        return;
-    }
-    switch (v) {  // round variant (A/B)
-    case 0: k_decimal<ALG, W, kVarPlain><<<grid, 128, 0, s>>>(start, count, d_out); break;
-    case 2: k_decimal<ALG, W, kVarBal2><<<grid, 128, 0, s>>>(start, count, d_out); break;
-    case 3: k_decimal<ALG, W, kVarBal3><<<grid, 128, 0, s>>>(start, count, d_out); break;
-    default: k_decimal<ALG, W, kVarBal><<<grid, 128, 0, s>>>(start, count, d_out); break;
+    // variant 1 (SHA-1: 3).  A/B arms: $HB_CONST_VARIANT = 1 | 3, $HB_FMA_DIGITS=0
+    // (IMAD.HI + SHF digits, variant 1).  Plain / variant-2 rounds lost 4-14 %
+    // (profiles/ab_decimal_r1b.txt) and are no longer instantiated here.
+    if (!env_u64("HB_FMA_DIGITS", 1)) {
+        k_decimal<ALG, W, kVarBal, false><<<grid, 128, 0, s>>>(start, count, d_out);
+    } else if (env_u64("HB_CONST_VARIANT", ALG == kSha1 ? 3 : 1) == 3) {
+        k_decimal<ALG, W, kVarBal3, true><<<grid, 128, 0, s>>>(start, count, d_out);
+    } else {
+        k_decimal<ALG, W, kVarBal, true><<<grid, 128, 0, s>>>(start, count, d_out);
     }
 }
 

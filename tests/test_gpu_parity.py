@@ -184,7 +184,7 @@ def test_ratio_invariance_style_sharding():
         assert np.array_equal(batch_digest(alg, data, gpus=list(range(n)) + [0]), ref)  # uneven split, repeated dev
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "fma_digits"])
+@pytest.mark.parametrize("variant", ["1", "fma_digits"])
 def test_decimal_workload(golden, variant, monkeypatch):
     monkeypatch.setenv("HB_FMA_DIGITS", "0")
     if variant == "fma_digits":

@@ -15,7 +15,7 @@ for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
     out = torch.empty((n, {"md5": 16, "sha1": 20, "sm3": 32}[alg]), dtype=torch.uint8, device="cuda:0")
     ref, times = None, {}
     for _ in range(3):
-        for arm in ("v1", "v1_fma_digits", "v3", "v3_fma_digits"):
+        for arm in ("v1", "v1_fma_digits", "v3_fma_digits"):
             os.environ["HB_CONST_VARIANT"] = arm[1]
             os.environ["HB_FMA_DIGITS"] = "1" if "fma" in arm else "0"
             device.hash_decimal(alg, 0, n, 9, out=out)
