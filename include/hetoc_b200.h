@@ -150,6 +150,20 @@ int hb_sync_device(int gpu);
 /* Release every cached per-GPU context (streams, chunk buffers).            */
 int hb_shutdown(void);
 
+/* ---- peer-mapped digest buffers: the fused device-side gather ---------- */
+/* north_star: "NCCL is needed only for an optional device-side gather".  The
+ * fused form needs no collective at all: the root exports its (n, dlen)
+ * digest buffer, every rank maps it (cudaIpcOpenMemHandle; peer access over
+ * NVLink 5 / NVSwitch between GPUs) and passes root_ptr + s_i*dlen as d_out
+ * of hb_hash_*_dev -- the hash kernels' own digest stores are the gather (the
+ * copy-out rule dst_off = s*dlen of _emit_dev_launch,
+ * pkg/src/hetoc/passes/lower_hyper_for.py:316).                              */
+#define HB_IPC_HANDLE_BYTES 64
+/* handle of the allocation holding d_ptr (64 bytes) + d_ptr's byte offset in it */
+int hb_ipc_handle(const void *d_ptr, uint8_t *handle_out, uint64_t *offset_out);
+int hb_ipc_open(int gpu, const uint8_t *handle, void **d_ptr_out);     /* map it: base; add the offset */
+int hb_ipc_close(int gpu, void *d_ptr);
+
 /* ---- task splitting ---------------------------------------------------- */
 /* partition_range(lb, ub, ratios[0..k)): writes k+1 bounds.                 */
 int hb_partition_range(int64_t lb, int64_t ub, const double *ratios, int k, int64_t *bounds_out);

@@ -25,6 +25,7 @@ EXPORTS = (
     "hb_hash_fixed", "hb_hash_fixed_split", "hb_hash_varlen", "hb_hash_decimal", "hb_hash_fixed_dev", "hb_hash_varlen_dev",
     "hb_varlen_scratch_bytes", "hb_hash_decimal_dev", "hb_fill_random_dev", "hb_gen_decimal_dev",
     "hb_alloc_pinned", "hb_free_pinned", "hb_sync_device", "hb_shutdown", "hb_partition_range",
+    "hb_ipc_handle", "hb_ipc_open", "hb_ipc_close",
 )
 
 
@@ -91,6 +92,9 @@ _SIGS = {
     "hb_free_pinned": (_int, [_vp]),
     "hb_sync_device": (_int, [_int]),
     "hb_shutdown": (_int, []),
+    "hb_ipc_handle": (_int, [_vp, _u8p, _u64p]),
+    "hb_ipc_open": (_int, [_int, _u8p, ctypes.POINTER(_vp)]),
+    "hb_ipc_close": (_int, [_int, _vp]),
     "hb_partition_range": (_int, [ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), _int,
                                   ctypes.POINTER(ctypes.c_int64)]),
 }

@@ -12,6 +12,7 @@
 //       on separate streams so copies overlap compute.
 // One host thread per GPU drives its shard; all CUDA work of a shard is
 // asynchronous on that GPU's slot streams.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdint.h>
@@ -727,6 +728,64 @@ int hb_sync_device(int gpu) {
     if (gpu < 0 || gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
     DeviceGuard g(gpu);
     HB_CK(cudaDeviceSynchronize());
+    return HB_OK;
+}
+
+// ---- peer-mapped digest buffers (fused gather) -------------------------
+// IPC handles name whole cudaMalloc allocations; a pointer inside one (e.g. a
+// tensor carved out of PyTorch's caching allocator) is exported as the
+// handle of its allocation plus the byte offset of the pointer in it.
+typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+static PFN_memGetAddressRange get_mem_range() {
+    static PFN_memGetAddressRange fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_memGetAddressRange>(p);
+    });
+    return fn;
+}
+
+int hb_ipc_handle(const void* d_ptr, uint8_t* handle_out, uint64_t* offset_out) {
+    if (!d_ptr || !handle_out || !offset_out) return fail(HB_ERR_INVAL, "null pointer");
+    static_assert(sizeof(cudaIpcMemHandle_t) == HB_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaPointerAttributes a;
+    HB_CK(cudaPointerGetAttributes(&a, d_ptr));
+    if (a.type != cudaMemoryTypeDevice) return fail(HB_ERR_INVAL, "not a device allocation");
+    DeviceGuard g(a.device);
+    PFN_memGetAddressRange range = get_mem_range();
+    if (!range) return fail(HB_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS)
+        return fail(HB_ERR_CUDA, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    HB_CK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    memcpy(handle_out, &h, sizeof h);
+    *offset_out = reinterpret_cast<uint64_t>(d_ptr) - (uint64_t)base;
+    return HB_OK;
+}
+
+int hb_ipc_open(int gpu, const uint8_t* handle, void** d_ptr_out) {
+    if (!handle || !d_ptr_out) return fail(HB_ERR_INVAL, "null pointer");
+    const int nd = device_count();
+    if (gpu < 0 || gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
+    DeviceGuard g(gpu);
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    HB_CK(cudaIpcOpenMemHandle(d_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return HB_OK;
+}
+
+int hb_ipc_close(int gpu, void* d_ptr) {
+    if (!d_ptr) return HB_OK;
+    const int nd = device_count();
+    if (gpu < 0 || gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
+    DeviceGuard g(gpu);
+    HB_CK(cudaIpcCloseMemHandle(d_ptr));
     return HB_OK;
 }
 

@@ -47,3 +47,64 @@ def gather_digests(local, n_total: int, group=None):
     parts = [torch.empty_like(padded) for _ in range(world)]
     dist.all_gather(parts, padded, group=group)
     return torch.cat([p[: b - a] for p, (a, b) in zip(parts, bounds)], dim=0)
+
+
+def hash_fixed_gather_p2p(alg: str, msgs_local, n_total: int, root: int = 0, group=None):
+    """Fused hash + gather, no collective on the data path.
+
+    Every rank hashes its shard -- global rows ``[lo, hi)`` of
+    ``shard_bounds(n_total, world)`` given as the (hi-lo, L) CUDA tensor
+    ``msgs_local`` -- and the hash kernel stores its digests straight into the
+    root's (n_total, dlen) buffer through a CUDA IPC mapping (P2P stores over
+    NVLink 5 / NVSwitch when the ranks sit on different GPUs).  The only
+    messages exchanged through ``torch.distributed`` are the 64-byte memory
+    handle and a barrier.  Returns the full digest tensor on the root, None
+    elsewhere.
+    """
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from . import _native
+    from .crypto.batch import DIGEST_LEN, _check_alg
+
+    _check_alg(alg)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    lo, hi = shard_bounds(n_total, world)[rank]
+    if msgs_local.dim() != 2 or msgs_local.shape[0] != hi - lo or not msgs_local.is_cuda:
+        raise ValueError(f"rank {rank} must pass its shard [{lo}, {hi}) as a 2-D CUDA tensor")
+    dlen = DIGEST_LEN[alg]
+    gpu = msgs_local.device.index
+    lib = _native.lib()
+    out = None
+    handle = [None]
+    if rank == root:
+        out = torch.empty((n_total, dlen), dtype=torch.uint8, device=msgs_local.device)
+        h = (ctypes.c_uint8 * 64)()
+        off = ctypes.c_uint64(0)
+        _native.check(lib.hb_ipc_handle(out.data_ptr(), h, ctypes.byref(off)), "hb_ipc_handle")
+        handle[0] = (bytes(h), off.value)
+    torch.cuda.synchronize(gpu)  # the root's buffer exists before anyone writes into it
+    dist.broadcast_object_list(handle, src=root, group=group)
+    if rank == root:
+        base = out.data_ptr()
+    else:
+        ptr = ctypes.c_void_p()
+        h = (ctypes.c_uint8 * 64).from_buffer_copy(handle[0][0])
+        _native.check(lib.hb_ipc_open(gpu, h, ctypes.byref(ptr)), "hb_ipc_open")
+        mapped = ptr.value
+        base = mapped + handle[0][1]
+    try:
+        if hi > lo:
+            msgs = msgs_local.contiguous()
+            stream = torch.cuda.current_stream(gpu).cuda_stream
+            rc = lib.hb_hash_fixed_dev(_native.ALG_ID[alg], gpu, msgs.data_ptr(), hi - lo, msgs.shape[1],
+                                       base + lo * dlen, stream, 0)
+            _native.check(rc, "hb_hash_fixed_dev")
+        torch.cuda.synchronize(gpu)  # this rank's digest stores have landed in the root's buffer
+        dist.barrier(group=group)
+    finally:
+        if rank != root:
+            lib.hb_ipc_close(gpu, ctypes.c_void_p(mapped))
+    return out

@@ -71,3 +71,52 @@ def test_shard_bounds_rules():
     assert shard_bounds(3, 8)[0] == (0, 0)  # empty shards are legal
     with pytest.raises(ValueError):
         shard_for_rank(10, 2, 2)
+
+
+def _p2p_worker(rank, world, port, n, L, q):
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2407_09333_b200.distributed import hash_fixed_gather_p2p, shard_for_rank
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ngpu = torch.cuda.device_count()
+        dev = torch.device("cuda", rank % ngpu)
+        lo, hi = shard_for_rank(n, world, rank)
+        res = {}
+        for alg in ("sha1", "md5", "sm3"):
+            mine = torch.from_numpy(oracle.fill_random((hi - lo) * L, 23, lo * L).reshape(hi - lo, L)).to(dev)
+            full = hash_fixed_gather_p2p(alg, mine, n)
+            if rank == 0:
+                res[alg] = full.cpu().numpy()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_p2p_gather(world):
+    """The fused gather: every rank's hash kernel stores its digests straight
+    into rank 0's buffer through a CUDA IPC mapping (P2P over NVLink between
+    GPUs; here the ranks may share one GPU -- the mapping is the same).  Only the
+    64-byte handle and a barrier go through torch.distributed (gloo)."""
+    import oracle
+
+    n, L = 100003, 64
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, n, L, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    data = oracle.fill_random(n * L, 23).reshape(n, L)
+    for alg in ("sha1", "md5", "sm3"):
+        assert np.array_equal(got[0][alg], oracle.batch_fixed(alg, data, threads=8)), alg
