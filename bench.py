@@ -473,6 +473,14 @@ def run_ours(args):
     world, rank, local = dist_setup(args)
     w = make_workload(args.workload, rank, local, args.n, world)
     alg = w.alg
+    gather = None
+    if args.gather == "p2p" and world > 1 and w.kind == "fixed":
+        # fused device-side gather: each rank's kernel stores its digests into rank 0's buffer (CUDA IPC / NVLink)
+        from paper_2407_09333_b200.distributed import P2PDigestGather
+
+        gather = P2PDigestGather(alg, w.msgs, w.total_msgs)
+        w.graph = None
+        w.step = gather.launch
     stream = torch.cuda.current_stream(local)
     sampler = ClockSampler(local)
     sampler.start()
@@ -495,6 +503,11 @@ def run_ours(args):
     t_wall = time.perf_counter() - t_wall0
     sampler.active = False
     launches = _native.launch_count() - l0
+    if gather is not None:  # the gather wrote into rank 0's buffer; refill the local digests for the checks below
+        from paper_2407_09333_b200 import device as _device
+
+        _device.hash_fixed(alg, w.msgs, out=w.out)
+        torch.cuda.synchronize()
     if w.launches_per_step() is not None:  # CUDA-graph replays are not seen by the launch counter
         launches = w.launches_per_step() * args.steps
     barrier(world)
@@ -617,9 +630,13 @@ def run_ours(args):
                 "data": ("paper workload: decimal messages generated in-kernel" if w.kind == "decimal" else
                          f"synthetic: counter-based splitmix64 bytes (seed {w.seed}), generated on device"),
                 "config": dict(w.config(world), launch="cuda-graph replay per step" if w.launches_per_step()
-                               else "direct launch per step"), "mhash_per_s": round(mhash, 2), "clocks": clk, "e2e": e2e,
+                               else "direct launch per step",
+                               gather="fused P2P into rank 0 (CUDA IPC)" if gather is not None else "none"),
+                "mhash_per_s": round(mhash, 2), "clocks": clk, "e2e": e2e,
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "parity": parity}
         print(json.dumps(line), flush=True)
+    if gather is not None:
+        gather.close()
     if world > 1:
         import torch.distributed as dist
 
@@ -718,6 +735,8 @@ def main():
     ap.add_argument("--ref-step-seconds", type=float, default=1.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--gather", choices=["none", "p2p"], default="none",
+                    help="N>1: fused device-side digest gather into rank 0 (hash kernels store over NVLink)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("note: timing rules want >= 3 warm-up steps")

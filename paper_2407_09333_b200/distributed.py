@@ -49,62 +49,89 @@ def gather_digests(local, n_total: int, group=None):
     return torch.cat([p[: b - a] for p, (a, b) in zip(parts, bounds)], dim=0)
 
 
-def hash_fixed_gather_p2p(alg: str, msgs_local, n_total: int, root: int = 0, group=None):
-    """Fused hash + gather, no collective on the data path.
+class P2PDigestGather:
+    """Fused hash + gather with the peer mapping set up once.
 
     Every rank hashes its shard -- global rows ``[lo, hi)`` of
-    ``shard_bounds(n_total, world)`` given as the (hi-lo, L) CUDA tensor
-    ``msgs_local`` -- and the hash kernel stores its digests straight into the
-    root's (n_total, dlen) buffer through a CUDA IPC mapping (P2P stores over
-    NVLink 5 / NVSwitch when the ranks sit on different GPUs).  The only
-    messages exchanged through ``torch.distributed`` are the 64-byte memory
-    handle and a barrier.  Returns the full digest tensor on the root, None
-    elsewhere.
+    ``shard_bounds(n_total, world)``, the (hi-lo, L) CUDA tensor ``msgs_local``
+    -- and the hash kernel stores its digests straight into the root's
+    (n_total, dlen) buffer through a CUDA IPC mapping (P2P stores over NVLink 5
+    / NVSwitch when the ranks sit on different GPUs).  Only the 64-byte memory
+    handle (at construction) and barriers go through ``torch.distributed``.
+    ``launch()`` enqueues one hash pass on the current stream; ``out`` is the
+    full digest tensor on the root (None elsewhere), complete after
+    ``torch.cuda.synchronize()`` + a barrier.
     """
-    import ctypes
 
+    def __init__(self, alg: str, msgs_local, n_total: int, root: int = 0, group=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _native
+        from .crypto.batch import DIGEST_LEN, _check_alg
+
+        _check_alg(alg)
+        self.alg, self.group, self.root = alg, group, root
+        world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.lo, self.hi = shard_bounds(n_total, world)[self.rank]
+        if msgs_local.dim() != 2 or msgs_local.shape[0] != self.hi - self.lo or not msgs_local.is_cuda:
+            raise ValueError(f"rank {self.rank} must pass its shard [{self.lo}, {self.hi}) as a 2-D CUDA tensor")
+        self.msgs = msgs_local.contiguous()
+        self.dlen = DIGEST_LEN[alg]
+        self.gpu = self.msgs.device.index
+        self.lib = _native.lib()
+        self.out, self.mapped = None, None
+        handle = [None]
+        if self.rank == root:
+            self.out = torch.empty((n_total, self.dlen), dtype=torch.uint8, device=self.msgs.device)
+            h = (ctypes.c_uint8 * 64)()
+            off = ctypes.c_uint64(0)
+            _native.check(self.lib.hb_ipc_handle(self.out.data_ptr(), h, ctypes.byref(off)), "hb_ipc_handle")
+            handle[0] = (bytes(h), off.value)
+        torch.cuda.synchronize(self.gpu)  # the root's buffer exists before anyone maps it
+        dist.broadcast_object_list(handle, src=root, group=group)
+        if self.rank == root:
+            self.base = self.out.data_ptr()
+        else:
+            ptr = ctypes.c_void_p()
+            h = (ctypes.c_uint8 * 64).from_buffer_copy(handle[0][0])
+            _native.check(self.lib.hb_ipc_open(self.gpu, h, ctypes.byref(ptr)), "hb_ipc_open")
+            self.mapped = ptr.value
+            self.base = self.mapped + handle[0][1]
+
+    def launch(self, stream=None):
+        import torch
+
+        from . import _native
+
+        if self.hi <= self.lo:
+            return
+        s = stream if stream is not None else torch.cuda.current_stream(self.gpu).cuda_stream
+        rc = self.lib.hb_hash_fixed_dev(_native.ALG_ID[self.alg], self.gpu, self.msgs.data_ptr(), self.hi - self.lo,
+                                        self.msgs.shape[1], self.base + self.lo * self.dlen, s, 0)
+        _native.check(rc, "hb_hash_fixed_dev")
+
+    def close(self):
+        import ctypes
+
+        if self.mapped is not None:
+            self.lib.hb_ipc_close(self.gpu, ctypes.c_void_p(self.mapped))
+            self.mapped = None
+
+
+def hash_fixed_gather_p2p(alg: str, msgs_local, n_total: int, root: int = 0, group=None):
+    """One fused hash + gather pass (see :class:`P2PDigestGather`); returns the
+    full digest tensor on the root, None elsewhere."""
     import torch
     import torch.distributed as dist
 
-    from . import _native
-    from .crypto.batch import DIGEST_LEN, _check_alg
-
-    _check_alg(alg)
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
-    lo, hi = shard_bounds(n_total, world)[rank]
-    if msgs_local.dim() != 2 or msgs_local.shape[0] != hi - lo or not msgs_local.is_cuda:
-        raise ValueError(f"rank {rank} must pass its shard [{lo}, {hi}) as a 2-D CUDA tensor")
-    dlen = DIGEST_LEN[alg]
-    gpu = msgs_local.device.index
-    lib = _native.lib()
-    out = None
-    handle = [None]
-    if rank == root:
-        out = torch.empty((n_total, dlen), dtype=torch.uint8, device=msgs_local.device)
-        h = (ctypes.c_uint8 * 64)()
-        off = ctypes.c_uint64(0)
-        _native.check(lib.hb_ipc_handle(out.data_ptr(), h, ctypes.byref(off)), "hb_ipc_handle")
-        handle[0] = (bytes(h), off.value)
-    torch.cuda.synchronize(gpu)  # the root's buffer exists before anyone writes into it
-    dist.broadcast_object_list(handle, src=root, group=group)
-    if rank == root:
-        base = out.data_ptr()
-    else:
-        ptr = ctypes.c_void_p()
-        h = (ctypes.c_uint8 * 64).from_buffer_copy(handle[0][0])
-        _native.check(lib.hb_ipc_open(gpu, h, ctypes.byref(ptr)), "hb_ipc_open")
-        mapped = ptr.value
-        base = mapped + handle[0][1]
+    g = P2PDigestGather(alg, msgs_local, n_total, root, group)
     try:
-        if hi > lo:
-            msgs = msgs_local.contiguous()
-            stream = torch.cuda.current_stream(gpu).cuda_stream
-            rc = lib.hb_hash_fixed_dev(_native.ALG_ID[alg], gpu, msgs.data_ptr(), hi - lo, msgs.shape[1],
-                                       base + lo * dlen, stream, 0)
-            _native.check(rc, "hb_hash_fixed_dev")
-        torch.cuda.synchronize(gpu)  # this rank's digest stores have landed in the root's buffer
+        g.launch()
+        torch.cuda.synchronize(g.gpu)  # this rank's digest stores have landed in the root's buffer
         dist.barrier(group=group)
     finally:
-        if rank != root:
-            lib.hb_ipc_close(gpu, ctypes.c_void_p(mapped))
-    return out
+        g.close()
+    return g.out
