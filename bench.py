@@ -124,6 +124,13 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ distributed --
+# $HB_BENCH_BACKEND=gloo (test hook): run the N>1 path with ranks sharing the
+# visible GPUs round-robin -- NCCL needs one GPU per rank, gloo does not -- so
+# the multi-rank bench (sharding, max-over-ranks timing, the fused P2P gather)
+# can be exercised on a one-GPU box.  Production runs use NCCL, one GPU per rank.
+_BACKEND = os.environ.get("HB_BENCH_BACKEND", "nccl")
+
+
 def dist_setup(args):
     import torch
 
@@ -134,8 +141,13 @@ def dist_setup(args):
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if _BACKEND == "gloo":
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     return world, rank, local
@@ -154,7 +166,7 @@ def reduce_max(x: float, world: int, local: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if _BACKEND == "gloo" else f"cuda:{local}")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -471,7 +483,7 @@ def run_ours(args):
     from paper_2407_09333_b200 import _native
 
     world, rank, local = dist_setup(args)
-    w = make_workload(args.workload, rank, local, args.n, world)
+    w = make_workload(args.workload, rank, local, args.msgs, world)
     alg = w.alg
     gather = None
     if args.gather == "p2p" and world > 1 and w.kind == "fixed":
@@ -655,7 +667,7 @@ def run_reference(args):
         return
     spec = WORKLOADS[args.workload]
     alg = spec[0].split(":")[-1]
-    n = args.n or spec[1]
+    n = args.msgs or spec[1]
     seed, cfg_desc = spec[3], spec[4]
     threads = os.cpu_count() or 1
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -729,7 +741,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="md5_1k")
-    ap.add_argument("--n", type=int, default=0, help="override messages per GPU")
+    ap.add_argument("--msgs", type=int, default=0, help="override the message count (per GPU; total for strong-scaling workloads)")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=3.0)
     ap.add_argument("--ref-step-seconds", type=float, default=1.0)
