@@ -120,3 +120,24 @@ def test_fused_p2p_gather(world):
     data = oracle.fill_random(n * L, 23).reshape(n, L)
     for alg in ("sha1", "md5", "sm3"):
         assert np.array_equal(got[0][alg], oracle.batch_fixed(alg, data, threads=8)), alg
+
+
+@pytest.mark.gpu
+def test_bench_multirank_path():
+    """bench.py under torchrun with 2 ranks (gloo test hook: ranks share the
+    visible GPU): sharding, max-over-ranks timing and the fused P2P gather run
+    and print one JSON line whose end-to-end digests match the device run."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HB_BENCH_BACKEND="gloo")
+    for extra in (["--workload", "sha1_64"], ["--workload", "md5_1k", "--msgs", "65536", "--gather", "p2p"]):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+               "--gpus", "2", "--steps", "3", "--warmup", "3", "--e2e-steps", "2"] + extra
+        r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+        assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["matches_device_run"], line
