@@ -464,29 +464,49 @@ __device__ __forceinline__ void realign16(const uint32_t (&c)[20], uint32_t q, u
 // is realigned out of c[], so they are in flight during b's compression
 // (+20 registers; pays off once the windowed sort makes a warp's loads L2-
 // friendly, see profiles/ab_varlen_r1d.txt).
-__device__ __forceinline__ void load_full_window(const uint4* src, bool misaligned, uint32_t (&c)[20]) {
+// 16-byte chunk at p, never reading at or past `dend` (bytes there are zero):
+// used only for the granule that straddles the end of the data buffer.
+static __device__ __noinline__ uint4 ld16_bounded(const uint4* p, uintptr_t dend) {
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(p);
+    uint32_t w[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+        uint32_t x = 0;
+        for (int j = 0; j < 4; ++j) {
+            const uintptr_t q = reinterpret_cast<uintptr_t>(b + 4 * k + j);
+            if (q < dend) x |= (uint32_t)__ldg(b + 4 * k + j) << (8 * j);
+        }
+        w[k] = x;
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Chunk k of a 16-byte window, bounded by the data end when `edge` (the
+// message's last granule straddles it -- only ever the batch's final bytes).
+__device__ __forceinline__ uint4 ld16_edge(const uint4* p, bool edge, uintptr_t dend) {
+    return (edge && reinterpret_cast<uintptr_t>(p + 1) > dend) ? ld16_bounded(p, dend) : __ldg(p);
+}
+
+__device__ __forceinline__ void load_full_window(const uint4* src, bool misaligned, uint32_t (&c)[20],
+                                                 bool edge = false, uintptr_t dend = 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // chunks 0-3 end inside the block: never past the message
         const uint4 v = __ldg(src + k);
         c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
     }
     uint4 v4 = make_uint4(0, 0, 0, 0);
-    if (misaligned) v4 = __ldg(src + 4);
+    if (misaligned) v4 = ld16_edge(src + 4, edge, dend);
     c[16] = v4.x; c[17] = v4.y; c[18] = v4.z; c[19] = v4.w;
 }
 
-template <int ALG, bool PF = false>
-__global__ void __launch_bounds__(128)
-k_varlen16(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offsets, uint64_t offset_base,
-           const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+// One message of k_varlen16; EDGE: the message's last 16-byte granule
+// straddles the end of the data buffer (only the batch's final bytes), so the
+// granules that can cross it are loaded bounded.  The common path carries no
+// bounds checks at all.
+template <int ALG, bool PF, bool EDGE>
+__device__ __forceinline__ void varlen16_message(const uint4* w16, uintptr_t a, uint64_t len, uintptr_t dend,
+                                                 uint8_t* dout) {
     using H = HashAlg<ALG>;
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const uint64_t i = perm ? (uint64_t)perm[t] : t;
-    const uint64_t start = offsets[i] - offset_base;
-    const uint64_t len = offsets[i + 1] - offsets[i];
-    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
-    const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
     const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
     const bool misaligned = (a & 15u) != 0;
     uint32_t st[H::kStateWords];
@@ -495,15 +515,15 @@ k_varlen16(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offset
     uint32_t raw[16];
     const uint64_t nfull = len >> 6;
     if (PF) {
-        if (nfull) load_full_window(w16, misaligned, c);
+        if (nfull) load_full_window(w16, misaligned, c, EDGE, dend);
         for (uint64_t b = 0; b < nfull; ++b) {
             realign16(c, q, sh, raw);
-            if (b + 1 < nfull) load_full_window(w16 + 4 * (b + 1), misaligned, c);
+            if (b + 1 < nfull) load_full_window(w16 + 4 * (b + 1), misaligned, c, EDGE, dend);
             compress1<ALG>(st, raw);
         }
     } else {
         for (uint64_t b = 0; b < nfull; ++b) {
-            load_full_window(w16 + 4 * b, misaligned, c);
+            load_full_window(w16 + 4 * b, misaligned, c, EDGE, dend);
             realign16(c, q, sh, raw);
             compress1<ALG>(st, raw);
         }
@@ -515,13 +535,32 @@ k_varlen16(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offset
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
         uint4 v = make_uint4(0, 0, 0, 0);
-        if (reinterpret_cast<uintptr_t>(src + k) < tail_end) v = __ldg(src + k);
+        if (reinterpret_cast<uintptr_t>(src + k) < tail_end) v = ld16_edge(src + k, EDGE, dend);
         c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
     }
     realign16(c, q, sh, raw);
     mask_tail(raw, r);
     md_finish<ALG>(st, raw, r, len);
-    store_digest<ALG>(out + i * H::kDigestBytes, st);
+    store_digest<ALG>(dout, st);
+}
+
+template <int ALG, bool PF = false>
+__global__ void __launch_bounds__(128)
+k_varlen16(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+           uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = perm ? (uint64_t)perm[t] : t;
+    const uint64_t start = offsets[i] - offset_base;
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
+    const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    if (((a + len + 15u) & ~uintptr_t(15)) > dend)
+        varlen16_message<ALG, PF, true>(w16, a, len, dend, out + i * H::kDigestBytes);
+    else
+        varlen16_message<ALG, PF, false>(w16, a, len, dend, out + i * H::kDigestBytes);
 }
 
 // -------------------------------------------------------------------------
@@ -1224,9 +1263,11 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
         default: k_varlen_bulk<ALG, 3, 1><<<g, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out); break;
         }
     } else if (env_u64("HB_VARLEN_PREFETCH", 0)) {  // per-thread 128-bit loads, software-pipelined
-        k_varlen16<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
+        k_varlen16<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets, offset_base,
+                                                                   perm, n, d_out);
     } else {  // per-thread 128-bit loads
-        k_varlen16<ALG, false><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
+        k_varlen16<ALG, false><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets, offset_base,
+                                                                    perm, n, d_out);
     }
     note_launches(1);
     return cudaGetLastError();

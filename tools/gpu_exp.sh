@@ -1,15 +1,7 @@
 set -u
 mkdir -p gpurun_out
-T=${T:-exp26}
-export HB_BENCH_BACKEND=gloo
-for g in none p2p; do
-  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 \
-    bench.py --gpus 2 --workload md5_1k --msgs 2097152 --steps 5 --warmup 3 --gather $g > gpurun_out/bench2_${g}_$T.json 2> gpurun_out/bench2_${g}_$T.err
-  echo "bench2 $g rc=$?"; cut -c1-900 gpurun_out/bench2_${g}_$T.json; tail -3 gpurun_out/bench2_${g}_$T.err
-done
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 \
-    bench.py --gpus 2 --workload sm3_1k --msgs 1048576 --steps 3 --warmup 3 > gpurun_out/bench2_sm3_$T.json 2> gpurun_out/bench2_sm3_$T.err
-echo "bench2 sm3 rc=$?"; cut -c1-600 gpurun_out/bench2_sm3_$T.json
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 \
-    bench.py --gpus 2 --impl reference --steps 2 --warmup 1 > gpurun_out/bench2_ref_$T.json 2> gpurun_out/bench2_ref_$T.err
-echo "bench2 ref rc=$?"; cut -c1-300 gpurun_out/bench2_ref_$T.json
+T=${T:-exp27}
+timeout 900 python -m pytest tests -q -m gpu --timeout 600 -k "varlen or multirank or p2p" > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_$T.log
+timeout 600 python tools/ab_varlen.py > gpurun_out/ab_varlen_$T.txt 2>&1; echo "abv rc=$?"; grep -E '"default"|ld16_global' gpurun_out/ab_varlen_$T.txt
+timeout 900 compute-sanitizer --tool initcheck --error-exitcode 9 --print-limit 20 python tools/sanitize_cases.py > gpurun_out/sanitize_initcheck_$T.log 2>&1; echo "initcheck rc=$?"; tail -3 gpurun_out/sanitize_initcheck_$T.log
+grep "Device Frame" gpurun_out/sanitize_initcheck_$T.log | sed -E 's/\+0x[0-9a-f]+//' | sort | uniq -c
