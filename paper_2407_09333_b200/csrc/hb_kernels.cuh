@@ -188,7 +188,8 @@ template <int ALG, int NB, int STAGES, bool SLACK = true> struct WsOcc {
 // shared-memory offsets); the remainder blocks take the generic loop.
 template <int ALG, int V, int NB, int STAGES, bool UNR = false, bool SLACK = true>
 __global__ void __launch_bounds__((kWsComputeWarps + 1) * 32, (WsOcc<ALG, NB, STAGES, SLACK>::kMinCtas))
-k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
+k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out,
+               uint32_t evict_first) {
     using H = HashAlg<ALG, V>;
     using C = WsCfg<NB, STAGES, SLACK>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -214,11 +215,15 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
     if (warp == kWsComputeWarps) {  // ---------------- producer warp
         if (lane == 0) {
             prefetch_tmap(&tmap);
+            const uint64_t pol = evict_first ? policy_evict_first() : 0;
             uint32_t s = 0, ph = 0;
             for (uint32_t b = 0; b < nload; ++b) {
                 if (b >= (uint32_t)STAGES) mbar_wait_parity(&empty[s], ph ^ 1u);
                 mbar_arrive_expect_tx(&full[s], C::kStageBytes);
-                tma_load_2d(ring + s * C::kStageBytes, &tmap, &full[s], (int)(b * 64u), (int)row0);
+                if (evict_first)
+                    tma_load_2d_hint(ring + s * C::kStageBytes, &tmap, &full[s], (int)(b * 64u), (int)row0, pol);
+                else
+                    tma_load_2d(ring + s * C::kStageBytes, &tmap, &full[s], (int)(b * 64u), (int)row0);
                 if (++s == (uint32_t)STAGES) { s = 0; ph ^= 1u; }
             }
         }
@@ -1021,9 +1026,15 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     const cuuint64_t strides[1] = {L};
     const cuuint32_t box[2] = {64, (cuuint32_t)C::kRows};
     const cuuint32_t estr[2] = {1, 1};
+    // A/B knobs: $HB_TMA_L2 = L2 promotion (0 / 64 / 128 / 256 bytes, default 256),
+    // $HB_TMA_EVICT_FIRST = evict-first L2 policy on the message loads.
+    const uint64_t l2 = env_u64("HB_TMA_L2", 256);
+    const CUtensorMapL2promotion prom = l2 == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                        : l2 == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                        : l2 == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                    : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     CUresult rc = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_msgs), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (rc != CUDA_SUCCESS) {
         snprintf(tma_error_buf(), kTmaErrLen, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)rc);
         return cudaErrorInvalidValue;
@@ -1036,8 +1047,8 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     });
     if (attr_rc != cudaSuccess) return attr_rc;
     const uint32_t grid = (n + C::kRows - 1) / C::kRows;
-    k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK><<<grid, (kWsComputeWarps + 1) * 32, C::kSmem, stream>>>(map, n, L,
-                                                                                                       d_out);
+    k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK><<<grid, (kWsComputeWarps + 1) * 32, C::kSmem, stream>>>(map, n, L, d_out,
+                                                                                                       (uint32_t)env_u64("HB_TMA_EVICT_FIRST", 0));
     note_launches(1);
     return cudaGetLastError();
 }

@@ -1,7 +1,7 @@
 set -u
 mkdir -p gpurun_out
-T=${T:-exp27}
-timeout 900 python -m pytest tests -q -m gpu --timeout 600 -k "varlen or multirank or p2p" > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_$T.log
-timeout 600 python tools/ab_varlen.py > gpurun_out/ab_varlen_$T.txt 2>&1; echo "abv rc=$?"; grep -E '"default"|ld16_global' gpurun_out/ab_varlen_$T.txt
-timeout 900 compute-sanitizer --tool initcheck --error-exitcode 9 --print-limit 20 python tools/sanitize_cases.py > gpurun_out/sanitize_initcheck_$T.log 2>&1; echo "initcheck rc=$?"; tail -3 gpurun_out/sanitize_initcheck_$T.log
-grep "Device Frame" gpurun_out/sanitize_initcheck_$T.log | sed -E 's/\+0x[0-9a-f]+//' | sort | uniq -c
+T=${T:-exp29}
+timeout 600 python -m pytest tests -q -m gpu --timeout 300 -k "tile_configs or full_size" > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_$T.log
+export AB_ARMS='{"l2_256": {}, "l2_128": {"HB_TMA_L2": "128"}, "l2_0": {"HB_TMA_L2": "0"}, "evict_first": {"HB_TMA_EVICT_FIRST": "1"}, "l2_128_ef": {"HB_TMA_L2": "128", "HB_TMA_EVICT_FIRST": "1"}}'
+AB_ROUNDS=3 timeout 600 python tools/ab_env.py md5 16777216 1024 30 > gpurun_out/ab_tma_$T.txt 2>&1; echo "ab rc=$?"; cat gpurun_out/ab_tma_$T.txt
+AB_ROUNDS=2 timeout 600 python tools/ab_env.py sha1 16777216 1024 10 >> gpurun_out/ab_tma_$T.txt 2>&1; tail -5 gpurun_out/ab_tma_$T.txt
