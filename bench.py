@@ -239,20 +239,34 @@ class FixedWorkload:
         self.h2d_bytes, self.d2h_bytes = n * L, n * self.dlen
         # Small batches (a few microseconds of GPU work, configs[0]) are launched
         # as a CUDA-graph replay so the host call overhead does not idle the GPU.
-        self.graph = None
+        # A step of a small batch is a few microseconds of GPU work, less than a
+        # launch from Python: those steps run as CUDA-graph replays of
+        # GRAPH_STEPS back-to-back passes (each pass hashes the whole batch).
+        self.graph = self.graph1 = None
         if n * L <= (64 << 20):
-            self.graph = device.FixedHashGraph(alg, self.msgs, self.out)
+            self.graph = device.FixedHashGraph(alg, self.msgs, self.out, repeats=GRAPH_STEPS)
+            self.graph1 = device.FixedHashGraph(alg, self.msgs, self.out)
 
     def step(self):
         from paper_2407_09333_b200 import device
 
-        if self.graph is not None:
-            self.graph.replay()
+        if self.graph1 is not None:
+            self.graph1.replay()
         else:
             device.hash_fixed(self.alg, self.msgs, out=self.out)
 
+    def run_steps(self, k):
+        if self.graph is not None:
+            for _ in range(k // GRAPH_STEPS):
+                self.graph.replay()
+            for _ in range(k % GRAPH_STEPS):
+                self.graph1.replay()
+        else:
+            for _ in range(k):
+                self.step()
+
     def launches_per_step(self):
-        return self.graph.kernels_per_replay if self.graph is not None else None
+        return self.graph1.kernels_per_replay if self.graph1 is not None else None
 
     def host_inputs(self, lib):
         import ctypes
@@ -298,6 +312,9 @@ class FixedWorkload:
         return rows, rows * self.L, t, ok, f"first {rows} of the {self.n} x {self.L} B messages (same bytes)"
 
 
+GRAPH_STEPS = 10
+
+
 class VarlenWorkload:
     """configs[3]: n messages per GPU, lengths uniform 1..maxlen B, offsets
     layout (data bytes + u64 offsets[n+1])."""
@@ -331,6 +348,10 @@ class VarlenWorkload:
 
     def launches_per_step(self):
         return None
+
+    def run_steps(self, k):
+        for _ in range(k):
+            self.step()
 
     def step(self):
         from paper_2407_09333_b200 import device
@@ -412,6 +433,10 @@ class DecimalWorkload:
     def launches_per_step(self):
         return None
 
+    def run_steps(self, k):
+        for _ in range(k):
+            self.step()
+
     def host_inputs(self, lib):
         return -1  # nothing to stage: the API call takes only the index range
 
@@ -491,7 +516,7 @@ def run_ours(args):
         from paper_2407_09333_b200.distributed import P2PDigestGather
 
         gather = P2PDigestGather(alg, w.msgs, w.total_msgs)
-        w.graph = None
+        w.graph = w.graph1 = None
         w.step = gather.launch
     stream = torch.cuda.current_stream(local)
     sampler = ClockSampler(local)
@@ -503,14 +528,16 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # One event pair brackets the K back-to-back steps (whole-job throughput:
+    # per-step event pairs would add a launch latency, ~9 us on this box, to
+    # every small step); a few per-step pairs after it give the spread.
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = _native.launch_count()
     sampler.active = True
     t_wall0 = time.perf_counter()
-    for s, e in evs:
-        s.record(stream)
-        w.step()
-        e.record(stream)
+    t_start.record(stream)
+    w.run_steps(args.steps)
+    t_end.record(stream)
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall0
     sampler.active = False
@@ -523,15 +550,22 @@ def run_ours(args):
     if w.launches_per_step() is not None:  # CUDA-graph replays are not seen by the launch counter
         launches = w.launches_per_step() * args.steps
     barrier(world)
+    ms_local = t_start.elapsed_time(t_end) / args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+    for s, e in evs:  # spread of single steps (not part of the timed value)
+        s.record(stream)
+        w.step()
+        e.record(stream)
+    torch.cuda.synchronize()
     per_step = [s.elapsed_time(e) for s, e in evs]
-    ms_local = sum(per_step) / len(per_step)
     ms = reduce_max(ms_local, world, local)
     total_msgs = w.total_msgs  # messages hashed by all ranks in one step
     total_bytes = w.msg_bytes * world if w.kind == "varlen" else total_msgs * (w.L if w.kind == "fixed" else w.width)
     value = total_bytes / (ms * 1e-3) / 1e9
     mhash = total_msgs / (ms * 1e-3) / 1e6
-    log(f"[rank {rank}] kernel-only {w.name}: {ms_local:.3f} ms/step (min {min(per_step):.3f}, "
-        f"max {max(per_step):.3f}); wall {t_wall * 1e3 / args.steps:.3f} ms/step; {launches} launches")
+    log(f"[rank {rank}] kernel-only {w.name}: {ms_local:.4f} ms/step over {args.steps} back-to-back steps "
+        f"(single steps {min(per_step):.4f}-{max(per_step):.4f}); wall {t_wall * 1e3 / args.steps:.3f} ms/step; "
+        f"{launches} launches")
 
     # ---- end to end through the public API: pinned host input -> hb_hash_fixed / hb_hash_varlen
     e2e = None
@@ -641,8 +675,8 @@ def run_ours(args):
                 "dtype": "u32",
                 "data": ("paper workload: decimal messages generated in-kernel" if w.kind == "decimal" else
                          f"synthetic: counter-based splitmix64 bytes (seed {w.seed}), generated on device"),
-                "config": dict(w.config(world), launch="cuda-graph replay per step" if w.launches_per_step()
-                               else "direct launch per step",
+                "config": dict(w.config(world), launch=f"CUDA-graph replays of {GRAPH_STEPS} back-to-back steps"
+                               if w.launches_per_step() else "direct launch per step",
                                gather="fused P2P into rank 0 (CUDA IPC)" if gather is not None else "none"),
                 "mhash_per_s": round(mhash, 2), "clocks": clk, "e2e": e2e,
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "parity": parity}

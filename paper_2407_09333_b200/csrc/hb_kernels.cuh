@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__
     constexpr uint64_t kBits = (uint64_t)L * 8u;
     constexpr uint32_t kL14 = H::kBigEndian ? bswap_c((uint32_t)(kBits >> 32)) : (uint32_t)kBits;
     constexpr uint32_t kL15 = H::kBigEndian ? bswap_c((uint32_t)kBits) : (uint32_t)(kBits >> 32);
-    const uint64_t i = (uint64_t)blockIdx.x * 128u + threadIdx.x;
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint4* p = reinterpret_cast<const uint4*>(msgs + i * L);
     uint32_t w[L / 4];
@@ -1194,21 +1194,26 @@ static cudaError_t launch_fixed_alg(const uint8_t* d_msgs, uint64_t n, uint64_t 
     // folding the constant padding words does not pay for the lost ALU/FMA
     // balance (B200: MD5 16 B 1366 vs 1262 GB/s, profiles/ab_small_r1c.txt).
     const bool small_v1 = env_u64("HB_CONST_VARIANT", 1) == 1;
+    // CTA size of the compile-time-width kernel ($HB_SMALL_CTA: 32..128; A/B for
+    // small batches, where fewer threads per CTA spread a batch over more SMs)
+    uint64_t sb = env_u64("HB_SMALL_CTA", 128);
+    const unsigned sblk = sb >= 128 ? 128u : sb >= 64 ? 64u : 32u;  // __launch_bounds__(128)
+    const unsigned sgrid = (unsigned)((n + sblk - 1) / sblk);
     if (small_ok && L == 16) {
-        small_v1 ? k_fixed_small<ALG, 16, kVarBal><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out)
-                 : k_fixed_small<ALG, 16, kVarPlain><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? k_fixed_small<ALG, 16, kVarBal><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out)
+                 : k_fixed_small<ALG, 16, kVarPlain><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out);
     } else if (small_ok && L == 32) {
-        small_v1 ? k_fixed_small<ALG, 32, kVarBal><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out)
-                 : k_fixed_small<ALG, 32, kVarPlain><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? k_fixed_small<ALG, 32, kVarBal><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out)
+                 : k_fixed_small<ALG, 32, kVarPlain><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out);
     } else if (small_ok && L == 48) {
-        small_v1 ? k_fixed_small<ALG, 48, kVarBal><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out)
-                 : k_fixed_small<ALG, 48, kVarPlain><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? k_fixed_small<ALG, 48, kVarBal><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out)
+                 : k_fixed_small<ALG, 48, kVarPlain><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out);
     } else if (small_ok && L == 64) {
-        small_v1 ? k_fixed_small<ALG, 64, kVarBal><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out)
-                 : k_fixed_small<ALG, 64, kVarPlain><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? k_fixed_small<ALG, 64, kVarBal><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out)
+                 : k_fixed_small<ALG, 64, kVarPlain><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out);
     } else if (small_ok && L == 128) {
-        small_v1 ? k_fixed_small<ALG, 128, kVarBal><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out)
-                 : k_fixed_small<ALG, 128, kVarPlain><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? k_fixed_small<ALG, 128, kVarBal><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out)
+                 : k_fixed_small<ALG, 128, kVarPlain><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out);
     } else if (aligned) {
         k_fixed_direct<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, (uint32_t)L, d_out);
     } else {

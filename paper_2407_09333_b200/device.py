@@ -98,7 +98,9 @@ class FixedHashGraph:
     replays.  ``kernels_per_replay`` is the number of engine kernels in the
     graph (the process-wide ``launch_count`` only counts them at capture)."""
 
-    def __init__(self, alg: str, msgs, out=None, flags: int = 0):
+    def __init__(self, alg: str, msgs, out=None, flags: int = 0, repeats: int = 1):
+        """``repeats`` > 1 captures that many back-to-back passes over the batch
+        in the one graph (a launch-bound loop of small batches)."""
         import torch
 
         if out is None:
@@ -112,8 +114,10 @@ class FixedHashGraph:
         self.graph = torch.cuda.CUDAGraph()
         before = _native.launch_count()
         with torch.cuda.graph(self.graph):
-            hash_fixed(alg, msgs, out=out, flags=flags)
+            for _ in range(max(1, int(repeats))):
+                hash_fixed(alg, msgs, out=out, flags=flags)
         self.kernels_per_replay = _native.launch_count() - before
+        self.repeats = max(1, int(repeats))
 
     def replay(self):
         self.graph.replay()
