@@ -76,7 +76,11 @@ def fixed_point(alg, n, L, seed, steps, out, tag):
     device.fill_random(buf, seed)
     msgs = buf.view(n, L)
     dig = torch.empty((n, DLEN[alg]), dtype=torch.uint8, device="cuda:0")
-    ms = timed(lambda: device.hash_fixed(alg, msgs, out=dig), steps)
+    if n * L <= (64 << 20):  # launch-bound sizes: CUDA-graph replays of 10 passes (as bench.py)
+        g = device.FixedHashGraph(alg, msgs, dig, repeats=10)
+        ms = timed(g.replay, max(1, steps // 10)) / 10
+    else:
+        ms = timed(lambda: device.hash_fixed(alg, msgs, out=dig), steps)
     rows = np.unique(np.concatenate([np.random.default_rng(seed).integers(0, n, 256), [0, n - 1]]))
     sample = np.stack([oracle.fill_random(L, seed, int(r) * L) for r in rows]) if L % 8 == 0 else \
         buf.cpu().numpy().reshape(n, L)[rows]
