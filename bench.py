@@ -5,17 +5,20 @@ Default workload = BASELINE.json configs[1]: MD5 over 2^24 random 1 KiB
 messages per GPU (weak scaling under torchrun: rank r hashes global messages
 [r*2^24, (r+1)*2^24)).  Prints ONE JSON line (rank 0):
 
-  value        kernel-only GB/s of message bytes, inputs resident in HBM, CUDA
-               events on the launching stream, max over ranks, summed over ranks
-  e2e          the same metric through the public API (crypto.batch_digest on a
-               pinned host array -> hb_hash_fixed): H2D + kernel + D2H per step
-  roofline     dominant kernel (k_fixed_tma<MD5>) vs the measured HBM copy peak
+  value        kernel-only GB/s of message bytes, inputs resident in HBM: one
+               CUDA-event pair on the launching stream around K back-to-back
+               steps, max over ranks; bytes summed over ranks
+  e2e          the same metric through the public API (crypto.batch_digest /
+               batch_digest_varlen / hash_decimal on pinned host arrays):
+               H2D + kernels + D2H every step; its roofline is the pinned-copy
+               bandwidth measured in the same run
+  roofline     the dominant kernel vs the HBM copy peak or the ALU-pipe peak
   cpu_baseline the CPU oracle (C port of the reference algorithm) on a bounded
                sample of the same bytes, all host threads; its digests are also
                compared bit-for-bit with the GPU's for that sample
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload md5_1k|sha1_1k|sm3_1k|sha1_64|varlen_md5|varlen_sha1|varlen_sm3]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--gather none|p2p]
+                  [--workload md5_1k|sha1_1k|sm3_1k|sha1_64|varlen_{md5,sha1,sm3}|paper_{sha1,md5,sm3}]
 """
 
 from __future__ import annotations
