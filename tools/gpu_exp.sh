@@ -1,5 +1,5 @@
 set -u
 mkdir -p gpurun_out
-T=${T:-exp32}
-for w in sha1_64 md5_1k; do timeout 600 python bench.py --workload $w --no-cpu > gpurun_out/b_${w}_$T.json 2> gpurun_out/b_${w}_$T.err; echo "$w rc=$?"; python -c "import json,sys; d=json.load(open('gpurun_out/b_${w}_$T.json')); print(d['ms_per_step'], d['value'], d['roofline']['frac'], d['e2e']['value'], d['gpu_launches'], d['config']['launch'])"; grep "kernel-only" gpurun_out/b_${w}_$T.err; done
-timeout 600 python -m pytest tests -q -m gpu -k "graph or multirank" > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_$T.log
+T=${T:-exp33}
+nproc; lscpu | grep -E "Model name|Socket|Core|Thread|NUMA node" | head -8
+timeout 900 python tools/e2e_pageable.py md5 4194304 1024 > gpurun_out/e2e_pageable_$T.txt 2>&1; echo "rc=$?"; cat gpurun_out/e2e_pageable_$T.txt
