@@ -975,6 +975,21 @@ __global__ void __launch_bounds__(128) k_decimal(uint64_t start, uint64_t count,
     store_digest<ALG>(out + i * H::kDigestBytes, st);
 }
 
+// Run `set` (a cudaFuncSetAttribute call) once per device: kernel attributes
+// such as the dynamic shared-memory limit are per device, so a process driving
+// several GPUs must set them on each (a process-wide call_once would not).
+template <class F>
+static cudaError_t set_smem_attr_once(std::atomic<uint64_t>& done, F set) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = set();
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
+
 template <int ALG, int V, int NB, int STAGES, int W = kTmaWarps>
 static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
                                         cudaStream_t stream) {
@@ -998,10 +1013,9 @@ static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint3
         snprintf(tma_error_buf(), kTmaErrLen, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)rc);
         return cudaErrorInvalidValue;
     }
-    static std::once_flag attr_once;
-    static cudaError_t attr_rc = cudaSuccess;
-    std::call_once(attr_once, [] {
-        attr_rc = cudaFuncSetAttribute(k_fixed_tma<ALG, V, NB, STAGES, W>,
+    static std::atomic<uint64_t> attr_done{0};  // function attributes are per device
+    const cudaError_t attr_rc = set_smem_attr_once(attr_done, [] {
+        return cudaFuncSetAttribute(k_fixed_tma<ALG, V, NB, STAGES, W>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     });
     if (attr_rc != cudaSuccess) return attr_rc;
@@ -1039,10 +1053,9 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
         snprintf(tma_error_buf(), kTmaErrLen, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)rc);
         return cudaErrorInvalidValue;
     }
-    static std::once_flag attr_once;
-    static cudaError_t attr_rc = cudaSuccess;
-    std::call_once(attr_once, [] {
-        attr_rc = cudaFuncSetAttribute(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK>,
+    static std::atomic<uint64_t> attr_done{0};  // function attributes are per device
+    const cudaError_t attr_rc = set_smem_attr_once(attr_done, [] {
+        return cudaFuncSetAttribute(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     });
     if (attr_rc != cudaSuccess) return attr_rc;
