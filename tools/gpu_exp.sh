@@ -1,4 +1,4 @@
 set -u
 mkdir -p gpurun_out
-T=${T:-exp34}
-timeout 900 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_$T.log
+T=${T:-exp35}
+timeout 900 python tools/e2e_pageable.py md5 4194304 1024 > gpurun_out/e2e_pageable_$T.txt 2>&1; echo "rc=$?"; cat gpurun_out/e2e_pageable_$T.txt
