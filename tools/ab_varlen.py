@@ -23,18 +23,10 @@ d_off = torch.from_numpy(off).cuda()
 scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch.uint8, device="cuda:0")
 C = _native.HB_FLAG_VARLEN_COOP
 P = _native.HB_FLAG_VARLEN_COOP_OFF
-ARMS = {"default": ({}, 0),
-        "ld16_win8k": ({"HB_VARLEN_LD": "16", "HB_VARLEN_SORT": "window"}, 0),
-        "ld32_win8k": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "window"}, 0),
-        "ld32_win16k": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "window", "HB_SORT_WINDOW": "16384"}, 0),
-        "ld32_q4_win8k": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "window", "HB_VARLEN_Q": "4"}, 0),
-        "ld32_q4_win16k": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "window", "HB_VARLEN_Q": "4",
-                            "HB_SORT_WINDOW": "16384"}, 0),
-        "ld32_global": ({"HB_VARLEN_LD": "32", "HB_VARLEN_SORT": "global"}, 0),
-        "ld16_global": ({"HB_VARLEN_LD": "16", "HB_VARLEN_SORT": "global"}, 0)}
+ARMS = {"default": ({}, 0), "prefetch": ({"HB_VARLEN_PREFETCH": "1"}, 0)}
 for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
     ref, times = None, {}
-    for _ in range(3):
+    for _ in range(int(os.environ.get("AB_ROUNDS", 3))):
         for arm, (env, flags) in ARMS.items():
             for k in ("HB_VC_STAGES", "HB_VC_PF", "HB_VARLEN_SORT", "HB_SORT_WINDOW", "HB_VARLEN_PREFETCH",
                       "HB_VARLEN_BULK", "HB_VARLEN_LD", "HB_VARLEN_Q"):
