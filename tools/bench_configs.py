@@ -128,11 +128,11 @@ def varlen_point(alg, n, maxlen, seed, steps, out, flags=0):
 
 def sweep(out):
     """configs[4]: message size 16 B .. 64 KiB (13 powers of two) x batch count
-    2^12 / 2^16 / 2^20 / the largest power of two with n*L <= 16 GiB (cap 2^24)."""
+    2^12, 2^14, ..., 2^22 and the largest power of two with n*L <= 16 GiB (cap 2^24)."""
     for k in range(13):
         L = 16 << k
         nmax = min(1 << 24, (16 << 30) // L)
-        for n in sorted({x for x in (1 << 12, 1 << 16, 1 << 20, nmax) if x <= nmax}):
+        for n in sorted({x for x in (1 << 12, 1 << 14, 1 << 16, 1 << 18, 1 << 20, 1 << 22, nmax) if x <= nmax}):
             for alg in ("sha1", "md5", "sm3"):
                 fixed_point(alg, n, L, 5000 + k, 5 if n * L > (1 << 30) else 30, out, "C5")
                 torch.cuda.empty_cache()
