@@ -975,6 +975,64 @@ __global__ void __launch_bounds__(128) k_decimal(uint64_t start, uint64_t count,
     store_digest<ALG>(out + i * H::kDigestBytes, st);
 }
 
+// Runs of ten: thread t renders u = start/10 + t once into the first WIDTH-1
+// digit bytes and hashes v = 10u + j, j = 0..9 (the messages that fall inside
+// [start, start+count)), changing only the last digit byte between messages.
+// The digit extraction -- 27 FMA-pipe ops per 9-digit message in k_decimal --
+// is amortised ten ways, so the compression's pipe balance is what remains.
+// Same bytes as gen_messages (batch.py:96-98): the low WIDTH digits of v are
+// the low WIDTH-1 digits of u followed by v mod 10 = j.  Needs u < 2^30
+// (umulhi reciprocal exact) -- v below ~1.07e10.
+template <int ALG, int WIDTH, int V = -1>
+__global__ void __launch_bounds__(128) k_decimal_run(uint64_t start, uint64_t count, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG, V>;
+    static_assert(WIDTH >= 2 && WIDTH <= 10, "width");
+    const uint64_t u = start / 10u + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t end = start + count;
+    if (u * 10u >= end) return;
+    uint32_t pre[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) pre[j] = 0u;
+    uint32_t u32 = (uint32_t)u;
+#pragma unroll
+    for (int pos = WIDTH - 2; pos >= 0; --pos) {
+        const uint32_t q = __umulhi(u32, 0x1999999Au);
+        const uint32_t d = u32 - q * 10u;
+        pre[pos >> 2] = d * c_opaque[8 * (pos & 3)] + pre[pos >> 2];
+        u32 = q;
+    }
+#pragma unroll
+    for (int w = 0; w < (WIDTH + 3) / 4; ++w) {  // '0' of every digit byte, the last one included
+        uint32_t ascii = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (4 * w + k < WIDTH) ascii |= 0x30u << (8 * k);
+        pre[w] += ascii;
+    }
+    constexpr int kLastW = (WIDTH - 1) >> 2, kLastSh = 8 * ((WIDTH - 1) & 3);
+    auto one = [&](uint32_t j, uint8_t* dst) {
+        uint32_t raw[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) raw[k] = pre[k];
+        raw[kLastW] = pre[kLastW] + (j << kLastSh);
+        uint32_t st[H::kStateWords];
+        H::init(st);
+        md_finish<ALG, V>(st, raw, (uint32_t)WIDTH, (uint64_t)WIDTH);
+        store_digest<ALG>(dst, st);
+    };
+    if (u * 10u >= start && u * 10u + 10u <= end) {  // all but the first / last thread: no range checks
+        uint8_t* dst = out + (u * 10u - start) * H::kDigestBytes;
+#pragma unroll 1
+        for (uint32_t j = 0; j < 10u; ++j) one(j, dst + j * H::kDigestBytes);
+    } else {
+#pragma unroll 1
+        for (uint32_t j = 0; j < 10u; ++j) {
+            const uint64_t v = u * 10u + j;
+            if (v >= start && v < end) one(j, out + (v - start) * H::kDigestBytes);
+        }
+    }
+}
+
 // Run `set` (a cudaFuncSetAttribute call) once per device: kernel attributes
 // such as the dynamic shared-memory limit are per device, so a process driving
 // several GPUs must set them on each (a process-wide call_once would not).
@@ -1309,6 +1367,21 @@ static void dec_launch(uint64_t start, uint64_t count, uint8_t* d_out, cudaStrea
     // variant 1 (SHA-1: 3).  A/B arms: $HB_CONST_VARIANT = 1 | 3, $HB_FMA_DIGITS=0
     // (IMAD.HI + SHF digits, variant 1).  Plain / variant-2 rounds lost 4-14 %
     // (profiles/ab_decimal_r1b.txt) and are no longer instantiated here.
+    if (count == 0) return;
+    if constexpr (W >= 2 && W <= 10) {
+        if (env_u64("HB_DEC_RUN", 1) && (start + count) / 10u < (1ull << 30) - 1) {
+            const uint64_t threads = (start + count + 9u) / 10u - start / 10u;
+            const unsigned g = (unsigned)((threads + 127) / 128);
+            // variant 1 for all three (profiles/ab_decimal_r1d.txt: variant 2
+            // ties on MD5 and loses 4-35 % elsewhere, so it is not instantiated;
+            // SHA-1's variant 3, best for k_decimal, loses 35 % here)
+            switch (env_u64("HB_CONST_VARIANT", 1)) {
+            case 3: k_decimal_run<ALG, W, kVarBal3><<<g, 128, 0, s>>>(start, count, d_out); break;
+            default: k_decimal_run<ALG, W, kVarBal><<<g, 128, 0, s>>>(start, count, d_out); break;
+            }
+            return;
+        }
+    }
     if (!env_u64("HB_FMA_DIGITS", 1)) {
         k_decimal<ALG, W, kVarBal, false><<<grid, 128, 0, s>>>(start, count, d_out);
     } else if (env_u64("HB_CONST_VARIANT", ALG == kSha1 ? 3 : 1) == 3) {

@@ -1,0 +1,23 @@
+"""CPU checks of bench.py's roofline cost model (no GPU): the constant-folded
+ALU-op count of the paper's decimal workload against the per-block counts it
+specialises."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+
+
+def test_decimal_alu_ops_width9():
+    assert [bench.alu_ops_decimal(a, 9) for a in ("md5", "sha1", "sm3")] == [127, 404, 1010]
+
+
+def test_decimal_alu_ops_bounded_by_block_model():
+    for alg in ("md5", "sha1", "sm3"):
+        prev = 0
+        for w in range(1, 56):
+            ops = bench.alu_ops_decimal(alg, w)
+            # more varying words never make the block cheaper; folding never
+            # exceeds the arbitrary-data count (which adds 16 byte swaps for SHA-1/SM3)
+            assert prev <= ops <= bench.ALU_OPS_PER_BLOCK[alg]
+            prev = ops

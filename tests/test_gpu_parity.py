@@ -184,8 +184,12 @@ def test_ratio_invariance_style_sharding():
         assert np.array_equal(batch_digest(alg, data, gpus=list(range(n)) + [0]), ref)  # uneven split, repeated dev
 
 
+@pytest.mark.parametrize("dec_run", ["1", "0"])
 @pytest.mark.parametrize("variant", ["1", "fma_digits"])
-def test_decimal_workload(golden, variant, monkeypatch):
+def test_decimal_workload(golden, variant, dec_run, monkeypatch):
+    """HB_DEC_RUN=1 (default): runs-of-ten kernel for widths 2..10 below
+    v ~ 1.07e10, the one-message-per-thread kernel elsewhere; 0: the latter only."""
+    monkeypatch.setenv("HB_DEC_RUN", dec_run)
     monkeypatch.setenv("HB_FMA_DIGITS", "0")
     if variant == "fma_digits":
         monkeypatch.setenv("HB_FMA_DIGITS", "1")
@@ -214,6 +218,25 @@ def test_decimal_workload(golden, variant, monkeypatch):
         msgs = oracle.gen_decimal(start, cnt, w) if w <= 20 else gen_messages(start, cnt, w).as_array()
         for alg in ALGS:
             assert np.array_equal(hash_decimal(alg, start, cnt, w), oracle.batch_fixed(alg, msgs)), (alg, w)
+
+
+@pytest.mark.parametrize("variant", ["1", "3"])
+def test_decimal_runs_ragged(variant, monkeypatch):
+    """Runs-of-ten kernel: every start residue mod 10 x short counts (first and
+    last thread partial, one thread both), the end of the width-10 range and
+    the 2^32 boundary (u = v / 10 stays below 2^30 for every width <= 10)."""
+    monkeypatch.setenv("HB_CONST_VARIANT", variant)
+    for w in (2, 3, 9, 10):
+        for r in range(10):
+            for cnt in (c for c in (1, 2, 9, 10, 11, 19, 21, 1283) if c <= 10**w):
+                start = max(0, min(10**w - cnt, 10**(w - 1) + 37 * 10 + r))
+                for alg in ALGS:
+                    assert np.array_equal(hash_decimal(alg, start, cnt, w),
+                                          oracle.batch_fixed(alg, oracle.gen_decimal(start, cnt, w))), (alg, w, start, cnt)
+    for start, cnt in ((10**10 - 1000, 1000), (10**10 - 1001, 1001), (10**10 - 37, 37), (2**32 - 15, 40)):
+        for alg in ALGS:
+            assert np.array_equal(hash_decimal(alg, start, cnt, 10),
+                                  oracle.batch_fixed(alg, oracle.gen_decimal(start, cnt, 10))), (alg, start, cnt)
 
 
 def test_error_mapping():

@@ -1,5 +1,6 @@
 """A/B of the in-kernel decimal workload (paper: 10^9 x 9 digits) across round
-variants ($HB_CONST_VARIANT), kernel-only, digests cross-checked."""
+variants ($HB_CONST_VARIANT) and kernels ($HB_DEC_RUN: runs of ten vs one
+message per thread), kernel-only, digests cross-checked.  Arms: $AB_ARMS."""
 import json
 import os
 import statistics
@@ -15,9 +16,10 @@ for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
     out = torch.empty((n, {"md5": 16, "sha1": 20, "sm3": 32}[alg]), dtype=torch.uint8, device="cuda:0")
     ref, times = None, {}
     for _ in range(3):
-        for arm in ("v1", "v1_fma_digits", "v3_fma_digits"):
+        for arm in os.environ.get("AB_ARMS", "v1_fma_digits,v3_fma_digits,v1_run,v3_run").split(","):
             os.environ["HB_CONST_VARIANT"] = arm[1]
-            os.environ["HB_FMA_DIGITS"] = "1" if "fma" in arm else "0"
+            os.environ["HB_FMA_DIGITS"] = "1" if "fma" in arm or "run" in arm else "0"
+            os.environ["HB_DEC_RUN"] = "1" if "run" in arm else "0"
             device.hash_decimal(alg, 0, n, 9, out=out)
             torch.cuda.synchronize()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
