@@ -17,7 +17,7 @@ for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
     ref, times = None, {}
     for _ in range(3):
         for arm in os.environ.get("AB_ARMS", "v1_fma_digits,v3_fma_digits,v1_run,v3_run").split(","):
-            os.environ["HB_CONST_VARIANT"] = arm[1]
+            os.environ["HB_CONST_VARIANT"] = arm[1:].split("_")[0]
             os.environ["HB_FMA_DIGITS"] = "1" if "fma" in arm or "run" in arm else "0"
             os.environ["HB_DEC_RUN"] = "1" if "run" in arm else "0"
             device.hash_decimal(alg, 0, n, 9, out=out)
