@@ -99,6 +99,21 @@ static uint64_t env_u64(const char* name, uint64_t dflt) {
     return (end && *end == '\0' && x > 0) ? (uint64_t)x : dflt;
 }
 static uint64_t chunk_bytes() { return env_u64("HB_CHUNK_BYTES", 256ull << 20); }
+// Chunk budget for a shard of `staged` input bytes and `out` digest bytes.
+// When the digests are big enough for their copy-out to matter (short
+// messages: >= HB_PIPE_MIN_OUT, 4 MiB), the shard is cut into at least
+// HB_PIPE_CHUNKS (4) chunks of >= HB_MIN_CHUNK_BYTES (8 MiB), so chunk k's
+// kernel + D2H overlap chunk k+1's H2D across the slot ring instead of running
+// back to back.  Smaller shards, or long messages with few digest bytes, stay
+// one chunk: every extra chunk costs ~10-20 us of copy/launch latency
+// (profiles/ab_pipe_r1.txt: +7..17 % e2e at 16-64 MB of 64-byte messages,
+// -3..-40 % if 4 MB batches or 1 KiB messages were split).
+static uint64_t pipelined_budget(uint64_t staged, uint64_t out) {
+    if (out < env_u64("HB_PIPE_MIN_OUT", 4ull << 20)) return chunk_bytes();
+    const uint64_t parts = env_u64("HB_PIPE_CHUNKS", 4);
+    const uint64_t floor_b = env_u64("HB_MIN_CHUNK_BYTES", 8ull << 20);
+    return std::min(chunk_bytes(), std::max(floor_b, (staged + parts - 1) / parts));
+}
 static int memcpy_threads(int n_gpus) {
     uint64_t t = env_u64("HB_MEMCPY_THREADS", 0);
     if (t) return (int)t;
@@ -287,7 +302,10 @@ static int run_shard_locked(GpuCtx& c, const ShardJob& j, ShardStats& st) {
     int rc = ctx_init(c);
     if (rc) return rc;
     const int dlen = digest_len(j.alg);
-    const uint64_t budget = chunk_bytes();
+    const uint64_t staged = j.kind == 0 ? (j.hi - j.lo) * j.msg_len
+                          : j.kind == 1 ? j.offsets[j.hi] - j.offsets[j.lo]
+                                        : (j.hi - j.lo) * (uint64_t)dlen;  // decimal: digests only
+    const uint64_t budget = pipelined_budget(staged, (j.hi - j.lo) * (uint64_t)dlen);
     uint64_t slot_k = 0;
     const uint64_t l0 = hb::launches_total();
     uint64_t i = j.lo;
@@ -310,7 +328,7 @@ static int run_shard_locked(GpuCtx& c, const ShardJob& j, ShardStats& st) {
             in_off = j.offsets[i];
             in_bytes = j.offsets[e] - j.offsets[i];
         } else {
-            const uint64_t per = std::max<uint64_t>(1, budget / 32);
+            const uint64_t per = std::max<uint64_t>(1, budget / (uint64_t)dlen);
             e = std::min(j.hi, i + per);
         }
         const uint64_t cn = e - i;

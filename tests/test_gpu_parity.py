@@ -165,6 +165,36 @@ def test_engine_chunking_and_pinned(monkeypatch):
         assert np.array_equal(batch_digest_varlen(alg, vdata, off), oracle.batch_varlen(alg, vdata, off, 8))
 
 
+def test_engine_pipelined_chunks(monkeypatch):
+    """Chunk pipelining of host-buffer calls: a shard whose digests reach
+    HB_PIPE_MIN_OUT is cut into >= HB_PIPE_CHUNKS chunks of >= HB_MIN_CHUNK_BYTES
+    (H2D of chunk k+1 overlaps kernel + D2H of chunk k); a 4 MiB batch of
+    64-byte messages stays one chunk by default.  The digests are the oracle's
+    either way (fixed, varlen, decimal)."""
+    n, L = 65536, 64
+    data = oracle.fill_random(n * L, 37).reshape(n, L)
+    lens = np.random.default_rng(3).integers(0, 129, 40000).astype(np.uint64)
+    off = np.zeros(len(lens) + 1, np.uint64)
+    off[1:] = np.cumsum(lens)
+    vdata = oracle.fill_random(int(off[-1]), 9)
+    for alg in ALGS:
+        ref = oracle.batch_fixed(alg, data, threads=8)
+        vref = oracle.batch_varlen(alg, vdata, off, 8)
+        dref = oracle.batch_fixed(alg, oracle.gen_decimal(10**6, 300000, 9), threads=8)
+        for env, chunks in (({}, (1, 1)), ({"HB_PIPE_MIN_OUT": "1", "HB_MIN_CHUNK_BYTES": str(1 << 20)}, (4, 4)),
+                            ({"HB_PIPE_MIN_OUT": "1", "HB_MIN_CHUNK_BYTES": "65536", "HB_PIPE_CHUNKS": "16"}, (16, 16)),
+                            ({"HB_PIPE_MIN_OUT": "1", "HB_PIPE_CHUNKS": "1"}, (1, 1))):
+            for k in ("HB_PIPE_MIN_OUT", "HB_MIN_CHUNK_BYTES", "HB_PIPE_CHUNKS"):
+                monkeypatch.delenv(k, raising=False)
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            t = {}
+            assert np.array_equal(batch_digest(alg, data, timing=t), ref)
+            assert chunks[0] <= t["chunks"] <= chunks[1], (alg, env, t["chunks"])
+            assert np.array_equal(batch_digest_varlen(alg, vdata, off), vref)
+            assert np.array_equal(hash_decimal(alg, 10**6, 300000, 9), dref)
+
+
 def test_hash_batch_and_thread_invariance():
     b = gen_messages(0, 3)
     for alg in ALGS:
