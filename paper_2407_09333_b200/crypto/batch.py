@@ -287,9 +287,26 @@ def hash_batch(alg: str, batch, threads: int = 1, accel: bool = False, *,
                                   batch.offsets_array(), gpus=gpus)
     else:
         out = batch_digest(alg, batch.as_array(), accel=accel, gpus=gpus)
+    return _digest_list(alg, out.tobytes(), batch.count)
+
+
+def _digest_list(alg: str, raw: bytes, count: int) -> list[Digest]:
+    """``count`` Digest objects over consecutive ``DIGEST_LEN[alg]``-byte slices
+    of ``raw``.  Their fields are valid by construction (``alg`` checked by the
+    caller, every slice exactly dlen bytes), so the per-object ``__post_init__``
+    is skipped: the fields go straight into each frozen instance's ``__dict__``
+    (the same state the dataclass ``__init__`` leaves).  About half the Python
+    cost per digest -- the list building dominates ``hash_batch`` at large n
+    (reference: ~70 % of a 10^6 x 9 B batch)."""
     dlen = DIGEST_LEN[alg]
-    raw = out.tobytes()
-    return [Digest(alg, raw[i * dlen : (i + 1) * dlen]) for i in range(batch.count)]
+    new = object.__new__
+    out = []
+    append = out.append
+    for i in range(0, count * dlen, dlen):
+        d = new(Digest)
+        d.__dict__.update(alg=alg, data=raw[i : i + dlen])
+        append(d)
+    return out
 
 
 def sha1(msg: bytes) -> bytes:

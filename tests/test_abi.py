@@ -194,3 +194,24 @@ def test_out_argument_validation():
         batch_digest_varlen("sha1", np.zeros(8, np.uint8), np.array([0, 8], np.uint64), out=np.zeros((2, 20), np.uint8))
     with pytest.raises(ValueError):
         hash_decimal("sm3", 0, 3, out=np.zeros((3, 20), np.uint8))
+
+
+def test_digest_list_matches_constructor():
+    """hash_batch's fast Digest construction leaves the same objects the
+    validating dataclass __init__ does (equality, hash, repr, frozenness)."""
+    import dataclasses
+
+    from paper_2407_09333_b200.crypto import Digest
+    from paper_2407_09333_b200.crypto.batch import _digest_list
+
+    for alg, dlen in (("md5", 16), ("sha1", 20), ("sm3", 32)):
+        raw = bytes(range(256)) * 2
+        n = len(raw) // dlen
+        fast = _digest_list(alg, raw, n)
+        ref = [Digest(alg, raw[i * dlen:(i + 1) * dlen]) for i in range(n)]
+        assert fast == ref
+        assert [hash(d) for d in fast] == [hash(d) for d in ref]
+        assert repr(fast[1]) == repr(ref[1]) and fast[1].hex() == ref[1].hex()
+        with pytest.raises(dataclasses.FrozenInstanceError):
+            fast[0].data = b""
+    assert _digest_list("md5", b"", 0) == []
