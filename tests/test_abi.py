@@ -201,13 +201,23 @@ def test_digest_list_matches_constructor():
     validating dataclass __init__ does (equality, hash, repr, frozenness)."""
     import dataclasses
 
-    from paper_2407_09333_b200.crypto import Digest
+    from paper_2407_09333_b200.crypto import Digest, batch
     from paper_2407_09333_b200.crypto.batch import _digest_list
 
+    assert batch._hb_pyobj is not None, "csrc/hb_pyobj.c not built"
+    helper = batch._hb_pyobj
     for alg, dlen in (("md5", 16), ("sha1", 20), ("sm3", 32)):
         raw = bytes(range(256)) * 2
         n = len(raw) // dlen
         fast = _digest_list(alg, raw, n)
+        batch._hb_pyobj = None  # the pure-Python reference loop
+        try:
+            assert _digest_list(alg, raw, n) == fast
+        finally:
+            batch._hb_pyobj = helper
+        assert helper.digest_list(Digest, alg, memoryview(raw), dlen, n) == fast
+        arr = np.frombuffer(raw, np.uint8)[: n * dlen].reshape(n, dlen)  # the digest-array form hash_batch passes
+        assert _digest_list(alg, arr, n) == fast
         ref = [Digest(alg, raw[i * dlen:(i + 1) * dlen]) for i in range(n)]
         assert fast == ref
         assert [hash(d) for d in fast] == [hash(d) for d in ref]
@@ -215,3 +225,7 @@ def test_digest_list_matches_constructor():
         with pytest.raises(dataclasses.FrozenInstanceError):
             fast[0].data = b""
     assert _digest_list("md5", b"", 0) == []
+    with pytest.raises(ValueError):
+        helper.digest_list(Digest, "md5", b"x" * 31, 16, 2)  # buffer shorter than count * dlen
+    with pytest.raises(TypeError):
+        helper.digest_list(int, "md5", b"x" * 32, 16, 2)  # not a Python class
