@@ -175,6 +175,12 @@ def _out_array(out, n: int, alg: str) -> np.ndarray:
     return out
 
 
+def _timing_arg(t, timing):
+    """hb_timing out-parameter: NULL unless the caller asked for timings (the
+    engine then skips its per-stage events, a few driver calls per chunk)."""
+    return ctypes.byref(t) if timing is not None else None
+
+
 def batch_digest(alg: str, data, accel: bool = False, *, gpus=None, ratios=None, flags: int = 0,
                  timing: dict | None = None, out=None) -> np.ndarray:
     """Hash each row of an (n, width) uint8 array; returns a new (n, digest_len) uint8 array.
@@ -198,10 +204,10 @@ def batch_digest(alg: str, data, accel: bool = False, *, gpus=None, ratios=None,
     if ratios is not None:
         r = (ctypes.c_double * len(ratios))(*[float(x) for x in ratios])
         rc = _native.lib().hb_hash_fixed_split(_native.ALG_ID[alg], _ptr(rows), n, width, out.ctypes.data, garr,
-                                               r, ng, int(flags), ctypes.byref(t))
+                                               r, ng, int(flags), _timing_arg(t, timing))
     else:
         rc = _native.lib().hb_hash_fixed(_native.ALG_ID[alg], _ptr(rows), n, width, out.ctypes.data, garr, ng,
-                                         int(flags), ctypes.byref(t))
+                                         int(flags), _timing_arg(t, timing))
     _native.check(rc, "hb_hash_fixed")
     if timing is not None:
         timing.update(t.as_dict())
@@ -230,7 +236,7 @@ def batch_digest_varlen(alg: str, data, offsets, *, gpus=None, flags: int = 0,
     garr, ng = _native.gpu_array(gpus)
     t = _native.HbTiming()
     rc = _native.lib().hb_hash_varlen(_native.ALG_ID[alg], _ptr(buf), off.ctypes.data, n, out.ctypes.data, garr,
-                                      ng, int(flags), ctypes.byref(t))
+                                      ng, int(flags), _timing_arg(t, timing))
     _native.check(rc, "hb_hash_varlen")
     if timing is not None:
         timing.update(t.as_dict())
@@ -258,7 +264,7 @@ def hash_decimal(alg: str, start_index: int, count: int, width: int = 9, *, gpus
     garr, ng = _native.gpu_array(gpus)
     t = _native.HbTiming()
     rc = _native.lib().hb_hash_decimal(_native.ALG_ID[alg], start_index, count, width, out.ctypes.data, garr, ng,
-                                       0, ctypes.byref(t))
+                                       0, _timing_arg(t, timing))
     _native.check(rc, "hb_hash_decimal")
     if timing is not None:
         timing.update(t.as_dict())

@@ -192,6 +192,7 @@ struct Slot {
     HostBuf h_in, h_out, h_off;
     bool in_use = false;
     bool has_h2d = false;
+    bool timed = false;  // ev[0..4] recorded (the caller asked for hb_timing)
     // deferred copy-out (pageable destination)
     uint8_t* pend_dst = nullptr;
     uint64_t pend_bytes = 0;
@@ -242,9 +243,11 @@ static int retire_slot(Slot& s, ShardStats& st, int mt) {
     if (!s.in_use) return HB_OK;
     HB_CK(cudaEventSynchronize(s.ev[5]));
     float ms = 0;
-    if (s.has_h2d && cudaEventElapsedTime(&ms, s.ev[0], s.ev[1]) == cudaSuccess) st.h2d_ms += ms;
-    if (cudaEventElapsedTime(&ms, s.ev[2], s.ev[3]) == cudaSuccess) st.kernel_ms += ms;
-    if (cudaEventElapsedTime(&ms, s.ev[4], s.ev[5]) == cudaSuccess) st.d2h_ms += ms;
+    if (s.timed) {
+        if (s.has_h2d && cudaEventElapsedTime(&ms, s.ev[0], s.ev[1]) == cudaSuccess) st.h2d_ms += ms;
+        if (cudaEventElapsedTime(&ms, s.ev[2], s.ev[3]) == cudaSuccess) st.kernel_ms += ms;
+        if (cudaEventElapsedTime(&ms, s.ev[4], s.ev[5]) == cudaSuccess) st.d2h_ms += ms;
+    }
     if (s.pend_bytes) parallel_memcpy(s.pend_dst, s.h_out.p, s.pend_bytes, mt);
     s.pend_bytes = 0;
     s.in_use = false;
@@ -296,6 +299,7 @@ struct ShardJob {
     bool in_pinned = false, off_pinned = false, out_pinned = false;
     uint32_t flags = 0;
     int mt = 1;
+    bool timed = true;  // record per-stage events (hb_timing requested)
 };
 
 static int run_shard_locked(GpuCtx& c, const ShardJob& j, ShardStats& st) {
@@ -339,8 +343,10 @@ static int run_shard_locked(GpuCtx& c, const ShardJob& j, ShardStats& st) {
         HB_CK(s.d_out.ensure(cn * dlen));
         if (in_bytes) HB_CK(s.d_in.ensure(in_bytes + 64));
         s.has_h2d = false;
-        // ---- copy in
-        HB_CK(cudaEventRecord(s.ev[0], s.stream));
+        // ---- copy in (the per-stage events only when the caller wants hb_timing:
+        // each record is a driver call on a small batch's critical path)
+        s.timed = j.timed;
+        if (j.timed) HB_CK(cudaEventRecord(s.ev[0], s.stream));
         if (j.kind == 0 && in_bytes) {
             rc = stage_in(s, s.d_in, s.h_in, j.msgs + in_off, in_bytes, j.in_pinned, j.mt);
             if (rc) return rc;
@@ -355,10 +361,10 @@ static int run_shard_locked(GpuCtx& c, const ShardJob& j, ShardStats& st) {
             }
             s.has_h2d = true;
         }
-        HB_CK(cudaEventRecord(s.ev[1], s.stream));
+        if (j.timed) HB_CK(cudaEventRecord(s.ev[1], s.stream));
         st.h2d_bytes += in_bytes + (j.kind == 1 ? (cn + 1) * 8 : 0);
         // ---- kernel
-        HB_CK(cudaEventRecord(s.ev[2], s.stream));
+        if (j.timed) HB_CK(cudaEventRecord(s.ev[2], s.stream));
         uint8_t* dout = static_cast<uint8_t*>(s.d_out.p);
         if (j.kind == 0) {
             HB_CK(launch_fixed(j.alg, static_cast<const uint8_t*>(s.d_in.p), cn, j.msg_len, dout, s.stream, j.flags));
@@ -374,9 +380,11 @@ static int run_shard_locked(GpuCtx& c, const ShardJob& j, ShardStats& st) {
         } else {
             HB_CK(launch_decimal(j.alg, j.start + i, cn, j.width, dout, s.stream));
         }
-        HB_CK(cudaEventRecord(s.ev[3], s.stream));
+        if (j.timed) {
+            HB_CK(cudaEventRecord(s.ev[3], s.stream));
+            HB_CK(cudaEventRecord(s.ev[4], s.stream));
+        }
         // ---- copy out (dst_off = s*dlen)
-        HB_CK(cudaEventRecord(s.ev[4], s.stream));
         rc = stage_out(s, j.out + i * dlen, cn * dlen, j.out_pinned);
         if (rc) return rc;
         HB_CK(cudaEventRecord(s.ev[5], s.stream));
@@ -476,6 +484,7 @@ static int run_sharded(ShardJob proto, uint64_t n, const std::vector<int>& devs,
     int rc = partition(0, (int64_t)n, ratios.data(), k, bounds.data());
     if (rc) return rc;
     proto.mt = memcpy_threads(k);
+    proto.timed = t != nullptr;
     std::vector<ShardJob> jobs;
     for (int d = 0; d < k; ++d) {
         if (bounds[d + 1] <= bounds[d]) continue;
