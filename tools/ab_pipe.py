@@ -16,10 +16,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2407_09333_b200 import crypto  # noqa: E402
 
 DLEN = {"md5": 16, "sha1": 20, "sm3": 32}
-# arm "P" or "P@M": HB_PIPE_CHUNKS=P, HB_MIN_CHUNK_BYTES=M MiB (engine default otherwise)
+# arm "P" or "P@M": HB_PIPE_CHUNKS=P, HB_MIN_CHUNK_BYTES=M MiB and no digest-size threshold
+# (engine defaults otherwise)
 ARMS = os.environ.get("AB_ARMS", "1,4@1,4@4,4@8,4@16").split(",")
 CASES = [("sha1", 65536, 64), ("sha1", 1 << 17, 64), ("sha1", 1 << 18, 64), ("sha1", 1 << 19, 64),
          ("sha1", 1 << 20, 64), ("sm3", 1 << 19, 64), ("md5", 1 << 16, 1024), ("md5", 1 << 20, 1024)]
+if os.environ.get("AB_CASES") == "small":
+    CASES = [("sha1", 16384, 64), ("sha1", 65536, 64), ("md5", 65536, 64), ("sha1", 1 << 17, 64), ("md5", 4096, 1024)]
 
 
 def pinned(shape):
@@ -36,8 +39,10 @@ for alg, n, L in CASES:
         for arm in ARMS:
             os.environ["HB_PIPE_CHUNKS"] = arm.split("@")[0]
             os.environ.pop("HB_MIN_CHUNK_BYTES", None)
-            if "@" in arm:
-                os.environ["HB_MIN_CHUNK_BYTES"] = str(int(arm.split("@")[1]) << 20)
+            os.environ.pop("HB_PIPE_MIN_OUT", None)
+            if "@" in arm:  # explicit floor: split regardless of the digest-size threshold
+                os.environ["HB_MIN_CHUNK_BYTES"] = str(int(float(arm.split("@")[1]) * (1 << 20)))
+                os.environ["HB_PIPE_MIN_OUT"] = "1"
             crypto.batch_digest(alg, src, out=out)
             t0 = time.perf_counter()
             for _ in range(reps):
