@@ -101,7 +101,8 @@ uint64_t hb_launch_count(void);           /* kernels launched by this process so
  * streams its slice through a ring of pinned/device chunk buffers (H2D, kernel,
  * D2H overlapped on separate streams).  Host buffers may be pageable or
  * pinned (pinned is copied directly).  gpus == NULL / n_gpus == 0 means "all
- * devices".  t may be NULL.  msg_len 0 hashes empty messages.                */
+ * devices".  t may be NULL (then no per-stage CUDA events are recorded, which
+ * saves ~30 us per call on small batches).  msg_len 0 hashes empty messages. */
 int hb_hash_fixed(int alg, const uint8_t *msgs, uint64_t n, uint64_t msg_len, uint8_t *out,
                   const int *gpus, int n_gpus, uint32_t flags, hb_timing *t);
 
