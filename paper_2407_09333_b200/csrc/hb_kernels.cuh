@@ -40,6 +40,34 @@ static inline uint64_t env_u64(const char* name, uint64_t dflt) {
     return v ? strtoull(v, nullptr, 10) : dflt;
 }
 
+// Launch with programmatic stream serialization: the kernel may be scheduled
+// while the previous kernel in the stream drains; it orders itself with
+// griddepcontrol.wait.  $HB_PDL=0 launches normally (A/B).
+template <class... KArgs, class... Args>
+static void launch_pdl_smem(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                            Args... args) {
+    if (!env_u64("HB_PDL", 1)) {
+        kernel<<<grid, block, smem, s>>>(args...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+template <class... KArgs, class... Args>
+static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+    launch_pdl_smem(kernel, grid, block, 0, s, args...);
+}
+
 // =========================================================================
 // Fixed-width, TMA-staged kernel (the hot path).
 //
@@ -211,6 +239,10 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
         fence_mbar_init();
     }
     __syncthreads();
+    // Programmatic dependent launch (launch_pdl_smem): the barrier setup above
+    // overlaps the previous grid's tail; global memory is touched only after it
+    // completes.  The next grid is triggered once the digests are computed.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == kWsComputeWarps) {  // ---------------- producer warp
         if (lane == 0) {
@@ -293,6 +325,7 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
             for (int j = 0; j < 16; ++j) raw[q][j] = 0u;
     }
     md_finish_n<ALG, V, NB>(st, raw, r, msg_len);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
         const uint32_t grow = row0 + row + 128u * q;
@@ -357,6 +390,11 @@ __global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__
     constexpr uint64_t kBits = (uint64_t)L * 8u;
     constexpr uint32_t kL14 = H::kBigEndian ? bswap_c((uint32_t)(kBits >> 32)) : (uint32_t)kBits;
     constexpr uint32_t kL15 = H::kBigEndian ? bswap_c((uint32_t)kBits) : (uint32_t)(kBits >> 32);
+    // Programmatic dependent launch (launch_pdl): wait for the previous grid's
+    // completion and memory before touching global memory; the trigger for
+    // the next grid comes once this thread's hash is done (both no-ops for a
+    // normal launch).  A stream of short batches then hides the launch gap.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint4* p = reinterpret_cast<const uint4*>(msgs + i * L);
@@ -379,6 +417,7 @@ __global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__
         if (b == kNb - 1) { raw[14] = kL14; raw[15] = kL15; }
         compress1<ALG, V>(st, raw);
     }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     store_digest<ALG>(out + i * H::kDigestBytes, st);
 }
 
@@ -1118,8 +1157,8 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     });
     if (attr_rc != cudaSuccess) return attr_rc;
     const uint32_t grid = (n + C::kRows - 1) / C::kRows;
-    k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK><<<grid, (kWsComputeWarps + 1) * 32, C::kSmem, stream>>>(map, n, L, d_out,
-                                                                                                       (uint32_t)env_u64("HB_TMA_EVICT_FIRST", 0));
+    launch_pdl_smem(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK>, grid, (kWsComputeWarps + 1) * 32, C::kSmem, stream,
+                    map, n, L, d_out, (uint32_t)env_u64("HB_TMA_EVICT_FIRST", 0));
     note_launches(1);
     return cudaGetLastError();
 }
@@ -1271,20 +1310,20 @@ static cudaError_t launch_fixed_alg(const uint8_t* d_msgs, uint64_t n, uint64_t 
     const unsigned sblk = sb >= 128 ? 128u : sb >= 64 ? 64u : 32u;  // __launch_bounds__(128)
     const unsigned sgrid = (unsigned)((n + sblk - 1) / sblk);
     if (small_ok && L == 16) {
-        small_v1 ? k_fixed_small<ALG, 16, kVarBal><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out)
-                 : k_fixed_small<ALG, 16, kVarPlain><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? launch_pdl(k_fixed_small<ALG, 16, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out)
+                 : launch_pdl(k_fixed_small<ALG, 16, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
     } else if (small_ok && L == 32) {
-        small_v1 ? k_fixed_small<ALG, 32, kVarBal><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out)
-                 : k_fixed_small<ALG, 32, kVarPlain><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? launch_pdl(k_fixed_small<ALG, 32, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out)
+                 : launch_pdl(k_fixed_small<ALG, 32, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
     } else if (small_ok && L == 48) {
-        small_v1 ? k_fixed_small<ALG, 48, kVarBal><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out)
-                 : k_fixed_small<ALG, 48, kVarPlain><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? launch_pdl(k_fixed_small<ALG, 48, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out)
+                 : launch_pdl(k_fixed_small<ALG, 48, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
     } else if (small_ok && L == 64) {
-        small_v1 ? k_fixed_small<ALG, 64, kVarBal><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out)
-                 : k_fixed_small<ALG, 64, kVarPlain><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? launch_pdl(k_fixed_small<ALG, 64, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out)
+                 : launch_pdl(k_fixed_small<ALG, 64, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
     } else if (small_ok && L == 128) {
-        small_v1 ? k_fixed_small<ALG, 128, kVarBal><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out)
-                 : k_fixed_small<ALG, 128, kVarPlain><<<sgrid, sblk, 0, stream>>>(d_msgs, n, d_out);
+        small_v1 ? launch_pdl(k_fixed_small<ALG, 128, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out)
+                 : launch_pdl(k_fixed_small<ALG, 128, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
     } else if (aligned) {
         k_fixed_direct<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, (uint32_t)L, d_out);
     } else {
