@@ -45,8 +45,8 @@ static inline uint64_t env_u64(const char* name, uint64_t dflt) {
 // griddepcontrol.wait.  $HB_PDL=0 launches normally (A/B).
 template <class... KArgs, class... Args>
 static void launch_pdl_smem(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
-                            Args... args) {
-    if (!env_u64("HB_PDL", 1)) {
+                            bool pdl, Args... args) {
+    if (!pdl || !env_u64("HB_PDL", 1)) {
         kernel<<<grid, block, smem, s>>>(args...);
         return;
     }
@@ -65,7 +65,20 @@ static void launch_pdl_smem(void (*kernel)(KArgs...), unsigned grid, unsigned bl
 
 template <class... KArgs, class... Args>
 static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
-    launch_pdl_smem(kernel, grid, block, 0, s, args...);
+    launch_pdl_smem(kernel, grid, block, 0, s, true, args...);
+}
+
+// SMs of the current device (cached per device).
+static int device_sms() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (!v) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        cache[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
 }
 
 // =========================================================================
@@ -1157,8 +1170,14 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     });
     if (attr_rc != cudaSuccess) return attr_rc;
     const uint32_t grid = (n + C::kRows - 1) / C::kRows;
+    // PDL pays for short kernels (launch gap hidden: +5-17 %) and for grids
+    // that fill every SM anyway.  A sub-wave grid of long messages is bound by
+    // each message's dependent chain; early-launched CTAs can land two to an
+    // SM there and run up to 30 % slower (profiles/ab_pdl_r1.txt), so those
+    // launch normally.
+    const bool pdl = grid >= (uint32_t)device_sms() || (L + 8u) / 64u + 1u <= 17u;
     launch_pdl_smem(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK>, grid, (kWsComputeWarps + 1) * 32, C::kSmem, stream,
-                    map, n, L, d_out, (uint32_t)env_u64("HB_TMA_EVICT_FIRST", 0));
+                    pdl, map, n, L, d_out, (uint32_t)env_u64("HB_TMA_EVICT_FIRST", 0));
     note_launches(1);
     return cudaGetLastError();
 }
