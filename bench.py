@@ -220,6 +220,9 @@ class ClockSampler:
 _BACKEND = os.environ.get("HB_BENCH_BACKEND", "nccl")
 
 
+HOST_AFFINITY = ["unbound (one process, N=1)"]
+
+
 def dist_setup(args):
     import torch
 
@@ -237,6 +240,11 @@ def dist_setup(args):
         else:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # host side next to this rank's GPU (pinned e2e buffers are allocated later)
+        from paper_2407_09333_b200.device import bind_host_to_gpu
+
+        cores = bind_host_to_gpu(local)
+        HOST_AFFINITY[0] = f"{len(cores)} GPU-local cores (NVML)" if cores else "unbound (NVML gave no mask)"
     else:
         torch.cuda.set_device(0)
     return world, rank, local
@@ -775,7 +783,8 @@ def run_ours(args):
                          f"synthetic: counter-based splitmix64 bytes (seed {w.seed}), generated on device"),
                 "config": dict(w.config(world), launch=f"CUDA-graph replays of {GRAPH_STEPS} back-to-back steps"
                                if w.launches_per_step() else "direct launch per step",
-                               gather="fused P2P into rank 0 (CUDA IPC)" if gather is not None else "none"),
+                               gather="fused P2P into rank 0 (CUDA IPC)" if gather is not None else "none",
+                               host_affinity=HOST_AFFINITY[0]),
                 "mhash_per_s": round(mhash, 2), "clocks": clk, "e2e": e2e,
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "parity": parity}
         print(json.dumps(line), flush=True)

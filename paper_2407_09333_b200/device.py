@@ -122,3 +122,43 @@ class FixedHashGraph:
     def replay(self):
         self.graph.replay()
         return self.out
+
+
+def bind_host_to_gpu(ordinal: int):
+    """Restrict this process's CPU affinity to the cores NVML reports as local
+    to CUDA device ``ordinal`` (its NUMA node) and return them, or None when
+    NVML cannot say.  Call it before allocating pinned host buffers: the
+    driver first-touches page-locked memory from the calling thread, so the
+    buffers -- and the engine's host staging threads, which inherit the mask --
+    then sit next to the GPU's PCIe root instead of across the socket link.
+    One process per GPU (``bench.py`` under torchrun) calls it for its own GPU.
+    """
+    import os
+
+    try:
+        import pynvml
+        import torch
+
+        uuid = str(torch.cuda.get_device_properties(ordinal).uuid).lower().removeprefix("gpu-")
+        pynvml.nvmlInit()
+        try:
+            for i in range(pynvml.nvmlDeviceGetCount()):
+                h = pynvml.nvmlDeviceGetHandleByIndex(i)
+                u = pynvml.nvmlDeviceGetUUID(h)
+                u = (u.decode() if isinstance(u, bytes) else u).lower().removeprefix("gpu-")
+                if u != uuid:
+                    continue
+                words = ((os.cpu_count() or 1) + 63) // 64
+                masks = pynvml.nvmlDeviceGetCpuAffinity(h, words)
+                allowed = os.sched_getaffinity(0)
+                cores = sorted(64 * w + b for w, m in enumerate(masks) for b in range(64)
+                               if (m >> b) & 1 and 64 * w + b in allowed)
+                if not cores:
+                    return None
+                os.sched_setaffinity(0, cores)
+                return cores
+        finally:
+            pynvml.nvmlShutdown()
+    except Exception:  # no NVML / no GPU / unsupported: leave the affinity alone
+        return None
+    return None

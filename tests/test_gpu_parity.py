@@ -195,6 +195,22 @@ def test_engine_pipelined_chunks(monkeypatch):
             assert np.array_equal(hash_decimal(alg, 10**6, 300000, 9), dref)
 
 
+def test_bind_host_to_gpu():
+    """NVML's GPU-local core set becomes this process's affinity (bench.py
+    does this per rank before allocating pinned buffers)."""
+    import os
+
+    from paper_2407_09333_b200.device import bind_host_to_gpu
+
+    before = os.sched_getaffinity(0)
+    try:
+        cores = bind_host_to_gpu(0)
+        assert cores, "NVML returned no CPU affinity for GPU 0"
+        assert set(cores) <= before and os.sched_getaffinity(0) == set(cores)
+    finally:
+        os.sched_setaffinity(0, before)
+
+
 def test_hash_batch_and_thread_invariance():
     b = gen_messages(0, 3)
     for alg in ALGS:
