@@ -126,7 +126,11 @@ int hb_hash_decimal(int alg, uint64_t start, uint64_t count, int width, uint8_t 
 
 /* ---- device-resident (kernel-only) entry points ------------------------ */
 /* All pointers are device pointers on `gpu`; work is enqueued on `stream`
- * (NULL = legacy default stream) and NOT synchronised.                       */
+ * (NULL = legacy default stream) and NOT synchronised.  Fixed-width kernels
+ * are launched with programmatic stream serialization (PDL): one may be
+ * scheduled while the previous kernel on the stream drains, but it waits for
+ * that kernel's completion (griddepcontrol.wait) before touching global
+ * memory, so stream order holds as for a normal launch ($HB_PDL=0 disables). */
 int hb_hash_fixed_dev(int alg, int gpu, const void *d_msgs, uint64_t n, uint64_t msg_len, void *d_out,
                       void *stream, uint32_t flags);
 /* d_data must be readable up to round_up(address of the last byte + 1, 16)
