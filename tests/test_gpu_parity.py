@@ -195,6 +195,42 @@ def test_engine_pipelined_chunks(monkeypatch):
             assert np.array_equal(hash_decimal(alg, 10**6, 300000, 9), dref)
 
 
+@pytest.mark.parametrize("L", [64, 1024])
+def test_pdl_stream_order(L):
+    """Programmatic dependent launch keeps stream order: (1) a torch kernel
+    writes the messages right before each hash launch; (2) a chain of hash
+    launches where each consumes the previous one's digests as its messages
+    (the producer triggers its dependents before storing them, so only
+    griddepcontrol.wait's completion semantics make this correct).  Small
+    (k_fixed_small) and TMA (k_fixed_tma_ws) shapes, no synchronisation
+    between the launches."""
+    import torch
+
+    from paper_2407_09333_b200 import device
+
+    n = 20000
+    buf = torch.empty((n, L), dtype=torch.uint8, device="cuda:0")
+    outs = []
+    for k in range(6):
+        buf.fill_(k + 1)
+        outs.append(device.hash_fixed("md5", buf))
+    torch.cuda.synchronize()
+    for k, o in enumerate(outs):
+        ref = oracle.batch_fixed("md5", np.full((1, L), k + 1, np.uint8))
+        assert np.array_equal(o.cpu().numpy(), np.repeat(ref, n, axis=0)), k
+    per = L // 32  # SM3 digests per L-byte row of the next round
+    rows = per ** 3 if L > 64 else 1 << 14
+    data = oracle.fill_random(rows * L, 41).reshape(rows, L)
+    cur = torch.from_numpy(data).cuda()
+    ref = data
+    while rows >= per:
+        rows //= per
+        cur = device.hash_fixed("sm3", cur).reshape(rows, L)
+        ref = oracle.batch_fixed("sm3", ref, threads=8).reshape(rows, L)
+    torch.cuda.synchronize()
+    assert np.array_equal(cur.cpu().numpy(), ref)
+
+
 def test_bind_host_to_gpu():
     """NVML's GPU-local core set becomes this process's affinity (bench.py
     does this per rank before allocating pinned buffers)."""
