@@ -14,6 +14,9 @@
 // asynchronous on that GPU's slot streams.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <ctype.h>
+#include <pthread.h>
+#include <sched.h>
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -405,6 +408,50 @@ static int run_shard_locked(GpuCtx& c, const ShardJob& j, ShardStats& st) {
     return HB_OK;
 }
 
+// Pin the calling shard thread to the CPUs local to GPU `dev` (the sysfs
+// local_cpulist of its PCI function), intersected with the allowed set.  A
+// multi-GPU call runs one such thread per GPU; the GPU's pinned staging ring
+// (first allocated by this thread) and the host-copy helpers it spawns then
+// stay on the GPU's NUMA node.  Best effort; $HB_BIND_NUMA=0 disables.
+static void bind_thread_near_gpu(int dev) {
+    const char* off = getenv("HB_BIND_NUMA");
+    if (off && off[0] == '0') return;
+    char bus[32];
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    for (char* q = bus; *q; ++q) *q = (char)tolower((unsigned char)*q);
+    char path[128];
+    snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/local_cpulist", bus);
+    FILE* f = fopen(path, "r");
+    if (!f) return;
+    char buf[4096];
+    const size_t m = fread(buf, 1, sizeof buf - 1, f);
+    fclose(f);
+    buf[m] = '\0';
+    cpu_set_t want;
+    CPU_ZERO(&want);
+    for (char* q = buf; *q;) {  // "0-15,32-47\n"
+        char* e = nullptr;
+        const long a = strtol(q, &e, 10);
+        if (e == q) break;
+        long b = a;
+        q = e;
+        if (*q == '-') {
+            b = strtol(q + 1, &e, 10);
+            q = e;
+        }
+        for (long c = a; c <= b && c < CPU_SETSIZE; ++c)
+            if (c >= 0) CPU_SET((int)c, &want);
+        while (*q == ',' || *q == '\n' || *q == ' ') ++q;
+    }
+    cpu_set_t have;
+    if (pthread_getaffinity_np(pthread_self(), sizeof have, &have) != 0) return;
+    CPU_AND(&want, &want, &have);
+    if (CPU_COUNT(&want) > 0) pthread_setaffinity_np(pthread_self(), sizeof want, &want);
+}
+
 static void run_shard(const ShardJob& j, ShardStats& st) {
     GpuCtx* c = nullptr;
     int rc = get_ctx(j.dev, &c);
@@ -499,7 +546,11 @@ static int run_sharded(ShardJob proto, uint64_t n, const std::vector<int>& devs,
         run_shard(jobs[0], stats[0]);
     } else {
         std::vector<std::thread> ts;
-        for (size_t q = 0; q < jobs.size(); ++q) ts.emplace_back(run_shard, std::cref(jobs[q]), std::ref(stats[q]));
+        for (size_t q = 0; q < jobs.size(); ++q)
+            ts.emplace_back([&, q] {
+                bind_thread_near_gpu(jobs[q].dev);  // a worker thread: the caller's own affinity is untouched
+                run_shard(jobs[q], stats[q]);
+            });
         for (auto& th : ts) th.join();
     }
     hb_timing agg;

@@ -231,6 +231,22 @@ def test_pdl_stream_order(L):
     assert np.array_equal(cur.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("bind", ["1", "0"])
+def test_multi_shard_numa_binding(bind, monkeypatch):
+    """A multi-GPU call (here two shards on GPU 0) runs one worker thread per
+    shard, each pinned to its GPU's local CPUs (sysfs local_cpulist); the
+    digests are unchanged and the caller's own affinity is untouched."""
+    import os
+
+    monkeypatch.setenv("HB_BIND_NUMA", bind)
+    n, L = 30001, 200
+    data = oracle.fill_random(n * L, 43).reshape(n, L)
+    before = os.sched_getaffinity(0)
+    for alg in ALGS:
+        assert np.array_equal(batch_digest(alg, data, gpus=[0, 0]), oracle.batch_fixed(alg, data, threads=8))
+    assert os.sched_getaffinity(0) == before
+
+
 def test_bind_host_to_gpu():
     """NVML's GPU-local core set becomes this process's affinity (bench.py
     does this per rank before allocating pinned buffers)."""
