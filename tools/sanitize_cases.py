@@ -75,6 +75,19 @@ def main():
             out = device.hash_decimal(alg, 5, 4000, w).cpu().numpy()
             assert np.array_equal(out, oracle.batch_fixed(alg, oracle.gen_decimal(5, 4000, w), 8))
             cases += 1
+    # programmatic dependent launch: a chain of launches on one stream, each
+    # consuming the previous one's digests, no host synchronisation between
+    for L in (64, 1024):
+        per = L // 32
+        rows = per ** 3 if L > 64 else 1 << 10
+        data = oracle.fill_random(rows * L, 47).reshape(rows, L)
+        cur, ref = torch.from_numpy(data).cuda(), data
+        while rows >= per:
+            rows //= per
+            cur = device.hash_fixed("sm3", cur).reshape(rows, L)
+            ref = oracle.batch_fixed("sm3", ref, 8).reshape(rows, L)
+            cases += 1
+        assert np.array_equal(cur.cpu().numpy(), ref)
     torch.cuda.synchronize()
     print(f"sanitize cases ok: {cases} invocations bit-exact")
 
