@@ -269,12 +269,27 @@ def reduce_max(x: float, world: int, local: int) -> float:
 
 
 def load_peaks():
+    """Roofline denominators: the driver-measured HBM copy bandwidth from
+    MEASURED_PEAKS.json ("of measured"), else B200_PROFILING.md's fallback
+    ("of fallback").  Only a positive numeric `hbm_gbs` is taken from the file;
+    anything else in it is ignored rather than trusted."""
+    peaks = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(p):
+    if not os.path.exists(p):
+        return peaks, "fallback (B200_PROFILING.md)"
+    try:
         with open(p) as f:
             d = json.load(f)
-        return d, "measured (MEASURED_PEAKS.json)"
-    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+        hbm = d.get("hbm_gbs") if isinstance(d, dict) else None
+        if isinstance(hbm, (int, float)) and hbm > 0:
+            peaks["hbm_gbs"] = float(hbm)
+            mhz = d.get("sm_max_mhz")
+            if isinstance(mhz, (int, float)) and mhz > 0:
+                peaks["sm_max_mhz"] = float(mhz)
+            return peaks, "measured (MEASURED_PEAKS.json)"
+    except (OSError, ValueError):
+        pass
+    return peaks, "fallback (B200_PROFILING.md; MEASURED_PEAKS.json unreadable or without hbm_gbs)"
 
 
 def load_ncu_traffic(workload: str):
