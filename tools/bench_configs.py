@@ -25,8 +25,9 @@ import oracle  # noqa: E402
 from paper_2407_09333_b200 import _native, device  # noqa: E402
 
 DLEN = {"sha1": 20, "md5": 16, "sm3": 32}
-PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
-    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+import bench  # noqa: E402  (the same defensive MEASURED_PEAKS.json reader)
+
+PEAK = bench.load_peaks()[0]["hbm_gbs"]
 # minimal ALU-pipe ops per 64-byte block and the 64 lanes/clk/SM ALU rate
 ALU_OPS = {"md5": 128, "sha1": 448, "sm3": 1084}
 # Dependent-chain latency of one compression with nothing to overlap it (one
