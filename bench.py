@@ -646,16 +646,28 @@ def run_ours(args):
     # per-step event pairs would add a launch latency, ~9 us on this box, to
     # every small step); a few per-step pairs after it give the spread.
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    l0 = _native.launch_count()
-    sampler.active = True
-    t_wall0 = time.perf_counter()
-    t_start.record(stream)
-    w.run_steps(args.steps)
-    t_end.record(stream)
-    torch.cuda.synchronize()
-    t_wall = time.perf_counter() - t_wall0
-    sampler.active = False
-    launches = _native.launch_count() - l0
+    remeasured = False
+    for attempt in range(2):
+        sampler.lines.clear()
+        l0 = _native.launch_count()
+        sampler.active = True
+        t_wall0 = time.perf_counter()
+        t_start.record(stream)
+        w.run_steps(args.steps)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+        sampler.active = False
+        launches = _native.launch_count() - l0
+        # a region that saw hardware / thermal throttling is measured once more
+        # (sw_power_cap is the normal state of a long integer kernel: kept, noted)
+        bad = set(sampler.summary()["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+        if attempt == 1 or not reduce_max(1.0 if bad else 0.0, world, local):
+            break
+        log(f"[rank {rank}] throttling during the timed region ({sorted(bad)}): re-measuring once")
+        remeasured = True
+        barrier(world)
+        torch.cuda.synchronize()
     if gather is not None:  # the gather wrote into rank 0's buffer; refill the local digests for the checks below
         from paper_2407_09333_b200 import device as _device
 
@@ -764,6 +776,8 @@ def run_ours(args):
     peaks, peak_src = load_peaks()
     achieved = w.alg_bytes / (ms_local * 1e-3) / 1e9
     clk = sampler.summary()
+    if remeasured:
+        clk["remeasured"] = True
     f_max = peaks.get("sm_max_mhz", 1965.0)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     alu_peak = sms * 64 * f_max * 1e6  # ALU-pipe lane-ops/s at max clock
