@@ -100,24 +100,32 @@ class FixedHashGraph:
 
     def __init__(self, alg: str, msgs, out=None, flags: int = 0, repeats: int = 1):
         """``repeats`` > 1 captures that many back-to-back passes over the batch
-        in the one graph (a launch-bound loop of small batches)."""
+        in the one graph (a launch-bound loop of small batches).  ``msgs`` may
+        also be a list of same-shape batches: each repeat then makes one pass
+        over every batch in order (rotating inputs, e.g. to keep them out of L2)."""
         import torch
 
+        batches = list(msgs) if isinstance(msgs, (list, tuple)) else [msgs]
+        first = batches[0]
+        if any(b.shape != first.shape for b in batches):
+            raise ValueError("all batches of a FixedHashGraph must have the same shape")
         if out is None:
-            out = torch.empty((msgs.shape[0], DIGEST_LEN[alg]), dtype=torch.uint8, device=msgs.device)
-        self.alg, self.msgs, self.out, self.flags = alg, msgs, out, flags
-        side = torch.cuda.Stream(device=msgs.device)
-        side.wait_stream(torch.cuda.current_stream(msgs.device))
+            out = torch.empty((first.shape[0], DIGEST_LEN[alg]), dtype=torch.uint8, device=first.device)
+        self.alg, self.msgs, self.out, self.flags = alg, first, out, flags
+        side = torch.cuda.Stream(device=first.device)
+        side.wait_stream(torch.cuda.current_stream(first.device))
         with torch.cuda.stream(side):  # warm-up outside capture: one-time attribute setup, tensor-map encoder
-            hash_fixed(alg, msgs, out=out, flags=flags)
-        torch.cuda.current_stream(msgs.device).wait_stream(side)
+            hash_fixed(alg, first, out=out, flags=flags)
+        torch.cuda.current_stream(first.device).wait_stream(side)
         self.graph = torch.cuda.CUDAGraph()
         before = _native.launch_count()
         with torch.cuda.graph(self.graph):
             for _ in range(max(1, int(repeats))):
-                hash_fixed(alg, msgs, out=out, flags=flags)
+                for b in batches:
+                    hash_fixed(alg, b, out=out, flags=flags)
         self.kernels_per_replay = _native.launch_count() - before
         self.repeats = max(1, int(repeats))
+        self.passes = self.repeats * len(batches)
 
     def replay(self):
         self.graph.replay()

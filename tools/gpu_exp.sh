@@ -1,6 +1,4 @@
 set -u
 mkdir -p gpurun_out
-T=${T:-exp63}
-timeout 900 python -m pytest tests/test_multiproc.py -x -q -m gpu -k "multirank" > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_$T.log
-timeout 600 python bench.py --workload sha1_64 --steps 20 --warmup 3 2>/dev/null | tail -1 | cut -c1-400
-timeout 600 python bench.py --workload md5_1k --steps 10 --warmup 3 --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['clocks'], d['roofline']['peak_source'])"
+T=${T:-exp66}
+for r in 1 2; do timeout 600 python bench.py --workload sha1_64 --no-cpu > gpurun_out/b64_${r}_$T.json 2>gpurun_out/b64_${r}_$T.err; python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['gpu_launches'], d['parity'])" gpurun_out/b64_${r}_$T.json; grep "kernel-only" gpurun_out/b64_${r}_$T.err; done
