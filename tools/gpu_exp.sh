@@ -1,6 +1,7 @@
 set -u
 mkdir -p gpurun_out
-T=${T:-exp67}
-timeout 600 python bench.py --workload sha1_64 > gpurun_out/bench_sha1_64_$T.json 2>gpurun_out/bench_sha1_64_$T.err; echo rc=$?
-python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['e2e']['value'], d['cpu_baseline']['value'], d['parity'], d['config']['l2'])" gpurun_out/bench_sha1_64_$T.json
-timeout 900 python -m pytest tests -q -m gpu --timeout 900 > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_$T.log
+T=${T:-exp68}
+for r in 1 2; do for e in 0 1; do
+HB_PDL_EARLY=$e timeout 600 python bench.py --workload sha1_64 --no-cpu --no-e2e > gpurun_out/b64_${e}_$T.json 2>/dev/null; echo "early=$e $(python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'])" gpurun_out/b64_${e}_$T.json)"
+done; done
+HB_PDL_EARLY=1 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "pdl or width or geometry" 2>&1 | tail -1
