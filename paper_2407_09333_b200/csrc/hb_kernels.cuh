@@ -1035,7 +1035,7 @@ __global__ void __launch_bounds__(128) k_decimal(uint64_t start, uint64_t count,
 // Same bytes as gen_messages (batch.py:96-98): the low WIDTH digits of v are
 // the low WIDTH-1 digits of u followed by v mod 10 = j.  Needs u < 2^30
 // (umulhi reciprocal exact) -- v below ~1.07e10.
-template <int ALG, int WIDTH, int V = -1>
+template <int ALG, int WIDTH, int V = -1, bool PAIR = false>
 __global__ void __launch_bounds__(128) k_decimal_run(uint64_t start, uint64_t count, uint8_t* __restrict__ out) {
     using H = HashAlg<ALG, V>;
     static_assert(WIDTH >= 2 && WIDTH <= 10, "width");
@@ -1072,7 +1072,32 @@ __global__ void __launch_bounds__(128) k_decimal_run(uint64_t start, uint64_t co
         md_finish<ALG, V>(st, raw, (uint32_t)WIDTH, (uint64_t)WIDTH);
         store_digest<ALG>(dst, st);
     };
-    if (u * 10u >= start && u * 10u + 10u <= end) {  // all but the first / last thread: no range checks
+    if (PAIR && u * 10u >= start && u * 10u + 10u <= end) {
+        // messages j and j+5 compressed together (two independent chains per
+        // thread for the scheduler to interleave; MD5 default, $HB_DEC_PAIR)
+        uint8_t* dst = out + (u * 10u - start) * H::kDigestBytes;
+        constexpr uint32_t kPad = 0x80u << ((WIDTH & 3) * 8);
+        constexpr uint64_t kBits = (uint64_t)WIDTH * 8u;
+        constexpr uint32_t kL14 = H::kBigEndian ? 0u : (uint32_t)kBits;
+        constexpr uint32_t kL15 = H::kBigEndian ? bswap_c((uint32_t)kBits) : 0u;
+#pragma unroll 1
+        for (uint32_t j = 0; j < 5u; ++j) {
+            uint32_t raw[2][16], st[2][H::kStateWords];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) raw[q][k] = pre[k];
+                raw[q][kLastW] = pre[kLastW] + ((j + 5u * q) << kLastSh);
+                raw[q][WIDTH >> 2] |= kPad;
+                raw[q][14] = kL14;
+                raw[q][15] = kL15;
+                H::init(st[q]);
+            }
+            H::template compress_n<2>(st, raw);
+            store_digest<ALG>(dst + j * H::kDigestBytes, st[0]);
+            store_digest<ALG>(dst + (j + 5u) * H::kDigestBytes, st[1]);
+        }
+    } else if (u * 10u >= start && u * 10u + 10u <= end) {  // all but the first / last thread: no range checks
         uint8_t* dst = out + (u * 10u - start) * H::kDigestBytes;
 #pragma unroll 1
         for (uint32_t j = 0; j < 10u; ++j) one(j, dst + j * H::kDigestBytes);
@@ -1435,7 +1460,14 @@ static void dec_launch(uint64_t start, uint64_t count, uint8_t* d_out, cudaStrea
             // SHA-1's variant 3, best for k_decimal, loses 35 % here)
             switch (env_u64("HB_CONST_VARIANT", 1)) {
             case 3: k_decimal_run<ALG, W, kVarBal3><<<g, 128, 0, s>>>(start, count, d_out); break;
-            default: k_decimal_run<ALG, W, kVarBal><<<g, 128, 0, s>>>(start, count, d_out); break;
+            default:
+                // MD5: two messages per compression call (+3 %); SHA-1 / SM3
+                // lose 28 / 6 % that way (register pressure), profiles/ab_decimal_r1d.txt
+                if (env_u64("HB_DEC_PAIR", ALG == kMd5 ? 1 : 0))
+                    k_decimal_run<ALG, W, kVarBal, true><<<g, 128, 0, s>>>(start, count, d_out);
+                else
+                    k_decimal_run<ALG, W, kVarBal><<<g, 128, 0, s>>>(start, count, d_out);
+                break;
             }
             return;
         }

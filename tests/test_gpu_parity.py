@@ -318,13 +318,16 @@ def test_decimal_workload(golden, variant, dec_run, monkeypatch):
             assert np.array_equal(hash_decimal(alg, start, cnt, w), oracle.batch_fixed(alg, msgs)), (alg, w)
 
 
-@pytest.mark.parametrize("variant", ["1", "3"])
+@pytest.mark.parametrize("variant", ["1", "3", "pair", "nopair"])
 def test_decimal_runs_ragged(variant, monkeypatch):
     """Runs-of-ten kernel: every start residue mod 10 x short counts (first and
     last thread partial, one thread both), the end of the width-10 range and
     the 2^32 boundary (u = v / 10 stays below 2^30 for every width <= 10)."""
-    monkeypatch.setenv("HB_CONST_VARIANT", variant)
-    for w in (2, 3, 9, 10):
+    if variant in ("pair", "nopair"):  # two messages per compression call (MD5 default) or one
+        monkeypatch.setenv("HB_DEC_PAIR", "1" if variant == "pair" else "0")
+    else:
+        monkeypatch.setenv("HB_CONST_VARIANT", variant)
+    for w in (2, 3, 4, 8, 9, 10):
         for r in range(10):
             for cnt in (c for c in (1, 2, 9, 10, 11, 19, 21, 1283) if c <= 10**w):
                 start = max(0, min(10**w - cnt, 10**(w - 1) + 37 * 10 + r))
