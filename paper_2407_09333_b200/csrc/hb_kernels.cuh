@@ -394,11 +394,12 @@ __host__ __device__ constexpr uint32_t bswap_c(uint32_t x) {
     return (x >> 24) | ((x >> 8) & 0xFF00u) | ((x << 8) & 0xFF0000u) | (x << 24);
 }
 
-template <int ALG, int L, int V = -1>
+template <int ALG, int L, int V = -1, int NB = 1>
 __global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__ msgs, uint64_t n,
                                                      uint8_t* __restrict__ out) {
     using H = HashAlg<ALG, V>;
     static_assert(L % 16 == 0 && L >= 16 && L <= 128, "width");
+    static_assert(NB == 1 || NB == 2, "messages per thread");
     constexpr int kNb = (L + 8) / 64 + 1;  // blocks including padding
     constexpr uint64_t kBits = (uint64_t)L * 8u;
     constexpr uint32_t kL14 = H::kBigEndian ? bswap_c((uint32_t)(kBits >> 32)) : (uint32_t)kBits;
@@ -408,30 +409,46 @@ __global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__
     // the next grid comes once this thread's hash is done (both no-ops for a
     // normal launch).  A stream of short batches then hides the launch gap.
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint4* p = reinterpret_cast<const uint4*>(msgs + i * L);
-    uint32_t w[L / 4];
+    // NB = 2: rows 2t and 2t+1 (contiguous bytes) hashed as two independent
+    // chains in one compress call; a missing second row re-hashes the first
+    // and is not stored.
+    const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * NB;
+    if (i0 >= n) return;
+    uint32_t w[NB][L / 4];
 #pragma unroll
-    for (int c = 0; c < L / 16; ++c) {
-        const uint4 v = __ldg(p + c);
-        w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
+    for (int q = 0; q < NB; ++q) {
+        const uint64_t row = i0 + q < n ? i0 + q : i0;
+        const uint4* p = reinterpret_cast<const uint4*>(msgs + row * L);
+#pragma unroll
+        for (int c = 0; c < L / 16; ++c) {
+            const uint4 v = __ldg(p + c);
+            w[q][4 * c] = v.x; w[q][4 * c + 1] = v.y; w[q][4 * c + 2] = v.z; w[q][4 * c + 3] = v.w;
+        }
     }
-    uint32_t st[H::kStateWords];
-    H::init(st);
+    uint32_t st[NB][H::kStateWords];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) H::init(st[q]);
 #pragma unroll
     for (int b = 0; b < kNb; ++b) {
-        uint32_t raw[16];
+        uint32_t raw[NB][16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int pos = 64 * b + 4 * j;  // _pad: data, 0x80, zeros, 64-bit bit length
-            raw[j] = pos < L ? w[pos / 4] : pos == L ? 0x80u : 0u;
+        for (int q = 0; q < NB; ++q) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int pos = 64 * b + 4 * j;  // _pad: data, 0x80, zeros, 64-bit bit length
+                raw[q][j] = pos < L ? w[q][pos / 4] : pos == L ? 0x80u : 0u;
+            }
+            if (b == kNb - 1) { raw[q][14] = kL14; raw[q][15] = kL15; }
         }
-        if (b == kNb - 1) { raw[14] = kL14; raw[15] = kL15; }
-        compress1<ALG, V>(st, raw);
+        if (NB == 1)
+            compress1<ALG, V>(st[0], raw[0]);
+        else
+            H::template compress_n<NB>(st, raw);
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    store_digest<ALG>(out + i * H::kDigestBytes, st);
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+        if (i0 + q < n) store_digest<ALG>(out + (i0 + q) * H::kDigestBytes, st[q]);
 }
 
 // =========================================================================
@@ -1353,20 +1370,30 @@ static cudaError_t launch_fixed_alg(const uint8_t* d_msgs, uint64_t n, uint64_t 
     uint64_t sb = env_u64("HB_SMALL_CTA", 128);
     const unsigned sblk = sb >= 128 ? 128u : sb >= 64 ? 64u : 32u;  // __launch_bounds__(128)
     const unsigned sgrid = (unsigned)((n + sblk - 1) / sblk);
+    // two rows per thread for MD5 one-block messages (L <= 32) in batches
+    // large enough that halving the thread count still fills the GPU: +3-4 %;
+    // 48-byte rows (near the HBM bound) lose 2 %, two-block rows 1-9 % (profiles/ab_small_r1d.txt)
+    const bool pair = ALG == kMd5 && n >= (1ull << 20) && L <= 32 && env_u64("HB_SMALL_PAIR", 1);
+    const unsigned sgrid2 = (unsigned)(((n + 1) / 2 + sblk - 1) / sblk);
     if (small_ok && L == 16) {
-        small_v1 ? launch_pdl(k_fixed_small<ALG, 16, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out)
+        small_v1 ? (pair ? launch_pdl(k_fixed_small<ALG, 16, kVarBal, 2>, sgrid2, sblk, stream, d_msgs, n, d_out)
+                         : launch_pdl(k_fixed_small<ALG, 16, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out))
                  : launch_pdl(k_fixed_small<ALG, 16, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
     } else if (small_ok && L == 32) {
-        small_v1 ? launch_pdl(k_fixed_small<ALG, 32, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out)
+        small_v1 ? (pair ? launch_pdl(k_fixed_small<ALG, 32, kVarBal, 2>, sgrid2, sblk, stream, d_msgs, n, d_out)
+                         : launch_pdl(k_fixed_small<ALG, 32, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out))
                  : launch_pdl(k_fixed_small<ALG, 32, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
     } else if (small_ok && L == 48) {
-        small_v1 ? launch_pdl(k_fixed_small<ALG, 48, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out)
+        small_v1 ? (pair ? launch_pdl(k_fixed_small<ALG, 48, kVarBal, 2>, sgrid2, sblk, stream, d_msgs, n, d_out)
+                         : launch_pdl(k_fixed_small<ALG, 48, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out))
                  : launch_pdl(k_fixed_small<ALG, 48, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
     } else if (small_ok && L == 64) {
-        small_v1 ? launch_pdl(k_fixed_small<ALG, 64, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out)
+        small_v1 ? (pair ? launch_pdl(k_fixed_small<ALG, 64, kVarBal, 2>, sgrid2, sblk, stream, d_msgs, n, d_out)
+                         : launch_pdl(k_fixed_small<ALG, 64, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out))
                  : launch_pdl(k_fixed_small<ALG, 64, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
     } else if (small_ok && L == 128) {
-        small_v1 ? launch_pdl(k_fixed_small<ALG, 128, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out)
+        small_v1 ? (pair ? launch_pdl(k_fixed_small<ALG, 128, kVarBal, 2>, sgrid2, sblk, stream, d_msgs, n, d_out)
+                         : launch_pdl(k_fixed_small<ALG, 128, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out))
                  : launch_pdl(k_fixed_small<ALG, 128, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
     } else if (aligned) {
         k_fixed_direct<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, (uint32_t)L, d_out);

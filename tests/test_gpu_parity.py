@@ -195,6 +195,19 @@ def test_engine_pipelined_chunks(monkeypatch):
             assert np.array_equal(hash_decimal(alg, 10**6, 300000, 9), dref)
 
 
+@pytest.mark.parametrize("pair", ["0", "1"])
+def test_small_rows_pairs(pair, monkeypatch):
+    """Compile-time-width kernel with two rows per thread (HB_SMALL_PAIR, MD5,
+    >= 2^20 rows): odd row counts (the last thread's second row missing) and
+    every short width, all rows against the oracle."""
+    monkeypatch.setenv("HB_SMALL_PAIR", pair)
+    for L in (16, 32, 48, 64, 128):
+        n = (1 << 20) + 1
+        data = oracle.fill_random(n * L, 53 + L).reshape(n, L)
+        for alg in ALGS:
+            assert np.array_equal(batch_digest(alg, data, gpus=[0]), oracle.batch_fixed(alg, data, threads=16)), (alg, L)
+
+
 @pytest.mark.parametrize("L", [64, 1024])
 def test_pdl_stream_order(L):
     """Programmatic dependent launch keeps stream order: (1) a torch kernel

@@ -1,5 +1,8 @@
 set -u
 mkdir -p gpurun_out
-T=${T:-exp71}
-timeout 900 python bench.py --workload paper_md5 > gpurun_out/bench_paper_md5_$T.json 2>gpurun_out/bench_paper_md5_$T.err; echo rc=$?
-python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(d['value'], d['mhash_per_s'], d['roofline']['frac'], d['e2e']['value'], d['e2e']['mhash_per_s'], d['cpu_baseline']['mhash_per_s'], d['parity'], d['clocks'])" gpurun_out/bench_paper_md5_$T.json
+T=${T:-exp73}
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "pairs or width or geometry or pdl" > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_$T.log
+A='{"default": {}, "nopair": {"HB_SMALL_PAIR": "0"}}'
+for c in "md5 16777216 16 20" "md5 16777216 48 20" "md5 16777216 64 20"; do
+  AB_ARMS="$A" timeout 600 python tools/ab_env.py $c 2>&1 | tail -2
+done
