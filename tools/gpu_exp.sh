@@ -1,8 +1,8 @@
 set -u
 mkdir -p gpurun_out
-T=${T:-exp73}
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "pairs or width or geometry or pdl" > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_$T.log
-A='{"default": {}, "nopair": {"HB_SMALL_PAIR": "0"}}'
-for c in "md5 16777216 16 20" "md5 16777216 48 20" "md5 16777216 64 20"; do
-  AB_ARMS="$A" timeout 600 python tools/ab_env.py $c 2>&1 | tail -2
-done
+T=${T:-final3}
+timeout 1500 python -m pytest tests -q -m gpu --timeout 900 > gpurun_out/pytest_$T.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_$T.log
+timeout 300 python __graft_entry__.py 2>&1 | tail -1
+timeout 2400 python tools/bench_configs.py gpurun_out/configs_$T.jsonl > /dev/null 2> gpurun_out/configs_$T.err; echo "configs rc=$?"; wc -l < gpurun_out/configs_$T.jsonl; grep -c '"bit_exact_sample": true' gpurun_out/configs_$T.jsonl
+timeout 900 python bench.py > gpurun_out/bench_$T.json 2> gpurun_out/bench_$T.err; echo "bench rc=$?"
+python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(d['value'], d['roofline']['frac'], d['e2e']['value'], d['clocks'], d['parity'])" gpurun_out/bench_$T.json
