@@ -32,9 +32,12 @@ def main():
     if os.path.isdir(src) and not os.path.isdir(dst):
         run("git", "mv", src, dst)
     os.makedirs(dst, exist_ok=True)
-    for stale in glob.glob(os.path.join(dst, "gpu_r1v*.txt")) + glob.glob(os.path.join(dst, "pytest_gpu_*.log")) + \
-            glob.glob(os.path.join(dst, "smoke_*.log")) + glob.glob(os.path.join(dst, "*_final.*")):
-        run("git", "rm", "-q", "-f", stale)
+    stale = set(glob.glob(os.path.join(dst, "gpu_r1v*.txt")) + glob.glob(os.path.join(dst, "pytest_gpu_*.log")) +
+                glob.glob(os.path.join(dst, "smoke_*.log")) + glob.glob(os.path.join(dst, "*_final.*")))
+    for f in sorted(stale):
+        run("git", "rm", "-q", "-f", "--ignore-unmatch", f)
+        if os.path.exists(f):
+            os.remove(f)
     shutil.copy(os.path.join(OUT, f"bench_{tag}.json"), os.path.join(dst, "bench.json"))
     shutil.copy(os.path.join(OUT, f"bench_ref_{tag}.json"), os.path.join(dst, "bench_ref.json"))
     for w in WORKLOADS:
