@@ -858,6 +858,9 @@ def run_reference(args):
     """The reference algorithm's CPU implementation (oracle port of hetoc.crypto;
     the reference itself is pure Python/numpy and is not installed on the box)
     on all host threads, each step a bounded sample of the same workload."""
+    # each step a bounded sample: --ref-step-seconds, shrunk so the whole
+    # --steps K --warmup W run stays within --ref-budget-seconds
+    step_s = min(args.ref_step_seconds, max(0.05, args.ref_budget_seconds / max(1, args.steps + args.warmup)))
     import oracle
 
     rank = int(os.environ.get("RANK", "0"))
@@ -873,7 +876,7 @@ def run_reference(args):
         from paper_2407_09333_b200.crypto import gen_messages
 
         width = spec[2]
-        rows = cpu_sample_rows(alg, width, n, threads, args.ref_step_seconds)
+        rows = cpu_sample_rows(alg, width, n, threads, step_s)
         data = gen_messages(0, rows, width).as_array()
         run = lambda: oracle.batch_fixed(alg, data, threads=threads)  # noqa: E731
         nbytes = rows * width
@@ -890,7 +893,7 @@ def run_reference(args):
         t0 = time.perf_counter()
         oracle.batch_varlen(alg, probe, off[: probe_k + 1], threads=1)
         per_msg = max((time.perf_counter() - t0) / probe_k, 1e-9)
-        k = max(threads * 16, min(n, int(args.ref_step_seconds * threads / per_msg)))
+        k = max(threads * 16, min(n, int(step_s * threads / per_msg)))
         data = oracle.fill_random(int(off[k]), seed)
         run = lambda: oracle.batch_varlen(alg, data, off[: k + 1], threads=threads)  # noqa: E731
         nbytes, rows = int(off[k]), k
@@ -899,7 +902,7 @@ def run_reference(args):
                   "alg": alg, "msgs_per_gpu": n, "msg_len": f"uniform 1-{maxlen}"}
     else:
         L = spec[2]
-        rows = cpu_sample_rows(alg, L, n, threads, args.ref_step_seconds)
+        rows = cpu_sample_rows(alg, L, n, threads, step_s)
         data = oracle.fill_random(rows * L, seed).reshape(rows, L)
         run = lambda: oracle.batch_fixed(alg, data, threads=threads)  # noqa: E731
         nbytes = rows * L
@@ -943,6 +946,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=3.0)
     ap.add_argument("--ref-step-seconds", type=float, default=1.0)
+    ap.add_argument("--ref-budget-seconds", type=float, default=150.0,
+                    help="--impl reference: upper bound on the whole run's CPU time")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--gather", choices=["none", "p2p"], default="none",
