@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 1
+#define HB_ABI_VERSION 2
 
 typedef enum {
     HB_OK = 0,
@@ -59,6 +59,9 @@ typedef enum { HB_SHA1 = 0, HB_MD5 = 1, HB_SM3 = 2 } hb_alg;
 #define HB_FLAG_NO_TMA   0x1u  /* fixed width: direct-load kernel instead of TMA staging */
 #define HB_FLAG_NO_SORT  0x2u  /* varlen: skip the length-bucket sort                    */
 #define HB_FLAG_SYNC_H2D 0x4u  /* engine: no copy/compute overlap (diagnostics)          */
+/* A/B kernel arms: honoured only by a library built with -DHB_AB
+ * (hb_built_with_ab() == 1); the default build returns HB_ERR_CUDA with
+ * hb_last_error() saying so for VARLEN_WORDS / VARLEN_COOP.                 */
 #define HB_FLAG_VARLEN_WORDS 0x8u /* varlen: per-thread 32-bit-load kernel (A/B baseline)       */
 #define HB_FLAG_VARLEN_COOP_OFF 0x10u /* varlen: per-thread 128-bit-load kernel (the default;
                                          kept so callers can pin it explicitly)                 */
@@ -66,14 +69,26 @@ typedef enum { HB_SHA1 = 0, HB_MD5 = 1, HB_SM3 = 2 } hb_alg;
 
 typedef struct {
     double total_ms;       /* host wall time of the call                              */
-    double kernel_ms;      /* max over GPUs of summed hash-kernel device time         */
-    double h2d_ms;         /* max over GPUs of summed H2D device time                 */
-    double d2h_ms;         /* max over GPUs of summed D2H device time                 */
+    double kernel_ms;      /* max over GPUs of the union of hash-kernel busy intervals */
+    double h2d_ms;         /* max over GPUs of the union of H2D busy intervals         */
+    double d2h_ms;         /* max over GPUs of the union of D2H busy intervals         */
     uint64_t h2d_bytes;    /* total bytes copied host -> device                       */
     uint64_t d2h_bytes;    /* total bytes copied device -> host                       */
     uint64_t chunks;       /* sub-batches (chunks) executed over all GPUs             */
     uint64_t launches;     /* kernels launched by this call                           */
+    uint64_t shards;       /* GPUs that received a non-empty message range           */
+    uint64_t device_mask;  /* bit d set: GPU d ran a shard                            */
 } hb_timing;
+
+/* One stage of one chunk on one GPU (hb_last_timeline): stage 0 = H2D,
+ * 1 = hash kernel(s), 2 = D2H; times in ms from that GPU's first event of
+ * the call (device clock, CUDA events).                                     */
+typedef struct {
+    int32_t dev;
+    int32_t stage;
+    uint64_t chunk;
+    double t0_ms, t1_ms;
+} hb_span;
 
 typedef struct {
     int ordinal;
@@ -101,8 +116,15 @@ uint64_t hb_launch_count(void);           /* kernels launched by this process so
  * streams its slice through a ring of pinned/device chunk buffers (H2D, kernel,
  * D2H overlapped on separate streams).  Host buffers may be pageable or
  * pinned (pinned is copied directly).  gpus == NULL / n_gpus == 0 means "all
- * devices".  t may be NULL (then no per-stage CUDA events are recorded, which
- * saves ~30 us per call on small batches).  msg_len 0 hashes empty messages. */
+ * devices" for calls staging >= $HB_MULTI_GPU_MIN_BYTES (32 MiB); smaller
+ * calls run on ONE GPU chosen per calling thread (round-robin over threads).
+ * Single-GPU calls run on the calling thread; multi-GPU calls hand their
+ * shards to persistent per-GPU worker threads (NUMA-bound to their GPU).
+ * t may be NULL (then no per-stage CUDA events are recorded, which saves
+ * ~30 us per call on small batches).  msg_len 0 hashes empty messages.
+ * Each GPU stages through kSlots = 3 chunk buffers whose size is capped by
+ * that GPU's budget (free HBM at first use minus $HB_DEVICE_RESERVE, 2 GiB):
+ * hb_engine_budget reports it.                                              */
 int hb_hash_fixed(int alg, const uint8_t *msgs, uint64_t n, uint64_t msg_len, uint8_t *out,
                   const int *gpus, int n_gpus, uint32_t flags, hb_timing *t);
 
@@ -120,12 +142,15 @@ int hb_hash_varlen(int alg, const uint8_t *data, const uint64_t *offsets, uint64
                    const int *gpus, int n_gpus, uint32_t flags, hb_timing *t);
 
 /* Paper workload (gen_messages): digests of the zero-padded decimal strings
- * of start .. start+count-1, width bytes each, generated on the GPU.       */
+ * of start .. start+count-1, width bytes each, generated on the GPU.
+ * HB_ERR_INVAL unless start + count <= 10^width and does not wrap 2^64.    */
 int hb_hash_decimal(int alg, uint64_t start, uint64_t count, int width, uint8_t *out,
                     const int *gpus, int n_gpus, uint32_t flags, hb_timing *t);
 
 /* ---- device-resident (kernel-only) entry points ------------------------ */
 /* All pointers are device pointers on `gpu`; work is enqueued on `stream`
+ * (d_out rows are written with 16-byte stores for MD5 / SM3 and 4-byte
+ * stores for SHA-1: d_out must be 16- / 4-byte aligned).
  * (NULL = legacy default stream) and NOT synchronised.  Fixed-width kernels
  * are launched with programmatic stream serialization (PDL): one may be
  * scheduled while the previous kernel on the stream drains, but it waits for
@@ -168,6 +193,20 @@ int hb_shutdown(void);
 int hb_ipc_handle(const void *d_ptr, uint8_t *handle_out, uint64_t *offset_out);
 int hb_ipc_open(int gpu, const uint8_t *handle, void **d_ptr_out);     /* map it: base; add the offset */
 int hb_ipc_close(int gpu, void *d_ptr);
+
+/* ---- engine introspection and tuning ----------------------------------- */
+/* Re-read the $HB_* tuning environment (parsed once at first use otherwise).
+ * Not synchronised with concurrent hash calls.                              */
+int hb_tuning_reload(void);
+int hb_built_with_ab(void);               /* 1 if the A/B kernel arms are compiled in */
+/* Demangled name of the last hash kernel launched for the calling thread
+ * (directly by *_dev, or by the engine for its last call).                  */
+int hb_last_kernel_name(char *buf, int cap);
+/* Stage spans of the calling thread's last call that passed an hb_timing:
+ * copies min(count, cap) spans into out (may be NULL), returns count.       */
+int hb_last_timeline(hb_span *out, int cap);
+/* Per-GPU chunk-ring budget (bytes) and the largest input chunk it allows.  */
+int hb_engine_budget(int gpu, uint64_t *budget, uint64_t *chunk_cap);
 
 /* ---- task splitting ---------------------------------------------------- */
 /* partition_range(lb, ub, ratios[0..k)): writes k+1 bounds.                 */

@@ -12,7 +12,10 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhetoc_b200.so")
+# $HETOC_B200_LIB selects another in-tree build (A/B tools use the -DHB_AB
+# library, ``make -C paper_2407_09333_b200/csrc ab``); a bare name is looked
+# up next to this file.
+LIB_PATH = os.path.join(_HERE, os.environ.get("HETOC_B200_LIB", "libhetoc_b200.so"))
 
 HB_OK, HB_ERR_ALG, HB_ERR_INVAL, HB_ERR_CUDA, HB_ERR_NOMEM, HB_ERR_NODEV = range(6)
 HB_FLAG_NO_TMA, HB_FLAG_NO_SORT, HB_FLAG_SYNC_H2D, HB_FLAG_VARLEN_WORDS = 0x1, 0x2, 0x4, 0x8
@@ -26,6 +29,7 @@ EXPORTS = (
     "hb_varlen_scratch_bytes", "hb_hash_decimal_dev", "hb_fill_random_dev", "hb_gen_decimal_dev",
     "hb_alloc_pinned", "hb_free_pinned", "hb_sync_device", "hb_shutdown", "hb_partition_range",
     "hb_ipc_handle", "hb_ipc_open", "hb_ipc_close",
+    "hb_tuning_reload", "hb_built_with_ab", "hb_last_kernel_name", "hb_last_timeline", "hb_engine_budget",
 )
 
 
@@ -39,10 +43,22 @@ class HbTiming(ctypes.Structure):
         ("d2h_bytes", ctypes.c_uint64),
         ("chunks", ctypes.c_uint64),
         ("launches", ctypes.c_uint64),
+        ("shards", ctypes.c_uint64),
+        ("device_mask", ctypes.c_uint64),
     ]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class HbSpan(ctypes.Structure):
+    _fields_ = [
+        ("dev", ctypes.c_int32),
+        ("stage", ctypes.c_int32),
+        ("chunk", ctypes.c_uint64),
+        ("t0_ms", ctypes.c_double),
+        ("t1_ms", ctypes.c_double),
+    ]
 
 
 class HbDeviceInfo(ctypes.Structure):
@@ -97,6 +113,11 @@ _SIGS = {
     "hb_ipc_close": (_int, [_int, _vp]),
     "hb_partition_range": (_int, [ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), _int,
                                   ctypes.POINTER(ctypes.c_int64)]),
+    "hb_tuning_reload": (_int, []),
+    "hb_built_with_ab": (_int, []),
+    "hb_last_kernel_name": (_int, [ctypes.c_char_p, _int]),
+    "hb_last_timeline": (_int, [ctypes.POINTER(HbSpan), _int]),
+    "hb_engine_budget": (_int, [_int, _u64p, _u64p]),
 }
 
 
@@ -163,6 +184,41 @@ def device_info(ordinal: int) -> dict:
 
 def launch_count() -> int:
     return int(lib().hb_launch_count())
+
+
+def reload_tuning() -> None:
+    """Re-read the $HB_* tuning environment (the library parses it once)."""
+    check(lib().hb_tuning_reload(), "hb_tuning_reload")
+
+
+def built_with_ab() -> bool:
+    return bool(lib().hb_built_with_ab())
+
+
+def last_kernel_name() -> str:
+    """Demangled name of the last hash kernel this thread launched (directly
+    or through the engine's last call) -- what ncu's launch list shows."""
+    buf = ctypes.create_string_buffer(512)
+    check(lib().hb_last_kernel_name(buf, 512), "hb_last_kernel_name")
+    return buf.value.decode(errors="replace")
+
+
+STAGES = ("h2d", "kernel", "d2h")
+
+
+def last_timeline() -> list[dict]:
+    """Per-chunk stage spans of this thread's last call made with timing."""
+    n = lib().hb_last_timeline(None, 0)
+    arr = (HbSpan * max(1, n))()
+    n = lib().hb_last_timeline(arr, n)
+    return [{"dev": s.dev, "stage": STAGES[s.stage], "chunk": s.chunk, "t0_ms": s.t0_ms, "t1_ms": s.t1_ms}
+            for s in arr[:n]]
+
+
+def engine_budget(gpu: int) -> dict:
+    b, c = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    check(lib().hb_engine_budget(gpu, ctypes.byref(b), ctypes.byref(c)), "hb_engine_budget")
+    return {"budget_bytes": b.value, "chunk_cap_bytes": c.value}
 
 
 def gpu_array(gpus):

@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <ctype.h>
+#include <cxxabi.h>
 #include <pthread.h>
 #include <sched.h>
 #include <stdarg.h>
@@ -27,11 +28,16 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/hetoc_b200.h"
 #include "hb_internal.h"
@@ -94,32 +100,24 @@ static int device_count() {
 }
 
 // ---------------------------------------------------------------- tuning --
-static uint64_t env_u64(const char* name, uint64_t dflt) {
-    const char* v = getenv(name);
-    if (!v || !*v) return dflt;
-    char* end = nullptr;
-    unsigned long long x = strtoull(v, &end, 0);
-    return (end && *end == '\0' && x > 0) ? (uint64_t)x : dflt;
-}
-static uint64_t chunk_bytes() { return env_u64("HB_CHUNK_BYTES", 256ull << 20); }
 // Chunk budget for a shard of `staged` input bytes and `out` digest bytes.
 // When the digests are big enough for their copy-out to matter (short
-// messages: >= HB_PIPE_MIN_OUT, 4 MiB), the shard is cut into at least
-// HB_PIPE_CHUNKS (4) chunks of >= HB_MIN_CHUNK_BYTES (8 MiB), so chunk k's
+// messages: >= pipe_min_out, 4 MiB), the shard is cut into at least
+// pipe_chunks (4) chunks of >= min_chunk_bytes (8 MiB), so chunk k's
 // kernel + D2H overlap chunk k+1's H2D across the slot ring instead of running
 // back to back.  Smaller shards, or long messages with few digest bytes, stay
 // one chunk: every extra chunk costs ~10-20 us of copy/launch latency
 // (profiles/ab_pipe_r1.txt: +7..17 % e2e at 16-64 MB of 64-byte messages,
-// -3..-40 % if 4 MB batches or 1 KiB messages were split).
-static uint64_t pipelined_budget(uint64_t staged, uint64_t out) {
-    if (out < env_u64("HB_PIPE_MIN_OUT", 4ull << 20)) return chunk_bytes();
-    const uint64_t parts = env_u64("HB_PIPE_CHUNKS", 4);
-    const uint64_t floor_b = env_u64("HB_MIN_CHUNK_BYTES", 8ull << 20);
-    return std::min(chunk_bytes(), std::max(floor_b, (staged + parts - 1) / parts));
+// -3..-40 % if 4 MB batches or 1 KiB messages were split).  `cap` is the
+// GPU's chunk limit from its HBM budget (GpuCtx::chunk_cap).
+static uint64_t pipelined_budget(uint64_t staged, uint64_t out, uint64_t cap) {
+    const Tuning& T = tuning();
+    const uint64_t chunk = std::min(T.chunk_bytes, cap);
+    if (out < T.pipe_min_out) return chunk;
+    return std::min(chunk, std::max(T.min_chunk_bytes, (staged + T.pipe_chunks - 1) / T.pipe_chunks));
 }
 static int memcpy_threads(int n_gpus) {
-    uint64_t t = env_u64("HB_MEMCPY_THREADS", 0);
-    if (t) return (int)t;
+    if (tuning().memcpy_threads) return (int)tuning().memcpy_threads;
     unsigned hw = std::thread::hardware_concurrency();
     int per = (int)(hw ? hw : 8) / std::max(1, n_gpus);
     return std::max(1, std::min(8, per));
@@ -159,6 +157,10 @@ static bool is_pinned(const void* p, uint64_t bytes) {
 // ------------------------------------------------------- per-GPU context --
 constexpr int kSlots = 3;
 
+// Device buffers of the chunk ring.  They only grow (to the largest chunk
+// seen, rounded up to 2 MiB) and live until hb_shutdown; the ring's total is
+// bounded by the GPU's budget (GpuCtx::chunk_cap), so growth never fails for
+// lack of HBM that cudaMemGetInfo said was there.
 struct DevBuf {
     void* p = nullptr;
     uint64_t cap = 0;
@@ -167,7 +169,7 @@ struct DevBuf {
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
-        const uint64_t want = (bytes + 4095) & ~4095ull;
+        const uint64_t want = (bytes + (2ull << 20) - 1) & ~((2ull << 20) - 1);
         cudaError_t e = cudaMalloc(&p, want);
         if (e == cudaSuccess) cap = want;
         return e;
@@ -188,6 +190,8 @@ struct HostBuf {
     }
 };
 
+enum Stage { kH2D = 0, kKernel = 1, kD2H = 2 };
+
 struct Slot {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};  // h2d0, h2d1, k0, k1, d2h0, d2h1
@@ -196,6 +200,7 @@ struct Slot {
     bool in_use = false;
     bool has_h2d = false;
     bool timed = false;  // ev[0..4] recorded (the caller asked for hb_timing)
+    uint64_t chunk = 0;  // chunk index of the work in flight
     // deferred copy-out (pageable destination)
     uint8_t* pend_dst = nullptr;
     uint64_t pend_bytes = 0;
@@ -205,6 +210,9 @@ struct GpuCtx {
     int dev = -1;
     std::mutex mu;
     bool ready = false;
+    cudaEvent_t ev_ref = nullptr;  // t = 0 of a timed shard's timeline
+    uint64_t budget = 0;           // HBM the ring may use: free at init - device_reserve
+    uint64_t chunk_cap = 0;        // largest input chunk the ring is allowed
     Slot slots[kSlots];
 };
 
@@ -224,34 +232,89 @@ static int get_ctx(int dev, GpuCtx** out) {
     return HB_OK;
 }
 
+// The per-GPU memory pool of the reference's Arena (runtime/arena.py:28-63,
+// capacity from the device spec) sized from what the device actually has:
+// at first use, budget = free HBM - device_reserve; each of the kSlots slots
+// may stage at most chunk_cap input bytes (plus its digests/offsets), so the
+// ring never outgrows the budget; larger shards are sub-batched, as
+// _run_group does for over-capacity groups (runtime/executor.py:603-699).
 static int ctx_init(GpuCtx& c) {  // caller holds c.mu and has set the device
     if (c.ready) return HB_OK;
     for (Slot& s : c.slots) {
         HB_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
         for (auto& e : s.ev) HB_CK(cudaEventCreate(&e));
     }
+    HB_CK(cudaEventCreate(&c.ev_ref));
+    size_t fr = 0, tot = 0;
+    HB_CK(cudaMemGetInfo(&fr, &tot));
+    const uint64_t reserve = tuning().device_reserve;
+    c.budget = fr > reserve + (64ull << 20) ? fr - reserve : (64ull << 20);
+    // input chunk + its digests (<= 1/2 of it for 64-byte rows: 32 B / 64 B) + offsets/scratch (<= 12 B per
+    // 1-byte message, capped by the 64-byte-per-message chunk rule in run_shard_locked) ~ 2x the input chunk
+    c.chunk_cap = std::max<uint64_t>(1ull << 20, c.budget / (2 * kSlots));
     c.ready = true;
     return HB_OK;
 }
 
+struct Span {
+    int stage;
+    uint64_t chunk;
+    double t0, t1;  // ms since the shard's reference event
+};
+
 struct ShardStats {
-    double kernel_ms = 0, h2d_ms = 0, d2h_ms = 0;
+    int dev = -1;
+    double kernel_ms = 0, h2d_ms = 0, d2h_ms = 0;  // union of busy intervals per stage
     uint64_t h2d_bytes = 0, d2h_bytes = 0, chunks = 0, launches = 0;
+    std::vector<Span> spans;
+    const void* last_kernel = nullptr;
     int status = HB_OK;
     std::string err;
 };
 
+// Length of the union of [t0, t1) intervals of one stage (the slots' copies
+// and kernels overlap each other: summing them would over-count).
+static double union_ms(std::vector<Span>& v, int stage) {
+    std::vector<std::pair<double, double>> iv;
+    for (const Span& s : v)
+        if (s.stage == stage && s.t1 > s.t0) iv.emplace_back(s.t0, s.t1);
+    std::sort(iv.begin(), iv.end());
+    double total = 0, cur0 = 0, cur1 = -1e300;
+    for (auto& x : iv) {
+        if (x.first > cur1) {
+            if (cur1 > cur0) total += cur1 - cur0;
+            cur0 = x.first;
+            cur1 = x.second;
+        } else {
+            cur1 = std::max(cur1, x.second);
+        }
+    }
+    if (cur1 > cur0) total += cur1 - cur0;
+    return total;
+}
+
 // Wait for a slot's previous chunk, land its deferred copy-out, bank timings.
-static int retire_slot(Slot& s, ShardStats& st, int mt) {
+static int retire_slot(GpuCtx& c, Slot& s, ShardStats& st, int mt) {
     if (!s.in_use) return HB_OK;
     HB_CK(cudaEventSynchronize(s.ev[5]));
-    float ms = 0;
     if (s.timed) {
-        if (s.has_h2d && cudaEventElapsedTime(&ms, s.ev[0], s.ev[1]) == cudaSuccess) st.h2d_ms += ms;
-        if (cudaEventElapsedTime(&ms, s.ev[2], s.ev[3]) == cudaSuccess) st.kernel_ms += ms;
-        if (cudaEventElapsedTime(&ms, s.ev[4], s.ev[5]) == cudaSuccess) st.d2h_ms += ms;
+        float a = 0, b = 0;
+        auto span = [&](int stage, int e0, int e1) {
+            if (cudaEventElapsedTime(&a, c.ev_ref, s.ev[e0]) == cudaSuccess &&
+                cudaEventElapsedTime(&b, c.ev_ref, s.ev[e1]) == cudaSuccess)
+                st.spans.push_back({stage, s.chunk, (double)a, (double)b});
+            else
+                cudaGetLastError();
+        };
+        if (s.has_h2d) span(kH2D, 0, 1);
+        span(kKernel, 2, 3);
+        span(kD2H, 4, 5);
     }
-    if (s.pend_bytes) parallel_memcpy(s.pend_dst, s.h_out.p, s.pend_bytes, mt);
+    if (s.pend_bytes) {
+        nvtxRangePushA("hb d2h staging memcpy");
+        parallel_memcpy(s.pend_dst, s.h_out.p, s.pend_bytes, mt);
+        nvtxRangePop();
+    }
     s.pend_bytes = 0;
     s.in_use = false;
     return HB_OK;
@@ -264,7 +327,9 @@ static int stage_in(Slot& s, DevBuf& dst, HostBuf& stage, const void* src, uint6
         HB_CK(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, s.stream));
     } else {
         HB_CK(stage.ensure(bytes));
+        nvtxRangePushA("hb h2d staging memcpy");
         parallel_memcpy(stage.p, src, bytes, mt);
+        nvtxRangePop();
         HB_CK(cudaMemcpyAsync(dst.p, stage.p, bytes, cudaMemcpyHostToDevice, s.stream));
     }
     return HB_OK;
@@ -312,15 +377,18 @@ static int run_shard_locked(GpuCtx& c, const ShardJob& j, ShardStats& st) {
     const uint64_t staged = j.kind == 0 ? (j.hi - j.lo) * j.msg_len
                           : j.kind == 1 ? j.offsets[j.hi] - j.offsets[j.lo]
                                         : (j.hi - j.lo) * (uint64_t)dlen;  // decimal: digests only
-    const uint64_t budget = pipelined_budget(staged, (j.hi - j.lo) * (uint64_t)dlen);
+    const uint64_t budget = pipelined_budget(staged, (j.hi - j.lo) * (uint64_t)dlen, c.chunk_cap);
     uint64_t slot_k = 0;
     const uint64_t l0 = hb::launches_total();
+    if (j.timed) HB_CK(cudaEventRecord(c.ev_ref, c.slots[0].stream));
     uint64_t i = j.lo;
     while (i < j.hi) {
         // ---- plan the chunk [i, e)
         uint64_t e, in_bytes = 0, in_off = 0;
         if (j.kind == 0) {
             uint64_t per = j.msg_len ? std::max<uint64_t>(1, budget / j.msg_len) : (j.hi - j.lo);
+            // digests of a chunk of short rows stay within the same budget
+            per = std::min<uint64_t>(per, std::max<uint64_t>(1, budget / (uint64_t)dlen));
             if (per >= 256) per &= ~127ull;
             e = std::min(j.hi, i + per);
             in_bytes = (e - i) * j.msg_len;
@@ -334,15 +402,20 @@ static int run_shard_locked(GpuCtx& c, const ShardJob& j, ShardStats& st) {
             e = std::min(e, i + max_msgs);
             in_off = j.offsets[i];
             in_bytes = j.offsets[e] - j.offsets[i];
+            if (in_bytes > c.chunk_cap + (c.chunk_cap >> 1))
+                return fail(HB_ERR_NOMEM, "message %llu (%llu bytes) exceeds the GPU %d chunk budget (%llu bytes)",
+                            (unsigned long long)i, (unsigned long long)in_bytes, c.dev,
+                            (unsigned long long)c.chunk_cap);
         } else {
             const uint64_t per = std::max<uint64_t>(1, budget / (uint64_t)dlen);
             e = std::min(j.hi, i + per);
         }
         const uint64_t cn = e - i;
         Slot& s = c.slots[slot_k % kSlots];
-        ++slot_k;
-        rc = retire_slot(s, st, j.mt);
+        rc = retire_slot(c, s, st, j.mt);
         if (rc) return rc;
+        s.chunk = slot_k;
+        ++slot_k;
         HB_CK(s.d_out.ensure(cn * dlen));
         if (in_bytes) HB_CK(s.d_in.ensure(in_bytes + 64));
         s.has_h2d = false;
@@ -395,27 +468,30 @@ static int run_shard_locked(GpuCtx& c, const ShardJob& j, ShardStats& st) {
         st.chunks += 1;
         s.in_use = true;
         if (j.flags & HB_FLAG_SYNC_H2D) {
-            rc = retire_slot(s, st, j.mt);
+            rc = retire_slot(c, s, st, j.mt);
             if (rc) return rc;
         }
         i = e;
     }
     for (Slot& s : c.slots) {
-        rc = retire_slot(s, st, j.mt);
+        rc = retire_slot(c, s, st, j.mt);
         if (rc) return rc;
     }
     st.launches = hb::launches_total() - l0;
+    st.h2d_ms = union_ms(st.spans, kH2D);
+    st.kernel_ms = union_ms(st.spans, kKernel);
+    st.d2h_ms = union_ms(st.spans, kD2H);
     return HB_OK;
 }
 
-// Pin the calling shard thread to the CPUs local to GPU `dev` (the sysfs
-// local_cpulist of its PCI function), intersected with the allowed set.  A
-// multi-GPU call runs one such thread per GPU; the GPU's pinned staging ring
-// (first allocated by this thread) and the host-copy helpers it spawns then
-// stay on the GPU's NUMA node.  Best effort; $HB_BIND_NUMA=0 disables.
+// Pin the calling thread to the CPUs local to GPU `dev` (the sysfs
+// local_cpulist of its PCI function), intersected with the allowed set.
+// Called once by each GPU's worker thread when it starts: the GPU's pinned
+// staging ring (first allocated by that thread) and the host-copy helpers it
+// spawns then stay on the GPU's NUMA node.  Best effort; $HB_BIND_NUMA=0
+// disables.  The caller's own affinity is never changed.
 static void bind_thread_near_gpu(int dev) {
-    const char* off = getenv("HB_BIND_NUMA");
-    if (off && off[0] == '0') return;
+    if (!tuning().bind_numa) return;
     char bus[32];
     if (cudaDeviceGetPCIBusId(bus, sizeof bus, dev) != cudaSuccess) {
         cudaGetLastError();
@@ -454,11 +530,16 @@ static void bind_thread_near_gpu(int dev) {
 
 static void run_shard(const ShardJob& j, ShardStats& st) {
     GpuCtx* c = nullptr;
+    st.dev = j.dev;
     int rc = get_ctx(j.dev, &c);
     if (rc == HB_OK) {
         std::lock_guard<std::mutex> lk(c->mu);
         DeviceGuard g(j.dev);
+        char label[48];
+        snprintf(label, sizeof label, "hb shard gpu %d", j.dev);
+        nvtxRangePushA(label);
         rc = run_shard_locked(*c, j, st);
+        nvtxRangePop();
         if (rc != HB_OK) {
             // leave the context reusable: drain whatever is in flight
             for (Slot& s : c->slots) {
@@ -469,8 +550,61 @@ static void run_shard(const ShardJob& j, ShardStats& st) {
             cudaGetLastError();
         }
     }
+    st.last_kernel = last_hash_kernel();
     st.status = rc;
     if (rc != HB_OK) st.err = g_err;
+}
+
+// ------------------------------------------------------ per-GPU workers --
+// One persistent host thread per GPU (created on first multi-GPU call, NUMA-
+// bound once) serves the shards of multi-GPU calls; a call whose work lands on
+// a single GPU runs on the caller's own thread (no hand-off).  The reference
+// calls the boundary concurrently from pool threads (executor.py:596-599,
+// batch.py:310-313): shards of concurrent calls queue on each GPU's worker and
+// serialise on that GPU's context mutex.
+struct Worker {
+    int dev = -1;
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<std::function<void()>> q;
+    bool stop = false;
+    void loop() {
+        bind_thread_near_gpu(dev);
+        for (;;) {
+            std::function<void()> f;
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return stop || !q.empty(); });
+                if (stop && q.empty()) return;
+                f = std::move(q.front());
+                q.pop_front();
+            }
+            f();
+        }
+    }
+    void submit(std::function<void()> f) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            q.push_back(std::move(f));
+        }
+        cv.notify_one();
+    }
+};
+// Leaked on purpose at exit (threads parked in cv.wait must not see their
+// mutex destroyed by static destructors); hb_shutdown joins and frees them.
+static std::vector<Worker*> g_workers;
+
+static Worker* get_worker(int dev) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    if ((int)g_workers.size() <= dev) g_workers.resize(dev + 1, nullptr);
+    if (!g_workers[dev]) {
+        Worker* w = new Worker();
+        w->dev = dev;
+        w->th = std::thread([w] { w->loop(); });
+        g_workers[dev] = w;
+    }
+    return g_workers[dev];
 }
 
 // partition_range, pkg/src/hetoc/passes/partition.py:17-31 (same double
@@ -491,11 +625,27 @@ static int partition(int64_t lb, int64_t ub, const double* ratios, int k, int64_
     return HB_OK;
 }
 
-static int resolve_gpus(const int* gpus, int n_gpus, std::vector<int>& out) {
+// The default device set ("all GPUs") for a call of `bytes` staged bytes: a
+// call below tuning().multi_gpu_min_bytes (32 MiB) would spend more on
+// per-shard setup than it saves in PCIe time, so it runs on ONE GPU, picked
+// per calling thread round-robin (pool threads of the reference's executor
+// and hash_batch spread over the GPUs instead of all fanning out to all).
+static int pick_default_gpu(int nd) {
+    static std::atomic<int> next{0};
+    static thread_local int mine = -1;
+    if (mine < 0) mine = next.fetch_add(1, std::memory_order_relaxed);
+    return mine % nd;
+}
+
+static int resolve_gpus(const int* gpus, int n_gpus, uint64_t bytes, std::vector<int>& out) {
     const int nd = device_count();
     if (nd == 0) return fail(HB_ERR_NODEV, "no CUDA device visible");
     out.clear();
     if (!gpus || n_gpus <= 0) {
+        if (nd > 1 && bytes < tuning().multi_gpu_min_bytes) {
+            out.push_back(pick_default_gpu(nd));
+            return HB_OK;
+        }
         for (int d = 0; d < nd; ++d) out.push_back(d);
     } else {
         for (int k = 0; k < n_gpus; ++k) {
@@ -519,8 +669,11 @@ static int check_ratios(const double* r, int k) {
     return HB_OK;
 }
 
-// Split [0, n) over the GPUs (equal ratios unless given), run one host thread
-// per shard, merge stats.
+// Per calling thread: the stage timeline of its last timed call.
+static thread_local std::vector<hb_span> t_timeline;
+
+// Split [0, n) over the GPUs (equal ratios unless given), run the shards
+// (one on the caller's thread, several on the GPUs' workers), merge stats.
 static int run_sharded(ShardJob proto, uint64_t n, const std::vector<int>& devs, hb_timing* t,
                        const double* user_ratios = nullptr) {
     const auto t0 = std::chrono::steady_clock::now();
@@ -545,16 +698,21 @@ static int run_sharded(ShardJob proto, uint64_t n, const std::vector<int>& devs,
     if (jobs.size() == 1) {
         run_shard(jobs[0], stats[0]);
     } else {
-        std::vector<std::thread> ts;
+        std::mutex mu;
+        std::condition_variable cv;
+        size_t left = jobs.size();
         for (size_t q = 0; q < jobs.size(); ++q)
-            ts.emplace_back([&, q] {
-                bind_thread_near_gpu(jobs[q].dev);  // a worker thread: the caller's own affinity is untouched
+            get_worker(jobs[q].dev)->submit([&, q] {
                 run_shard(jobs[q], stats[q]);
+                std::lock_guard<std::mutex> lk(mu);
+                if (--left == 0) cv.notify_one();
             });
-        for (auto& th : ts) th.join();
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return left == 0; });
     }
     hb_timing agg;
     memset(&agg, 0, sizeof agg);
+    if (t) t_timeline.clear();
     for (auto& s : stats) {
         if (s.status != HB_OK) {
             g_err = s.err;
@@ -567,9 +725,31 @@ static int run_sharded(ShardJob proto, uint64_t n, const std::vector<int>& devs,
         agg.d2h_bytes += s.d2h_bytes;
         agg.chunks += s.chunks;
         agg.launches += s.launches;
+        agg.shards += 1;
+        if (s.dev >= 0 && s.dev < 64) agg.device_mask |= 1ull << s.dev;
+        if (s.last_kernel) set_last_hash_kernel(s.last_kernel);
+        if (t)
+            for (const Span& sp : s.spans) t_timeline.push_back({s.dev, sp.stage, sp.chunk, sp.t0, sp.t1});
     }
     agg.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (t) *t = agg;
+    return HB_OK;
+}
+
+// gen_messages' range rule (batch.py:86-99: indices must fit in `width`
+// digits) on 64-bit indices: start + count must not wrap, and must not
+// exceed 10^width (10^20 > 2^64, so width 20 only needs the wrap check).
+static int check_decimal_range(uint64_t start, uint64_t count, int width) {
+    if (start > UINT64_MAX - count)
+        return fail(HB_ERR_INVAL, "index range [%llu, +%llu) overflows 64 bits", (unsigned long long)start,
+                    (unsigned long long)count);
+    if (width < 20) {
+        uint64_t p = 1;
+        for (int k = 0; k < width; ++k) p *= 10u;
+        if (start + count > p)
+            return fail(HB_ERR_INVAL, "index range [%llu, %llu) does not fit in %d digits", (unsigned long long)start,
+                        (unsigned long long)(start + count), width);
+    }
     return HB_OK;
 }
 
@@ -633,8 +813,9 @@ int hb_hash_fixed(int alg, const uint8_t* msgs, uint64_t n, uint64_t msg_len, ui
     if (!out || (!msgs && msg_len)) return fail(HB_ERR_INVAL, "null buffer");
     if (msg_len && n > UINT64_MAX / msg_len) return fail(HB_ERR_INVAL, "n*msg_len overflows");
     std::vector<int> devs;
-    int rc = resolve_gpus(gpus, n_gpus, devs);
+    int rc = resolve_gpus(gpus, n_gpus, n * msg_len, devs);
     if (rc) return rc;
+    nvtxRangePushA("hb_hash_fixed");
     ShardJob j;
     j.kind = 0;
     j.alg = alg;
@@ -644,7 +825,9 @@ int hb_hash_fixed(int alg, const uint8_t* msgs, uint64_t n, uint64_t msg_len, ui
     j.flags = flags;
     j.in_pinned = is_pinned(msgs, n * msg_len);
     j.out_pinned = is_pinned(out, n * (uint64_t)dlen);
-    return run_sharded(j, n, devs, t);
+    rc = run_sharded(j, n, devs, t);
+    nvtxRangePop();
+    return rc;
 }
 
 int hb_hash_fixed_split(int alg, const uint8_t* msgs, uint64_t n, uint64_t msg_len, uint8_t* out, const int* gpus,
@@ -659,7 +842,7 @@ int hb_hash_fixed_split(int alg, const uint8_t* msgs, uint64_t n, uint64_t msg_l
     if (!out || (!msgs && msg_len)) return fail(HB_ERR_INVAL, "null buffer");
     if (msg_len && n > UINT64_MAX / msg_len) return fail(HB_ERR_INVAL, "n*msg_len overflows");
     std::vector<int> devs;
-    rc = resolve_gpus(gpus, n_gpus, devs);
+    rc = resolve_gpus(gpus, n_gpus, n * msg_len, devs);
     if (rc) return rc;
     ShardJob j;
     j.kind = 0;
@@ -684,8 +867,9 @@ int hb_hash_varlen(int alg, const uint8_t* data, const uint64_t* offsets, uint64
         if (offsets[i + 1] < offsets[i]) return fail(HB_ERR_INVAL, "offsets must be non-decreasing (at %llu)", (unsigned long long)i);
     if (!data && offsets[n] > offsets[0]) return fail(HB_ERR_INVAL, "null data");
     std::vector<int> devs;
-    int rc = resolve_gpus(gpus, n_gpus, devs);
+    int rc = resolve_gpus(gpus, n_gpus, offsets[n] - offsets[0], devs);
     if (rc) return rc;
+    nvtxRangePushA("hb_hash_varlen");
     ShardJob j;
     j.kind = 1;
     j.alg = alg;
@@ -696,7 +880,9 @@ int hb_hash_varlen(int alg, const uint8_t* data, const uint64_t* offsets, uint64
     j.in_pinned = is_pinned(data + offsets[0], offsets[n] - offsets[0]);
     j.off_pinned = is_pinned(offsets, (n + 1) * 8);
     j.out_pinned = is_pinned(out, n * (uint64_t)dlen);
-    return run_sharded(j, n, devs, t);
+    rc = run_sharded(j, n, devs, t);
+    nvtxRangePop();
+    return rc;
 }
 
 int hb_hash_decimal(int alg, uint64_t start, uint64_t count, int width, uint8_t* out, const int* gpus, int n_gpus,
@@ -707,8 +893,10 @@ int hb_hash_decimal(int alg, uint64_t start, uint64_t count, int width, uint8_t*
     if (width < 1 || width > 20) return fail(HB_ERR_INVAL, "width must be in [1, 20] for on-device generation");
     if (count == 0) return HB_OK;
     if (!out) return fail(HB_ERR_INVAL, "null buffer");
+    int rc = check_decimal_range(start, count, width);
+    if (rc) return rc;
     std::vector<int> devs;
-    int rc = resolve_gpus(gpus, n_gpus, devs);
+    rc = resolve_gpus(gpus, n_gpus, count * (uint64_t)dlen, devs);
     if (rc) return rc;
     ShardJob j;
     j.kind = 2;
@@ -754,6 +942,7 @@ int hb_hash_decimal_dev(int alg, int gpu, uint64_t start, uint64_t count, int wi
     if (width < 1 || width > 20) return fail(HB_ERR_INVAL, "width must be in [1, 20]");
     if (count == 0) return HB_OK;
     if (!d_out) return fail(HB_ERR_INVAL, "null buffer");
+    if (int rc = check_decimal_range(start, count, width)) return rc;
     const int nd = device_count();
     if (gpu < 0 || gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
     DeviceGuard g(gpu);
@@ -775,6 +964,7 @@ int hb_fill_random_dev(int gpu, void* d_buf, uint64_t nbytes, uint64_t seed, uin
 int hb_gen_decimal_dev(int gpu, uint64_t start, uint64_t count, int width, void* d_out, void* stream) {
     if (width < 1) return fail(HB_ERR_INVAL, "width must be positive");
     if (count == 0) return HB_OK;
+    if (int rc = check_decimal_range(start, count, width)) return rc;
     if (!d_out) return fail(HB_ERR_INVAL, "null buffer");
     const int nd = device_count();
     if (gpu < 0 || gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
@@ -867,7 +1057,64 @@ int hb_ipc_close(int gpu, void* d_ptr) {
     return HB_OK;
 }
 
+int hb_tuning_reload(void) {
+    tuning_reload();
+    return HB_OK;
+}
+
+int hb_built_with_ab(void) { return built_with_ab() ? 1 : 0; }
+
+int hb_last_kernel_name(char* buf, int cap) {
+    if (!buf || cap < 1) return fail(HB_ERR_INVAL, "null buffer");
+    buf[0] = '\0';
+    const void* fn = last_hash_kernel();
+    if (!fn) return fail(HB_ERR_INVAL, "no hash kernel launched by this thread yet");
+    const char* mangled = nullptr;
+    HB_CK(cudaFuncGetName(&mangled, fn));
+    int st = 0;
+    char* dem = abi::__cxa_demangle(mangled, nullptr, nullptr, &st);
+    snprintf(buf, (size_t)cap, "%s", st == 0 && dem ? dem : mangled);
+    free(dem);
+    return HB_OK;
+}
+
+int hb_last_timeline(hb_span* out, int cap) {
+    const int n = (int)t_timeline.size();
+    if (out)
+        for (int i = 0; i < n && i < cap; ++i) out[i] = t_timeline[i];
+    return n;
+}
+
+int hb_engine_budget(int gpu, uint64_t* budget, uint64_t* chunk_cap) {
+    if (!budget || !chunk_cap) return fail(HB_ERR_INVAL, "null pointer");
+    GpuCtx* c = nullptr;
+    int rc = get_ctx(gpu, &c);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(gpu);
+    rc = ctx_init(*c);
+    if (rc) return rc;
+    *budget = c->budget;
+    *chunk_cap = std::min(c->chunk_cap, tuning().chunk_bytes);
+    return HB_OK;
+}
+
 int hb_shutdown(void) {
+    std::vector<Worker*> ws;
+    {
+        std::lock_guard<std::mutex> lk(g_ctx_mu);
+        ws.swap(g_workers);
+    }
+    for (Worker* w : ws) {
+        if (!w) continue;
+        {
+            std::lock_guard<std::mutex> lk(w->mu);
+            w->stop = true;
+        }
+        w->cv.notify_one();
+        w->th.join();
+        delete w;
+    }
     std::lock_guard<std::mutex> lk(g_ctx_mu);
     for (auto& cp : g_ctx) {
         if (!cp) continue;
@@ -886,6 +1133,7 @@ int hb_shutdown(void) {
                 if (e) cudaEventDestroy(e);
             if (s.stream) cudaStreamDestroy(s.stream);
         }
+        if (cp->ev_ref) cudaEventDestroy(cp->ev_ref);
         cp.reset();
     }
     g_ctx.clear();

@@ -6,8 +6,60 @@
 
 namespace hb {
 
-// Launch-count bookkeeping (bench.py reports gpu_launches from this).
+// ------------------------------------------------------------------ tuning --
+// Every knob of the engine and the kernel dispatch, parsed ONCE from the
+// environment (first use, or hb_tuning_reload()).  Launch paths read these
+// fields; none calls getenv.  Defaults are the B200-measured best (DESIGN.md
+// §4).  The fields under "A/B" only have an effect in a -DHB_AB build, which
+// also instantiates the losing kernel arms they select.
+struct Tuning {
+    // engine (hb_engine.cu)
+    uint64_t chunk_bytes = 256ull << 20;        // $HB_CHUNK_BYTES: sub-batch (chunk) input bytes
+    uint64_t pipe_min_out = 4ull << 20;         // $HB_PIPE_MIN_OUT: digest bytes from which a shard is pipelined
+    uint64_t pipe_chunks = 4;                   // $HB_PIPE_CHUNKS
+    uint64_t min_chunk_bytes = 8ull << 20;      // $HB_MIN_CHUNK_BYTES
+    uint64_t memcpy_threads = 0;                // $HB_MEMCPY_THREADS (0 = auto)
+    bool bind_numa = true;                      // $HB_BIND_NUMA=0 disables worker NUMA pinning
+    uint64_t multi_gpu_min_bytes = 32ull << 20; // $HB_MULTI_GPU_MIN_BYTES: smaller default-GPU calls use one GPU
+    uint64_t device_reserve = 2ull << 30;       // $HB_DEVICE_RESERVE: HBM left free when sizing the chunk ring
+    // kernels (hb_kernels.cuh)
+    bool pdl = true;                            // $HB_PDL
+    uint64_t small_n = 1ull << 18;              // $HB_SMALL_N: below it, one message per thread in TMA tiles
+    uint64_t direct_max_len = 128;              // $HB_DIRECT_MAX_L: rows up to it use the per-thread-load kernels
+    bool small_pair = true;                     // $HB_SMALL_PAIR: MD5 <= 32 B rows, two per thread at >= 2^20
+    bool dec_run = true;                        // $HB_DEC_RUN: runs-of-ten decimal kernel
+    int varlen_sort = -1;                       // $HB_VARLEN_SORT: -1 per algorithm, 0 global, 1 window
+    // A/B (-DHB_AB)
+    int tma_cfg = -1;                           // $HB_TMA_CFG
+    int variant = -1;                           // $HB_VARIANT
+    uint32_t tma_l2 = 256;                      // $HB_TMA_L2
+    uint32_t tma_evict_first = 0;               // $HB_TMA_EVICT_FIRST
+    bool small_kernel = true;                   // $HB_NO_SMALL_KERNEL
+    bool small_kernel_ab = false;               // $HB_CONST_VARIANT=0 / $HB_SMALL_CTA set
+    int const_variant = -1;                     // $HB_CONST_VARIANT
+    uint32_t small_cta = 128;                   // $HB_SMALL_CTA
+    bool dec_ab = false;                        // any of $HB_DEC_PAIR / $HB_FMA_DIGITS / $HB_CONST_VARIANT set
+    int dec_pair = -1;                          // $HB_DEC_PAIR
+    bool fma_digits = true;                     // $HB_FMA_DIGITS
+    uint32_t sort_window = 8192;                // $HB_SORT_WINDOW
+    uint32_t varlen_ld = 16;                    // $HB_VARLEN_LD
+    uint32_t varlen_q = 8;                      // $HB_VARLEN_Q
+    uint32_t varlen_prefetch = 0;               // $HB_VARLEN_PREFETCH
+    uint32_t varlen_bulk = 0;                   // $HB_VARLEN_BULK
+    int vc_stages = -1;                         // $HB_VC_STAGES
+    uint32_t vc_pf = 256;                       // $HB_VC_PF
+};
+const Tuning& tuning();
+void tuning_reload();
+bool built_with_ab();
+
+// Launch bookkeeping: a process-wide count (bench.py reports gpu_launches
+// from it) and, per calling thread, the last hash kernel launched (its symbol
+// is resolved by hb_last_kernel_name, so reports name the kernel that ran).
+void note_launch(const void* kernel, bool hash_kernel);
 void note_launches(uint64_t k);
+const void* last_hash_kernel();
+void set_last_hash_kernel(const void* kernel);  // propagate a worker thread's launch to the caller
 
 // Fixed-width messages already resident on the current device.
 //   d_msgs: n*msg_len bytes (row i at i*msg_len), d_out: n*dlen bytes.

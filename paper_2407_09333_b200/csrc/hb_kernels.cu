@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 
 #include "hb_algos.cuh"
@@ -24,8 +25,96 @@
 
 namespace hb {
 
+// ------------------------------------------------------------------ tuning --
+static uint64_t env_u64(const char* name, uint64_t dflt) {
+    const char* v = getenv(name);
+    if (!v || !*v) return dflt;
+    char* end = nullptr;
+    const unsigned long long x = strtoull(v, &end, 0);
+    return (end && *end == '\0') ? (uint64_t)x : dflt;
+}
+#ifdef HB_AB
+static bool env_set(const char* name) {
+    const char* v = getenv(name);
+    return v && *v;
+}
+#endif
+
+static Tuning parse_tuning() {
+    Tuning t;
+    t.chunk_bytes = std::max<uint64_t>(1ull << 16, env_u64("HB_CHUNK_BYTES", t.chunk_bytes));
+    t.pipe_min_out = env_u64("HB_PIPE_MIN_OUT", t.pipe_min_out);
+    t.pipe_chunks = std::max<uint64_t>(1, env_u64("HB_PIPE_CHUNKS", t.pipe_chunks));
+    t.min_chunk_bytes = std::max<uint64_t>(1ull << 16, env_u64("HB_MIN_CHUNK_BYTES", t.min_chunk_bytes));
+    t.memcpy_threads = env_u64("HB_MEMCPY_THREADS", 0);
+    t.bind_numa = env_u64("HB_BIND_NUMA", 1) != 0;
+    t.multi_gpu_min_bytes = env_u64("HB_MULTI_GPU_MIN_BYTES", t.multi_gpu_min_bytes);
+    t.device_reserve = env_u64("HB_DEVICE_RESERVE", t.device_reserve);
+    t.pdl = env_u64("HB_PDL", 1) != 0;
+    t.small_n = env_u64("HB_SMALL_N", t.small_n);
+    t.direct_max_len = env_u64("HB_DIRECT_MAX_L", t.direct_max_len);
+    t.small_pair = env_u64("HB_SMALL_PAIR", 1) != 0;
+    t.dec_run = env_u64("HB_DEC_RUN", 1) != 0;
+    if (const char* v = getenv("HB_VARLEN_SORT")) t.varlen_sort = strcmp(v, "global") == 0 ? 0 : 1;
+#ifdef HB_AB
+    static const char* const kCfgNames[] = {"1x3", "2x2", "2x3", "ws2", "ws3", "1x2", "ws2x2", "ws3x2",
+                                            "ws3u", "ws3x2u", "ws3n"};
+    if (const char* v = getenv("HB_TMA_CFG"))
+        for (int k = 0; k < (int)(sizeof kCfgNames / sizeof *kCfgNames); ++k)
+            if (!strcmp(v, kCfgNames[k])) t.tma_cfg = k;
+    if (const char* v = getenv("HB_VARIANT"))
+        if (*v >= '0' && *v <= '3' && v[1] == '\0') t.variant = *v - '0';
+    if (t.tma_cfg >= 0) t.direct_max_len = env_u64("HB_DIRECT_MAX_L", 0);  // a forced tile applies to every width
+    t.tma_l2 = (uint32_t)env_u64("HB_TMA_L2", 256);
+    t.tma_evict_first = (uint32_t)env_u64("HB_TMA_EVICT_FIRST", 0);
+    t.small_kernel = !env_set("HB_NO_SMALL_KERNEL");
+    t.const_variant = env_set("HB_CONST_VARIANT") ? (int)env_u64("HB_CONST_VARIANT", 1) : -1;
+    t.small_cta = (uint32_t)env_u64("HB_SMALL_CTA", 128);
+    t.small_kernel_ab = t.const_variant == 0 || t.small_cta != 128;
+    t.dec_pair = env_set("HB_DEC_PAIR") ? (int)env_u64("HB_DEC_PAIR", 0) : -1;
+    t.fma_digits = env_u64("HB_FMA_DIGITS", 1) != 0;
+    t.dec_ab = t.dec_pair >= 0 || !t.fma_digits || t.const_variant >= 0;
+    t.sort_window = (uint32_t)env_u64("HB_SORT_WINDOW", 8192);
+    t.varlen_ld = (uint32_t)env_u64("HB_VARLEN_LD", 16);
+    t.varlen_q = (uint32_t)env_u64("HB_VARLEN_Q", 8);
+    t.varlen_prefetch = (uint32_t)env_u64("HB_VARLEN_PREFETCH", 0);
+    t.varlen_bulk = (uint32_t)env_u64("HB_VARLEN_BULK", 0);
+    t.vc_stages = env_set("HB_VC_STAGES") ? (int)env_u64("HB_VC_STAGES", 4) : -1;
+    t.vc_pf = (uint32_t)env_u64("HB_VC_PF", 256);
+#endif
+    return t;
+}
+
+static Tuning g_tuning;
+static std::once_flag g_tuning_once;
+const Tuning& tuning() {
+    std::call_once(g_tuning_once, [] { g_tuning = parse_tuning(); });
+    return g_tuning;
+}
+// Not synchronised against concurrent launches: call it between hash calls
+// (tests and A/B tools do, after changing the environment).
+void tuning_reload() {
+    tuning();
+    g_tuning = parse_tuning();
+}
+bool built_with_ab() {
+#ifdef HB_AB
+    return true;
+#else
+    return false;
+#endif
+}
+
+// ----------------------------------------------------------- bookkeeping --
 static std::atomic<uint64_t> g_launches{0};
+static thread_local const void* t_last_hash_kernel = nullptr;
 void note_launches(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+void note_launch(const void* kernel, bool hash_kernel) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (hash_kernel) t_last_hash_kernel = kernel;
+}
+const void* last_hash_kernel() { return t_last_hash_kernel; }
+void set_last_hash_kernel(const void* kernel) { t_last_hash_kernel = kernel; }
 uint64_t launches_total() { return g_launches.load(std::memory_order_relaxed); }
 
 __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __restrict__ offsets, uint64_t n,
@@ -177,11 +266,12 @@ cudaError_t launch_varlen_sort(int alg, const uint8_t* d_data, const uint64_t* d
     // Sort mode: windowed for MD5 (HBM-bound: locality wins), global for SHA-1/SM3
     // (ALU-bound: full (block count, alignment) uniformity wins); B200 A/B in
     // profiles/ab_varlen_r1b.txt.  $HB_VARLEN_SORT = window | global, $HB_SORT_WINDOW.
-    const char* sm = getenv("HB_VARLEN_SORT");
-    const bool window = sm ? strcmp(sm, "global") != 0 : alg == kMd5;
+    const Tuning& T = tuning();
+    const bool window = T.varlen_sort >= 0 ? T.varlen_sort == 1 : alg == kMd5;
     if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch && window) {
         uint32_t* p = static_cast<uint32_t*>(d_scratch) + kSortBuckets;
-        const uint64_t w = env_u64("HB_SORT_WINDOW", 8192);
+#ifdef HB_AB
+        const uint64_t w = T.sort_window;
         const bool q8 = qclasses == 8;
 #define HB_WIN(W)                                                                                            \
     q8 ? k_sort_window<W, 8><<<(unsigned)((n + W - 1) / W), 1024, 0, stream>>>(d_offsets, n, bias0, p)     \
@@ -193,7 +283,11 @@ cudaError_t launch_varlen_sort(int alg, const uint8_t* d_data, const uint64_t* d
         else
             HB_WIN(4096);
 #undef HB_WIN
-        note_launches(1);
+#else
+        (void)qclasses;
+        k_sort_window<8192, 4><<<(unsigned)((n + 8191) / 8192), 1024, 0, stream>>>(d_offsets, n, bias0, p);
+#endif
+        note_launch(nullptr, false);
         perm = p;
     } else if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch) {
         uint32_t* hist = static_cast<uint32_t*>(d_scratch);
@@ -311,7 +405,7 @@ cudaError_t launch_fill_random(uint8_t* d_buf, uint64_t nbytes, uint64_t seed, u
     uint64_t grid = (nwords + 255) / 256;
     if (grid > 148ull * 64) grid = 148ull * 64;
     k_fill_random<<<(unsigned)grid, 256, 0, stream>>>(d_buf, nbytes, seed, byte_offset / 8);
-    note_launches(1);
+    note_launch(nullptr, false);
     return cudaGetLastError();
 }
 
@@ -329,7 +423,7 @@ cudaError_t launch_decimal(int alg, uint64_t start, uint64_t count, int width, u
 cudaError_t launch_gen_decimal(uint64_t start, uint64_t count, int width, uint8_t* d_out, cudaStream_t stream) {
     if (count == 0) return cudaSuccess;
     k_gen_decimal<<<(unsigned)((count + 127) / 128), 128, 0, stream>>>(start, count, width, d_out);
-    note_launches(1);
+    note_launch(nullptr, false);
     return cudaGetLastError();
 }
 

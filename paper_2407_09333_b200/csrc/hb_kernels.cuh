@@ -35,18 +35,17 @@ PFN_encodeTiled get_encode_tiled();
 char* tma_error_buf();  // thread-local, 160 bytes
 constexpr size_t kTmaErrLen = 160;
 
-static inline uint64_t env_u64(const char* name, uint64_t dflt) {
-    const char* v = getenv(name);
-    return v ? strtoull(v, nullptr, 10) : dflt;
-}
 
 // Launch with programmatic stream serialization: the kernel may be scheduled
 // while the previous kernel in the stream drains; it orders itself with
-// griddepcontrol.wait.  $HB_PDL=0 launches normally (A/B).
+// griddepcontrol.wait.  tuning().pdl = false ($HB_PDL=0) launches normally.
+// Every launch is recorded (note_launch) so the C ABI can name the kernel
+// that actually ran (hb_last_kernel_name).
 template <class... KArgs, class... Args>
 static void launch_pdl_smem(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
                             bool pdl, Args... args) {
-    if (!pdl || !env_u64("HB_PDL", 1)) {
+    note_launch(reinterpret_cast<const void*>(kernel), true);
+    if (!pdl || !tuning().pdl) {
         kernel<<<grid, block, smem, s>>>(args...);
         return;
     }
@@ -66,6 +65,13 @@ static void launch_pdl_smem(void (*kernel)(KArgs...), unsigned grid, unsigned bl
 template <class... KArgs, class... Args>
 static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
     launch_pdl_smem(kernel, grid, block, 0, s, true, args...);
+}
+
+// Plain launch of a hash kernel, recorded like launch_pdl.
+template <class... KArgs, class... Args>
+static void launch_plain(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+    note_launch(reinterpret_cast<const void*>(kernel), true);
+    kernel<<<grid, block, 0, s>>>(static_cast<KArgs>(args)...);
 }
 
 // SMs of the current device (cached per device).
@@ -110,96 +116,6 @@ template <int ALG, int NB, int STAGES, int W = kTmaWarps> struct TmaOcc {  // CT
                   : (STAGES == 2 && ALG != kSm3 ? 6 : 4);
 };
 
-template <int ALG, int V, int NB, int STAGES, int W = kTmaWarps>
-__global__ void __launch_bounds__(W * 32, (TmaOcc<ALG, NB, STAGES, W>::kMinCtas))
-k_fixed_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG, V>;
-    using C = TmaCfg<NB, STAGES, W>;
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t row0 = (blockIdx.x * W + warp) * C::kRows;
-    if (row0 >= n) return;  // warp-uniform
-
-    // 1024-align the ring (the swizzle pattern is a function of address bits 7:8).
-    const uint32_t base_s = smem_u32(smem_raw);
-    uint8_t* ring = smem_raw + (((base_s + 1023u) & ~1023u) - base_s);
-    uint8_t* wring = ring + warp * (STAGES * C::kStageBytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + W * STAGES * C::kStageBytes) + warp * STAGES;
-
-    const uint32_t nload = (msg_len + 63u) >> 6;  // blocks holding message bytes
-    if (lane == 0) {
-        prefetch_tmap(&tmap);
-#pragma unroll
-        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
-        fence_mbar_init();
-        const uint32_t pro = nload < (uint32_t)STAGES ? nload : (uint32_t)STAGES;
-        for (uint32_t b = 0; b < pro; ++b) {
-            mbar_arrive_expect_tx(&bars[b], C::kStageBytes);
-            tma_load_2d(wring + b * C::kStageBytes, &tmap, &bars[b], (int)(b * 64u), (int)row0);
-        }
-    }
-    __syncwarp();
-
-    uint32_t st[NB][H::kStateWords];
-#pragma unroll
-    for (int q = 0; q < NB; ++q) H::init(st[q]);
-    // SWIZZLE_64B: the 16-byte chunk index is XORed with address bits 7:8, i.e.
-    // (row >> 1) & 3; rows lane and lane+32q share it.
-    const uint32_t swz = (lane >> 1) & 3u;
-    uint32_t stage = 0, phase = 0;
-    uint32_t raw[NB][16];
-    // Shared-memory byte offsets of this lane's four 16-byte chunks in stage 0;
-    // a stage adds a warp-uniform base, so each read is LDS.128 [R + UR].
-    uint32_t choff[NB][4];
-#pragma unroll
-    for (int q = 0; q < NB; ++q)
-#pragma unroll
-        for (uint32_t c = 0; c < 4; ++c) choff[q][c] = smem_u32(wring) + (lane + 32u * q) * 64u + ((c ^ swz) << 4);
-    auto read_stage = [&](uint32_t s) {
-        const uint32_t sbase = s * C::kStageBytes;
-#pragma unroll
-        for (int q = 0; q < NB; ++q) {
-#pragma unroll
-            for (uint32_t c = 0; c < 4; ++c) {
-                uint32_t x, y, z, w;
-                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
-                             : "r"(choff[q][c] + sbase)
-                             : "memory");
-                raw[q][4 * c + 0] = x; raw[q][4 * c + 1] = y; raw[q][4 * c + 2] = z; raw[q][4 * c + 3] = w;
-            }
-        }
-    };
-    const uint32_t nfull = msg_len >> 6;
-    for (uint32_t b = 0; b < nfull; ++b) {
-        mbar_wait_parity(&bars[stage], phase);
-        read_stage(stage);
-        H::template compress_n<NB>(st, raw);
-        __syncwarp();  // every lane has consumed this stage (its registers fed compress)
-        if (lane == 0 && b + STAGES < nload) {
-            fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&bars[stage], C::kStageBytes);
-            tma_load_2d(wring + stage * C::kStageBytes, &tmap, &bars[stage], (int)((b + STAGES) * 64u), (int)row0);
-        }
-        if (++stage == (uint32_t)STAGES) { stage = 0; phase ^= 1u; }
-    }
-    const uint32_t r = msg_len & 63u;
-    if (r) {  // partial data block: TMA zero-filled the columns >= msg_len
-        mbar_wait_parity(&bars[stage], phase);
-        read_stage(stage);
-    } else {  // padding-only final block (0x80, zeros, length)
-#pragma unroll
-        for (int q = 0; q < NB; ++q)
-#pragma unroll
-            for (int j = 0; j < 16; ++j) raw[q][j] = 0u;
-    }
-    md_finish_n<ALG, V, NB>(st, raw, r, msg_len);
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-        const uint32_t row = row0 + lane + 32u * q;
-        if (row < n) store_digest<ALG>(out + (uint64_t)row * H::kDigestBytes, st[q]);
-    }
-}
 
 // -------------------------------------------------------------------------
 // Warp-specialised variant: 4 compute warps + 1 producer warp per CTA.  The
@@ -637,323 +553,6 @@ k_varlen16(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint
         varlen16_message<ALG, PF, false>(w16, a, len, dend, out + i * H::kDigestBytes);
 }
 
-// -------------------------------------------------------------------------
-// Variable-length kernel, 256-bit loads (LDG.E.ENL2.256, sm_100).
-//
-// The 16-byte kernel is bound by the L1 data pipe: each LDG.128 of a warp
-// touches 32 scattered lines (one wavefront each), 4-5 per block.  A 256-bit
-// load moves the same line traffic in half the instructions, so each block
-// costs 2-3 wavefronts per lane instead of 4-5.  The message's 32-aligned
-// 96-byte window around block b is realigned by a word select over
-// q = (address >> 2) mod 8 (warp-uniform: the sort key uses 8 alignment
-// classes) and one funnel shift.  Loads never cross `data_end`: a chunk that
-// would (only possible for the batch's last message) is read word by word.
-// -------------------------------------------------------------------------
-__device__ __forceinline__ void ld256_nc(const uint32_t* p, uint32_t* w) {
-    asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
-                 : "l"(p));
-}
-
-// 32-byte chunk at p (32-aligned): bytes < lim are read, the rest are zero
-// (lim = min(message end, data_end) is only binding in the tail; full blocks
-// pass lim = data_end).
-__device__ __forceinline__ void load_chunk32(const uint8_t* p, uintptr_t lim, uint32_t* w) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    if (a + 32u <= lim) {
-        ld256_nc(reinterpret_cast<const uint32_t*>(p), w);
-    } else {
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            w[k] = (a + 4u * k < lim) ? __ldg(reinterpret_cast<const uint32_t*>(p) + k) : 0u;
-    }
-}
-
-__device__ __forceinline__ void realign32(const uint32_t (&c)[24], uint32_t q, uint32_t sh, uint32_t (&raw)[16]) {
-#define HB_RA(Q)                                                                    \
-    _Pragma("unroll") for (int j = 0; j < 16; ++j) raw[j] = __funnelshift_r(c[j + Q], c[j + Q + 1], sh);
-    switch (q) {
-    case 0: HB_RA(0) break;
-    case 1: HB_RA(1) break;
-    case 2: HB_RA(2) break;
-    case 3: HB_RA(3) break;
-    case 4: HB_RA(4) break;
-    case 5: HB_RA(5) break;
-    case 6: HB_RA(6) break;
-    default: HB_RA(7) break;
-    }
-#undef HB_RA
-}
-
-template <int ALG>
-__global__ void __launch_bounds__(128)
-k_varlen32(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
-           uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG>;
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const uint64_t i = perm ? (uint64_t)perm[t] : t;
-    const uint64_t start = offsets[i] - offset_base;
-    const uint64_t len = offsets[i + 1] - offsets[i];
-    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
-    const uint8_t* w32 = reinterpret_cast<const uint8_t*>(a & ~uintptr_t(31));
-    const uint32_t q = (uint32_t)(a >> 2) & 7u, sh = (uint32_t)(a & 3u) * 8u;
-    const bool misaligned = (a & 31u) != 0;
-    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
-    uint32_t st[H::kStateWords];
-    H::init(st);
-    uint32_t c[24];
-    uint32_t raw[16];
-    const uint64_t nfull = len >> 6;
-    for (uint64_t b = 0; b < nfull; ++b) {
-        const uint8_t* src = w32 + 64 * b;
-        load_chunk32(src, dend, c);
-        load_chunk32(src + 32, dend, c + 8);
-        if (misaligned) {
-            load_chunk32(src + 64, dend, c + 16);
-        } else {
-#pragma unroll
-            for (int k = 16; k < 24; ++k) c[k] = 0u;
-        }
-        realign32(c, q, sh, raw);
-        compress1<ALG>(st, raw);
-    }
-    // tail: the r = len % 64 remaining bytes (chunks overlapping [p, p + r) only)
-    const uint32_t r = (uint32_t)(len & 63u);
-    const uintptr_t mend = a + len;
-    const uintptr_t lim = mend < dend ? mend : dend;
-    const uint8_t* src = w32 + 64 * nfull;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        if (reinterpret_cast<uintptr_t>(src + 32 * k) < mend) {
-            load_chunk32(src + 32 * k, lim, c + 8 * k);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) c[8 * k + j] = 0u;
-        }
-    }
-    realign32(c, q, sh, raw);
-    mask_tail(raw, r);
-    md_finish<ALG>(st, raw, r, len);
-    store_digest<ALG>(out + i * H::kDigestBytes, st);
-}
-
-// -------------------------------------------------------------------------
-// Variable-length kernel, per-lane bulk copies (TMA engine).
-//
-// The per-thread kernel is bound by the L1 data pipe (ncu: LSU wavefronts at
-// 85 % of peak): every LDG.128 of a warp touches 32 scattered lines.  Here
-// each lane asks the TMA engine for its own message's 16-aligned window of
-// block b (<= 80 bytes, clipped at the message's last 16-byte chunk) with one
-// cp.async.bulk into its slot of a per-warp STAGES-deep ring; completion is
-// counted on the stage's mbarrier (32 arrivals + tx bytes).  Lanes then read
-// their slot with LDS.128 (conflict-free at an 80-byte stride), realign,
-// apply padding in registers and compress.  Opt-in ($HB_VARLEN_BULK): on the
-// B200 the TMA engine does not keep up with 32 tiny (<= 80 B) copies per warp
-// step -- 3.9-4.2 vs 2.06 ms for MD5 at configs[3] (profiles/ab_varlen_r1e.txt).
-// -------------------------------------------------------------------------
-template <int ALG, int STAGES, int MINB = 1>
-__global__ void __launch_bounds__(128, MINB)
-k_varlen_bulk(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offsets, uint64_t offset_base,
-              const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG>;
-    constexpr int kWarps = 4, kSlot = 80, kStage = 32 * kSlot;
-    __shared__ __align__(128) uint8_t ring[kWarps][STAGES][kStage];
-    __shared__ __align__(8) uint64_t bars[kWarps][STAGES];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t wbase = ((uint64_t)blockIdx.x * kWarps + warp) * 32u;
-    if (wbase >= n) return;  // warp-uniform
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < STAGES; ++k) mbar_init(&bars[warp][k], 32);
-        fence_mbar_init();
-    }
-    __syncwarp();
-    const uint64_t t = wbase + lane;
-    const bool live = t < n;
-    uint64_t i = 0, len = 0;
-    uintptr_t a = reinterpret_cast<uintptr_t>(data);
-    if (live) {
-        i = perm ? (uint64_t)perm[t] : t;
-        a = reinterpret_cast<uintptr_t>(data + (offsets[i] - offset_base));
-        len = offsets[i + 1] - offsets[i];
-    }
-    const uint32_t nb = live ? (uint32_t)((len + 8u) / 64u + 1u) : 0u;  // blocks incl. padding
-    const uint32_t nfull = (uint32_t)(len >> 6);
-    const uint32_t nbmax = __reduce_max_sync(0xFFFFFFFFu, nb);
-    const uintptr_t w16 = a & ~uintptr_t(15);
-    const uintptr_t end16 = (a + len + 15u) & ~uintptr_t(15);  // message bytes live in [w16, end16)
-    const uint32_t slot = smem_u32(&ring[warp][0][0]) + lane * kSlot;
-    auto issue = [&](uint32_t b) {
-        const uint32_t s = b % STAGES;
-        const uintptr_t ws = w16 + 64u * (uintptr_t)b;
-        // only blocks holding message bytes are fetched (b <= nfull); at most 80 bytes
-        const uint32_t bytes = (b > nfull || ws >= end16) ? 0u
-                               : (end16 - ws >= 80u ? 80u : (uint32_t)(end16 - ws));
-        mbar_arrive_expect_tx(&bars[warp][s], bytes);
-        if (bytes) bulk_copy_g2s(slot + s * kStage, reinterpret_cast<const void*>(ws), bytes, &bars[warp][s]);
-    };
-#pragma unroll
-    for (int k = 0; k < STAGES - 1; ++k)
-        if ((uint32_t)k < nbmax) issue(k);
-
-    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
-    const uint32_t r = (uint32_t)(len & 63u);
-    const uint64_t bits = len * 8ull;
-    const uint32_t l14 = H::kBigEndian ? bswap((uint32_t)(bits >> 32)) : (uint32_t)bits;
-    const uint32_t l15 = H::kBigEndian ? bswap((uint32_t)bits) : (uint32_t)(bits >> 32);
-    uint32_t st[H::kStateWords];
-    H::init(st);
-    for (uint32_t b = 0; b < nbmax; ++b) {
-        if (b + STAGES - 1 < nbmax) {
-            fence_proxy_async_smem();  // this lane's generic reads of the stage happened before (syncwarp below)
-            issue(b + STAGES - 1);
-        }
-        const uint32_t s = b % STAGES;
-        mbar_wait_parity(&bars[warp][s], (b / STAGES) & 1u);
-        uint32_t c[20];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            uint32_t x, y, z, w;
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
-                         : "r"(slot + s * kStage + 16u * k)
-                         : "memory");
-            c[4 * k] = x; c[4 * k + 1] = y; c[4 * k + 2] = z; c[4 * k + 3] = w;
-        }
-        __syncwarp();  // every lane has read stage s before it is refilled
-        if (b < nb) {
-            uint32_t raw[16];
-            realign16(c, q, sh, raw);
-            if (b >= nfull) {  // the last one or two blocks: keep bytes [0, r) (none after), 0x80, length
-                mask_tail(raw, b == nfull ? r : 0u);
-                const uint32_t pad = b == nfull ? 0x80u << ((r & 3u) * 8u) : 0u, pw = r >> 2;
-#pragma unroll
-                for (int j = 0; j < 16; ++j) raw[j] |= (pw == (uint32_t)j) ? pad : 0u;
-                if (b == nb - 1u) { raw[14] = l14; raw[15] = l15; }
-            }
-            compress1<ALG>(st, raw);
-        }
-    }
-    if (live) store_digest<ALG>(out + i * H::kDigestBytes, st);
-}
-
-// -------------------------------------------------------------------------
-// Variable-length kernel, warp-cooperative staging (the default).
-//
-// A warp owns 32 messages (after the length sort: equal block counts and the
-// same word alignment).  Per 64-byte step every message needs the 80-byte
-// 16-aligned window around its block: 32 x 5 = 160 16-byte chunks.  Lane l
-// copies chunks c = l + 32j (j < 5) -- message c/5, chunk c%5 -- with
-// cp.async (zero-filled past the message end), so five consecutive lanes
-// fetch one message's 80 contiguous bytes: each warp instruction touches ~7
-// messages instead of 32 (per-thread LDG.128 touches 32 lines per
-// instruction and the L1 tag stage, not HBM, was the limit for MD5).  Chunks
-// land in a STAGES-deep per-warp ring (slot m at m*80: conflict-free
-// LDS.128 reads); the owner lane realigns its window (word select + funnel
-// shift) and compresses.  Padding is applied in registers on the last one
-// or two blocks (bytes past the end arrive as zeros), so there is one
-// compress call site and the loop runs to the warp's largest block count.
-// -------------------------------------------------------------------------
-constexpr int kVcWarps = 4;
-constexpr int kVcSlot = 80;                   // bytes per message per stage
-constexpr int kVcWarpStage = 32 * kVcSlot;    // 2,560 bytes
-
-// STAGES-deep ring (smem 10 KiB per stage per CTA), MINB CTAs/SM register
-// target, PF = L2 prefetch size of the cp.async copies.
-template <int ALG, int STAGES = 4, int MINB = 5, int PF = 256>
-__global__ void __launch_bounds__(kVcWarps * 32, MINB)
-k_varlen_coop(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offsets, uint64_t offset_base,
-              const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
-    using H = HashAlg<ALG>;
-    __shared__ __align__(128) uint8_t ring[kVcWarps][STAGES][kVcWarpStage];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t wbase = ((uint64_t)blockIdx.x * kVcWarps + warp) * 32u;
-    if (wbase >= n) return;  // warp-uniform
-    const uint64_t t = wbase + lane;
-    const bool live = t < n;
-    uint64_t i = 0, len = 0;
-    uintptr_t a = reinterpret_cast<uintptr_t>(data);
-    if (live) {
-        i = perm ? (uint64_t)perm[t] : t;
-        a = reinterpret_cast<uintptr_t>(data + (offsets[i] - offset_base));
-        len = offsets[i + 1] - offsets[i];
-    }
-    const uint32_t nb = live ? (uint32_t)((len + 8u) / 64u + 1u) : 0u;   // blocks incl. padding
-    const uint32_t nfull = (uint32_t)(len >> 6);
-    const uint32_t nbmax = __reduce_max_sync(0xFFFFFFFFu, nb);
-
-    // This lane's five copy slots: source message m = c/5, chunk k = c%5.
-    uintptr_t src0[5];
-    int64_t avail0[5];  // bytes of the chunk inside the message at step 0 (minus 64 per step)
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-        const uint32_t c = lane + 32u * j, m = c / 5u, k = c % 5u;
-        const uintptr_t am = __shfl_sync(0xFFFFFFFFu, a, m);
-        const uint64_t lm = __shfl_sync(0xFFFFFFFFu, len, m);
-        src0[j] = (am & ~uintptr_t(15)) + 16u * k;
-        const bool need = (k < 4u) || (am & 15u);  // chunk 4 only for a misaligned window
-        avail0[j] = (need && lm) ? (int64_t)lm + (int64_t)(am & 15u) - 16 * (int64_t)k : INT64_MIN / 2;
-    }
-    uint8_t* wring = &ring[warp][0][0];
-    const uint32_t sring = smem_u32(wring);
-    auto issue = [&](uint32_t b) {
-        const uint32_t sdst = sring + (b % STAGES) * kVcWarpStage;
-#pragma unroll
-        for (int j = 0; j < 5; ++j) {
-            const int64_t av = avail0[j] - 64 * (int64_t)b;
-            const uint32_t sz = av <= 0 ? 0u : av >= 16 ? 16u : (uint32_t)av;
-            const uintptr_t src = sz ? src0[j] + 64u * (uintptr_t)b : reinterpret_cast<uintptr_t>(data);
-            cp_async16_zfill<PF>(sdst + 16u * (lane + 32u * j), reinterpret_cast<const void*>(src), sz);
-        }
-    };
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if ((uint32_t)s < nbmax) issue(s);
-        cp_async_commit();
-    }
-
-    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
-    const uint32_t r = (uint32_t)(len & 63u);
-    const uint64_t bits = len * 8ull;
-    const uint32_t l14 = H::kBigEndian ? bswap((uint32_t)(bits >> 32)) : (uint32_t)bits;
-    const uint32_t l15 = H::kBigEndian ? bswap((uint32_t)bits) : (uint32_t)(bits >> 32);
-    uint32_t st[H::kStateWords];
-    H::init(st);
-    const uint32_t slot = smem_u32(wring) + lane * kVcSlot;
-    for (uint32_t b = 0; b < nbmax; ++b) {
-        if (b + STAGES - 1 < nbmax) issue(b + STAGES - 1);
-        cp_async_commit();
-        cp_async_wait<STAGES - 1>();  // this lane's copies of step b have landed
-        __syncwarp();                    // ... and every other lane's
-        uint32_t c[20];
-        const uint32_t sbase = slot + (b % STAGES) * kVcWarpStage;
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            uint32_t x, y, z, w;
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
-                         : "r"(sbase + 16u * k)
-                         : "memory");
-            c[4 * k] = x; c[4 * k + 1] = y; c[4 * k + 2] = z; c[4 * k + 3] = w;
-        }
-        __syncwarp();  // the stage may be refilled from the next iteration on
-        if (b < nb) {
-            uint32_t raw[16];
-            realign16(c, q, sh, raw);
-            if (b >= nfull) {  // the final one or two blocks: 0x80, zero fill, bit length
-                if (b == nfull) {
-                    const uint32_t pad = 0x80u << ((r & 3u) * 8u), pw = r >> 2;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) raw[j] |= (pw == (uint32_t)j) ? pad : 0u;
-                }
-                if (b == nb - 1u) { raw[14] = l14; raw[15] = l15; }
-            }
-            compress1<ALG>(st, raw);
-        }
-    }
-    if (live) store_digest<ALG>(out + i * H::kDigestBytes, st);
-}
 
 // ---------------------------------------------------- length-bucket sort --
 // Counting sort of message indices by block count, longest first.  Three
@@ -1127,6 +726,15 @@ __global__ void __launch_bounds__(128) k_decimal_run(uint64_t start, uint64_t co
     }
 }
 
+// =========================================================================
+// Host-side launchers.  Every knob comes from tuning() (parsed once from the
+// environment when the library loads, hb_tuning_reload() re-reads it), so a
+// launch costs no getenv/strcmp.  The default build instantiates only the
+// tuned kernel shapes; the A/B arms measured in profiles/ (per-warp TMA rings,
+// other tile configurations and round variants, the 32-byte / bulk-copy /
+// cooperative varlen kernels) exist only in a -DHB_AB build (hb_ab_kernels.cuh).
+// =========================================================================
+
 // Run `set` (a cudaFuncSetAttribute call) once per device: kernel attributes
 // such as the dynamic shared-memory limit are per device, so a process driving
 // several GPUs must set them on each (a process-wide call_once would not).
@@ -1142,75 +750,48 @@ static cudaError_t set_smem_attr_once(std::atomic<uint64_t>& done, F set) {
     return e;
 }
 
-template <int ALG, int V, int NB, int STAGES, int W = kTmaWarps>
-static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
-                                        cudaStream_t stream) {
-    using C = TmaCfg<NB, STAGES, W>;
+// The (n, L) byte matrix as a 2-D TMA tensor: dim0 = bytes of a row
+// (contiguous), dim1 = rows with stride L.  Box = one 64-byte block of `rows`
+// rows, 64-byte swizzle, L2 promotion `l2` bytes.
+static cudaError_t encode_rows_map(CUtensorMap* map, const uint8_t* d_msgs, uint32_t n, uint32_t L, uint32_t rows,
+                                   uint32_t l2) {
     PFN_encodeTiled enc = get_encode_tiled();
     if (!enc) {
         snprintf(tma_error_buf(), kTmaErrLen, "cuTensorMapEncodeTiled unavailable");
         return cudaErrorNotSupported;
     }
-    // The (n, L) byte matrix as a 2-D tensor: dim0 = bytes of a row (contiguous),
-    // dim1 = rows with stride L.  Box = one 64-byte block of kRows rows.
-    CUtensorMap map;
     const cuuint64_t dims[2] = {L, n};
     const cuuint64_t strides[1] = {L};
-    const cuuint32_t box[2] = {64, (cuuint32_t)C::kRows};
+    const cuuint32_t box[2] = {64, rows};
     const cuuint32_t estr[2] = {1, 1};
-    CUresult rc = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_msgs), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const CUtensorMapL2promotion prom = l2 == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                        : l2 == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                        : l2 == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                    : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    const CUresult rc = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_msgs), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, prom,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (rc != CUDA_SUCCESS) {
         snprintf(tma_error_buf(), kTmaErrLen, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)rc);
         return cudaErrorInvalidValue;
     }
-    static std::atomic<uint64_t> attr_done{0};  // function attributes are per device
-    const cudaError_t attr_rc = set_smem_attr_once(attr_done, [] {
-        return cudaFuncSetAttribute(k_fixed_tma<ALG, V, NB, STAGES, W>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    });
-    if (attr_rc != cudaSuccess) return attr_rc;
-    const uint32_t rows_per_cta = W * C::kRows;
-    const uint32_t grid = (n + rows_per_cta - 1) / rows_per_cta;
-    k_fixed_tma<ALG, V, NB, STAGES, W><<<grid, W * 32, C::kSmem, stream>>>(map, n, L, d_out);
-    note_launches(1);
-    return cudaGetLastError();
+    return cudaSuccess;
 }
 
 template <int ALG, int V, int NB, int STAGES, bool UNR = false, bool SLACK = true>
 static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
                                        cudaStream_t stream) {
     using C = WsCfg<NB, STAGES, SLACK>;
-    PFN_encodeTiled enc = get_encode_tiled();
-    if (!enc) {
-        snprintf(tma_error_buf(), kTmaErrLen, "cuTensorMapEncodeTiled unavailable");
-        return cudaErrorNotSupported;
-    }
+    const Tuning& T = tuning();
     CUtensorMap map;
-    const cuuint64_t dims[2] = {L, n};
-    const cuuint64_t strides[1] = {L};
-    const cuuint32_t box[2] = {64, (cuuint32_t)C::kRows};
-    const cuuint32_t estr[2] = {1, 1};
-    // A/B knobs: $HB_TMA_L2 = L2 promotion (0 / 64 / 128 / 256 bytes, default 256),
-    // $HB_TMA_EVICT_FIRST = evict-first L2 policy on the message loads.
-    const uint64_t l2 = env_u64("HB_TMA_L2", 256);
-    const CUtensorMapL2promotion prom = l2 == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                                        : l2 == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                                        : l2 == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                                                    : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    CUresult rc = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_msgs), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (rc != CUDA_SUCCESS) {
-        snprintf(tma_error_buf(), kTmaErrLen, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)rc);
-        return cudaErrorInvalidValue;
-    }
+    cudaError_t e = encode_rows_map(&map, d_msgs, n, L, (uint32_t)C::kRows, T.tma_l2);
+    if (e != cudaSuccess) return e;
     static std::atomic<uint64_t> attr_done{0};  // function attributes are per device
-    const cudaError_t attr_rc = set_smem_attr_once(attr_done, [] {
+    e = set_smem_attr_once(attr_done, [] {
         return cudaFuncSetAttribute(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     });
-    if (attr_rc != cudaSuccess) return attr_rc;
+    if (e != cudaSuccess) return e;
     const uint32_t grid = (n + C::kRows - 1) / C::kRows;
     // PDL pays for short kernels (launch gap hidden: +5-17 %) and for grids
     // that fill every SM anyway.  A sub-wave grid of long messages is bound by
@@ -1218,190 +799,80 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     // SM there and run up to 30 % slower (profiles/ab_pdl_r1.txt), so those
     // launch normally.
     const bool pdl = grid >= (uint32_t)device_sms() || (L + 8u) / 64u + 1u <= 17u;
-    launch_pdl_smem(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK>, grid, (kWsComputeWarps + 1) * 32, C::kSmem, stream,
-                    pdl, map, n, L, d_out, (uint32_t)env_u64("HB_TMA_EVICT_FIRST", 0));
-    note_launches(1);
+    launch_pdl_smem(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK>, grid, (kWsComputeWarps + 1) * 32, C::kSmem,
+                    stream, pdl, map, n, L, d_out, (uint32_t)T.tma_evict_first);
     return cudaGetLastError();
 }
 
-// Tile configuration and round variant.  Defaults are the B200-measured best
-// (profiles/variant_sweep_r1*.txt); $HB_TMA_CFG ("1x3", "2x2", "2x3" =
-// messages-per-thread x ring stages) and $HB_VARIANT (0-3) override them for
-// A/B experiments.
-enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4, kCfg1x2 = 5, kCfgWs2x2 = 6, kCfgWs3x2 = 7,
-                kCfgWs3u = 8, kCfgWs3x2u = 9, kCfgWs3n = 10 };
-// B200-measured (profiles/variant_sweep_r1d.txt and _r1e.txt, interleaved
-// rounds): the warp-specialised 3-stage ring is best for MD5 and SM3 (SM3's
-// 61 registers make two messages per thread lose occupancy); SHA-1 gains 4 %
-// from two messages per thread (ws3x2: 7.38 vs 7.69 ms at 2^24 x 1 KiB).
-template <int ALG> struct DefaultTmaCfg { static constexpr int value = ALG == kSha1 ? kCfgWs3x2 : kCfgWs3; };
+#ifdef HB_AB
+#include "hb_ab_kernels.cuh"
+#endif
 
-static int tma_variant(int alg) {
-    const char* v = getenv("HB_VARIANT");
-    if (v && *v >= '0' && *v <= '3' && v[1] == '\0') return *v - '0';
-    switch (alg) {
-    case kSha1: return DefaultVariant<kSha1>::value;
-    case kMd5: return DefaultVariant<kMd5>::value;
-    default: return DefaultVariant<kSm3>::value;
-    }
-}
-
-static int tma_cfg(int alg) {
-    const char* v = getenv("HB_TMA_CFG");
-    if (v && !strcmp(v, "1x3")) return kCfg1x3;
-    if (v && !strcmp(v, "2x2")) return kCfg2x2;
-    if (v && !strcmp(v, "2x3")) return kCfg2x3;
-    if (v && !strcmp(v, "ws2")) return kCfgWs2;
-    if (v && !strcmp(v, "1x2")) return kCfg1x2;
-    if (v && !strcmp(v, "ws3")) return kCfgWs3;
-    if (v && !strcmp(v, "ws2x2")) return kCfgWs2x2;
-    if (v && !strcmp(v, "ws3x2")) return kCfgWs3x2;
-    if (v && !strcmp(v, "ws3u")) return kCfgWs3u;
-    if (v && !strcmp(v, "ws3x2u")) return kCfgWs3x2u;
-    if (v && !strcmp(v, "ws3n")) return kCfgWs3n;
-    switch (alg) {
-    case kSha1: return DefaultTmaCfg<kSha1>::value;
-    case kMd5: return DefaultTmaCfg<kMd5>::value;
-    default: return DefaultTmaCfg<kSm3>::value;
-    }
-}
-
-// Shape selection by batch geometry (B200-measured, profiles/ab_small_r1.txt):
-//  * fewer than $HB_SMALL_N (default 2^18) messages: one message per thread
-//    (NB=1) so the grid still covers all SMs -- SHA-1's tuned NB=2 tiles
-//    halve the CTA count (4096 x 64 KiB: 251 vs 428 GB/s);
-//  * messages of <= $HB_DIRECT_MAX_L (default 128) bytes: the direct
-//    per-thread-load kernel (one or two blocks per message, the 8 KiB TMA
-//    stage would be mostly padding: MD5 2^24 x 16 B 1121 vs 683 GB/s).
-static uint64_t small_n_threshold() { return env_u64("HB_SMALL_N", 1ull << 18); }
-static uint64_t direct_max_len() { return env_u64("HB_DIRECT_MAX_L", 128); }
-
+// Default tile per algorithm (B200-measured, profiles/variant_sweep_r1d.txt and
+// _r1e.txt, interleaved rounds): the warp-specialised 3-stage ring with round
+// variant 1 for MD5 and SM3 (SM3's 61 registers make two messages per thread
+// lose occupancy); SHA-1 gains 4 % from two messages per thread (7.38 vs
+// 7.69 ms at 2^24 x 1 KiB).  Below tuning().small_n messages (2^18) one
+// message per thread so the grid still covers every SM (SHA-1's NB=2 tiles
+// halve the CTA count: 4096 x 64 KiB 251 vs 428 GB/s, profiles/ab_small_r1.txt).
 template <int ALG>
 static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t L, uint8_t* dst, cudaStream_t s) {
-    const int cfg = tma_cfg(ALG);
-    const int v = tma_variant(ALG);
-    if (!getenv("HB_TMA_CFG") && (uint64_t)n < small_n_threshold())
-        return launch_fixed_tma_ws<ALG, DefaultVariant<ALG>::value, 1, 3>(src, n, L, dst, s);
-    if (cfg == kCfg1x2) {
-        switch (v) {
-        case 0: return launch_fixed_tma_alg<ALG, 0, 1, 2>(src, n, L, dst, s);
-        default: return launch_fixed_tma_alg<ALG, 1, 1, 2>(src, n, L, dst, s);
+#ifdef HB_AB
+    if (tuning().tma_cfg >= 0 || tuning().variant >= 0) return launch_tma_ab<ALG>(src, n, L, dst, s);
+#endif
+    if ((uint64_t)n < tuning().small_n || ALG != kSha1)
+        return launch_fixed_tma_ws<ALG, kVarBal, 1, 3>(src, n, L, dst, s);
+    return launch_fixed_tma_ws<ALG, kVarBal, 2, 3>(src, n, L, dst, s);
+}
+
+// Compile-time-width kernel for L in {16, 32, 48, 64, 128}; MD5 one-block
+// rows (<= 32 B) in batches >= 2^20 take two adjacent rows per thread (+3-4 %;
+// 48-byte rows lose 2 %, two-block rows 1-9 %, profiles/ab_small_r1d.txt).
+template <int ALG, int L>
+static void launch_small(const uint8_t* d_msgs, uint64_t n, uint8_t* d_out, cudaStream_t s) {
+    constexpr unsigned kBlk = 128;
+    if constexpr (ALG == kMd5 && L <= 32) {
+        if (n >= (1ull << 20) && tuning().small_pair) {
+            launch_pdl(k_fixed_small<ALG, L, kVarBal, 2>, (unsigned)(((n + 1) / 2 + kBlk - 1) / kBlk), kBlk, s,
+                       d_msgs, n, d_out);
+            return;
         }
     }
-    if (cfg == kCfgWs2) {
-        switch (v) {
-        case 0: return launch_fixed_tma_ws<ALG, 0, 1, 2>(src, n, L, dst, s);
-        default: return launch_fixed_tma_ws<ALG, 1, 1, 2>(src, n, L, dst, s);
-        }
-    }
-    if (cfg == kCfgWs3) {
-        switch (v) {
-        case 0: return launch_fixed_tma_ws<ALG, 0, 1, 3>(src, n, L, dst, s);
-        case 2: return launch_fixed_tma_ws<ALG, 2, 1, 3>(src, n, L, dst, s);
-        case 3: return launch_fixed_tma_ws<ALG, 3, 1, 3>(src, n, L, dst, s);
-        default: return launch_fixed_tma_ws<ALG, 1, 1, 3>(src, n, L, dst, s);
-        }
-    }
-    if (cfg == kCfgWs3u) return launch_fixed_tma_ws<ALG, DefaultVariant<ALG>::value, 1, 3, true>(src, n, L, dst, s);
-    if (cfg == kCfgWs3n)
-        return launch_fixed_tma_ws<ALG, DefaultVariant<ALG>::value, 1, 3, false, false>(src, n, L, dst, s);
-    if (cfg == kCfgWs3x2u) return launch_fixed_tma_ws<ALG, DefaultVariant<ALG>::value, 2, 3, true>(src, n, L, dst, s);
-    if (cfg == kCfgWs2x2) {
-        switch (v) {
-        case 3: return launch_fixed_tma_ws<ALG, 3, 2, 2>(src, n, L, dst, s);
-        default: return launch_fixed_tma_ws<ALG, 1, 2, 2>(src, n, L, dst, s);
-        }
-    }
-    if (cfg == kCfgWs3x2) {
-        switch (v) {
-        case 3: return launch_fixed_tma_ws<ALG, 3, 2, 3>(src, n, L, dst, s);
-        default: return launch_fixed_tma_ws<ALG, 1, 2, 3>(src, n, L, dst, s);
-        }
-    }
-    if (cfg == kCfg2x2) {
-        switch (v) {
-        case 0: return launch_fixed_tma_alg<ALG, 0, 2, 2>(src, n, L, dst, s);
-        case 2: return launch_fixed_tma_alg<ALG, 2, 2, 2>(src, n, L, dst, s);
-        default: return launch_fixed_tma_alg<ALG, 1, 2, 2>(src, n, L, dst, s);
-        }
-    }
-    if (cfg == kCfg2x3) {
-        switch (v) {
-        case 0: return launch_fixed_tma_alg<ALG, 0, 2, 3>(src, n, L, dst, s);
-        case 2: return launch_fixed_tma_alg<ALG, 2, 2, 3>(src, n, L, dst, s);
-        default: return launch_fixed_tma_alg<ALG, 1, 2, 3>(src, n, L, dst, s);
-        }
-    }
-    switch (v) {
-    case 0: return launch_fixed_tma_alg<ALG, 0, 1, 3>(src, n, L, dst, s);
-    case 2: return launch_fixed_tma_alg<ALG, 2, 1, 3>(src, n, L, dst, s);
-    case 3: return launch_fixed_tma_alg<ALG, 3, 1, 3>(src, n, L, dst, s);
-    default: return launch_fixed_tma_alg<ALG, 1, 1, 3>(src, n, L, dst, s);
-    }
+    launch_pdl(k_fixed_small<ALG, L, kVarBal>, (unsigned)((n + kBlk - 1) / kBlk), kBlk, s, d_msgs, n, d_out);
 }
 
 template <int ALG>
 static cudaError_t launch_fixed_alg(const uint8_t* d_msgs, uint64_t n, uint64_t L, uint8_t* d_out,
                                     cudaStream_t stream, uint32_t flags) {
     using H = HashAlg<ALG>;
+    const Tuning& T = tuning();
     const bool aligned = L > 0 && (L % 16) == 0 && (reinterpret_cast<uintptr_t>(d_msgs) % 16) == 0 &&
                          L < (1ull << 31);
-    const bool direct = (flags & HB_FLAG_NO_TMA) || (!getenv("HB_TMA_CFG") && L <= direct_max_len());
+    const bool direct = (flags & HB_FLAG_NO_TMA) || L <= T.direct_max_len;
     if (aligned && !direct) {
         // TMA coordinates are int32: split very large batches into row slabs.
         const uint64_t slab = 1ull << 30;
         for (uint64_t r0 = 0; r0 < n; r0 += slab) {
             const uint64_t rn = (n - r0) < slab ? (n - r0) : slab;
-            const uint8_t* src = d_msgs + r0 * L;
-            uint8_t* dst = d_out + r0 * H::kDigestBytes;
-            const cudaError_t e = launch_tma_dispatch<ALG>(src, (uint32_t)rn, (uint32_t)L, dst, stream);
+            const cudaError_t e = launch_tma_dispatch<ALG>(d_msgs + r0 * L, (uint32_t)rn, (uint32_t)L,
+                                                           d_out + r0 * H::kDigestBytes, stream);
             if (e != cudaSuccess) return e;
         }
         return cudaSuccess;
     }
-    const uint64_t grid = (n + 127) / 128;
-    const bool small_ok = aligned && !getenv("HB_NO_SMALL_KERNEL");
-    // Pipe-balanced rounds (default) or the plain ones ($HB_CONST_VARIANT=0):
-    // folding the constant padding words does not pay for the lost ALU/FMA
-    // balance (B200: MD5 16 B 1366 vs 1262 GB/s, profiles/ab_small_r1c.txt).
-    const bool small_v1 = env_u64("HB_CONST_VARIANT", 1) == 1;
-    // CTA size of the compile-time-width kernel ($HB_SMALL_CTA: 32..128; A/B for
-    // small batches, where fewer threads per CTA spread a batch over more SMs)
-    uint64_t sb = env_u64("HB_SMALL_CTA", 128);
-    const unsigned sblk = sb >= 128 ? 128u : sb >= 64 ? 64u : 32u;  // __launch_bounds__(128)
-    const unsigned sgrid = (unsigned)((n + sblk - 1) / sblk);
-    // two rows per thread for MD5 one-block messages (L <= 32) in batches
-    // large enough that halving the thread count still fills the GPU: +3-4 %;
-    // 48-byte rows (near the HBM bound) lose 2 %, two-block rows 1-9 % (profiles/ab_small_r1d.txt)
-    const bool pair = ALG == kMd5 && n >= (1ull << 20) && L <= 32 && env_u64("HB_SMALL_PAIR", 1);
-    const unsigned sgrid2 = (unsigned)(((n + 1) / 2 + sblk - 1) / sblk);
-    if (small_ok && L == 16) {
-        small_v1 ? (pair ? launch_pdl(k_fixed_small<ALG, 16, kVarBal, 2>, sgrid2, sblk, stream, d_msgs, n, d_out)
-                         : launch_pdl(k_fixed_small<ALG, 16, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out))
-                 : launch_pdl(k_fixed_small<ALG, 16, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
-    } else if (small_ok && L == 32) {
-        small_v1 ? (pair ? launch_pdl(k_fixed_small<ALG, 32, kVarBal, 2>, sgrid2, sblk, stream, d_msgs, n, d_out)
-                         : launch_pdl(k_fixed_small<ALG, 32, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out))
-                 : launch_pdl(k_fixed_small<ALG, 32, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
-    } else if (small_ok && L == 48) {
-        small_v1 ? (pair ? launch_pdl(k_fixed_small<ALG, 48, kVarBal, 2>, sgrid2, sblk, stream, d_msgs, n, d_out)
-                         : launch_pdl(k_fixed_small<ALG, 48, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out))
-                 : launch_pdl(k_fixed_small<ALG, 48, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
-    } else if (small_ok && L == 64) {
-        small_v1 ? (pair ? launch_pdl(k_fixed_small<ALG, 64, kVarBal, 2>, sgrid2, sblk, stream, d_msgs, n, d_out)
-                         : launch_pdl(k_fixed_small<ALG, 64, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out))
-                 : launch_pdl(k_fixed_small<ALG, 64, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
-    } else if (small_ok && L == 128) {
-        small_v1 ? (pair ? launch_pdl(k_fixed_small<ALG, 128, kVarBal, 2>, sgrid2, sblk, stream, d_msgs, n, d_out)
-                         : launch_pdl(k_fixed_small<ALG, 128, kVarBal>, sgrid, sblk, stream, d_msgs, n, d_out))
-                 : launch_pdl(k_fixed_small<ALG, 128, kVarPlain>, sgrid, sblk, stream, d_msgs, n, d_out);
-    } else if (aligned) {
-        k_fixed_direct<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, n, (uint32_t)L, d_out);
-    } else {
-        k_generic<ALG, false><<<(unsigned)grid, 128, 0, stream>>>(d_msgs, d_msgs + n * L, nullptr, 0, nullptr, L, n,
-                                                                  d_out);
-    }
-    note_launches(1);
+#ifdef HB_AB
+    if (aligned && T.small_kernel_ab) return launch_small_ab<ALG>(d_msgs, n, L, d_out, stream);
+#endif
+    const unsigned grid = (unsigned)((n + 127) / 128);
+    const bool small_ok = aligned && T.small_kernel;
+    if (small_ok && L == 16) launch_small<ALG, 16>(d_msgs, n, d_out, stream);
+    else if (small_ok && L == 32) launch_small<ALG, 32>(d_msgs, n, d_out, stream);
+    else if (small_ok && L == 48) launch_small<ALG, 48>(d_msgs, n, d_out, stream);
+    else if (small_ok && L == 64) launch_small<ALG, 64>(d_msgs, n, d_out, stream);
+    else if (small_ok && L == 128) launch_small<ALG, 128>(d_msgs, n, d_out, stream);
+    else if (aligned) launch_plain(k_fixed_direct<ALG>, grid, 128, stream, d_msgs, n, (uint32_t)L, d_out);
+    else launch_plain(k_generic<ALG, false>, grid, 128, stream, d_msgs, d_msgs + n * L,
+                      (const uint64_t*)nullptr, (uint64_t)0, (const uint32_t*)nullptr, L, n, d_out);
     return cudaGetLastError();
 }
 
@@ -1409,103 +880,43 @@ template <int ALG>
 static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes, const uint64_t* d_offsets,
                                      uint64_t offset_base, uint64_t n, uint8_t* d_out, void* d_scratch,
                                      cudaStream_t stream, uint32_t flags) {
-    // 256-bit-load kernel: opt-in ($HB_VARLEN_LD=32; its sort uses 8 alignment
-    // classes).  It relieves the L1 data pipe but the 8-class sort splits a
-    // window's warps over more (block count, alignment) buckets: MD5 at
-    // configs[3] 2.24-2.28 vs 2.03 ms for the 16-byte kernel (ab_varlen_r1g.txt).
-    const bool special = (flags & (HB_FLAG_VARLEN_WORDS | HB_FLAG_VARLEN_COOP | HB_FLAG_VARLEN_COOP_OFF)) ||
-                         env_u64("HB_VARLEN_BULK", 0) || env_u64("HB_VARLEN_PREFETCH", 0);
-    const bool wide = !special && env_u64("HB_VARLEN_LD", 16) == 32;
+#ifdef HB_AB
+    if (varlen_ab_selected(flags)) return launch_varlen_ab<ALG>(d_data, data_bytes, d_offsets, offset_base, n, d_out,
+                                                                d_scratch, stream, flags);
+#endif
+    if (flags & (HB_FLAG_VARLEN_WORDS | HB_FLAG_VARLEN_COOP)) {
+        snprintf(tma_error_buf(), kTmaErrLen, "A/B varlen kernel flags need a -DHB_AB build");
+        return cudaErrorInvalidValue;
+    }
     const uint32_t* perm = nullptr;
-    {
-        const int qcls = wide ? (int)env_u64("HB_VARLEN_Q", 8) : 4;  // A/B: 4-class sort with the wide kernel
-        const cudaError_t e = launch_varlen_sort(ALG, d_data, d_offsets, offset_base, n, d_scratch, stream, flags,
-                                                 &perm, qcls == 4 ? 4 : 8);
-        if (e != cudaSuccess) return e;
-    }
-    const uint64_t grid = (n + 127) / 128;
-    if (wide) {
-        k_varlen32<ALG><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets, offset_base, perm,
-                                                            n, d_out);
-    } else if (flags & HB_FLAG_VARLEN_WORDS) {  // A/B baseline: per-thread 32-bit loads
-        k_generic<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets,
-                                                                 offset_base, perm, 0, n, d_out);
-    } else if ((flags & HB_FLAG_VARLEN_COOP) && data_bytes < (1ull << 37)) {  // block counts fit u32
-        // Opt-in.  It beat the per-thread kernel for MD5 under the global sort
-        // (2.38 vs 4.36 ms at configs[3]) because its coalesced staging hid the
-        // scattered reads; with the windowed sort the per-thread kernel reads
-        // neighbouring messages together and wins (2.24 vs 2.85 ms).
-        const uint64_t g = (n + kVcWarps * 32 - 1) / (kVcWarps * 32);
-        // A/B knobs: $HB_VC_STAGES (ring depth; 4 -> 5 CTAs/SM by smem, 3 -> 7), $HB_VC_PF (L2 prefetch).
-        // B200 (profiles/ab_varlen_r1.txt): MD5 best at 3 stages (2.52 vs 2.62 ms for 4), 256 B prefetch.
-        const int stages = (int)env_u64("HB_VC_STAGES", ALG == kMd5 ? 3 : 4), pf = (int)env_u64("HB_VC_PF", 256);
-        const unsigned gg = (unsigned)g;
-        constexpr int T = kVcWarps * 32;
-        if (stages == 3)
-            k_varlen_coop<ALG, 3, 7, 256><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
-        else if (stages == 2)
-            k_varlen_coop<ALG, 2, 8, 256><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
-        else if (pf == 128)
-            k_varlen_coop<ALG, 4, 5, 128><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
-        else if (pf == 0)
-            k_varlen_coop<ALG, 4, 5, 0><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
-        else
-            k_varlen_coop<ALG, 4, 5, 256><<<gg, T, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out);
-    } else if (env_u64("HB_VARLEN_BULK", 0)) {  // per-lane TMA bulk copies (A/B)
-        const unsigned g = (unsigned)((n + 127) / 128);
-        switch (env_u64("HB_VARLEN_BULK", 0)) {  // ring depth x register cap
-        case 2: k_varlen_bulk<ALG, 2, 1><<<g, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out); break;
-        case 4: k_varlen_bulk<ALG, 3, 6><<<g, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out); break;
-        case 5: k_varlen_bulk<ALG, 2, 8><<<g, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out); break;
-        default: k_varlen_bulk<ALG, 3, 1><<<g, 128, 0, stream>>>(d_data, d_offsets, offset_base, perm, n, d_out); break;
-        }
-    } else if (env_u64("HB_VARLEN_PREFETCH", 0)) {  // per-thread 128-bit loads, software-pipelined
-        k_varlen16<ALG, true><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets, offset_base,
-                                                                   perm, n, d_out);
-    } else {  // per-thread 128-bit loads
-        k_varlen16<ALG, false><<<(unsigned)grid, 128, 0, stream>>>(d_data, d_data + data_bytes, d_offsets, offset_base,
-                                                                    perm, n, d_out);
-    }
-    note_launches(1);
+    cudaError_t e = launch_varlen_sort(ALG, d_data, d_offsets, offset_base, n, d_scratch, stream, flags, &perm, 4);
+    if (e != cudaSuccess) return e;
+    launch_plain(k_varlen16<ALG, false>, (unsigned)((n + 127) / 128), 128, stream, d_data, d_data + data_bytes,
+                 d_offsets, offset_base, perm, n, d_out);
     return cudaGetLastError();
 }
 
+// Paper workload.  Widths 2-10 below ~1.07e10: the runs-of-ten kernel (MD5
+// compresses messages j and j+5 together, +3 %; SHA-1 / SM3 lose 28 / 6 % that
+// way); otherwise one message per thread with FMA-pipe digits (round variant
+// 3 for SHA-1, 1 otherwise; profiles/ab_decimal_r1b-d.txt).
 template <int ALG, int W>
 static void dec_launch(uint64_t start, uint64_t count, uint8_t* d_out, cudaStream_t s) {
-    const unsigned grid = (unsigned)((count + 127) / 128);
-    // Defaults (B200, profiles/ab_decimal_r1c.txt): FMA-pipe digits, round
-    // variant 1 (SHA-1: 3).  A/B arms: $HB_CONST_VARIANT = 1 | 3, $HB_FMA_DIGITS=0
-    // (IMAD.HI + SHF digits, variant 1).  Plain / variant-2 rounds lost 4-14 %
-    // (profiles/ab_decimal_r1b.txt) and are no longer instantiated here.
+    const Tuning& T = tuning();
     if (count == 0) return;
+#ifdef HB_AB
+    if (T.dec_ab) { dec_launch_ab<ALG, W>(start, count, d_out, s); return; }
+#endif
     if constexpr (W >= 2 && W <= 10) {
-        if (env_u64("HB_DEC_RUN", 1) && (start + count) / 10u < (1ull << 30) - 1) {
+        if (T.dec_run && (start + count) / 10u < (1ull << 30) - 1) {
             const uint64_t threads = (start + count + 9u) / 10u - start / 10u;
             const unsigned g = (unsigned)((threads + 127) / 128);
-            // variant 1 for all three (profiles/ab_decimal_r1d.txt: variant 2
-            // ties on MD5 and loses 4-35 % elsewhere, so it is not instantiated;
-            // SHA-1's variant 3, best for k_decimal, loses 35 % here)
-            switch (env_u64("HB_CONST_VARIANT", 1)) {
-            case 3: k_decimal_run<ALG, W, kVarBal3><<<g, 128, 0, s>>>(start, count, d_out); break;
-            default:
-                // MD5: two messages per compression call (+3 %); SHA-1 / SM3
-                // lose 28 / 6 % that way (register pressure), profiles/ab_decimal_r1d.txt
-                if (env_u64("HB_DEC_PAIR", ALG == kMd5 ? 1 : 0))
-                    k_decimal_run<ALG, W, kVarBal, true><<<g, 128, 0, s>>>(start, count, d_out);
-                else
-                    k_decimal_run<ALG, W, kVarBal><<<g, 128, 0, s>>>(start, count, d_out);
-                break;
-            }
+            launch_plain(k_decimal_run<ALG, W, kVarBal, ALG == kMd5>, g, 128, s, start, count, d_out);
             return;
         }
     }
-    if (!env_u64("HB_FMA_DIGITS", 1)) {
-        k_decimal<ALG, W, kVarBal, false><<<grid, 128, 0, s>>>(start, count, d_out);
-    } else if (env_u64("HB_CONST_VARIANT", ALG == kSha1 ? 3 : 1) == 3) {
-        k_decimal<ALG, W, kVarBal3, true><<<grid, 128, 0, s>>>(start, count, d_out);
-    } else {
-        k_decimal<ALG, W, kVarBal, true><<<grid, 128, 0, s>>>(start, count, d_out);
-    }
+    const unsigned grid = (unsigned)((count + 127) / 128);
+    launch_plain(k_decimal<ALG, W, ALG == kSha1 ? kVarBal3 : kVarBal, true>, grid, 128, s, start, count, d_out);
 }
 
 template <int ALG>
@@ -1519,7 +930,6 @@ static cudaError_t launch_decimal_alg(uint64_t start, uint64_t count, int width,
 #undef HB_DEC_CASE
     default: return cudaErrorInvalidValue;
     }
-    note_launches(1);
     return cudaGetLastError();
 }
 

@@ -17,6 +17,22 @@ def _stream_ptr(torch, dev: int) -> int:
     return torch.cuda.current_stream(dev).cuda_stream
 
 
+def _check_out(torch, out, n: int, alg: str, device):
+    """The kernels write n rows of dlen bytes with 16-byte (MD5/SM3) or 4-byte
+    (SHA-1) stores straight through the pointer: anything but a contiguous
+    uint8 (n, dlen) tensor on the batch's device, suitably aligned, would be
+    an out-of-bounds or misaligned device write."""
+    dlen = DIGEST_LEN[alg]
+    if out is None:
+        return torch.empty((n, dlen), dtype=torch.uint8, device=device)
+    align = 4 if alg == "sha1" else 16
+    if (out.dtype != torch.uint8 or tuple(out.shape) != (n, dlen) or out.device != device
+            or not out.is_contiguous() or out.data_ptr() % align):
+        raise ValueError(f"out must be a contiguous uint8 ({n}, {dlen}) tensor on {device}, "
+                         f"{align}-byte aligned")
+    return out
+
+
 def hash_fixed(alg: str, msgs, out=None, flags: int = 0):
     """Digest each row of a 2-D uint8 CUDA tensor; returns (n, dlen) uint8 CUDA tensor."""
     import torch
@@ -27,8 +43,7 @@ def hash_fixed(alg: str, msgs, out=None, flags: int = 0):
     msgs = msgs.contiguous()
     n, L = msgs.shape
     dev = msgs.device.index
-    if out is None:
-        out = torch.empty((n, DIGEST_LEN[alg]), dtype=torch.uint8, device=msgs.device)
+    out = _check_out(torch, out, n, alg, msgs.device)
     if n:
         rc = _native.lib().hb_hash_fixed_dev(_native.ALG_ID[alg], dev, msgs.data_ptr(), n, L, out.data_ptr(),
                                              _stream_ptr(torch, dev), int(flags))
@@ -46,14 +61,20 @@ def hash_varlen(alg: str, data, offsets, out=None, scratch=None, flags: int = 0,
     _check_alg(alg)
     if data.dtype != torch.uint8 or offsets.dtype not in (torch.int64, torch.uint64) or not data.is_cuda:
         raise ValueError("data must be uint8 and offsets int64/uint64 CUDA tensors")
+    if offsets.device != data.device or offsets.dim() != 1:
+        raise ValueError("offsets must be a 1-D tensor on the data's device")
+    if not data.is_contiguous() or not offsets.is_contiguous():
+        raise ValueError("data and offsets must be contiguous")
     n = offsets.numel() - 1
     dev = data.device.index
-    if out is None:
-        out = torch.empty((max(n, 0), DIGEST_LEN[alg]), dtype=torch.uint8, device=data.device)
+    out = _check_out(torch, out, max(n, 0), alg, data.device)
     if n <= 0:
         return out
     if scratch is None and not (flags & _native.HB_FLAG_NO_SORT):
         scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch.uint8, device=data.device)
+    elif scratch is not None and (scratch.device != data.device or not scratch.is_contiguous() or
+                                  scratch.numel() * scratch.element_size() < int(_native.lib().hb_varlen_scratch_bytes(n))):
+        raise ValueError("scratch must be a contiguous tensor of hb_varlen_scratch_bytes(n) bytes on the data's device")
     base = int(offsets[0].item()) if offset_base is None else int(offset_base)
     rc = _native.lib().hb_hash_varlen_dev(_native.ALG_ID[alg], dev, data.data_ptr(), data.numel(),
                                           offsets.data_ptr(), base, n, out.data_ptr(),
@@ -67,8 +88,7 @@ def hash_decimal(alg: str, start: int, count: int, width: int = 9, device: int =
     import torch
 
     _check_alg(alg)
-    if out is None:
-        out = torch.empty((count, DIGEST_LEN[alg]), dtype=torch.uint8, device=f"cuda:{device}")
+    out = _check_out(torch, out, count, alg, torch.device("cuda", device))
     if count:
         rc = _native.lib().hb_hash_decimal_dev(_native.ALG_ID[alg], device, start, count, width, out.data_ptr(),
                                                _stream_ptr(torch, device))

@@ -76,8 +76,9 @@ class P2PDigestGather:
         self.alg, self.group, self.root = alg, group, root
         world, self.rank = dist.get_world_size(group), dist.get_rank(group)
         self.lo, self.hi = shard_bounds(n_total, world)[self.rank]
-        if msgs_local.dim() != 2 or msgs_local.shape[0] != self.hi - self.lo or not msgs_local.is_cuda:
-            raise ValueError(f"rank {self.rank} must pass its shard [{self.lo}, {self.hi}) as a 2-D CUDA tensor")
+        if (msgs_local.dim() != 2 or msgs_local.shape[0] != self.hi - self.lo or not msgs_local.is_cuda
+                or msgs_local.dtype != torch.uint8):
+            raise ValueError(f"rank {self.rank} must pass its shard [{self.lo}, {self.hi}) as a 2-D uint8 CUDA tensor")
         self.msgs = msgs_local.contiguous()
         self.dlen = DIGEST_LEN[alg]
         self.gpu = self.msgs.device.index

@@ -159,8 +159,13 @@ class _Executor:
         if buf.nbytes > self.in_use[buf.device]:
             raise ExecError(f"{loc}: dealloc of unknown or already-freed buffer on '{buf.device}'")
         self.in_use[buf.device] -= buf.nbytes
-        # the tensor is released when the last reference goes; it was allocated on
-        # this device's stream, so the caching allocator reuses it in stream order.
+        # The tensor is released when the last reference goes.  It may have been
+        # used on either ping-pong stream of its device: mark it in use on both,
+        # so the caching allocator does not hand its memory out again before
+        # the work already enqueued on them has finished with it.
+        if buf.dev is not None:
+            for s in self.streams.get(buf.device, ()):
+                buf.dev.record_stream(s)
 
     def _host_sync(self, buf: _Buf) -> None:
         for ev in buf.pending:
@@ -298,9 +303,12 @@ class _Executor:
         else:  # device to device (same or peer GPU)
             dev = dst.device
             if src.device != dst.device:
-                ev = torch.cuda.Event()
-                ev.record(self._stream(src.device))
-                self._stream(dev).wait_event(ev)
+                # the source may have been written on either ping-pong stream of its device
+                self._stream(src.device)
+                for ss in self.streams[src.device]:
+                    ev = torch.cuda.Event()
+                    ev.record(ss)
+                    self._stream(dev).wait_event(ev)
             self._timed(dev, self.copy_ev, lambda s: dst.dev[b0:b0 + nbytes].copy_(src.dev[a0:a1], non_blocking=True))
             self.copied[dev] += nbytes
 
@@ -377,7 +385,13 @@ class _Executor:
         stride_of = {o.result: o.attrs.get("slice_stride") for o in allocs}
         copies_in = [o for o in ops if o.opcode == "hyper.memcpy" and o.operands[1] in alloc_ids]
         copies_out = [o for o in ops if o.opcode == "hyper.memcpy" and o.operands[0] in alloc_ids]
-        self._stream(dev)
+        torch = self.torch
+        s0, s1 = self._stream(dev), self.streams[dev][1]
+        # stream 1 joins stream 0's order before the group (buffers written
+        # earlier on stream 0 may be read by sub-batches on stream 1) ...
+        ev = torch.cuda.Event()
+        ev.record(s0)
+        s1.wait_event(ev)
         for ci, (c0, c1) in enumerate(chunks):
             self.cur[dev] = ci % 2  # ping-pong: chunk c+1's copy-in overlaps chunk c's kernel
             cn = c1 - c0
@@ -402,6 +416,11 @@ class _Executor:
                                count=cn * stride)
             for a in allocs:
                 self._dealloc(self.value(a.result), loc)
+        # ... and stream 0 waits for stream 1 after it, so later ops on stream 0
+        # see every sub-batch's writes
+        ev = torch.cuda.Event()
+        ev.record(s1)
+        s0.wait_event(ev)
         self.cur[dev] = 0
 
 

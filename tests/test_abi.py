@@ -54,7 +54,7 @@ def test_library_is_sm100a():
 
 def test_abi_basics():
     lib = _native.lib()
-    assert lib.hb_abi_version() == 1
+    assert lib.hb_abi_version() == 2
     assert [lib.hb_digest_len(i) for i in range(3)] == [20, 16, 32]
     assert lib.hb_digest_len(7) == -1
     assert hb.launch_count() >= 0

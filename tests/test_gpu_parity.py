@@ -108,18 +108,7 @@ def test_varlen_golden(golden):
             assert sha(batch_digest_varlen(alg, data, off)) == row[alg]
 
 
-@pytest.mark.parametrize("sort", ["window4096", "window16384", "global", "prefetch", "bulk", "ld32", "ld16"])
-@pytest.mark.parametrize("alg", ALGS)
-def test_varlen_random_sorted_and_unsorted(alg, sort, monkeypatch):
-    monkeypatch.setenv("HB_VARLEN_SORT", "global" if sort == "global" else "window")
-    if sort.startswith("window"):
-        monkeypatch.setenv("HB_SORT_WINDOW", sort[6:])
-    if sort == "prefetch":
-        monkeypatch.setenv("HB_VARLEN_PREFETCH", "1")
-    if sort == "bulk":
-        monkeypatch.setenv("HB_VARLEN_BULK", "2")
-    if sort.startswith("ld"):
-        monkeypatch.setenv("HB_VARLEN_LD", sort[2:])
+def _varlen_random_case():
     rng = np.random.default_rng(12)
     n = 20000  # above the sort threshold
     lens = rng.integers(0, 4097, n).astype(np.uint64)
@@ -128,6 +117,48 @@ def test_varlen_random_sorted_and_unsorted(alg, sort, monkeypatch):
     off[1:] = np.cumsum(lens) + 5  # non-zero base offset
     off[0] = 5
     data = oracle.fill_random(int(off[-1]) + 3, 99)
+    return data, off
+
+
+@pytest.mark.parametrize("sort", ["default", "window", "global"])
+@pytest.mark.parametrize("alg", ALGS)
+def test_varlen_random_sorted_and_unsorted(alg, sort, hb_env):
+    """The shipped varlen path: windowed (MD5 default) or global length sort,
+    or none (HB_FLAG_NO_SORT), per-thread 128-bit-load kernel."""
+    if sort != "default":
+        hb_env.set(HB_VARLEN_SORT=sort)
+    data, off = _varlen_random_case()
+    ref = oracle.batch_varlen(alg, data, off, threads=8)
+    for fl in (0, _native.HB_FLAG_NO_SORT, _native.HB_FLAG_VARLEN_COOP_OFF,
+               _native.HB_FLAG_VARLEN_COOP_OFF | _native.HB_FLAG_NO_SORT):
+        assert np.array_equal(batch_digest_varlen(alg, data, off, flags=fl), ref), fl
+        assert "k_varlen16" in _native.last_kernel_name()
+
+
+def test_varlen_ab_flags_rejected_in_default_build():
+    if _native.built_with_ab():
+        pytest.skip("A/B library loaded")
+    data, off = _varlen_random_case()
+    for fl in (_native.HB_FLAG_VARLEN_WORDS, _native.HB_FLAG_VARLEN_COOP):
+        with pytest.raises(RuntimeError, match="HB_AB"):
+            batch_digest_varlen("md5", data, off, flags=fl)
+
+
+@pytest.mark.ab
+@pytest.mark.parametrize("sort", ["window4096", "window16384", "global", "prefetch", "bulk", "ld32", "ld16"])
+@pytest.mark.parametrize("alg", ALGS)
+def test_varlen_ab_arms(alg, sort, hb_env):
+    env = {"HB_VARLEN_SORT": "global" if sort == "global" else "window"}
+    if sort.startswith("window"):
+        env["HB_SORT_WINDOW"] = sort[6:]
+    if sort == "prefetch":
+        env["HB_VARLEN_PREFETCH"] = "1"
+    if sort == "bulk":
+        env["HB_VARLEN_BULK"] = "2"
+    if sort.startswith("ld"):
+        env["HB_VARLEN_LD"] = sort[2:]
+    hb_env.set(**env)
+    data, off = _varlen_random_case()
     ref = oracle.batch_varlen(alg, data, off, threads=8)
     for fl in (0, _native.HB_FLAG_NO_SORT, _native.HB_FLAG_VARLEN_WORDS,
                _native.HB_FLAG_VARLEN_WORDS | _native.HB_FLAG_NO_SORT, _native.HB_FLAG_VARLEN_COOP_OFF,
@@ -136,12 +167,12 @@ def test_varlen_random_sorted_and_unsorted(alg, sort, monkeypatch):
         assert np.array_equal(batch_digest_varlen(alg, data, off, flags=fl), ref), fl
 
 
-def test_engine_chunking_and_pinned(monkeypatch):
+def test_engine_chunking_and_pinned(hb_env):
     # many sub-batches (the _run_group contract, executor.py:603-699) and pinned vs pageable host buffers
     n, L = 5000, 200
     data = oracle.fill_random(n * L, 31).reshape(n, L)
     ref = {a: oracle.batch_fixed(a, data, threads=8) for a in ALGS}
-    monkeypatch.setenv("HB_CHUNK_BYTES", str(64 * 1024))
+    hb_env.set(HB_CHUNK_BYTES=64 * 1024)
     lib = _native.lib()
     p = lib.hb_alloc_pinned(n * L)
     assert p
@@ -165,7 +196,7 @@ def test_engine_chunking_and_pinned(monkeypatch):
         assert np.array_equal(batch_digest_varlen(alg, vdata, off), oracle.batch_varlen(alg, vdata, off, 8))
 
 
-def test_engine_pipelined_chunks(monkeypatch):
+def test_engine_pipelined_chunks(hb_env):
     """Chunk pipelining of host-buffer calls: a shard whose digests reach
     HB_PIPE_MIN_OUT is cut into >= HB_PIPE_CHUNKS chunks of >= HB_MIN_CHUNK_BYTES
     (H2D of chunk k+1 overlaps kernel + D2H of chunk k); a 4 MiB batch of
@@ -184,10 +215,7 @@ def test_engine_pipelined_chunks(monkeypatch):
         for env, chunks in (({}, (1, 1)), ({"HB_PIPE_MIN_OUT": "1", "HB_MIN_CHUNK_BYTES": str(1 << 20)}, (4, 4)),
                             ({"HB_PIPE_MIN_OUT": "1", "HB_MIN_CHUNK_BYTES": "65536", "HB_PIPE_CHUNKS": "16"}, (16, 16)),
                             ({"HB_PIPE_MIN_OUT": "1", "HB_PIPE_CHUNKS": "1"}, (1, 1))):
-            for k in ("HB_PIPE_MIN_OUT", "HB_MIN_CHUNK_BYTES", "HB_PIPE_CHUNKS"):
-                monkeypatch.delenv(k, raising=False)
-            for k, v in env.items():
-                monkeypatch.setenv(k, v)
+            hb_env.reset(("HB_PIPE_MIN_OUT", "HB_MIN_CHUNK_BYTES", "HB_PIPE_CHUNKS"), **env)
             t = {}
             assert np.array_equal(batch_digest(alg, data, timing=t), ref)
             assert chunks[0] <= t["chunks"] <= chunks[1], (alg, env, t["chunks"])
@@ -196,11 +224,11 @@ def test_engine_pipelined_chunks(monkeypatch):
 
 
 @pytest.mark.parametrize("pair", ["0", "1"])
-def test_small_rows_pairs(pair, monkeypatch):
+def test_small_rows_pairs(pair, hb_env):
     """Compile-time-width kernel with two rows per thread (HB_SMALL_PAIR, MD5,
     >= 2^20 rows): odd row counts (the last thread's second row missing) and
     every short width, all rows against the oracle."""
-    monkeypatch.setenv("HB_SMALL_PAIR", pair)
+    hb_env.set(HB_SMALL_PAIR=pair)
     for L in (16, 32, 48, 64, 128):
         n = (1 << 20) + 1
         data = oracle.fill_random(n * L, 53 + L).reshape(n, L)
@@ -245,13 +273,14 @@ def test_pdl_stream_order(L):
 
 
 @pytest.mark.parametrize("bind", ["1", "0"])
-def test_multi_shard_numa_binding(bind, monkeypatch):
-    """A multi-GPU call (here two shards on GPU 0) runs one worker thread per
-    shard, each pinned to its GPU's local CPUs (sysfs local_cpulist); the
-    digests are unchanged and the caller's own affinity is untouched."""
+def test_multi_shard_numa_binding(bind, hb_env):
+    """A multi-GPU call (here two shards on GPU 0) hands its shards to the
+    per-GPU worker threads, each pinned to its GPU's local CPUs (sysfs
+    local_cpulist); the digests are unchanged and the caller's own affinity is
+    untouched."""
     import os
 
-    monkeypatch.setenv("HB_BIND_NUMA", bind)
+    hb_env.set(HB_BIND_NUMA=bind)
     n, L = 30001, 200
     data = oracle.fill_random(n * L, 43).reshape(n, L)
     before = os.sched_getaffinity(0)
@@ -296,25 +325,22 @@ def test_ratio_invariance_style_sharding():
 
 
 @pytest.mark.parametrize("dec_run", ["1", "0"])
-@pytest.mark.parametrize("variant", ["1", "fma_digits"])
-def test_decimal_workload(golden, variant, dec_run, monkeypatch):
+def test_decimal_workload(golden, dec_run, hb_env):
     """HB_DEC_RUN=1 (default): runs-of-ten kernel for widths 2..10 below
     v ~ 1.07e10, the one-message-per-thread kernel elsewhere; 0: the latter only."""
-    monkeypatch.setenv("HB_DEC_RUN", dec_run)
-    monkeypatch.setenv("HB_FMA_DIGITS", "0")
-    if variant == "fma_digits":
-        monkeypatch.setenv("HB_FMA_DIGITS", "1")
-        # the FMA digit path ends at index 2^30; straddle it and check every width it serves
-        for w, v in [(w, v) for w in range(1, 10) for v in ("1", "3")]:
-            monkeypatch.setenv("HB_CONST_VARIANT", v)
-            for start, cnt in ((max(0, 10**w - 300), min(300, 10**w)), (2**30 - 150, 300)):
-                if start + cnt > 10**w:
-                    continue
-                for alg in ALGS:
-                    assert np.array_equal(hash_decimal(alg, start, cnt, w),
-                                          oracle.batch_fixed(alg, oracle.gen_decimal(start, cnt, w))), (alg, w, start)
-    else:
-        monkeypatch.setenv("HB_CONST_VARIANT", variant)
+    hb_env.set(HB_DEC_RUN=dec_run)
+    # the FMA digit path of the one-message kernel ends at index 2^30; straddle it at every width it serves
+    for w in range(1, 10):
+        for start, cnt in ((max(0, 10**w - 300), min(300, 10**w)), (2**30 - 150, 300)):
+            if start + cnt > 10**w:
+                continue
+            for alg in ALGS:
+                assert np.array_equal(hash_decimal(alg, start, cnt, w),
+                                      oracle.batch_fixed(alg, oracle.gen_decimal(start, cnt, w))), (alg, w, start)
+    _decimal_common(golden)
+
+
+def _decimal_common(golden):
     # the 32-bit digit path ends exactly at index 2^32 - 1; straddle it
     start, cnt = 2**32 - 150, 300
     for alg in ALGS:
@@ -331,26 +357,70 @@ def test_decimal_workload(golden, variant, dec_run, monkeypatch):
             assert np.array_equal(hash_decimal(alg, start, cnt, w), oracle.batch_fixed(alg, msgs)), (alg, w)
 
 
-@pytest.mark.parametrize("variant", ["1", "3", "pair", "nopair"])
-def test_decimal_runs_ragged(variant, monkeypatch):
-    """Runs-of-ten kernel: every start residue mod 10 x short counts (first and
-    last thread partial, one thread both), the end of the width-10 range and
-    the 2^32 boundary (u = v / 10 stays below 2^30 for every width <= 10)."""
-    if variant in ("pair", "nopair"):  # two messages per compression call (MD5 default) or one
-        monkeypatch.setenv("HB_DEC_PAIR", "1" if variant == "pair" else "0")
+@pytest.mark.ab
+@pytest.mark.parametrize("dec_run", ["1", "0"])
+@pytest.mark.parametrize("variant", ["1", "fma_digits"])
+def test_decimal_workload_ab(golden, variant, dec_run, hb_env):
+    hb_env.set(HB_DEC_RUN=dec_run, HB_FMA_DIGITS="0")
+    if variant == "fma_digits":
+        hb_env.set(HB_FMA_DIGITS="1")
+        for w, v in [(w, v) for w in range(1, 10) for v in ("1", "3")]:
+            hb_env.set(HB_CONST_VARIANT=v)
+            for start, cnt in ((max(0, 10**w - 300), min(300, 10**w)), (2**30 - 150, 300)):
+                if start + cnt > 10**w:
+                    continue
+                for alg in ALGS:
+                    assert np.array_equal(hash_decimal(alg, start, cnt, w),
+                                          oracle.batch_fixed(alg, oracle.gen_decimal(start, cnt, w))), (alg, w, start)
     else:
-        monkeypatch.setenv("HB_CONST_VARIANT", variant)
+        hb_env.set(HB_CONST_VARIANT=variant)
+    _decimal_common(golden)
+
+
+def test_decimal_range_checked():
+    """gen_messages' range rule at the C ABI: indices past 10^width
+    or a 64-bit wrap are rejected, not silently reduced."""
+    lib = _native.lib()
+    out = np.empty((10, 16), np.uint8)
+    for start, count, width in ((10**9 - 5, 10, 9), (2**64 - 5, 10, 20), (0, 101, 2)):
+        rc = lib.hb_hash_decimal(1, start, count, width, out.ctypes.data, None, 0, 0, None)
+        assert rc == _native.HB_ERR_INVAL, (start, count, width)
+        rc = lib.hb_hash_decimal_dev(1, 0, start, count, width, None, None)
+        assert rc == _native.HB_ERR_INVAL
+    with pytest.raises(ValueError):
+        hash_decimal("md5", 2**64 - 5, 10, 20)
+
+
+def _decimal_ragged_cases():
     for w in (2, 3, 4, 8, 9, 10):
         for r in range(10):
             for cnt in (c for c in (1, 2, 9, 10, 11, 19, 21, 1283) if c <= 10**w):
-                start = max(0, min(10**w - cnt, 10**(w - 1) + 37 * 10 + r))
-                for alg in ALGS:
-                    assert np.array_equal(hash_decimal(alg, start, cnt, w),
-                                          oracle.batch_fixed(alg, oracle.gen_decimal(start, cnt, w))), (alg, w, start, cnt)
+                yield w, max(0, min(10**w - cnt, 10**(w - 1) + 37 * 10 + r)), cnt
     for start, cnt in ((10**10 - 1000, 1000), (10**10 - 1001, 1001), (10**10 - 37, 37), (2**32 - 15, 40)):
+        yield 10, start, cnt
+
+
+def test_decimal_runs_ragged():
+    """Runs-of-ten kernel: every start residue mod 10 x short counts (first and
+    last thread partial, one thread both), the end of the width-10 range and
+    the 2^32 boundary (u = v / 10 stays below 2^30 for every width <= 10)."""
+    for w, start, cnt in _decimal_ragged_cases():
         for alg in ALGS:
-            assert np.array_equal(hash_decimal(alg, start, cnt, 10),
-                                  oracle.batch_fixed(alg, oracle.gen_decimal(start, cnt, 10))), (alg, start, cnt)
+            assert np.array_equal(hash_decimal(alg, start, cnt, w),
+                                  oracle.batch_fixed(alg, oracle.gen_decimal(start, cnt, w))), (alg, w, start, cnt)
+
+
+@pytest.mark.ab
+@pytest.mark.parametrize("variant", ["1", "3", "pair", "nopair"])
+def test_decimal_runs_ragged_ab(variant, hb_env):
+    if variant in ("pair", "nopair"):  # two messages per compression call (MD5 default) or one
+        hb_env.set(HB_DEC_PAIR="1" if variant == "pair" else "0")
+    else:
+        hb_env.set(HB_CONST_VARIANT=variant)
+    for w, start, cnt in _decimal_ragged_cases():
+        for alg in ALGS:
+            assert np.array_equal(hash_decimal(alg, start, cnt, w),
+                                  oracle.batch_fixed(alg, oracle.gen_decimal(start, cnt, w))), (alg, w, start, cnt)
 
 
 def test_error_mapping():
@@ -427,19 +497,20 @@ def test_full_size_sampled_and_cross_path():
     del buf
 
 
+@pytest.mark.ab
 @pytest.mark.parametrize("cfg", ["1x3", "2x2", "2x3", "ws2", "ws3", "ws2x2", "ws3x2", "ws3u", "ws3x2u", "ws3n"])
-def test_tma_tile_configs_and_variants(cfg, monkeypatch):
+def test_tma_tile_configs_and_variants(cfg, hb_env):
     """Every compiled TMA tile configuration x round variant is bit-exact
     (the tuned default is only one of them; $HB_TMA_CFG/$HB_VARIANT select)."""
     variants = (["0", "1", "2", "3"] if cfg == "1x3" else ["1", "3"] if cfg.endswith("x2") and cfg.startswith("ws")
                 else ["0", "1", "2", "3"] if cfg == "ws3" else ["0", "1"] if cfg.startswith("ws") else ["0", "1", "2"])
-    monkeypatch.setenv("HB_TMA_CFG", cfg)
+    hb_env.set(HB_TMA_CFG=cfg)
     for L in (16, 48, 64, 112, 128, 1024, 1040):
         n = 333
         data = oracle.fill_random(n * L, 7 * L + 1).reshape(n, L)
         refs = {a: oracle.batch_fixed(a, data, threads=8) for a in ALGS}
         for v in variants:
-            monkeypatch.setenv("HB_VARIANT", v)
+            hb_env.set(HB_VARIANT=v)
             for alg in ALGS:
                 assert np.array_equal(batch_digest(alg, data), refs[alg]), (cfg, v, alg, L)
 
@@ -459,53 +530,73 @@ def test_duty_ratio_invariance():
             assert np.array_equal(got, ref), (alg, x)
 
 
-@pytest.mark.parametrize("alg", ALGS)
-def test_batch_geometry_dispatch_matches(alg, monkeypatch):
-    """The fixed-width dispatch picks a kernel shape by batch geometry (direct
-    loads for short rows, one message per thread below $HB_SMALL_N, the tuned
-    tiles otherwise); every shape must give the oracle's digests."""
-    arms = [{}, {"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"}, {"HB_SMALL_N": str(1 << 40), "HB_DIRECT_MAX_L": "0"},
-            {"HB_NO_SMALL_KERNEL": "1"}, {"HB_CONST_VARIANT": "0"}]
+GEOMETRY_KEYS = ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_CONST_VARIANT")
+
+
+def _geometry_arms(alg, arms, hb_env):
     for L in (16, 32, 48, 64, 96, 128, 144, 1024):
         n = 3001
         data = oracle.fill_random(n * L, 5 * L + 3).reshape(n, L)
         ref = oracle.batch_fixed(alg, data, threads=8)
         for env in arms:
-            for k in ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_CONST_VARIANT"):
-                monkeypatch.delenv(k, raising=False)
-            for k, v in env.items():
-                monkeypatch.setenv(k, v)
+            hb_env.reset(GEOMETRY_KEYS, **env)
             assert np.array_equal(batch_digest(alg, data), ref), (alg, L, env)
 
 
 @pytest.mark.parametrize("alg", ALGS)
-def test_varlen_every_length_and_alignment(alg, monkeypatch):
-    """Every length 0..260 (x3, shuffled, so message starts take every
-    alignment mod 16) in one batch and in partial warps (n not a multiple of
-    32), with several leading offsets, sorted and unsorted, every kernel."""
+def test_batch_geometry_dispatch_matches(alg, hb_env):
+    """The fixed-width dispatch picks a kernel shape by batch geometry (direct
+    loads for short rows, one message per thread below $HB_SMALL_N, the tuned
+    tiles otherwise); every shape must give the oracle's digests."""
+    _geometry_arms(alg, [{}, {"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"},
+                         {"HB_SMALL_N": str(1 << 40), "HB_DIRECT_MAX_L": "0"}], hb_env)
+
+
+@pytest.mark.ab
+@pytest.mark.parametrize("alg", ALGS)
+def test_batch_geometry_dispatch_ab(alg, hb_env):
+    _geometry_arms(alg, [{"HB_NO_SMALL_KERNEL": "1"}, {"HB_CONST_VARIANT": "0"}, {"HB_SMALL_CTA": "32"}], hb_env)
+
+
+def _every_length_cases():
     lens = np.array([L for L in range(261) for _ in range(3)], np.uint64)
     np.random.default_rng(5).shuffle(lens)
     for shift in (0, 1, 3, 7, 13):
         off = np.zeros(len(lens) + 1, np.uint64)
         off[1:] = np.cumsum(lens)
         off += np.uint64(shift)
-        buf = oracle.fill_random(int(off[-1]) + 5, 17 + shift)
+        yield shift, off, oracle.fill_random(int(off[-1]) + 5, 17 + shift)
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_varlen_every_length_and_alignment(alg):
+    """Every length 0..260 (x3, shuffled, so message starts take every
+    alignment mod 16) in one batch and in partial warps (n not a multiple of
+    32), with several leading offsets, sorted and unsorted."""
+    for shift, off, buf in _every_length_cases():
         ref = oracle.batch_varlen(alg, buf, off, threads=8)
-        for k in (len(lens), 31, 33, 1):
-            for fl in (0, _native.HB_FLAG_NO_SORT, _native.HB_FLAG_VARLEN_COOP_OFF, _native.HB_FLAG_VARLEN_COOP):
+        for k in (len(off) - 1, 31, 33, 1):
+            for fl in (0, _native.HB_FLAG_NO_SORT, _native.HB_FLAG_VARLEN_COOP_OFF):
                 got = batch_digest_varlen(alg, buf, off[: k + 1], flags=fl)
                 assert np.array_equal(got, ref[:k]), (alg, shift, k, fl)
-        C = _native.HB_FLAG_VARLEN_COOP
+
+
+@pytest.mark.ab
+@pytest.mark.parametrize("alg", ALGS)
+def test_varlen_every_length_and_alignment_ab(alg, hb_env):
+    C = _native.HB_FLAG_VARLEN_COOP
+    for shift, off, buf in _every_length_cases():
+        ref = oracle.batch_varlen(alg, buf, off, threads=8)
+        for k in (len(off) - 1, 31, 33, 1):
+            assert np.array_equal(batch_digest_varlen(alg, buf, off[: k + 1], flags=C), ref[:k]), (alg, shift, k)
         for env, fl in (({"HB_VC_STAGES": "3"}, C), ({"HB_VC_STAGES": "2"}, C), ({"HB_VC_PF": "128"}, C),
                         ({"HB_VC_PF": "0"}, C), ({"HB_VARLEN_PREFETCH": "1"}, 0), ({"HB_VARLEN_BULK": "3"}, 0),
                         ({"HB_VARLEN_BULK": "5"}, 0), ({"HB_VARLEN_LD": "32"}, 0), ({"HB_VARLEN_LD": "16"}, 0),
                         ({"HB_VARLEN_LD": "32", "HB_VARLEN_Q": "4"}, 0)):
-            for key, v in env.items():
-                monkeypatch.setenv(key, v)
+            hb_env.set(**env)
             got = batch_digest_varlen(alg, buf, off, flags=fl)
             assert np.array_equal(got, ref), (alg, shift, env)
-            for key in env:
-                monkeypatch.delenv(key)
+            hb_env.clear(*env)
 
 
 def test_hash_batch_var_message_batch():
@@ -596,8 +687,8 @@ def test_concurrent_callers_thread_safe():
         assert all(ex.map(run, range(len(jobs))))
 
 
-@pytest.mark.parametrize("ld", ["16", "32"])
-def test_varlen_last_message_at_buffer_end(ld, monkeypatch):
+@pytest.mark.parametrize("ld", ["16", pytest.param("32", marks=pytest.mark.ab)])
+def test_varlen_last_message_at_buffer_end(ld, hb_env):
     """The wide loads never read past the data buffer: the batch's last message
     ends exactly at the end of a device allocation whose size is not a
     multiple of 32 (checked with every tail length 0..95)."""
@@ -605,7 +696,7 @@ def test_varlen_last_message_at_buffer_end(ld, monkeypatch):
 
     from paper_2407_09333_b200 import device
 
-    monkeypatch.setenv("HB_VARLEN_LD", ld)
+    hb_env.set(HB_VARLEN_LD=ld)
     for tail in range(0, 96):
         lens = np.array([100, 37, 64 + tail], np.int64)
         off = np.zeros(4, np.int64)
@@ -629,3 +720,106 @@ def test_accel_generic_equivalence_1e6():
     assert np.array_equal(batch_digest("sha1", data, accel=False), ref)
     assert [d.data for d in hash_batch("sha1", MessageBatch(n, L, data.tobytes()), accel=True)[:1000]] == \
         [bytes(r) for r in ref[:1000]]
+
+
+# ------------------------------------------------------------ engine (r2) --
+def test_small_default_call_runs_on_one_gpu():
+    """A drop-in call with the default device set ("all GPUs") on a small
+    batch -- 4 KiB, the size of the reference executor's per-thread
+    _fast_digest slices -- runs on exactly one GPU (no fan-out, no worker
+    hand-off); an explicit list with two shards goes to the GPU workers."""
+    data = oracle.fill_random(64 * 64, 3).reshape(64, 64)
+    for alg in ALGS:
+        t = {}
+        got = batch_digest(alg, data, timing=t)
+        assert np.array_equal(got, oracle.batch_fixed(alg, data))
+        assert t["shards"] == 1 and bin(t["device_mask"]).count("1") == 1, t
+        t = {}
+        assert np.array_equal(batch_digest(alg, data, gpus=[0, 0], timing=t), oracle.batch_fixed(alg, data))
+        assert t["shards"] == 2 and t["device_mask"] == 1, t
+
+
+def test_timing_is_a_union_of_busy_intervals():
+    """hb_timing's per-stage times are unions of the chunk ring's busy
+    intervals (overlapping slots are not double-counted), each at most the
+    call's wall time; the per-chunk timeline has one span per stage and chunk."""
+    n, L = 1 << 16, 1024
+    data = oracle.fill_random(n * L, 21).reshape(n, L)
+    for env in ({}, {"HB_CHUNK_BYTES": 4 << 20}):
+        t = {}
+        out = batch_digest("md5", data, timing=t, gpus=[0])
+        assert t["chunks"] >= (16 if env else 1)
+        for k in ("h2d_ms", "kernel_ms", "d2h_ms"):
+            assert 0 < t[k] <= t["total_ms"] * 1.05 + 0.05, (k, t)
+        spans = _native.last_timeline()
+        kern = [s for s in spans if s["stage"] == "kernel"]
+        assert len(kern) == t["chunks"]
+        assert all(s["t1_ms"] >= s["t0_ms"] for s in spans)
+        assert np.array_equal(out[:7], oracle.batch_fixed("md5", data[:7]))
+
+
+def test_engine_tuning_reload(hb_env):
+    data = oracle.fill_random(4000 * 256, 8).reshape(4000, 256)
+    t = {}
+    batch_digest("sha1", data, timing=t, gpus=[0])
+    assert t["chunks"] == 1
+    hb_env.set(HB_CHUNK_BYTES=65536)
+    t = {}
+    assert np.array_equal(batch_digest("sha1", data, timing=t, gpus=[0]), oracle.batch_fixed("sha1", data))
+    assert t["chunks"] == -(-4000 // 256), t
+
+
+def test_engine_budget():
+    b = _native.engine_budget(0)
+    info = _native.device_info(0)
+    assert 0 < b["budget_bytes"] <= info["total_mem"]
+    assert 0 < b["chunk_cap_bytes"] <= 256 << 20
+
+
+@pytest.mark.parametrize("n,L,expect", [(1 << 18, 1024, "k_fixed_tma_ws"), (4096, 1024, "k_fixed_tma_ws"),
+                                        (4096, 64, "k_fixed_small"), (4096, 96, "k_fixed_direct"),
+                                        (4096, 100, "k_generic")])
+def test_last_kernel_name(n, L, expect):
+    """hb_last_kernel_name names the kernel that actually ran (what the bench
+    reports as roofline.kernel), for the device and host-buffer paths."""
+    import torch
+
+    from paper_2407_09333_b200 import device
+
+    msgs = torch.zeros((n, L), dtype=torch.uint8, device="cuda:0")
+    device.hash_fixed("sha1", msgs)
+    name = _native.last_kernel_name()
+    assert name.startswith(f"void hb::{expect}<") or expect in name, name
+    batch_digest("md5", np.zeros((n, L), np.uint8), gpus=[0, 0])  # two shards on the workers
+    assert expect in _native.last_kernel_name()
+    device.hash_decimal("md5", 0, 1000, 9)
+    assert "k_decimal_run" in _native.last_kernel_name()
+
+
+def test_device_wrappers_reject_bad_buffers():
+    """the device-resident wrappers check what the kernels will
+    dereference (offsets on the data's device, contiguous inputs, an `out`
+    of the right shape, dtype, device and alignment)."""
+    import torch
+
+    from paper_2407_09333_b200 import device
+
+    msgs = torch.zeros((100, 64), dtype=torch.uint8, device="cuda:0")
+    with pytest.raises(ValueError):
+        device.hash_fixed("md5", msgs, out=torch.empty((99, 16), dtype=torch.uint8, device="cuda:0"))
+    with pytest.raises(ValueError):
+        device.hash_fixed("md5", msgs, out=torch.empty((100, 16), dtype=torch.int32, device="cuda:0"))
+    with pytest.raises(ValueError):
+        big = torch.empty(100 * 16 + 1, dtype=torch.uint8, device="cuda:0")
+        device.hash_fixed("md5", msgs, out=big[1:].view(100, 16))
+    with pytest.raises(ValueError):
+        device.hash_fixed("md5", msgs, out=torch.empty((100, 16), dtype=torch.uint8))
+    data = torch.zeros(1000, dtype=torch.uint8, device="cuda:0")
+    with pytest.raises(ValueError):
+        device.hash_varlen("md5", data, torch.tensor([0, 10, 20]))
+    with pytest.raises(ValueError):
+        device.hash_varlen("md5", data[::2], torch.tensor([0, 10, 20], device="cuda:0"))
+    ok = device.hash_varlen("md5", data, torch.tensor([0, 10, 20], device="cuda:0"))
+    torch.cuda.synchronize()
+    assert np.array_equal(ok.cpu().numpy(), oracle.batch_varlen("md5", np.zeros(20, np.uint8),
+                                                               np.array([0, 10, 20], np.uint64)))
