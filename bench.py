@@ -2,23 +2,35 @@
 """Benchmark of the B200 batched-hash engine (the BASELINE.json north-star path).
 
 Default workload = BASELINE.json configs[1]: MD5 over 2^24 random 1 KiB
-messages per GPU (weak scaling under torchrun: rank r hashes global messages
+messages per GPU (weak scaling: rank r hashes global messages
 [r*2^24, (r+1)*2^24)).  Prints ONE JSON line (rank 0):
 
   value        kernel-only GB/s of message bytes, inputs resident in HBM: one
                CUDA-event pair on the launching stream around K back-to-back
                steps, max over ranks; bytes summed over ranks
-  e2e          the same metric through the public API (crypto.batch_digest /
-               batch_digest_varlen / hash_decimal on pinned host arrays):
-               H2D + kernels + D2H every step; its roofline is the pinned-copy
-               bandwidth measured in the same run
-  roofline     the dominant kernel vs the HBM copy peak or the ALU-pipe peak
-  cpu_baseline the CPU oracle (C port of the reference algorithm) on a bounded
-               sample of the same bytes, all host threads; its digests are also
-               compared bit-for-bit with the GPU's for that sample
+  e2e          the same metric through the public API (crypto.batch_digest on
+               a pinned host array): H2D + kernels + D2H every step;
+               e2e_pageable: the reference call shape (pageable numpy in, fresh
+               array out)
+  roofline     the kernel that ran (its name from the library), against the
+               HBM copy peak or the ALU-pipe peak (+ the dependent-chain bound)
+  cpu_baseline the CPU oracle (C port of the reference algorithm) on the same
+               bytes, all host threads; its digests are compared with the GPU's
+  configs      every other BASELINE config measured the same way in the same
+               run: C1 (SHA-1 65,536 x 64 B), C3 (SM3 2^24 x 1 KiB split over
+               the GPUs), C4 (varlen U(1, 4 KiB) x 3 algorithms) and a reduced
+               C5 grid (16 B / 1 KiB / 64 KiB x three batch counts x 3
+               algorithms), each with kernel-only and e2e rates, roofline,
+               clocks and full-batch parity (N=1; a row sample per rank at N>1)
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--gather none|p2p]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--configs all|none] [--gather none|p2p] [--dry-run]
                   [--workload md5_1k|sha1_1k|sm3_1k|sha1_64|varlen_{md5,sha1,sm3}|paper_{sha1,md5,sm3}]
+
+--gpus N > 1 without WORLD_SIZE in the environment relaunches this script
+under torch.distributed.run with N ranks (one process per GPU); it fails
+loudly when fewer than N GPUs are visible (unless $HB_BENCH_BACKEND=gloo, the
+CPU test hook that lets ranks share GPUs).
 """
 
 from __future__ import annotations
@@ -26,6 +38,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -45,13 +58,16 @@ DLEN = {"sha1": 20, "md5": 16, "sm3": 32}
 # The ALU pipe retires 64 lanes/clk/SM on sm_100 (tools/pipe_bench.cu,
 # profiles/pipe_bench_r1.txt).  DESIGN.md §4 derives these counts.
 ALU_OPS_PER_BLOCK = {"md5": 128, "sha1": 448, "sm3": 1084}
-
-
 # SURVEY.md §8(d)'s roofline, reported alongside: fused integer instructions
 # per block (its Appendix B) at an issue peak of 128 lanes/clk/SM.  It is
 # looser than the ALU-pipe bound above for SHA-1 and SM3 -- their 448 / 1,084
 # boolean/rotate ops can only issue at 64 lanes/clk/SM -- so it reads lower.
 SURVEY_C_ALG = {"md5": 324, "sha1": 613, "sm3": 1412}
+# Dependent-chain latency of one compression (cycles, one warp per SM,
+# tools/bench_configs.py r1): a batch with too few messages to overlap cannot
+# finish before (blocks per message) x this.
+CHAIN_CYCLES = {"md5": 1509, "sha1": 1116, "sm3": 2514}
+_BACKEND = os.environ.get("HB_BENCH_BACKEND", "nccl")
 
 
 def alu_ops_decimal(alg, width):
@@ -132,8 +148,102 @@ def alu_ops_decimal(alg, width):
         raise ValueError(alg)
     return cost
 
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    """SM clock, max clock, power and clock-event (throttle) reasons of one GPU,
+    polled through NVML every 10 ms on a background thread (nvidia-smi -lms
+    as the fallback); begin()/end() bracket a timed region, and end() also
+    takes one synchronous sample so even a sub-10 ms region has a record."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples: list[tuple] = []  # (t, sm_mhz, max_mhz, power_w, reasons bitmask)
+        self.stop_ev = threading.Event()
+        self.thread = None
+        self.nvml = None
+        self.handle = None
+        self.source = "none"
+
+    def _query(self):
+        n = self.nvml
+        h = self.handle
+        sm = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
+        mx = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
+        try:
+            pw = n.nvmlDeviceGetPowerUsage(h) / 1000.0
+        except Exception:
+            pw = None
+        try:
+            rs = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            rs = n.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        return (time.perf_counter(), float(sm), float(mx), pw, int(rs))
+
+    def start(self):
+        try:
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(self.gpu).uuid).lower().removeprefix("gpu-")
+            for i in range(pynvml.nvmlDeviceGetCount()):
+                h = pynvml.nvmlDeviceGetHandleByIndex(i)
+                u = pynvml.nvmlDeviceGetUUID(h)
+                u = (u.decode() if isinstance(u, bytes) else u).lower().removeprefix("gpu-")
+                if u == uuid:
+                    self.handle = h
+            if self.handle is None:
+                self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.nvml = pynvml
+            self._query()
+            self.source = "NVML, 10 ms"
+        except Exception:
+            self.nvml = None
+            self.source = "unavailable"
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def _run(self):
+        while not self.stop_ev.wait(0.01):
+            try:
+                self.samples.append(self._query())
+            except Exception:
+                pass
+
+    def begin(self):
+        return time.perf_counter()
+
+    def end(self, t0):
+        if self.nvml is not None:
+            try:
+                self.samples.append(self._query())
+            except Exception:
+                pass
+        return self.summary([s for s in self.samples if s[0] >= t0])
+
+    def stop(self):
+        self.stop_ev.set()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self, samples):
+        if not samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": self.source}
+        reasons = sorted({name for s in samples for name, bit in self.REASONS.items() if s[4] & bit})
+        pw = [s[3] for s in samples if s[3] is not None]
+        return {"sm_mhz": statistics.median(s[1] for s in samples), "sm_min_mhz": min(s[1] for s in samples),
+                "sm_max_mhz": max(s[2] for s in samples), "power_w_max": round(max(pw), 1) if pw else None,
+                "reasons": reasons, "samples": len(samples), "source": self.source}
+
+
+
 WORKLOADS = {
-    # name: (alg | "varlen:"alg, n per GPU, msg_len | max varlen length, seed, BASELINE config)
+    # name: (alg | "varlen:"alg | "decimal:"alg | "strong:"alg, n per GPU, msg_len | max varlen length, seed, BASELINE config)
     "md5_1k": ("md5", 1 << 24, 1024, 2, "configs[1]: MD5 over 2^24 random 1 KiB messages per B200"),
     "sha1_1k": ("sha1", 1 << 24, 1024, 2, "SHA-1 over 2^24 random 1 KiB messages per B200 (configs[4] point)"),
     "sm3_1k": ("strong:sm3", 1 << 24, 1024, 3,
@@ -147,83 +257,38 @@ WORKLOADS = {
     "paper_sm3": ("decimal:sm3", 10**9, 9, 0, "paper workload: 10^9 x 9-digit messages, PAPER.md:206"),
 }
 
+# The reduced configs[4] grid of the suite: message size -> batch counts per
+# GPU (at most 16 GiB of messages per GPU), x the three algorithms.
+C5_GRID = {16: (1 << 16, 1 << 20, 1 << 24), 1024: (1 << 16, 1 << 20, 1 << 24), 65536: (1 << 12, 1 << 16, 1 << 18)}
+C5_SEED = 5000
+
+
+def suite_specs():
+    """(entry name, WORKLOADS-style spec) of every BASELINE config besides the headline."""
+    out = [("C1_sha1_64", WORKLOADS["sha1_64"]), ("C3_sm3_1k", WORKLOADS["sm3_1k"])]
+    for alg in ("md5", "sha1", "sm3"):
+        out.append((f"C4_varlen_{alg}", WORKLOADS[f"varlen_{alg}"]))
+    k = 0
+    for alg in ("md5", "sha1", "sm3"):
+        for L, counts in C5_GRID.items():
+            for n in counts:
+                out.append((f"C5_{alg}_{L}x{n}",
+                            (alg, n, L, C5_SEED + k, f"configs[4] point: {alg} {n} x {L} B per GPU")))
+                k += 1
+    return out
+
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-# ----------------------------------------------------------------- clocks --
-class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 50 ms while active."""
-
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, gpu: int):
-        self.gpu = gpu
-        self.proc = None
-        self.lines: list[str] = []
-        self.active = False
-        self.thread = None
-
-    def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
-            return
-        self.thread = threading.Thread(target=self._read, daemon=True)
-        self.thread.start()
-
-    def _read(self):
-        for line in self.proc.stdout:
-            if self.active:
-                self.lines.append(line.strip())
-
-    def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-
-    def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 9:
-                continue
-            try:
-                sm.append(float(p[1]))
-                mx.append(float(p[2]))
-            except ValueError:
-                continue
-            for name, v in zip(names, p[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
-
-
 # ------------------------------------------------------------ distributed --
-# $HB_BENCH_BACKEND=gloo (test hook): run the N>1 path with ranks sharing the
-# visible GPUs round-robin -- NCCL needs one GPU per rank, gloo does not -- so
-# the multi-rank bench (sharding, max-over-ranks timing, the fused P2P gather)
-# can be exercised on a one-GPU box.  Production runs use NCCL, one GPU per rank.
-_BACKEND = os.environ.get("HB_BENCH_BACKEND", "nccl")
+HOST = {"affinity": "unbound (one process, N=1)"}
 
 
-HOST_AFFINITY = ["unbound (one process, N=1)"]
-
-
-def dist_setup(args):
+def dist_setup():
+    """Process group (NCCL, one GPU per rank; gloo with ranks sharing GPUs as
+    the CPU test hook) and this rank's host side bound to its GPU's NUMA node."""
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -234,20 +299,32 @@ def dist_setup(args):
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if _BACKEND == "gloo":
-            local = local % torch.cuda.device_count()
+            local = local % max(1, torch.cuda.device_count())
             torch.cuda.set_device(local)
             dist.init_process_group("gloo")
         else:
             torch.cuda.set_device(local)
+            t0 = time.perf_counter()
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        # host side next to this rank's GPU (pinned e2e buffers are allocated later)
+            log(f"[rank {rank}] NCCL communicator on cuda:{local} initialised in "
+                f"{(time.perf_counter() - t0) * 1e3:.0f} ms (world {world})")
         from paper_2407_09333_b200.device import bind_host_to_gpu
 
         cores = bind_host_to_gpu(local)
-        HOST_AFFINITY[0] = f"{len(cores)} GPU-local cores (NVML)" if cores else "unbound (NVML gave no mask)"
+        HOST["affinity"] = f"{len(cores)} GPU-local cores (NVML)" if cores else "unbound (NVML gave no mask)"
     else:
         torch.cuda.set_device(0)
     return world, rank, local
+
+
+def rank_record(rank, local):
+    import torch
+
+    p = torch.cuda.get_device_properties(local)
+    return {"rank": rank, "local_rank": local, "cuda_device": local, "gpu": p.name,
+            "pci_bus_id": f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}",
+            "uuid": str(p.uuid), "pid": os.getpid(), "host": socket.gethostname(),
+            "cpu_affinity": len(os.sched_getaffinity(0)), "host_affinity": HOST["affinity"]}
 
 
 def barrier(world):
@@ -257,17 +334,46 @@ def barrier(world):
         dist.barrier()
 
 
-def reduce_max(x: float, world: int, local: int) -> float:
+def _reduce(x: float, world: int, local: int, op) -> float:
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
 
     t = torch.tensor([x], dtype=torch.float64, device="cpu" if _BACKEND == "gloo" else f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=op)
     return float(t.item())
 
 
+def reduce_max(x, world, local):
+    import torch.distributed as dist
+
+    return _reduce(x, world, local, dist.ReduceOp.MAX if world > 1 else None)
+
+
+def reduce_min(x, world, local):
+    import torch.distributed as dist
+
+    return _reduce(x, world, local, dist.ReduceOp.MIN if world > 1 else None)
+
+
+def reduce_sum(x, world, local):
+    import torch.distributed as dist
+
+    return _reduce(x, world, local, dist.ReduceOp.SUM if world > 1 else None)
+
+
+def gather_objects(obj, world):
+    if world == 1:
+        return [obj]
+    import torch.distributed as dist
+
+    out = [None] * world
+    dist.all_gather_object(out, obj)
+    return out
+
+
+# ------------------------------------------------------------- peaks/ncu --
 def load_peaks():
     """Roofline denominators: the driver-measured HBM copy bandwidth from
     MEASURED_PEAKS.json ("of measured"), else B200_PROFILING.md's fallback
@@ -292,30 +398,73 @@ def load_peaks():
     return peaks, "fallback (B200_PROFILING.md; MEASURED_PEAKS.json unreadable or without hbm_gbs)"
 
 
-def load_ncu_traffic(workload: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+def load_ncu(name: str):
+    """The committed ncu --set full record of this config's dominant kernel
+    (profiles/ncu_summary.json, tools/ncu_configs.py): dram bytes per launch."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
-        d = json.load(f)
-    k = d.get(workload)
-    return k.get("dram_bytes") if k else None
+        return json.load(f).get(name)
 
 
-# ------------------------------------------------------------ CPU oracle --
-def cpu_sample_rows(alg: str, L: int, n: int, threads: int, target_s: float):
-    """Pick a sample size giving ~target_s seconds of wall time on `threads` threads."""
-    import oracle
+def cpu_info():
+    """lscpu model / sockets x cores / threads and the SHA-NI flag."""
+    info = {"os_cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for ln in out.splitlines():
+            if ":" in ln:
+                k, v = ln.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info.update({"model": kv.get("Model name"), "sockets": kv.get("Socket(s)"),
+                     "cores_per_socket": kv.get("Core(s) per socket"), "threads_per_core": kv.get("Thread(s) per core"),
+                     "numa_nodes": kv.get("NUMA node(s)")})
+        flags = kv.get("Flags", "").split()
+        info["sha_ni"] = "sha_ni" in flags
+    except Exception as e:  # lscpu missing: keep what os gives
+        info["lscpu"] = f"unavailable ({e})"
+    return info
 
-    probe = oracle.fill_random(min(n, 2048) * L, 123).reshape(-1, L)
-    t0 = time.perf_counter()
-    oracle.batch_fixed(alg, probe, threads=1)
-    t = time.perf_counter() - t0
-    per_row = max(t / probe.shape[0], 1e-9)
-    rows = int(target_s * threads / per_row)
-    rows = max(threads * 16, min(n, rows))
-    return rows
+
+# ---------------------------------------------------------- host buffers --
+class PinnedPool:
+    """One page-locked host buffer per role, grown to the largest config and
+    reused (cudaHostAlloc of 16 GiB takes seconds; every config would pay it)."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, role: str, nbytes: int) -> np.ndarray:
+        import ctypes
+
+        from paper_2407_09333_b200 import _native
+
+        lib = _native.lib()
+        cur = self.bufs.get(role)
+        if cur is None or cur[1] < nbytes:
+            if cur is not None:
+                lib.hb_free_pinned(cur[0])
+            size = max(nbytes, 1)
+            p = lib.hb_alloc_pinned(size)
+            if not p:
+                raise MemoryError(f"hb_alloc_pinned({size}) failed: {_native.last_error()}")
+            self.bufs[role] = (p, size)
+            cur = self.bufs[role]
+        arr = np.ctypeslib.as_array(ctypes.cast(cur[0], ctypes.POINTER(ctypes.c_uint8)), shape=(cur[1],))
+        return arr[:nbytes]
+
+    def close(self):
+        from paper_2407_09333_b200 import _native
+
+        for p, _ in self.bufs.values():
+            _native.lib().hb_free_pinned(p)
+        self.bufs.clear()
+
+
+GRAPH_STEPS = 10
+L2_DEFEAT_BYTES = 2 * 126 * 10**6  # twice the B200's 126 MB L2
 
 
 # -------------------------------------------------------------- workloads --
@@ -330,9 +479,9 @@ class FixedWorkload:
         from paper_2407_09333_b200 import device
         from paper_2407_09333_b200.passes import partition_range
 
-        self.name, self.alg, self.L, self.seed, self.desc = name, alg, L, seed, desc
+        self.name, self.alg, self.L, self.seed, self.desc, self.local = name, alg, L, seed, desc, local
         self.scaling = "strong" if strong else "weak"
-        if strong:  # configs[2]: the SAME 2^24 messages split over the GPUs by message range
+        if strong:  # configs[2]: the SAME n messages split over the GPUs by message range
             lo, hi = partition_range(0, n, [1.0 / world] * world)[rank]
             self.total_msgs = n
         else:  # n messages per GPU: rank r hashes global messages [r*n, (r+1)*n)
@@ -341,16 +490,16 @@ class FixedWorkload:
         n = hi - lo
         self.n, self.lo = n, lo
         self.dlen = DLEN[alg]
-        self.buf = torch.empty(n * L, dtype=torch.uint8, device=f"cuda:{local}")
-        device.fill_random(self.buf, seed, byte_offset=lo * L)
-        self.msgs = self.buf.view(n, L)
+        self.buf = torch.empty(max(1, n * L), dtype=torch.uint8, device=f"cuda:{local}")
+        device.fill_random(self.buf[: n * L], seed, byte_offset=lo * L)
+        self.msgs = self.buf[: n * L].view(n, L)
         self.out = torch.empty((n, self.dlen), dtype=torch.uint8, device=f"cuda:{local}")
         self.msg_bytes = n * L
+        self.total_bytes = self.total_msgs * L
         self.alg_bytes = n * (L + self.dlen)  # message bytes read once + digests written once
-        self.blocks = n * ((L + 8) // 64 + 1)
+        self.blocks_per_msg = (L + 8) // 64 + 1
+        self.blocks = n * self.blocks_per_msg
         self.h2d_bytes, self.d2h_bytes = n * L, n * self.dlen
-        # Small batches (a few microseconds of GPU work, configs[0]) are launched
-        # as a CUDA-graph replay so the host call overhead does not idle the GPU.
         # A step of a small batch is a few microseconds of GPU work, less than a
         # launch from Python: those steps run as CUDA-graph replays of
         # GRAPH_STEPS back-to-back passes (each pass hashes the whole batch).
@@ -372,7 +521,6 @@ class FixedWorkload:
                 reps = GRAPH_STEPS // len(group) if len(group) < GRAPH_STEPS else 1
                 self.graphs.append(device.FixedHashGraph(alg, group, self.out, repeats=reps))
             self.graph1s = [device.FixedHashGraph(alg, c, self.out) for c in self.copies]
-        self.graph = self.graphs[0] if self.graphs else None  # kept for callers that test for graph mode
 
     def step(self):
         from paper_2407_09333_b200 import device
@@ -393,35 +541,61 @@ class FixedWorkload:
                 self.graphs[(self.turn % len(self.copies)) // GRAPH_STEPS].replay()
                 self.turn += GRAPH_STEPS
                 k -= GRAPH_STEPS
-            for _ in range(k):
-                self.step()
-        else:
-            for _ in range(k):
-                self.step()
+        for _ in range(k):
+            self.step()
 
     def launches_per_step(self):
         return self.graph1s[0].kernels_per_replay if self.graph1s else None
 
-    def host_inputs(self, lib):
-        import ctypes
+    def probe_kernel(self):
+        """One direct launch (outside any graph): the name of the kernel the dispatch picks."""
+        from paper_2407_09333_b200 import _native, device
 
-        import numpy as np
+        device.hash_fixed(self.alg, self.msgs, out=self.out)
+        return _native.last_kernel_name()
 
-        hp = lib.hb_alloc_pinned(self.n * self.L)
-        if not hp:
-            return None
-        host = np.ctypeslib.as_array(ctypes.cast(hp, ctypes.POINTER(ctypes.c_uint8)),
-                                     shape=(self.n * self.L,)).reshape(self.n, self.L)
+    def free_extra(self):
+        self.graphs, self.graph1s, self.copies = [], [], [self.msgs]
+
+    def stage_host(self, pool):
+        """The same bytes in page-locked host memory (the e2e input and the oracle's)."""
         import torch
 
-        torch.from_numpy(host.reshape(-1)).copy_(self.buf)  # same bytes as the device-resident run
-        self._host = host
-        return hp
+        host = pool.get("in", self.n * self.L)
+        if self.n * self.L:
+            torch.from_numpy(host).copy_(self.buf[: self.n * self.L])
+        self.host = host.reshape(self.n, self.L)
 
-    def e2e_step(self, local, tim):
+    def e2e_step(self, out_host):
         from paper_2407_09333_b200.crypto import batch_digest
 
-        return batch_digest(self.alg, self._host, gpus=[local], timing=tim, out=self._out_host)
+        return batch_digest(self.alg, self.host, gpus=[self.local], out=out_host)
+
+    def e2e_pageable_step(self):
+        from paper_2407_09333_b200.crypto import batch_digest
+
+        return batch_digest(self.alg, self.pageable, gpus=[self.local])
+
+    api = "paper_2407_09333_b200.crypto.batch_digest(pinned host array, out=pinned) -> hb_hash_fixed"
+
+    def parity(self, full, threads):
+        """Oracle digests of the staged bytes vs the device run: every row when
+        `full`, else 65,536 random rows plus the first and last."""
+        import oracle
+
+        dev = self.out.cpu().numpy()
+        t0 = time.perf_counter()
+        if full or self.n <= 65536:
+            ref = oracle.batch_fixed(self.alg, self.host, threads=threads)
+            rows = self.n
+            ok = bool(np.array_equal(ref, dev))
+        else:
+            idx = np.unique(np.concatenate([np.random.default_rng(self.seed).integers(0, self.n, 65536),
+                                            [0, self.n - 1]]))
+            ref = oracle.batch_fixed(self.alg, np.ascontiguousarray(self.host[idx]), threads=threads)
+            rows = len(idx)
+            ok = bool(np.array_equal(ref, dev[idx]))
+        return rows, ok, time.perf_counter() - t0, self.n * self.L if (full or self.n <= 65536) else rows * self.L
 
     def config(self, world):
         what = (f"{self.alg} {self.total_msgs} x {self.L} B fixed-width, split over the GPUs" if self.scaling == "strong"
@@ -429,30 +603,12 @@ class FixedWorkload:
         return {"workload": f"{what} ({self.desc})", "alg": self.alg,
                 "msgs_per_gpu": self.n, "msg_len": self.L, "global_batch_msgs": self.total_msgs,
                 "parallelism": f"message-range shards over {world} GPU(s), no collective",
-                "l2": ("inputs are %.1f GiB per GPU >> 126 MB L2; no flush needed" % (self.n * self.L / 2**30)
+                "l2": ("inputs are %.2f GiB per GPU > 2 x 126 MB L2; no flush needed" % (self.n * self.L / 2**30)
                        if len(self.copies) == 1 else
-                       "%.1f MiB batch rotated over %d identical copies (%.0f MB > 2 x 126 MB L2): each step "
+                       "%.2f MiB batch rotated over %d identical copies (%.0f MB > 2 x 126 MB L2): each step "
                        "reads a copy untouched for %d steps, from HBM" % (self.n * self.L / 2**20, len(self.copies),
                                                                             len(self.copies) * self.n * self.L / 1e6,
                                                                             len(self.copies) - 1))}
-
-    def kernel_name(self):
-        return "k_fixed_tma_ws<%s>" % self.alg
-
-    def cpu_sample(self, threads, target_s):
-        import oracle
-
-        rows = cpu_sample_rows(self.alg, self.L, self.n, threads, target_s)
-        sample = self.buf[: rows * self.L].cpu().numpy().reshape(rows, self.L)
-        t0 = time.perf_counter()
-        ref = oracle.batch_fixed(self.alg, sample, threads=threads)
-        t = time.perf_counter() - t0
-        ok = bool(np.array_equal(ref, self.out[:rows].cpu().numpy()))
-        return rows, rows * self.L, t, ok, f"first {rows} of the {self.n} x {self.L} B messages (same bytes)"
-
-
-GRAPH_STEPS = 10
-L2_DEFEAT_BYTES = 2 * 126 * 10**6  # twice the B200's 126 MB L2
 
 
 class VarlenWorkload:
@@ -460,14 +616,15 @@ class VarlenWorkload:
     layout (data bytes + u64 offsets[n+1])."""
 
     kind = "varlen"
+    scaling = "weak"
 
     def __init__(self, name, alg, n, maxlen, seed, desc, rank, local, world=1):
-        import numpy as np
         import torch
 
         from paper_2407_09333_b200 import _native, device
 
         self.name, self.alg, self.n, self.maxlen, self.seed, self.desc = name, alg, n, maxlen, seed, desc
+        self.local = local
         self.total_msgs = world * n
         self.dlen = DLEN[alg]
         lens = np.random.default_rng(seed + 1000 * rank).integers(1, maxlen + 1, n).astype(np.uint64)
@@ -482,9 +639,12 @@ class VarlenWorkload:
         self.scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch.uint8,
                                    device=f"cuda:{local}")
         self.msg_bytes = total
+        self.total_bytes = int(reduce_sum(float(total), world, local)) if world > 1 else total
         self.alg_bytes = total + 8 * (n + 1) + n * self.dlen
+        self.blocks_per_msg = (maxlen + 8) // 64 + 1
         self.blocks = int(((lens + 8) // 64 + 1).sum())
         self.h2d_bytes, self.d2h_bytes = total + 8 * (n + 1), n * self.dlen
+        self.copies = [self.buf]
 
     def launches_per_step(self):
         return None
@@ -498,23 +658,41 @@ class VarlenWorkload:
 
         device.hash_varlen(self.alg, self.buf, self.d_off, out=self.out, scratch=self.scratch, offset_base=0)
 
-    def host_inputs(self, lib):
-        import ctypes
+    def probe_kernel(self):
+        from paper_2407_09333_b200 import _native
 
-        import numpy as np
+        self.step()
+        return _native.last_kernel_name()
+
+    def free_extra(self):
+        pass
+
+    def stage_host(self, pool):
         import torch
 
-        hp = lib.hb_alloc_pinned(self.total)
-        if not hp:
-            return None
-        self._host = np.ctypeslib.as_array(ctypes.cast(hp, ctypes.POINTER(ctypes.c_uint8)), shape=(self.total,))
-        torch.from_numpy(self._host).copy_(self.buf)
-        return hp
+        host = pool.get("in", self.total)
+        torch.from_numpy(host).copy_(self.buf)
+        self.host = host
 
-    def e2e_step(self, local, tim):
+    def e2e_step(self, out_host):
         from paper_2407_09333_b200.crypto import batch_digest_varlen
 
-        return batch_digest_varlen(self.alg, self._host, self.off, gpus=[local], timing=tim, out=self._out_host)
+        return batch_digest_varlen(self.alg, self.host, self.off, gpus=[self.local], out=out_host)
+
+    api = ("paper_2407_09333_b200.crypto.batch_digest_varlen(pinned host data, offsets, out=pinned) "
+           "-> hb_hash_varlen")
+
+    def parity(self, full, threads):
+        import oracle
+
+        dev = self.out.cpu().numpy()
+        t0 = time.perf_counter()
+        if full:
+            ref = oracle.batch_varlen(self.alg, self.host, self.off, threads=threads)
+            return self.n, bool(np.array_equal(ref, dev)), time.perf_counter() - t0, self.total
+        k = min(self.n, 65536)  # a contiguous run of messages (rank-local offsets)
+        ref = oracle.batch_varlen(self.alg, self.host, self.off[: k + 1], threads=threads)
+        return k, bool(np.array_equal(ref, dev[:k])), time.perf_counter() - t0, int(self.off[k])
 
     def config(self, world):
         return {"workload": f"{self.alg} {self.n} messages of uniform 1-{self.maxlen} B per GPU, offsets layout "
@@ -522,21 +700,8 @@ class VarlenWorkload:
                 "msg_len": f"uniform 1-{self.maxlen}", "bytes_per_gpu": self.total,
                 "global_batch_msgs": world * self.n,
                 "parallelism": f"message-range shards over {world} GPU(s), no collective",
-                "l2": "inputs are %.1f GiB per GPU >> 126 MB L2; no flush needed" % (self.total / 2**30)}
-
-    def kernel_name(self):
-        return "k_varlen16<%s>" % self.alg
-
-    def cpu_sample(self, threads, target_s):
-        import oracle
-
-        k = min(self.n, max(threads * 16, int(self.n * min(1.0, target_s / 8.0))))
-        data = self.buf[: int(self.off[k])].cpu().numpy()
-        t0 = time.perf_counter()
-        ref = oracle.batch_varlen(self.alg, data, self.off[: k + 1], threads=threads)
-        t = time.perf_counter() - t0
-        ok = bool(np.array_equal(ref, self.out[:k].cpu().numpy()))
-        return k, int(self.off[k]), t, ok, f"first {k} of the {self.n} messages (same bytes)"
+                "l2": "inputs are %.1f GiB per GPU >> 126 MB L2; no flush needed" % (self.total / 2**30),
+                "step": "length sort (k_sort_window / k_sort_hist..scatter) + hash kernel, both timed"}
 
 
 class DecimalWorkload:
@@ -561,11 +726,14 @@ class DecimalWorkload:
         self.dlen = DLEN[alg]
         self.out = torch.empty((self.n, self.dlen), dtype=torch.uint8, device=f"cuda:{local}")
         self.msg_bytes = self.n * width
+        self.total_bytes = n * width
         self.alg_bytes = self.n * self.dlen  # message bytes never leave registers
-        self.blocks = self.n * ((width + 8) // 64 + 1)
+        self.blocks_per_msg = (width + 8) // 64 + 1
+        self.blocks = self.n * self.blocks_per_msg
         # ALU-pipe ops per block with the padding words constant-folded
         self.alu_ops_per_block = alu_ops_decimal(alg, width) if width + 9 <= 64 else ALU_OPS_PER_BLOCK[alg]
         self.h2d_bytes, self.d2h_bytes = 0, self.n * self.dlen
+        self.copies = []
 
     def step(self):
         from paper_2407_09333_b200 import device
@@ -579,13 +747,33 @@ class DecimalWorkload:
         for _ in range(k):
             self.step()
 
-    def host_inputs(self, lib):
-        return -1  # nothing to stage: the API call takes only the index range
+    def probe_kernel(self):
+        from paper_2407_09333_b200 import _native
 
-    def e2e_step(self, local, tim):
+        self.step()
+        return _native.last_kernel_name()
+
+    def free_extra(self):
+        pass
+
+    def stage_host(self, pool):
+        self.host = None  # nothing to stage: the API call takes only the index range
+
+    def e2e_step(self, out_host):
         from paper_2407_09333_b200.crypto import hash_decimal
 
-        return hash_decimal(self.alg, self.start, self.n, self.width, gpus=[local], timing=tim, out=self._out_host)
+        return hash_decimal(self.alg, self.start, self.n, self.width, gpus=[self.local], out=out_host)
+
+    api = "paper_2407_09333_b200.crypto.hash_decimal(start, count, 9, out=pinned) -> hb_hash_decimal"
+
+    def parity(self, full, threads):
+        import oracle
+
+        dev = self.out.cpu().numpy()
+        k = self.n if full else min(self.n, 1 << 22)
+        t0 = time.perf_counter()
+        ref = oracle.batch_fixed(self.alg, oracle.gen_decimal(self.start, k, self.width), threads=threads)
+        return k, bool(np.array_equal(ref, dev[:k])), time.perf_counter() - t0, k * self.width
 
     def config(self, world):
         return {"workload": f"{self.alg} over {self.total} messages of {self.width} decimal digits, generated "
@@ -594,25 +782,8 @@ class DecimalWorkload:
                 "parallelism": f"partition_range index split over {world} GPU(s), no collective",
                 "l2": "no input in memory; digests %.1f GB per GPU >> 126 MB L2" % (self.n * self.dlen / 1e9)}
 
-    def kernel_name(self):
-        return "k_decimal<%s, %d>" % (self.alg, self.width)
 
-    def cpu_sample(self, threads, target_s):
-        import oracle
-
-        from paper_2407_09333_b200.crypto import gen_messages
-
-        k = min(self.n, cpu_sample_rows(self.alg, self.width, self.n, threads, target_s))
-        rows = gen_messages(self.start, k, self.width).as_array()
-        t0 = time.perf_counter()
-        ref = oracle.batch_fixed(self.alg, rows, threads=threads)
-        t = time.perf_counter() - t0
-        ok = bool(np.array_equal(ref, self.out[:k].cpu().numpy()))
-        return k, k * self.width, t, ok, f"first {k} of the {self.n} decimal messages (same bytes)"
-
-
-def make_workload(name, rank, local, n_override=0, world=1):
-    spec = WORKLOADS[name]
+def make_workload(name, spec, rank, local, n_override=0, world=1):
     alg = spec[0].split(":")[-1]
     n = n_override or spec[1]
     if spec[0].startswith("decimal:"):
@@ -623,11 +794,11 @@ def make_workload(name, rank, local, n_override=0, world=1):
                          strong=spec[0].startswith("strong:"))
 
 
-def h2d_peak(buf_bytes: int, local: int, d2h: bool = False) -> float:
+def copy_peak(buf_bytes: int, local: int, d2h: bool = False) -> float:
     """Pinned host <-> device copy bandwidth (GB/s) on this GPU's link, same size class."""
     import torch
 
-    nbytes = min(buf_bytes, 1 << 30)
+    nbytes = max(1 << 20, min(buf_bytes, 1 << 30))
     h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{local}")
     src, dst = (d, h) if d2h else (h, d)
@@ -642,208 +813,350 @@ def h2d_peak(buf_bytes: int, local: int, d2h: bool = False) -> float:
     return 3 * nbytes / (s.elapsed_time(e) * 1e-3) / 1e9
 
 
-# ---------------------------------------------------------------- our arm --
-def run_ours(args):
-    import numpy as np  # noqa: F401
+# ------------------------------------------------------------- measuring --
+class Ctx:
+    def __init__(self, args, world, rank, local, sampler, pool):
+        self.args, self.world, self.rank, self.local = args, world, rank, local
+        self.sampler, self.pool = sampler, pool
+        self.peaks, self.peak_src = load_peaks()
+        import torch
+
+        self.sms = torch.cuda.get_device_properties(local).multi_processor_count
+        self.threads = len(os.sched_getaffinity(0)) or (os.cpu_count() or 1)
+        self.bw = {}
+
+    def link_peak(self, nbytes, d2h):
+        key = "d2h" if d2h else "h2d"
+        if key not in self.bw:
+            self.bw[key] = copy_peak(nbytes, self.local, d2h=d2h)
+        return self.bw[key]
+
+
+def time_kernel(w, ctx, steps, warmup, min_region_ms=0.0):
+    """K back-to-back steps between one CUDA-event pair on the launching
+    stream, after W warm-up steps, barrier + synchronize on both sides; clocks
+    sampled during the region; re-measured once on hardware/thermal throttling.
+    min_region_ms > 0 (suite entries): K is raised until the region lasts that
+    long (estimated from the warm-up), so every entry has a clock record."""
     import torch
 
     from paper_2407_09333_b200 import _native
 
-    world, rank, local = dist_setup(args)
-    w = make_workload(args.workload, rank, local, args.msgs, world)
-    alg = w.alg
-    gather = None
-    if args.gather == "p2p" and world > 1 and w.kind == "fixed":
-        # fused device-side gather: each rank's kernel stores its digests into rank 0's buffer (CUDA IPC / NVLink)
-        from paper_2407_09333_b200.distributed import P2PDigestGather
-
-        gather = P2PDigestGather(alg, w.msgs, w.total_msgs)
-        w.graph, w.graphs, w.graph1s, w.copies = None, [], [], [w.msgs]
-        w.step = gather.launch
+    world, rank, local = ctx.world, ctx.rank, ctx.local
     stream = torch.cuda.current_stream(local)
-    sampler = ClockSampler(local)
-    sampler.start()
-    torch.cuda.synchronize()
-
-    for _ in range(args.warmup):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(warmup):
         w.step()
+    e1.record(stream)
     torch.cuda.synchronize()
+    if min_region_ms > 0:
+        est = reduce_max(e0.elapsed_time(e1) / max(1, warmup), world, local)
+        need = int(min_region_ms / max(est, 1e-4)) + 1
+        if need > steps:
+            steps = -(-need // GRAPH_STEPS) * GRAPH_STEPS if w.launches_per_step() else need
     barrier(world)
     torch.cuda.synchronize()
-    # One event pair brackets the K back-to-back steps (whole-job throughput:
-    # per-step event pairs would add a launch latency, ~9 us on this box, to
-    # every small step); a few per-step pairs after it give the spread.
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     remeasured = False
     for attempt in range(2):
-        sampler.lines.clear()
+        mark = ctx.sampler.begin()
         l0 = _native.launch_count()
-        sampler.active = True
         t_wall0 = time.perf_counter()
         t_start.record(stream)
-        w.run_steps(args.steps)
+        w.run_steps(steps)
         t_end.record(stream)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
-        sampler.active = False
+        clk = ctx.sampler.end(mark)
         launches = _native.launch_count() - l0
         # a region that saw hardware / thermal throttling is measured once more
         # (sw_power_cap is the normal state of a long integer kernel: kept, noted)
-        bad = set(sampler.summary()["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+        bad = set(clk["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
         if attempt == 1 or not reduce_max(1.0 if bad else 0.0, world, local):
             break
-        log(f"[rank {rank}] throttling during the timed region ({sorted(bad)}): re-measuring once")
+        log(f"[rank {rank}] {w.name}: throttling during the timed region ({sorted(bad)}): re-measuring once")
         remeasured = True
         barrier(world)
         torch.cuda.synchronize()
-    if gather is not None:  # the gather wrote into rank 0's buffer; refill the local digests for the checks below
-        from paper_2407_09333_b200 import device as _device
-
-        _device.hash_fixed(alg, w.msgs, out=w.out)
-        torch.cuda.synchronize()
-    if w.launches_per_step() is not None:  # CUDA-graph replays are not seen by the launch counter
-        launches = w.launches_per_step() * args.steps
-    barrier(world)
-    ms_local = t_start.elapsed_time(t_end) / args.steps
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
-    for s, e in evs:  # spread of single steps (not part of the timed value)
-        s.record(stream)
-        w.step()
-        e.record(stream)
-    torch.cuda.synchronize()
-    per_step = [s.elapsed_time(e) for s, e in evs]
-    ms = reduce_max(ms_local, world, local)
-    total_msgs = w.total_msgs  # messages hashed by all ranks in one step
-    total_bytes = w.msg_bytes * world if w.kind == "varlen" else total_msgs * (w.L if w.kind == "fixed" else w.width)
-    value = total_bytes / (ms * 1e-3) / 1e9
-    mhash = total_msgs / (ms * 1e-3) / 1e6
-    log(f"[rank {rank}] kernel-only {w.name}: {ms_local:.4f} ms/step over {args.steps} back-to-back steps "
-        f"(single steps {min(per_step):.4f}-{max(per_step):.4f}); wall {t_wall * 1e3 / args.steps:.3f} ms/step; "
-        f"{launches} launches")
-
-    # ---- end to end through the public API: pinned host input -> hb_hash_fixed / hb_hash_varlen
-    e2e = None
-    lib = _native.lib()
-    hp = w.host_inputs(lib) if not args.no_e2e else None
-    hpo = lib.hb_alloc_pinned(w.n * w.dlen) if hp else None
-    if hp and hpo:
-        import ctypes
-
-        # digests land in one page-locked array reused across steps (the API's out= argument)
-        w._out_host = np.ctypeslib.as_array(ctypes.cast(hpo, ctypes.POINTER(ctypes.c_uint8)),
-                                            shape=(w.n * w.dlen,)).reshape(w.n, w.dlen)
-        e2e_steps = args.e2e_steps or min(args.steps, 3 if w.kind == "decimal" else 10)
-        tim = {}
-        for _ in range(max(1, min(args.warmup, 2))):
-            w.e2e_step(local, tim)
-        barrier(world)
-        torch.cuda.synchronize()
-        sampler.active = True
-        l1 = _native.launch_count()
-        t0 = time.perf_counter()
-        for k in range(e2e_steps):  # engine stage timings from the last step only (the API's default is untimed)
-            res = w.e2e_step(local, tim if k == e2e_steps - 1 else None)
-        t1 = time.perf_counter()
-        sampler.active = False
-        e2e_launches = _native.launch_count() - l1
-        barrier(world)
-        e2e_ms = reduce_max((t1 - t0) * 1e3 / e2e_steps, world, local)
-        if res.shape[0] <= (1 << 24):
-            ok = bool(np.array_equal(res, w.out.cpu().numpy()))
-        else:  # very large outputs (paper workload: 10^9 digests): compare a row sample
-            import torch
-
-            idx = np.unique(np.random.default_rng(0).integers(0, res.shape[0], 1 << 16))
-            ok = bool(np.array_equal(res[idx], w.out[torch.from_numpy(idx).to(w.out.device)].cpu().numpy()))
-        bw = h2d_peak(max(w.h2d_bytes, w.d2h_bytes), local, d2h=w.h2d_bytes < w.d2h_bytes)
-        e2e_gbs = total_bytes / (e2e_ms * 1e-3) / 1e9
-        # per-step bytes over all ranks (fixed/decimal: exact from the global message count)
-        if w.kind == "varlen":
-            h2d_tot, d2h_tot = world * w.h2d_bytes, world * w.d2h_bytes
-        else:
-            h2d_tot = w.total_msgs * w.L if w.kind == "fixed" else 0
-            d2h_tot = w.total_msgs * w.dlen
-        h2d_gbs = max(h2d_tot, d2h_tot) / (e2e_ms * 1e-3) / 1e9
-        e2e = {"value": round(e2e_gbs, 3), "unit": "GB/s",
-               "h2d_bytes_per_step": h2d_tot, "d2h_bytes_per_step": d2h_tot,
-               "ms_per_step": round(e2e_ms, 3), "mhash_per_s": round(total_msgs / (e2e_ms * 1e-3) / 1e6, 2),
-               "api": ("paper_2407_09333_b200.crypto.batch_digest(pinned host array, out=pinned) -> hb_hash_fixed"
-                       if w.kind == "fixed" else
-                       "paper_2407_09333_b200.crypto.batch_digest_varlen(pinned host data, offsets, out=pinned) "
-                       "-> hb_hash_varlen" if w.kind == "varlen" else
-                       "paper_2407_09333_b200.crypto.hash_decimal(start, count, 9, out=pinned) -> hb_hash_decimal"),
-               "steps": e2e_steps,
-               "roofline": {"bound": "pcie_h2d" if w.h2d_bytes >= w.d2h_bytes else "pcie_d2h",
-                            "achieved": round(h2d_gbs / world, 2), "peak": round(bw, 2),
-                            "unit": "GB/s per GPU", "frac": round(h2d_gbs / world / bw, 4),
-                            "peak_source": "pinned %s copy of 1 GiB on the same GPU, this run"
-                                           % ("host->device" if w.h2d_bytes >= w.d2h_bytes else "device->host")},
-               "engine_timing_last_step": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in tim.items()},
-               "gpu_launches": e2e_launches, "matches_device_run": ok}
-        log(f"[rank {rank}] e2e {e2e_ms:.1f} ms/step, H2D peak {bw:.1f} GB/s, engine {tim}")
-        w._host = None
-        w._out_host = res = None
-        if hp != -1:
-            lib.hb_free_pinned(hp)
-        lib.hb_free_pinned(hpo)
-    sampler.stop()
-
-    # ---- CPU baseline + bit-exact sample check (rank 0, N=1 only)
-    cpu = None
-    parity = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        rows, nbytes, t, ok, what = w.cpu_sample(threads, args.cpu_seconds)
-        parity = {"rows_checked": rows, "bit_exact": ok}
-        fn = "batch_fixed" if w.kind == "fixed" else "batch_varlen"
-        cpu = {"value": round(nbytes / t / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": f"{what}, oracle/hetoc_oracle.c {fn} on {threads} threads, {t:.2f} s",
-               "mhash_per_s": round(rows / t / 1e6, 4)}
-
-    # ---- roofline of the dominant kernel
-    peaks, peak_src = load_peaks()
-    achieved = w.alg_bytes / (ms_local * 1e-3) / 1e9
-    clk = sampler.summary()
     if remeasured:
         clk["remeasured"] = True
+    if w.launches_per_step() is not None:  # CUDA-graph replays are not seen by the launch counter
+        launches = w.launches_per_step() * steps
+    ms_local = t_start.elapsed_time(t_end) / steps
+    ms = reduce_max(ms_local, world, local)
+    return ms_local, ms, launches, clk, t_wall * 1e3 / steps, steps
+
+
+def roofline(w, ctx, ms_local, kernel, name):
+    peaks = ctx.peaks
     f_max = peaks.get("sm_max_mhz", 1965.0)
-    sms = torch.cuda.get_device_properties(local).multi_processor_count
-    alu_peak = sms * 64 * f_max * 1e6  # ALU-pipe lane-ops/s at max clock
-    ops = getattr(w, "alu_ops_per_block", ALU_OPS_PER_BLOCK[alg])
-    alu_ach = w.blocks * ops / (ms_local * 1e-3)
+    alu_peak = ctx.sms * 64 * f_max * 1e6  # ALU-pipe lane-ops/s at max clock
+    ops = getattr(w, "alu_ops_per_block", ALU_OPS_PER_BLOCK[w.alg])
+    t = ms_local * 1e-3
+    achieved = w.alg_bytes / t / 1e9
     t_hbm = w.alg_bytes / (peaks["hbm_gbs"] * 1e9)
     t_alu = w.blocks * ops / alu_peak
-    alu = {"achieved": round(alu_ach / 1e12, 3), "peak": round(alu_peak / 1e12, 3), "unit": "Tops/s",
-           "frac": round(alu_ach / alu_peak, 4), "alu_ops_per_block": ops,
-           "blocks_per_launch": w.blocks, "clock_mhz": f_max}
-    if t_hbm >= t_alu:
+    # a batch too small to overlap its messages' dependent chains is bound by one chain
+    t_chain = w.blocks_per_msg * CHAIN_CYCLES[w.alg] / (f_max * 1e6)
+    alu = {"achieved": round(w.blocks * ops / t / 1e12, 3), "peak": round(alu_peak / 1e12, 3), "unit": "Tops/s",
+           "frac": round(t_alu / t, 4), "alu_ops_per_block": ops, "blocks_per_launch": w.blocks,
+           "clock_mhz": f_max}
+    bound = max((("hbm", t_hbm), ("alu", t_alu), ("chain", t_chain)), key=lambda x: x[1])[0]
+    if bound == "hbm" or (bound == "chain" and t_hbm >= t_alu):
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved / peaks["hbm_gbs"], 4)}
     else:  # integer (ALU-pipe) bound: report against the ALU-pipe roofline, HBM alongside
         roof = {"bound": "alu", "achieved": alu["achieved"], "peak": alu["peak"], "unit": "Tops/s",
                 "frac": alu["frac"], "hbm_achieved_gbs": round(achieved, 1), "hbm_peak_gbs": peaks["hbm_gbs"]}
+    t_roof = max(t_hbm, t_alu, t_chain)
+    roof["max_bound"] = {"bound": bound, "t_ms": {"hbm": round(t_hbm * 1e3, 5), "alu": round(t_alu * 1e3, 5),
+                                                  "chain": round(t_chain * 1e3, 5)},
+                         "frac": round(t_roof / t, 4)}
     if w.kind != "decimal":  # the survey's per-block counts assume arbitrary message words
-        t_int = w.blocks * SURVEY_C_ALG[alg] / (sms * 128 * f_max * 1e6)
+        t_int = w.blocks * SURVEY_C_ALG[w.alg] / (ctx.sms * 128 * f_max * 1e6)
         roof["survey_issue_model"] = {
-            "c_alg": SURVEY_C_ALG[alg], "issue_peak_tops": round(sms * 128 * f_max * 1e6 / 1e12, 3),
-            "t_roof_ms": round(max(t_int, t_hbm) * 1e3, 4),
-            "frac": round(max(t_int, t_hbm) / (ms_local * 1e-3), 4)}
-    roof.update({"traffic": load_ncu_traffic(w.name), "kernel": w.kernel_name(),
-                 "bytes_per_launch": w.alg_bytes, "peak_source": peak_src,
-                 "t_roof_ms": round(max(t_hbm, t_alu) * 1e3, 4), "alu_pipe": alu})
+            "c_alg": SURVEY_C_ALG[w.alg], "issue_peak_tops": round(ctx.sms * 128 * f_max * 1e6 / 1e12, 3),
+            "t_roof_ms": round(max(t_int, t_hbm) * 1e3, 4), "frac": round(max(t_int, t_hbm) / t, 4)}
+    ncu = load_ncu(name)
+    roof.update({"traffic": ncu.get("dram_bytes") if ncu else None,
+                 "traffic_over_algorithmic": round(ncu["dram_bytes"] / w.alg_bytes, 4) if ncu else None,
+                 "ncu_kernel": ncu.get("kernel") if ncu else None, "kernel": kernel,
+                 "bytes_per_launch": w.alg_bytes, "peak_source": ctx.peak_src, "t_roof_ms": round(t_roof * 1e3, 5),
+                 "alu_pipe": alu})
+    return roof
+
+
+def time_e2e(w, ctx, steps, warmup=1):
+    """The same metric through the public API on page-locked host buffers,
+    host->device copies and the digests' device->host copy inside every step."""
+    import torch
+
+    from paper_2407_09333_b200 import _native
+
+    world, local = ctx.world, ctx.local
+    out_host = ctx.pool.get("out", w.n * w.dlen).reshape(w.n, w.dlen)
+    for _ in range(warmup):
+        w.e2e_step(out_host)
+    barrier(world)
+    torch.cuda.synchronize()
+    mark = ctx.sampler.begin()
+    l1 = _native.launch_count()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = w.e2e_step(out_host)
+    t1 = time.perf_counter()
+    clk = ctx.sampler.end(mark)
+    launches = _native.launch_count() - l1
+    barrier(world)
+    e2e_ms = reduce_max((t1 - t0) * 1e3 / steps, world, local)
+    ok = bool(np.array_equal(res, w.out.cpu().numpy())) if w.n <= (1 << 25) else None
+    # one more call with timing= for the engine's stage breakdown (not part of the timed steps)
+    tim = {}
+    if w.kind == "fixed":
+        from paper_2407_09333_b200.crypto import batch_digest
+
+        batch_digest(w.alg, w.host, gpus=[local], out=out_host, timing=tim)
+    elif w.kind == "varlen":
+        from paper_2407_09333_b200.crypto import batch_digest_varlen
+
+        batch_digest_varlen(w.alg, w.host, w.off, gpus=[local], out=out_host, timing=tim)
+    else:
+        from paper_2407_09333_b200.crypto import hash_decimal
+
+        hash_decimal(w.alg, w.start, w.n, w.width, gpus=[local], out=out_host, timing=tim)
+    d2h_dom = w.h2d_bytes < w.d2h_bytes
+    bw = ctx.link_peak(max(w.h2d_bytes, w.d2h_bytes), d2h_dom)
+    h2d_tot = int(reduce_sum(float(w.h2d_bytes), world, local))
+    d2h_tot = int(reduce_sum(float(w.d2h_bytes), world, local))
+    link_gbs = max(w.h2d_bytes, w.d2h_bytes) / (e2e_ms * 1e-3) / 1e9
+    return {"value": round(w.total_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d_tot, "d2h_bytes_per_step": d2h_tot,
+            "ms_per_step": round(e2e_ms, 4), "mhash_per_s": round(w.total_msgs / (e2e_ms * 1e-3) / 1e6, 2),
+            "api": w.api, "steps": steps,
+            "roofline": {"bound": "pcie_d2h" if d2h_dom else "pcie_h2d", "achieved": round(link_gbs, 2),
+                         "peak": round(bw, 2), "unit": "GB/s per GPU", "frac": round(link_gbs / bw, 4),
+                         "peak_source": "pinned %s copy of up to 1 GiB on the same GPU, this run"
+                                        % ("device->host" if d2h_dom else "host->device")},
+            "engine_timing": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in tim.items()},
+            "clocks": clk, "gpu_launches": launches, "matches_device_run": ok}
+
+
+def time_e2e_pageable(w, ctx, steps=2):
+    """The reference call shape: a pageable numpy array in, a fresh digest
+    array out (batch.py:274-290); the engine stages through its pinned ring."""
+    import torch
+
+    from paper_2407_09333_b200.crypto import batch_digest
+
+    w.pageable = np.empty_like(w.host)
+    np.copyto(w.pageable, w.host)
+    batch_digest(w.alg, w.pageable, gpus=[ctx.local])
+    barrier(ctx.world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = batch_digest(w.alg, w.pageable, gpus=[ctx.local])
+    ms = reduce_max((time.perf_counter() - t0) * 1e3 / steps, ctx.world, ctx.local)
+    ok = bool(np.array_equal(res, w.out.cpu().numpy()))
+    w.pageable = None
+    return {"value": round(w.total_bytes / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms, 3),
+            "steps": steps, "api": "paper_2407_09333_b200.crypto.batch_digest(pageable numpy array) -> new array",
+            "matches_device_run": ok}
+
+
+def measure(name, w, ctx, steps, warmup, e2e_steps, full_parity):
+    """One config: kernel-only rate, roofline of the kernel that ran, e2e rate
+    through the public API, clocks, parity against the CPU oracle."""
+    import torch
+
+    args = ctx.args
+    ms_local, ms, launches, clk, wall_ms, steps = time_kernel(w, ctx, steps, warmup, min_region_ms=60.0)
+    kernel = w.probe_kernel()
+    torch.cuda.synchronize()
+    value = w.total_bytes / (ms * 1e-3) / 1e9
+    ent = {"value": round(value, 3), "unit": "GB/s", "ms_per_step": round(ms, 5),
+           "mhash_per_s": round(w.total_msgs / (ms * 1e-3) / 1e6, 2), "steps": steps, "warmup": warmup,
+           "scaling": w.scaling, "config": w.config(ctx.world), "clocks": clk, "gpu_launches": launches,
+           "launch": f"CUDA-graph replays of {GRAPH_STEPS} back-to-back steps" if w.launches_per_step() else
+                     "direct launch per step",
+           "roofline": roofline(w, ctx, ms_local, kernel, name)}
+    log(f"[rank {ctx.rank}] {name}: {ms_local:.5f} ms/step ({value:.1f} GB/s), wall {wall_ms:.4f} ms/step, "
+        f"{launches} launches, kernel {kernel.split('(')[0]}")
+    w.free_extra()
+    w.stage_host(ctx.pool)
+    if not args.no_e2e:
+        ent["e2e"] = time_e2e(w, ctx, e2e_steps)
+        log(f"[rank {ctx.rank}] {name} e2e {ent['e2e']['ms_per_step']:.3f} ms/step ({ent['e2e']['value']} GB/s)")
+    rows, ok, t_cpu, nbytes = w.parity(full_parity, ctx.threads)
+    rows_all = int(reduce_sum(float(rows), ctx.world, ctx.local))
+    ok_all = bool(reduce_min(1.0 if ok else 0.0, ctx.world, ctx.local))
+    ent["parity"] = {"rows_checked": rows_all, "rows_total": w.total_msgs, "bit_exact": ok_all,
+                     "oracle": "oracle/hetoc_oracle.c (C restatement of hetoc.crypto)",
+                     "scope": "every row" if full_parity else "65,536 random rows per rank (+ first/last)"}
+    ent["_cpu"] = (rows, nbytes, t_cpu)
+    log(f"[rank {ctx.rank}] {name} parity {rows}/{w.n} rows bit_exact={ok} ({t_cpu:.1f} s on {ctx.threads} threads)")
+    return ent
+
+
+def measure_latency(ctx):
+    """Per-call latency of the drop-in API on tiny inputs (the reference's
+    scalar digest and a 4 KiB _fast_digest-sized batch_digest)."""
+    from paper_2407_09333_b200.crypto import batch_digest, digest
+
+    out = {}
+    msg = b"abc"
+    small = np.frombuffer(os.urandom(4096), np.uint8).reshape(64, 64).copy()
+    for _ in range(20):
+        digest("sha1", msg)
+        batch_digest("sha1", small)
+    for key, fn in (("digest_us", lambda: digest("sha1", msg)),
+                    ("batch_digest_4KiB_us", lambda: batch_digest("sha1", small))):
+        ts = []
+        for _ in range(200):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        out[key] = round(statistics.median(ts) * 1e6, 1)
+    out["note"] = "median of 200 calls, default device set (small calls run on one GPU), pageable input"
+    return out
+
+
+# ---------------------------------------------------------------- our arm --
+def run_ours(args):
+    import torch
+
+    from paper_2407_09333_b200 import _native
+
+    world, rank, local = dist_setup()
+    ranks = gather_objects(rank_record(rank, local), world)
+    sampler = ClockSampler(local)
+    sampler.start()
+    pool = PinnedPool()
+    ctx = Ctx(args, world, rank, local, sampler, pool)
+    spec = WORKLOADS[args.workload]
+    w = make_workload(args.workload, spec, rank, local, args.msgs, world)
+    gather = None
+    if args.gather == "p2p" and world > 1 and w.kind == "fixed":
+        # fused device-side gather: each rank's kernel stores its digests into rank 0's buffer (CUDA IPC / NVLink)
+        from paper_2407_09333_b200.distributed import P2PDigestGather
+
+        gather = P2PDigestGather(w.alg, w.msgs, w.total_msgs)
+        w.graphs, w.graph1s, w.copies = [], [], [w.msgs]
+        w.step = gather.launch
+    torch.cuda.synchronize()
+    ms_local, ms, launches, clk, wall_ms, _ = time_kernel(w, ctx, args.steps, args.warmup)
+    if gather is not None:  # the gather wrote into rank 0's buffer; refill the local digests for the checks below
+        from paper_2407_09333_b200 import device as _device
+
+        _device.hash_fixed(w.alg, w.msgs, out=w.out)
+        torch.cuda.synchronize()
+    kernel = w.probe_kernel()
+    value = w.total_bytes / (ms * 1e-3) / 1e9
+    log(f"[rank {rank}] headline {w.name}: {ms_local:.4f} ms/step, wall {wall_ms:.3f} ms/step, {launches} launches")
+    roof = roofline(w, ctx, ms_local, kernel, args.workload)
+    w.free_extra()
+    w.stage_host(pool)
+    e2e = e2e_pageable = None
+    if not args.no_e2e:
+        e2e = time_e2e(w, ctx, args.e2e_steps or min(args.steps, 3 if w.kind == "decimal" else 10))
+        if w.kind == "fixed":
+            e2e_pageable = time_e2e_pageable(w, ctx)
+        log(f"[rank {rank}] e2e {e2e['ms_per_step']:.1f} ms/step; pageable "
+            f"{e2e_pageable['ms_per_step'] if e2e_pageable else '-'} ms/step")
+    full = world == 1 and not args.sample_parity
+    rows, ok, t_cpu, nbytes = w.parity(full, ctx.threads)
+    rows_all = int(reduce_sum(float(rows), world, local))
+    ok_all = bool(reduce_min(1.0 if ok else 0.0, world, local))
+    parity = {"rows_checked": rows_all, "rows_total": w.total_msgs, "bit_exact": ok_all,
+              "scope": "every row" if full else "65,536 random rows per rank (+ first/last)"}
+    cpu = None
+    if rank == 0 and world == 1:
+        cpu = {"value": round(nbytes / t_cpu / 1e9, 4), "unit": "GB/s", "cores": ctx.threads, "kind": "port",
+               "sample": f"{'all' if full else rows} of the {w.n} messages (same bytes), oracle/hetoc_oracle.c on "
+                         f"{ctx.threads} threads, {t_cpu:.2f} s", "mhash_per_s": round(rows / t_cpu / 1e6, 4),
+               "host_cpu": cpu_info()}
+    latency = measure_latency(ctx) if rank == 0 and not args.no_e2e else None
+    head = {"config": w.config(world), "scaling": w.scaling, "total_msgs": w.total_msgs, "kind": w.kind,
+            "seed": w.seed}
+    del w
+    torch.cuda.empty_cache()
+
+    configs = {}
+    if args.configs == "all":
+        t_suite = time.perf_counter()
+        for name, sspec in suite_specs():
+            if world == 1 and name in ("C5_md5_1024x16777216",):  # == the headline at N=1
+                configs[name] = {"same_as": "headline (configs[1])"}
+                continue
+            if world == 1 and name == "C5_sm3_1024x16777216":  # == C3 at N=1
+                configs[name] = {"same_as": "C3_sm3_1k"}
+                continue
+            sw = make_workload(name, sspec, rank, local, 0, world)
+            steps = max(3, min(args.steps, 20))
+            configs[name] = measure(name, sw, ctx, steps, max(3, min(args.warmup, 5)),
+                                    args.suite_e2e_steps, world == 1 and not args.sample_parity)
+            cpu_rows, cpu_bytes, cpu_t = configs[name].pop("_cpu")
+            if rank == 0 and world == 1:
+                configs[name]["cpu_oracle"] = {"value": round(cpu_bytes / cpu_t / 1e9, 4), "unit": "GB/s",
+                                               "cores": ctx.threads, "seconds": round(cpu_t, 2)}
+            del sw
+            torch.cuda.empty_cache()
+        log(f"[rank {rank}] suite of {len(configs)} configs in {time.perf_counter() - t_suite:.1f} s")
+    sampler.stop()
+    pool.close()
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-                "higher_is_better": True, "scaling": getattr(w, "scaling", "weak"), "vs_baseline": None,
-                "dtype": "u32",
-                "data": ("paper workload: decimal messages generated in-kernel" if w.kind == "decimal" else
-                         f"synthetic: counter-based splitmix64 bytes (seed {w.seed}), generated on device"),
-                "config": dict(w.config(world), launch=f"CUDA-graph replays of {GRAPH_STEPS} back-to-back steps"
-                               if w.launches_per_step() else "direct launch per step",
-                               gather="fused P2P into rank 0 (CUDA IPC)" if gather is not None else "none",
-                               host_affinity=HOST_AFFINITY[0]),
-                "mhash_per_s": round(mhash, 2), "clocks": clk, "e2e": e2e,
-                "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "parity": parity}
+                "higher_is_better": True, "scaling": head["scaling"], "vs_baseline": None, "dtype": "u32",
+                "data": ("paper workload: decimal messages generated in-kernel" if head["kind"] == "decimal" else
+                         f"synthetic: counter-based splitmix64 bytes (seed {head['seed']}), generated on device"),
+                "config": dict(head["config"], gather="fused P2P into rank 0 (CUDA IPC)" if gather is not None
+                               else "none", host_affinity=HOST["affinity"]),
+                "mhash_per_s": round(head["total_msgs"] / (ms * 1e-3) / 1e6, 2), "clocks": clk,
+                "e2e": e2e, "e2e_pageable": e2e_pageable, "latency": latency,
+                "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "parity": parity,
+                "ranks": ranks, "configs": configs}
         print(json.dumps(line), flush=True)
     if gather is not None:
         gather.close()
@@ -854,64 +1167,113 @@ def run_ours(args):
 
 
 # --------------------------------------------------------- reference arm --
+def numpy_reference(alg, data, budget_s):
+    """The reference's own batch_digest (hetoc.crypto, numpy) as installed in
+    baseline/_ref, when present: 1 core as-is, and a process pool over the
+    np.linspace split of batch.py:305 on every host core -- a stated baseline
+    beside the C port (SURVEY §8(d) CPU reference timing 1-2)."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "hetoc")):
+        return {"unavailable": "baseline/_ref not installed on this box"}
+    code = r'''
+import json, os, sys, time
+import numpy as np
+from multiprocessing import Pool
+sys.path.insert(0, sys.argv[1])
+from hetoc.crypto import batch_digest
+alg, n, L, seed, budget = sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]), float(sys.argv[6])
+rng = np.random.default_rng(seed)
+data = rng.integers(0, 256, (n, L), dtype=np.uint8)
+t0 = time.perf_counter(); batch_digest(alg, data[:4096]); t1 = time.perf_counter()
+per_row = (t1 - t0) / 4096
+rows1 = int(max(4096, min(n, budget / 2 / per_row)))
+t0 = time.perf_counter(); batch_digest(alg, data[:rows1]); one = time.perf_counter() - t0
+cores = len(os.sched_getaffinity(0))
+rowsp = int(max(cores * 4096, min(n, budget / 2 / per_row * cores)))
+def part(b):
+    return batch_digest(alg, data[b[0]:b[1]])
+bounds = np.linspace(0, rowsp, cores + 1, dtype=np.int64)
+with Pool(cores) as p:
+    p.map(part, [(0, 1)] * cores)
+    t0 = time.perf_counter(); p.map(part, list(zip(bounds[:-1], bounds[1:]))); pool = time.perf_counter() - t0
+print(json.dumps({"one_core": {"value": rows1 * L / one / 1e9, "rows": rows1, "seconds": one},
+                  "pool": {"value": rowsp * L / pool / 1e9, "rows": rowsp, "seconds": pool, "cores": cores}}))
+'''
+    try:
+        n, L = data
+        out = subprocess.run([sys.executable, "-c", code, ref_dir, alg, str(n), str(L), "7", str(budget_s)],
+                             capture_output=True, text=True, timeout=budget_s * 4 + 120)
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+        return {"one_core_gbs": round(r["one_core"]["value"], 4), "pool_gbs": round(r["pool"]["value"], 4),
+                "pool_cores": r["pool"]["cores"],
+                "sample": f"{r['one_core']['rows']} rows on 1 core, {r['pool']['rows']} rows over a process pool "
+                          f"(np.linspace split, batch.py:305) of {L} B random messages",
+                "api": "hetoc.crypto.batch_digest (baseline/_ref, unmodified reference)"}
+    except Exception as e:
+        return {"unavailable": f"reference run failed: {type(e).__name__}: {str(e)[:200]}"}
+
+
 def run_reference(args):
-    """The reference algorithm's CPU implementation (oracle port of hetoc.crypto;
-    the reference itself is pure Python/numpy and is not installed on the box)
-    on all host threads, each step a bounded sample of the same workload."""
-    # each step a bounded sample: --ref-step-seconds, shrunk so the whole
-    # --steps K --warmup W run stays within --ref-budget-seconds
-    step_s = min(args.ref_step_seconds, max(0.05, args.ref_budget_seconds / max(1, args.steps + args.warmup)))
+    """The reference algorithm's CPU implementation on all host threads: the
+    oracle port of hetoc.crypto (the reference is pure Python/numpy, 10-50x
+    slower than the port), each step the FULL batch of the headline config
+    when the whole --steps K --warmup W run fits --ref-budget-seconds, else a
+    bounded sample; the numpy reference itself is timed beside it when
+    baseline/_ref exists."""
     import oracle
 
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     spec = WORKLOADS[args.workload]
     alg = spec[0].split(":")[-1]
     n = args.msgs or spec[1]
     seed, cfg_desc = spec[3], spec[4]
-    threads = os.cpu_count() or 1
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    threads = len(os.sched_getaffinity(0)) or (os.cpu_count() or 1)
+    total_steps = max(1, args.steps + args.warmup)
+    step_budget = args.ref_budget_seconds / total_steps
+    strong = spec[0].startswith(("strong:", "decimal:"))
+    # the same per-GPU work as our arm at N GPUs: weak configs n per GPU (one GPU's share here), strong the whole batch / N
+    n_cpu = n if not strong else -(-n // world)
     if spec[0].startswith("decimal:"):
-        from paper_2407_09333_b200.crypto import gen_messages
-
         width = spec[2]
-        rows = cpu_sample_rows(alg, width, n, threads, step_s)
-        data = gen_messages(0, rows, width).as_array()
+        per = cpu_rate_probe(lambda k: oracle.batch_fixed(alg, oracle.gen_decimal(0, k, width), threads=1), 1 << 14)
+        rows = min(n_cpu, max(threads * 16, int(step_budget * threads / per)))
+        data = oracle.gen_decimal(0, rows, width)
         run = lambda: oracle.batch_fixed(alg, data, threads=threads)  # noqa: E731
         nbytes = rows * width
-        sample = f"messages 0..{rows - 1} of the {n} decimal messages per step"
-        config = {"workload": f"{alg} over {n} messages of {width} decimal digits, generated in-kernel ({cfg_desc})",
-                  "alg": alg, "msgs_total": n, "msgs_per_gpu": n // world, "msg_len": width}
+        config = {"workload": f"{alg} over {n} messages of {width} decimal digits ({cfg_desc})", "alg": alg,
+                  "msgs_total": n, "msg_len": width}
+        np_ref = None
     elif spec[0].startswith("varlen:"):
         maxlen = spec[2]
         lens = np.random.default_rng(seed).integers(1, maxlen + 1, n).astype(np.uint64)
-        probe_k = min(n, 2048)
         off = np.zeros(n + 1, np.uint64)
         off[1:] = np.cumsum(lens)
+        probe_k = min(n, 2048)
         probe = oracle.fill_random(int(off[probe_k]), seed)
-        t0 = time.perf_counter()
-        oracle.batch_varlen(alg, probe, off[: probe_k + 1], threads=1)
-        per_msg = max((time.perf_counter() - t0) / probe_k, 1e-9)
-        k = max(threads * 16, min(n, int(step_s * threads / per_msg)))
-        data = oracle.fill_random(int(off[k]), seed)
-        run = lambda: oracle.batch_varlen(alg, data, off[: k + 1], threads=threads)  # noqa: E731
-        nbytes, rows = int(off[k]), k
-        sample = f"first {k} of the {n} messages (uniform 1-{maxlen} B) per step"
+        per = cpu_rate_probe(lambda k: oracle.batch_varlen(alg, probe, off[: k + 1], threads=1), probe_k)
+        rows = min(n, max(threads * 16, int(step_budget * threads / per)))
+        data = oracle.fill_random(int(off[rows]), seed)
+        run = lambda: oracle.batch_varlen(alg, data, off[: rows + 1], threads=threads)  # noqa: E731
+        nbytes = int(off[rows])
         config = {"workload": f"{alg} {n} messages of uniform 1-{maxlen} B per GPU, offsets layout ({cfg_desc})",
                   "alg": alg, "msgs_per_gpu": n, "msg_len": f"uniform 1-{maxlen}"}
+        np_ref = None
     else:
         L = spec[2]
-        rows = cpu_sample_rows(alg, L, n, threads, step_s)
+        probe = oracle.fill_random(2048 * L, 123).reshape(2048, L)
+        per = cpu_rate_probe(lambda k: oracle.batch_fixed(alg, probe[:k], threads=1), 2048)
+        rows = min(n_cpu, max(threads * 16, int(step_budget * threads / per * 0.9)))
         data = oracle.fill_random(rows * L, seed).reshape(rows, L)
         run = lambda: oracle.batch_fixed(alg, data, threads=threads)  # noqa: E731
         nbytes = rows * L
-        sample = f"{rows} of the {n} x {L} B messages per step"
-        strong = spec[0].startswith("strong:")
         what = (f"{alg} {n} x {L} B fixed-width, split over the GPUs" if strong
                 else f"{alg} {n} x {L} B fixed-width per GPU")
-        config = {"workload": f"{what} ({cfg_desc})", "alg": alg, "msgs_per_gpu": n // world if strong else n,
-                  "msg_len": L}
+        config = {"workload": f"{what} ({cfg_desc})", "alg": alg, "msgs_per_gpu": n_cpu, "msg_len": L}
+        np_ref = numpy_reference(alg, (min(n, 1 << 20), L), args.numpy_ref_seconds) if not args.no_numpy_ref else None
+    same = rows == n_cpu
     for _ in range(args.warmup):
         run()
     times = []
@@ -921,40 +1283,118 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
     value = nbytes / t / 1e9
-    dec = spec[0].startswith("decimal:") or spec[0].startswith("strong:")
+    sample = (f"the full batch ({rows} messages = one GPU's share at N={world}) per step" if same else
+              f"{rows} of the {n_cpu} messages per step (bounded: --ref-budget-seconds {args.ref_budget_seconds})")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
-            "scaling": "strong" if dec else "weak", "vs_baseline": None, "dtype": "u32",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "u32",
             "data": "paper workload: decimal messages (gen_messages)" if spec[0].startswith("decimal:") else
                     f"synthetic: counter-based splitmix64 bytes (seed {seed})", "config": config,
+            "same_config": same,
             "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "port",
                              "sample": f"{sample}, oracle/hetoc_oracle.c (C restatement of hetoc.crypto) "
-                                       f"on {threads} threads"},
+                                       f"on {threads} threads", "host_cpu": cpu_info()},
             "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "mhash_per_s": round(rows / t / 1e6, 4)}
+            "mhash_per_s": round(rows / t / 1e6, 4), "reference_numpy": np_ref}
     print(json.dumps(line), flush=True)
+
+
+def cpu_rate_probe(fn, k):
+    """Seconds per message of fn on one thread (k messages)."""
+    fn(min(k, 64))
+    t0 = time.perf_counter()
+    fn(k)
+    return max((time.perf_counter() - t0) / k, 1e-9)
+
+
+# -------------------------------------------------------------- launching --
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(args):
+    """--gpus N is authoritative: without WORLD_SIZE, N > 1 relaunches this
+    script under torch.distributed.run (one rank per GPU); returns the exit
+    code, or None when this process is already the right one."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None:
+        if int(env_world) != args.gpus:
+            log(f"error: --gpus {args.gpus} but WORLD_SIZE={env_world}")
+            return 2
+        return None
+    if args.gpus <= 1:
+        return None
+    if _BACKEND != "gloo" and not args.dry_run and args.impl == "ours":
+        try:
+            import torch
+
+            visible = torch.cuda.device_count()
+        except Exception:
+            visible = 0
+        if visible < args.gpus:
+            log(f"error: --gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {visible} "
+                "(set HB_BENCH_BACKEND=gloo to share GPUs between ranks for testing)")
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"launching {args.gpus} ranks: {' '.join(cmd)}")
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """--dry-run: the launch path only (process group, per-rank records), no
+    GPU work -- the CPU test of the --gpus N launch."""
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+    recs = gather_objects({"rank": rank, "local_rank": int(os.environ.get("LOCAL_RANK", "0")), "pid": os.getpid()},
+                          world)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "impl": args.impl, "n_gpus": world, "ranks": recs}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="md5_1k")
+    ap.add_argument("--configs", choices=["all", "none"], default="all",
+                    help="measure every other BASELINE config in the same run (default workload only)")
     ap.add_argument("--msgs", type=int, default=0, help="override the message count (per GPU; total for strong-scaling workloads)")
     ap.add_argument("--e2e-steps", type=int, default=0)
-    ap.add_argument("--cpu-seconds", type=float, default=3.0)
-    ap.add_argument("--ref-step-seconds", type=float, default=1.0)
+    ap.add_argument("--suite-e2e-steps", type=int, default=3)
+    ap.add_argument("--sample-parity", action="store_true", help="row sample instead of every row at N=1")
     ap.add_argument("--ref-budget-seconds", type=float, default=150.0,
                     help="--impl reference: upper bound on the whole run's CPU time")
+    ap.add_argument("--numpy-ref-seconds", type=float, default=20.0)
+    ap.add_argument("--no-numpy-ref", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--gather", choices=["none", "p2p"], default="none",
                     help="N>1: fused device-side digest gather into rank 0 (hash kernels store over NVLink)")
+    ap.add_argument("--dry-run", action="store_true")
     args = ap.parse_args()
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
+    if args.dry_run:
+        run_dry(args)
+        return
     if args.warmup < 3 and args.impl == "ours":
         log("note: timing rules want >= 3 warm-up steps")
+    if args.workload != "md5_1k" or args.msgs:
+        args.configs = "none"
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -739,13 +739,14 @@ def test_small_default_call_runs_on_one_gpu():
         assert t["shards"] == 2 and t["device_mask"] == 1, t
 
 
-def test_timing_is_a_union_of_busy_intervals():
+def test_timing_is_a_union_of_busy_intervals(hb_env):
     """hb_timing's per-stage times are unions of the chunk ring's busy
     intervals (overlapping slots are not double-counted), each at most the
     call's wall time; the per-chunk timeline has one span per stage and chunk."""
     n, L = 1 << 16, 1024
     data = oracle.fill_random(n * L, 21).reshape(n, L)
     for env in ({}, {"HB_CHUNK_BYTES": 4 << 20}):
+        hb_env.reset(("HB_CHUNK_BYTES",), **env)
         t = {}
         out = batch_digest("md5", data, timing=t, gpus=[0])
         assert t["chunks"] >= (16 if env else 1)
