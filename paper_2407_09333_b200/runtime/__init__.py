@@ -3,7 +3,8 @@
 ``program``  lowered-program records, the reference printer's text form, and
              an adapter for reference ``HirModule`` objects;
 ``lowering`` ``crypto.hash_batch`` -> per-GPU launch groups (partition +
-             staging contract of ``lower_hyper_for``);
+             staging contract of ``lower_hyper_for``), fixed width and
+             variable length (offsets re-based per shard);
 ``devices``  host + ``cuda`` device table (``detect_hardware``);
 ``executor`` ``execute`` / ``execute_batched`` on real GPUs;
 ``sweep``    ``Workload`` / ``run_point`` over GPU splits.
@@ -11,11 +12,12 @@
 
 from .devices import DeviceConfigError, DeviceSpec, DeviceTable, HOST_ID, detect_hardware, from_reference
 from .executor import ExecError, ExecReport, execute, execute_batched
-from .lowering import LoweringError, lower_hash_batch
-from .program import BufType, DigestLoop, Op, Program, ProgramError, from_hir, parse
+from .lowering import LoweringError, lower_hash_batch, lower_hash_batch_varlen
+from .program import BufType, DigestLoop, Op, Program, ProgramError, VarDigestLoop, from_hir, parse
 from .sweep import RunRecord, Workload, run_point
 
 __all__ = ["DeviceConfigError", "DeviceSpec", "DeviceTable", "HOST_ID", "detect_hardware", "from_reference",
            "ExecError", "ExecReport", "execute", "execute_batched", "LoweringError", "lower_hash_batch",
+           "lower_hash_batch_varlen", "VarDigestLoop",
            "BufType", "DigestLoop", "Op", "Program", "ProgramError", "from_hir", "parse", "RunRecord", "Workload",
            "run_point"]

@@ -40,7 +40,7 @@ import numpy as np
 from .. import _native
 from ..crypto.batch import DIGEST_LEN
 from .devices import DeviceTable
-from .program import ELEM_BYTES, Op, Program, ProgramError, parse
+from .program import ELEM_BYTES, Op, Program, ProgramError, VarDigestLoop, parse
 
 
 class ExecError(RuntimeError):
@@ -73,13 +73,14 @@ def _wrap(kind: str, v):  # executor.py:52-59
 
 
 class _Buf:
-    __slots__ = ("device", "elem", "length", "nbytes", "host", "dev", "ordinal", "pending")
+    __slots__ = ("device", "elem", "length", "nbytes", "host", "dev", "ordinal", "pending", "origin")
 
     def __init__(self, device, elem, length, host=None, dev=None, ordinal=-1):
         self.device, self.elem, self.length = device, elem, length
         self.nbytes = length * ELEM_BYTES[elem]
         self.host, self.dev, self.ordinal = host, dev, ordinal
         self.pending = []  # CUDA events of in-flight async writes into a host buffer
+        self.origin = None  # (host buffer, element shift): dev[j] was copied from host[j + shift]
 
 
 class _Executor:
@@ -293,6 +294,8 @@ class _Executor:
                     s.wait_event(ev)
                 dst.dev[b0:b0 + nbytes].copy_(src.host[a0:a1], non_blocking=True)
             self._timed(dev, self.copy_ev, h2d)
+            if src.elem == dst.elem:  # where a varlen launch finds the offsets' host values
+                dst.origin = (src, so - do)
             self.copied[dev] += nbytes
         elif dst.host is not None:  # D2H
             dev = src.device
@@ -311,6 +314,8 @@ class _Executor:
                     self._stream(dev).wait_event(ev)
             self._timed(dev, self.copy_ev, lambda s: dst.dev[b0:b0 + nbytes].copy_(src.dev[a0:a1], non_blocking=True))
             self.copied[dev] += nbytes
+            if src.origin is not None and src.elem == dst.elem:
+                dst.origin = (src.origin[0], src.origin[1] + so - do)
 
     def _launch(self, op: Op, loc: str, lb=None, ub=None, shift: int = 0) -> None:
         dev = op.attrs["device"]
@@ -324,6 +329,9 @@ class _Executor:
                             "path (no CPU fallback); give the host a duty ratio of 0")
         self.batches[dev] += 1
         d = op.body
+        if isinstance(d, VarDigestLoop):
+            self._launch_varlen(d, spec, dev, loc, lb, ub)
+            return
         base = d.base + (shift if d.from_const else 0)
         msgs, out = self.value(d.msgs), self.value(d.out)
         dlen = DIGEST_LEN[d.alg]
@@ -344,6 +352,45 @@ class _Executor:
             _native.check(rc, "hb_hash_fixed_dev")
         self._timed(dev, self.kernel_ev, k)
 
+    def _offset_at(self, offb: _Buf, j: int) -> int:
+        """Global byte offset held in element j of an i64 offsets buffer: from
+        the host buffer it was copied from (no device read), else read back."""
+        if offb.origin is not None:
+            src, shift = offb.origin
+            self._host_sync(src)
+            return int(src.host.numpy().view(np.int64)[j + shift])
+        return int(offb.dev[8 * j:8 * j + 8].cpu().numpy().view(np.int64)[0])
+
+    def _launch_varlen(self, d: VarDigestLoop, spec, dev: str, loc: str, lb: int, ub: int) -> None:
+        """Rows [lb, ub) of the varlen digest loop: message t is
+        msgs[offsets[t] - B, offsets[t+1] - B) with B the offset of the
+        buffer's first message (offsets re-based per shard / sub-batch)."""
+        msgs, offb, out = self.value(d.msgs), self.value(d.offsets), self.value(d.out)
+        dlen = DIGEST_LEN[d.alg]
+        if msgs.elem != "i8" or out.elem != "i8" or offb.elem not in ("i64", "index"):
+            raise ExecError(f"{loc}: varlen digest needs i8 data/digests and i64 offsets")
+        if lb < 0 or ub + 1 > offb.length or ub * dlen > out.length:
+            raise ExecError(f"varlen digest rows [{lb}, {ub}) out of bounds")
+        if any(b.dev is None or b.device != dev for b in (msgs, offb, out)):
+            raise ExecError(f"{loc}: dev.launch on '{dev}' must address buffers resident on '{dev}'")
+        base = self._offset_at(offb, 0)
+        lo_b, hi_b = self._offset_at(offb, lb) - base, self._offset_at(offb, ub) - base
+        if lo_b < 0 or hi_b > msgs.nbytes:
+            raise ExecError(f"{loc}: offsets address bytes [{lo_b}, {hi_b}) outside the {msgs.nbytes}-byte data buffer")
+        lib = _native.lib()
+        n = ub - lb
+        torch = self.torch
+
+        def k(s):
+            with torch.cuda.stream(s):
+                scratch = torch.empty(int(lib.hb_varlen_scratch_bytes(n)), dtype=torch.uint8,
+                                      device=f"cuda:{spec.ordinal}")
+            rc = lib.hb_hash_varlen_dev(_native.ALG_ID[d.alg], spec.ordinal, msgs.dev.data_ptr(), msgs.nbytes,
+                                        offb.dev.data_ptr() + 8 * lb, base, n, out.dev.data_ptr() + lb * dlen,
+                                        scratch.data_ptr(), s.cuda_stream, 0)
+            _native.check(rc, "hb_hash_varlen_dev")
+        self._timed(dev, self.kernel_ev, k)
+
     # -------------------------------------------------------- batched groups
     def _run_group(self, ops: list[Op], pos: int) -> None:
         """executor.py:603-699, sub-batches alternating between two streams."""
@@ -354,6 +401,9 @@ class _Executor:
                 self._run_op(o, loc)
             return
         launch = launches[0]
+        if isinstance(launch.body, VarDigestLoop):
+            self._run_group_varlen(ops, launch, loc)
+            return
         dev = launch.attrs["device"]
         spec = self._spec(dev)
         allocs = [o for o in ops if o.opcode == "hyper.alloc"]
@@ -418,6 +468,69 @@ class _Executor:
                 self._dealloc(self.value(a.result), loc)
         # ... and stream 0 waits for stream 1 after it, so later ops on stream 0
         # see every sub-batch's writes
+        ev = torch.cuda.Event()
+        ev.record(s1)
+        s0.wait_event(ev)
+        self.cur[dev] = 0
+
+
+    def _run_group_varlen(self, ops: list[Op], launch: Op, loc: str) -> None:
+        """The capacity sub-batching of _run_group (executor.py:603-699) for a
+        varlen group: if the group's buffers exceed the device's ``mem_bytes``,
+        its messages are cut into k equal-count chunks, k grown from the
+        reference's starting estimate until the largest chunk's data +
+        offsets + digests fit; each chunk copies in its own byte range and
+        offsets slice and launches with its own offset base."""
+        dev = launch.attrs["device"]
+        spec = self._spec(dev)
+        d = launch.body
+        allocs = {o.result: o for o in ops if o.opcode == "hyper.alloc"}
+        needed = sum(o.rtype.nbytes for o in allocs.values())
+        cap = spec.mem_bytes
+        if needed <= cap:
+            for o in ops:
+                self._run_op(o, loc)
+            return
+        n = launch.attrs["ub"] - launch.attrs["lb"]
+        cin = {o.operands[1]: o for o in ops if o.opcode == "hyper.memcpy" and o.operands[1] in allocs}
+        cout = [o for o in ops if o.opcode == "hyper.memcpy" and o.operands[0] in allocs]
+        if set(allocs) != {d.msgs, d.offsets, d.out} or d.msgs not in cin or d.offsets not in cin or len(cout) != 1:
+            raise ExecError(f"{loc}: varlen group is not the canonical lowering (data, offsets, digests)")
+        host_off = self.value(cin[d.offsets].operands[0])
+        if host_off.host is None:
+            raise ExecError(f"{loc}: over-capacity varlen group needs its offsets on the host")
+        s_off = cin[d.offsets].attrs.get("src_off", 0)
+        offs = host_off.host.numpy().view(np.int64)[s_off:s_off + n + 1].astype(np.int64)
+        dlen = DIGEST_LEN[d.alg]
+
+        def need(c0, c1):
+            return int(offs[c1] - offs[c0]) + 8 * (c1 - c0 + 1) + dlen * (c1 - c0)
+
+        k = min(max(1, math.ceil(needed / cap)), n)
+        chunks = _chunk_ranges(n, k)
+        while max(need(a, b) for a, b in chunks) > cap and k < n:
+            k += 1
+            chunks = _chunk_ranges(n, k)
+        if max(need(a, b) for a, b in chunks) > cap:
+            raise ExecError(f"{loc}: a single message exceeds device capacity {cap}")
+        torch = self.torch
+        s0, s1 = self._stream(dev), self.streams[dev][1]
+        ev = torch.cuda.Event()
+        ev.record(s0)
+        s1.wait_event(ev)
+        out_copy = cout[0]
+        for ci, (c0, c1) in enumerate(chunks):
+            self.cur[dev] = ci % 2
+            cn = c1 - c0
+            self.env[d.msgs] = self._alloc(dev, "i8", int(offs[c1] - offs[c0]))
+            self.env[d.offsets] = self._alloc(dev, allocs[d.offsets].rtype.elem, cn + 1)
+            self.env[d.out] = self._alloc(dev, "i8", cn * dlen)
+            self._copy(cin[d.msgs], loc, src_off=int(offs[c0]), dst_off=0, count=int(offs[c1] - offs[c0]))
+            self._copy(cin[d.offsets], loc, src_off=s_off + c0, dst_off=0, count=cn + 1)
+            self._launch(launch, loc, lb=0, ub=cn, shift=c0)
+            self._copy(out_copy, loc, src_off=0, dst_off=out_copy.attrs.get("dst_off", 0) + c0 * dlen, count=cn * dlen)
+            for r in (d.msgs, d.offsets, d.out):
+                self._dealloc(self.value(r), loc)
         ev = torch.cuda.Event()
         ev.record(s1)
         s0.wait_event(ev)

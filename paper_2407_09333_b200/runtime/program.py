@@ -18,6 +18,17 @@ Only the ops the lowering emits for hash workloads are representable:
 hyper.dealloc hyper.memcpy par.loop dev.launch return`` at top level, and the
 canonical digest loop body (``crypto.digest`` on the induction variable, or on
 ``iv + const`` -- ``_match_digest_loop``, ``executor.py:240-259``).
+
+Variable-length batches add one loop body the reference
+compiler cannot emit -- its ``crypto.hash_batch`` requires ``msg_len``
+(``pkg/src/hetoc/hir/verify.py:343-358``) and its lowering uses fixed strides
+(``pkg/src/hetoc/passes/lower_crypto.py:35-78``):
+
+    crypto.digest_varlen %msgs, %offsets, %out, %iv {alg="md5", offset_base=B}
+
+message ``iv`` is ``msgs[offsets[iv] - B, offsets[iv+1] - B)``: the offsets
+slice copied to a device keeps the batch's global byte offsets and ``B`` (the
+first offset of the slice) re-bases them onto the device's data slice.
 """
 
 from __future__ import annotations
@@ -65,13 +76,28 @@ class DigestLoop:
     from_const: bool = False
 
 
+@dataclass(frozen=True)
+class VarDigestLoop:
+    """The variable-length digest loop body: message t of the launch range is
+    ``msgs[offsets[t] - offset_base, offsets[t+1] - offset_base)`` (``offsets``
+    an i64 buffer of n+1 global byte offsets), digest into ``out`` row t."""
+
+    msgs: int
+    offsets: int
+    out: int
+    alg: str
+    offset_base: int
+    base: int = 0
+    from_const: bool = False
+
+
 @dataclass
 class Op:
     opcode: str
     operands: list[int] = field(default_factory=list)  # value ids
     result: int | None = None
     attrs: dict = field(default_factory=dict)
-    body: DigestLoop | None = None  # par.loop / dev.launch
+    body: DigestLoop | VarDigestLoop | None = None  # par.loop / dev.launch
     rtype: object = None  # BufType for allocs, scalar kind for const/addi/muli
 
 
@@ -151,8 +177,13 @@ def _format_op(op: Op, define, ref) -> list[str]:
             g = define(("addi", id(op)))
             inner += [f"{c} = const {d.base} : index", f"{g} = addi {iv}, {c} : index"]
             idx = g
-        attrs = {"accel": d.accel, "alg": d.alg, "msg_len": d.msg_len}
-        inner += [f"crypto.digest {ref(d.msgs)}, {ref(d.out)}, {idx}{_attr_dict(attrs)}", "yield"]
+        if isinstance(d, VarDigestLoop):
+            attrs = {"alg": d.alg, "offset_base": d.offset_base}
+            inner += [f"crypto.digest_varlen {ref(d.msgs)}, {ref(d.offsets)}, {ref(d.out)}, {idx}{_attr_dict(attrs)}",
+                      "yield"]
+        else:
+            attrs = {"accel": d.accel, "alg": d.alg, "msg_len": d.msg_len}
+            inner += [f"crypto.digest {ref(d.msgs)}, {ref(d.out)}, {idx}{_attr_dict(attrs)}", "yield"]
         return [head + " {"] + ["  " + x for x in inner] + ["}"]
     if o == "return":
         return ["return"]
@@ -173,6 +204,7 @@ _RE_HCOPY = re.compile(r"^hyper\.memcpy %(\d+), %(\d+)(?: \{(.*)\})?$")
 _RE_LOOP = re.compile(r'^(par\.loop|dev\.launch) %(\d+) = (-?\d+) to (-?\d+) device\("([^"]+)"\)'
                       r"(?: offset\((-?\d+)\))?(?: group\((\d+)\))? \{$")
 _RE_DIGEST = re.compile(r"^crypto\.digest %(\d+), %(\d+), %(\d+)(?: \{(.*)\})?$")
+_RE_VDIGEST = re.compile(r"^crypto\.digest_varlen %(\d+), %(\d+), %(\d+), %(\d+)(?: \{(.*)\})?$")
 
 
 def _parse_scalar(tok: str):
@@ -258,8 +290,18 @@ def parse(text: str, param_names: list[str] | None = None) -> Program:
     return Program(name, params, ops, param_names)
 
 
-def _parse_digest_body(body: list[str], iv: int, where: str) -> DigestLoop:
+def _parse_digest_body(body: list[str], iv: int, where: str) -> DigestLoop | VarDigestLoop:
     """Recognise the canonical digest loop (executor.py:240-259) in text."""
+    if len(body) == 2 and (m := _RE_VDIGEST.match(body[0])) and body[1] == "yield" and int(m.group(4)) == iv:
+        a = _parse_attrs(m.group(5))
+        return VarDigestLoop(int(m.group(1)), int(m.group(2)), int(m.group(3)), a["alg"], int(a["offset_base"]))
+    if len(body) == 4 and body[3] == "yield" and (v := _RE_VDIGEST.match(body[2])):
+        c, add = _RE_CONST.match(body[0]), _RE_BIN.match(body[1])
+        if c and add and add.group(2) == "addi" and int(v.group(4)) == int(add.group(1)) and \
+                {int(add.group(3)), int(add.group(4))} == {iv, int(c.group(1))}:
+            a = _parse_attrs(v.group(5))
+            return VarDigestLoop(int(v.group(1)), int(v.group(2)), int(v.group(3)), a["alg"], int(a["offset_base"]),
+                                 int(_parse_scalar(c.group(2))), True)
     if len(body) == 2 and (m := _RE_DIGEST.match(body[0])) and body[1] == "yield" and int(m.group(3)) == iv:
         a = _parse_attrs(m.group(4))
         return DigestLoop(int(m.group(1)), int(m.group(2)), a["alg"], int(a["msg_len"]), bool(a.get("accel")))

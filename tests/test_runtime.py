@@ -162,3 +162,108 @@ def test_from_reference_device_table():
     assert t.host.sha_accel and t.host.threads == 8
     with pytest.raises(DeviceConfigError):
         from_reference(RTable(RSpec("host", kind="host"), (RSpec("acc", host_mapped=True),)))
+
+
+# ------------------------------------------------- variable length (§8(f) 3)
+def _var_table(mem=1 << 30, k=3, ordinals=None):
+    host = DeviceSpec("host", kind="host", threads=4)
+    return DeviceTable(host, tuple(DeviceSpec(f"gpu{i}", kind="cuda", ordinal=(ordinals or {}).get(i, 0),
+                                              mem_bytes=mem) for i in range(k)))
+
+
+def _var_batch(n, seed, maxlen=3000, base=0):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, maxlen + 1, n).astype(np.int64)
+    lens[::53] = 0
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    off += base
+    return off
+
+
+def test_varlen_lowering_structure_and_roundtrip():
+    """Offsets re-based per shard: binding j's group copies bytes
+    [offsets[s], offsets[e]) and offsets [s, e] and launches with
+    offset_base = offsets[s]; digests go back to s*dlen.  Printed text
+    round-trips through the parser."""
+    from paper_2407_09333_b200.passes import partition_range
+    from paper_2407_09333_b200.runtime import VarDigestLoop, lower_hash_batch_varlen
+
+    off = _var_batch(1000, 1, base=7)
+    ratios = [0.25, 0.5, 0.25]
+    prog = lower_hash_batch_varlen("sm3", off, [(f"gpu{i}", r) for i, r in enumerate(ratios)], _var_table())
+    text = prog.format()
+    assert parse(text, ["msgs", "offsets", "out"]).format() == text
+    assert "crypto.digest_varlen" in text and "msg_len" not in text
+    launches = [o for o in prog.ops if o.opcode == "dev.launch"]
+    bounds = partition_range(0, 1000, ratios)
+    assert len(launches) == 3
+    for op, (s, e) in zip(launches, bounds):
+        assert isinstance(op.body, VarDigestLoop)
+        assert (op.attrs["lb"], op.attrs["ub"], op.attrs["offset"]) == (0, e - s, s)
+        assert op.body.offset_base == off[s]
+    copies = [o for o in prog.ops if o.opcode == "hyper.memcpy"]
+    data_in = [c for c in copies if c.operands[0] == 0]
+    assert [(c.attrs["src_off"], c.attrs["count"]) for c in data_in] == \
+        [(int(off[s]), int(off[e] - off[s])) for s, e in bounds]
+    outs = [c for c in copies if c.operands[1] == 2]
+    assert [c.attrs["dst_off"] for c in outs] == [s * 32 for s, _ in bounds]
+    # bindings with an empty range are dropped, host bindings refused
+    p2 = lower_hash_batch_varlen("md5", off, [("gpu0", 1.0), ("gpu1", 0.0)], _var_table())
+    assert sum(o.opcode == "dev.launch" for o in p2.ops) == 1
+    with pytest.raises(LoweringError):
+        lower_hash_batch_varlen("md5", off, [("host", 1.0)], _var_table())
+    with pytest.raises(LoweringError):
+        lower_hash_batch_varlen("md5", np.array([5, 3]), [("gpu0", 1.0)], _var_table())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("alg", ["sha1", "md5", "sm3"])
+def test_varlen_program_on_gpus(alg):
+    """Varlen programs across 3 device bindings (one per GPU when present),
+    unbatched and with over-capacity groups cut into sub-batches, bit-exact
+    against the oracle (itself pinned to the reference's scalar digest)."""
+    import oracle
+    from paper_2407_09333_b200 import _native
+    from paper_2407_09333_b200.runtime import lower_hash_batch_varlen
+
+    nd = _native.device_count()
+    off = _var_batch(6000, 2, base=0)
+    data = oracle.fill_random(int(off[-1]), 31)
+    ref = oracle.batch_varlen(alg, data, off.astype(np.uint64), threads=8).tobytes()
+    ords = {i: i % nd for i in range(3)}
+    for mem, ratios in ((1 << 30, (0.2, 0.5, 0.3)), (400000, (0.2, 0.5, 0.3)), (150000, (0.0, 1.0, 0.0))):
+        devs = _var_table(mem, ordinals=ords)
+        prog = lower_hash_batch_varlen(alg, off, [(f"gpu{i}", r) for i, r in enumerate(ratios)], devs)
+        inputs = {"msgs": data, "offsets": off}
+        if mem == 1 << 30:
+            rep = execute(prog, devs, inputs)
+            assert rep.outputs["out"] == ref
+        rep = execute_batched(prog.format(), devs, inputs, param_names=["msgs", "offsets", "out"])
+        assert rep.outputs["out"] == ref, (alg, mem, ratios)
+        if mem < (1 << 30):
+            assert max(rep.batch_count.values()) > 1, rep.batch_count
+        launched = sum(rep.batch_count.values())
+        assert launched >= sum(r > 0 for r in ratios)
+
+
+@pytest.mark.gpu
+def test_varlen_program_golden(golden):
+    """The reference's scalar digest per message (tests/golden/varlen_batches.json,
+    made by tests/golden/make_golden.py from hetoc.crypto.digest) through a
+    lowered two-GPU varlen program."""
+    import oracle
+    from paper_2407_09333_b200 import _native
+    from paper_2407_09333_b200.runtime import lower_hash_batch_varlen
+
+    nd = _native.device_count()
+    devs = _var_table(1 << 30, k=2, ordinals={0: 0, 1: 1 % nd})
+    for row in golden("varlen_batches.json"):
+        lens = np.array(row["lens"], np.int64)
+        off = np.zeros(len(lens) + 1, np.int64)
+        off[1:] = np.cumsum(lens)
+        data = oracle.fill_random(int(off[-1]), row["seed"])
+        for alg in ("sha1", "md5", "sm3"):
+            prog = lower_hash_batch_varlen(alg, off, [("gpu0", 0.4), ("gpu1", 0.6)], devs)
+            rep = execute_batched(prog, devs, {"msgs": data, "offsets": off})
+            assert hashlib.sha256(rep.outputs["out"]).hexdigest() == row[alg], (alg, len(lens))
