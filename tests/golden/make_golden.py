@@ -128,16 +128,55 @@ def partitions():
     return [{"lb": lb, "ub": ub, "ratios": r, "ranges": partition_range(lb, ub, r)} for lb, ub, r in cases]
 
 
+def scheduler_models():
+    """The reference's calibration (hetoc.scheduler.model.fit_model) and its
+    predictions on deterministic sample sets, incl. ones that clamp."""
+    from hetoc.scheduler.model import PerfModel, fit_model, predict_opt_ratio, t_opt
+
+    rnd = random.Random(11)
+    cases = []
+    sets = [([(1000, 0.01), (2000, 0.021), (4000, 0.039)], [(1000, 0.002), (2000, 0.0031), (8000, 0.0105)], 8),
+            ([(10, 1.0), (20, 2.0)], [(10, 5.0), (20, 1.0)], 1),  # negative device slope -> clamped
+            ([(100, 1.0), (300, 2.9)], [(100, 0.1), (300, 0.5)], 16)]  # negative intercept -> clamped
+    for _ in range(20):
+        k = rnd.randint(2, 6)
+        cpu = [(rnd.randint(1, 10**7), rnd.uniform(0.001, 50.0)) for _ in range(k)]
+        dev = [(rnd.randint(1, 10**7), rnd.uniform(0.0001, 5.0)) for _ in range(rnd.randint(2, 6))]
+        sets.append((cpu, dev, rnd.randint(1, 256)))
+    for cpu, dev, cores in sets:
+        m = fit_model(cpu, dev, cores)
+        row = {"cpu": cpu, "dev": dev, "n_core": cores,
+               "model": {k: getattr(m, k) for k in ("p_cpu", "n_core", "p_gpu_over_nthread", "t_alloc",
+                                                     "t_memcpy", "o_gpu")}}
+        try:
+            row["opt_ratio"] = {str(n): predict_opt_ratio(m, n) for n in (1, 1000, 10**6, 10**9)}
+        except ValueError:
+            row["opt_ratio"] = None
+        row["t_opt"] = {f"{n}:{x}": t_opt(m, n, x) for n in (1000, 10**6) for x in (0.0, 0.1, 0.5, 1.0)}
+        cases.append(row)
+    extra = PerfModel(p_cpu=2e-6, n_core=12, p_gpu_over_nthread=1e-8, t_alloc=2e-9, t_memcpy=3e-8, o_gpu=1e-3)
+    cases.append({"model": {k: getattr(extra, k) for k in ("p_cpu", "n_core", "p_gpu_over_nthread", "t_alloc",
+                                                           "t_memcpy", "o_gpu")},
+                  "opt_ratio": {str(n): predict_opt_ratio(extra, n) for n in (1, 1000, 10**6, 10**9)},
+                  "t_opt": {f"{n}:{x}": t_opt(extra, n, x) for n in (1000, 10**6) for x in (0.0, 0.1, 0.5, 1.0)}})
+    return cases
+
+
 def main():
     fixtures = {
-        "kats.json": kats(),
-        "boundary.json": boundary(),
-        "fixed_batches.json": fixed_batches(),
-        "varlen_batches.json": varlen_batches(),
-        "decimal_batches.json": decimal_batches(),
-        "partition.json": partitions(),
+        "kats.json": kats,
+        "boundary.json": boundary,
+        "fixed_batches.json": fixed_batches,
+        "varlen_batches.json": varlen_batches,
+        "decimal_batches.json": decimal_batches,
+        "partition.json": partitions,
+        "scheduler_model.json": scheduler_models,
     }
+    only = sys.argv[1:]
     for name, obj in fixtures.items():
+        if only and name not in only:
+            continue
+        obj = obj() if callable(obj) else obj
         with open(os.path.join(HERE, name), "w") as f:
             json.dump(obj, f, indent=0 if name != "partition.json" else None)
             f.write("\n")
