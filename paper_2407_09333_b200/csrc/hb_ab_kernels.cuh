@@ -520,7 +520,7 @@ static cudaError_t launch_small_ab(const uint8_t* d_msgs, uint64_t n, uint64_t L
 static bool varlen_ab_selected(uint32_t flags) {
     const Tuning& T = tuning();
     return (flags & (HB_FLAG_VARLEN_WORDS | HB_FLAG_VARLEN_COOP)) || T.varlen_bulk || T.varlen_prefetch ||
-           T.varlen_ld == 32;
+           T.varlen_ld == 32 || T.varlen_kernel >= 0;
 }
 
 template <int ALG>
@@ -558,6 +558,15 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
         case 5: launch_plain(k_varlen_bulk<ALG, 2, 8>, grid, 128, stream, d_data, d_offsets, offset_base, perm, n, d_out); break;
         default: launch_plain(k_varlen_bulk<ALG, 3, 1>, grid, 128, stream, d_data, d_offsets, offset_base, perm, n, d_out); break;
         }
+    } else if (T.varlen_kernel == 0) {  // the per-thread kernel with md_finish tails
+        launch_plain(k_varlen16<ALG, false>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base,
+                     perm, n, d_out);
+    } else if (T.varlen_kernel == 2) {  // uniform block loop, every addition on the FMA pipe
+        launch_plain(k_varlen16u<ALG, kVarBal2>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets,
+                     offset_base, perm, n, d_out);
+    } else if (T.varlen_kernel == 1) {  // uniform block loop, tuned variant
+        launch_plain(k_varlen16u<ALG, kVarBal>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets,
+                     offset_base, perm, n, d_out);
     } else if (T.varlen_prefetch) {
         launch_plain(k_varlen16<ALG, true>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base,
                      perm, n, d_out);

@@ -46,6 +46,7 @@ struct Tuning {
     uint32_t varlen_q = 8;                      // $HB_VARLEN_Q
     uint32_t varlen_prefetch = 0;               // $HB_VARLEN_PREFETCH
     uint32_t varlen_bulk = 0;                   // $HB_VARLEN_BULK
+    int varlen_kernel = -1;                     // $HB_VARLEN_KERNEL: 0 k_varlen16, 1 / 2 k_varlen16u variant 1 / 2
     int vc_stages = -1;                         // $HB_VC_STAGES
     uint32_t vc_pf = 256;                       // $HB_VC_PF
 };

@@ -79,6 +79,7 @@ static Tuning parse_tuning() {
     t.varlen_q = (uint32_t)env_u64("HB_VARLEN_Q", 8);
     t.varlen_prefetch = (uint32_t)env_u64("HB_VARLEN_PREFETCH", 0);
     t.varlen_bulk = (uint32_t)env_u64("HB_VARLEN_BULK", 0);
+    t.varlen_kernel = env_set("HB_VARLEN_KERNEL") ? (int)env_u64("HB_VARLEN_KERNEL", 0) : -1;
     t.vc_stages = env_set("HB_VC_STAGES") ? (int)env_u64("HB_VC_STAGES", 4) : -1;
     t.vc_pf = (uint32_t)env_u64("HB_VC_PF", 256);
 #endif

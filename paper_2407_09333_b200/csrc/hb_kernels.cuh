@@ -534,6 +534,84 @@ __device__ __forceinline__ void varlen16_message(const uint4* w16, uintptr_t a, 
     store_digest<ALG>(dout, st);
 }
 
+// -------------------------------------------------------------------------
+// Variable-length kernel with a warp-uniform block loop.  After the length
+// sort a warp's 32 messages share their block count nb = (len+8)/64 + 1,
+// but not whether the final data bytes and the padding need one block or
+// two (r = len % 64 >= 56 needs two): k_varlen16 runs the full-block loop to
+// len/64 and then md_finish's 1-2 compressions, so a warp with both kinds of
+// lanes executes nb + 1 compressions.  Here every lane runs exactly nb:
+// blocks 0 .. nb-3 are full data blocks for every lane, and the last two go
+// through one branch-free tail body (bytes past the message masked to zero,
+// 0x80 where the message ends, the bit length in the last block) -- one
+// compress call site per loop, no divergence when nb is warp-uniform.
+// V: round variant (1 = the tuned ALU/FMA balance, 2 = every addition on the
+// FMA pipe: the realignment's funnel shifts load the ALU pipe here).
+// -------------------------------------------------------------------------
+template <int ALG, int V, bool EDGE>
+__device__ __forceinline__ void varlen16u_message(const uint4* w16, uintptr_t a, uint64_t len, uintptr_t dend,
+                                                  uint8_t* dout) {
+    using H = HashAlg<ALG, V>;
+    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
+    const bool misaligned = (a & 15u) != 0;
+    uint32_t st[1][H::kStateWords];
+    H::init(st[0]);
+    uint32_t c[20];
+    uint32_t raw[1][16];
+    const uint64_t nb = (len + 8u) / 64u + 1u;
+    const uint64_t nmain = nb >= 2u ? nb - 2u : 0u;  // every lane: full data blocks
+    for (uint64_t b = 0; b < nmain; ++b) {
+        load_full_window(w16 + 4 * b, misaligned, c, EDGE, dend);
+        realign16(c, q, sh, raw[0]);
+        H::template compress_n<1>(st, raw);
+    }
+    const uint64_t bits = len * 8ull;
+    const uint32_t l14 = H::kBigEndian ? bswap((uint32_t)(bits >> 32)) : (uint32_t)bits;
+    const uint32_t l15 = H::kBigEndian ? bswap((uint32_t)bits) : (uint32_t)(bits >> 32);
+    const uintptr_t mend = a + len;
+#pragma unroll 1
+    for (uint64_t k = nmain; k < nb; ++k) {
+        const uint4* src = w16 + 4 * k;
+#pragma unroll
+        for (int kk = 0; kk < 5; ++kk) {  // the chunks that overlap the message's bytes of block k
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (reinterpret_cast<uintptr_t>(src + kk) < mend) v = ld16_edge(src + kk, EDGE, dend);
+            c[4 * kk] = v.x; c[4 * kk + 1] = v.y; c[4 * kk + 2] = v.z; c[4 * kk + 3] = v.w;
+        }
+        realign16(c, q, sh, raw[0]);
+        const int64_t rem = (int64_t)len - 64 * (int64_t)k;  // message bytes from this block's start
+        if (rem < 64) {
+            const uint32_t r = rem > 0 ? (uint32_t)rem : 0u;
+            mask_tail(raw[0], r);
+            const uint32_t pad = rem >= 0 ? 0x80u << ((r & 3u) * 8u) : 0u, pw = r >> 2;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) raw[0][j] |= (pw == (uint32_t)j) ? pad : 0u;
+        }
+        if (k == nb - 1u) { raw[0][14] = l14; raw[0][15] = l15; }
+        H::template compress_n<1>(st, raw);
+    }
+    store_digest<ALG>(dout, st[0]);
+}
+
+template <int ALG, int V>
+__global__ void __launch_bounds__(128)
+k_varlen16u(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = perm ? (uint64_t)perm[t] : t;
+    const uint64_t start = offsets[i] - offset_base;
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
+    const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    if (((a + len + 15u) & ~uintptr_t(15)) > dend)
+        varlen16u_message<ALG, V, true>(w16, a, len, dend, out + i * H::kDigestBytes);
+    else
+        varlen16u_message<ALG, V, false>(w16, a, len, dend, out + i * H::kDigestBytes);
+}
+
 template <int ALG, bool PF = false>
 __global__ void __launch_bounds__(128)
 k_varlen16(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,

@@ -1,6 +1,7 @@
-"""A/B of the varlen kernels on configs[3] (2^22 messages, uniform 1-4096 B):
-cooperative-staging knobs ($HB_VC_STAGES, $HB_VC_PF) and the per-thread
-kernel, interleaved rounds, digests cross-checked.  One JSON line per arm."""
+"""A/B of the varlen kernels on configs[3] (2^22 messages, uniform 1-4096 B),
+interleaved rounds, digests cross-checked.  One JSON line per arm.
+Arms: $AB_ARMS (JSON {name: {env}}), default per-thread kernel vs prefetch;
+run against the A/B library (HETOC_B200_LIB=libhetoc_b200_ab.so)."""
 import json
 import os
 import statistics
@@ -23,15 +24,18 @@ d_off = torch.from_numpy(off).cuda()
 scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(n)), dtype=torch.uint8, device="cuda:0")
 C = _native.HB_FLAG_VARLEN_COOP
 P = _native.HB_FLAG_VARLEN_COOP_OFF
-ARMS = {"default": ({}, 0), "prefetch": ({"HB_VARLEN_PREFETCH": "1"}, 0)}
+ARMS = {k: (v, 0) for k, v in json.loads(os.environ.get("AB_ARMS", '{"default": {}, "prefetch": {"HB_VARLEN_PREFETCH": "1"}}')).items()}
+KEYS = sorted({k for env, _ in ARMS.values() for k in env} | {"HB_VC_STAGES", "HB_VC_PF", "HB_VARLEN_SORT",
+                                                          "HB_SORT_WINDOW", "HB_VARLEN_PREFETCH", "HB_VARLEN_BULK",
+                                                          "HB_VARLEN_LD", "HB_VARLEN_Q"})
 for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
     ref, times = None, {}
     for _ in range(int(os.environ.get("AB_ROUNDS", 3))):
         for arm, (env, flags) in ARMS.items():
-            for k in ("HB_VC_STAGES", "HB_VC_PF", "HB_VARLEN_SORT", "HB_SORT_WINDOW", "HB_VARLEN_PREFETCH",
-                      "HB_VARLEN_BULK", "HB_VARLEN_LD", "HB_VARLEN_Q"):
+            for k in KEYS:
                 os.environ.pop(k, None)
             os.environ.update(env)
+            _native.reload_tuning()
             out = torch.empty((n, DLEN[alg]), dtype=torch.uint8, device="cuda:0")
             f = lambda: device.hash_varlen(alg, data, d_off, out=out, scratch=scratch, flags=flags,  # noqa: E731
                                            offset_base=0)
@@ -49,5 +53,7 @@ for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
             times.setdefault(arm, []).append(s.elapsed_time(e) / 5)
     for arm, ts in times.items():
         ms = statistics.median(ts)
-        print(json.dumps({"alg": alg, "arm": arm, "ms": round(ms, 4), "GBps": round(int(off[-1]) / ms / 1e6, 1)}),
-              flush=True)
+        alg_bytes = int(off[-1]) + 8 * (n + 1) + n * DLEN[alg]
+        print(json.dumps({"alg": alg, "arm": arm, "ms": round(ms, 4), "ms_min": round(min(ts), 4),
+                          "GBps": round(int(off[-1]) / ms / 1e6, 1),
+                          "frac_of_6459": round(alg_bytes / ms / 1e6 / 6459.3, 4)}), flush=True)
