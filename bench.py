@@ -238,7 +238,8 @@ class ClockSampler:
         pw = [s[3] for s in samples if s[3] is not None]
         return {"sm_mhz": statistics.median(s[1] for s in samples), "sm_min_mhz": min(s[1] for s in samples),
                 "sm_max_mhz": max(s[2] for s in samples), "power_w_max": round(max(pw), 1) if pw else None,
-                "reasons": reasons, "samples": len(samples), "source": self.source}
+                "reasons": reasons, "reason_masks": sorted({hex(s[4]) for s in samples}),
+                "samples": len(samples), "source": self.source}
 
 
 
@@ -465,6 +466,7 @@ class PinnedPool:
 
 GRAPH_STEPS = 10
 L2_DEFEAT_BYTES = 2 * 126 * 10**6  # twice the B200's 126 MB L2
+PROFILE_ONLY = False  # tools/ncu_configs.py: no rotated copies, no graphs (one launch per config)
 
 
 # -------------------------------------------------------------- workloads --
@@ -508,13 +510,13 @@ class FixedWorkload:
         # GRAPH_STEPS, >= 2 x 126 MB in total) that every step reads a copy
         # last touched >= 63 steps earlier, i.e. from HBM.
         self.copies = [self.msgs]
-        if n * L and n * L < L2_DEFEAT_BYTES:
+        if n * L and n * L < L2_DEFEAT_BYTES and not PROFILE_ONLY:
             r = -(-L2_DEFEAT_BYTES // (n * L))
             r = -(-r // GRAPH_STEPS) * GRAPH_STEPS
             self.copies += [self.msgs.clone() for _ in range(r - 1)]
         self.turn = 0
         self.graphs, self.graph1s = [], []
-        if n * L <= (64 << 20):
+        if n * L <= (64 << 20) and not PROFILE_ONLY:
             # GRAPH_STEPS consecutive copies per replayed graph, one single-pass graph per copy for remainders
             for j in range(0, len(self.copies), GRAPH_STEPS):
                 group = self.copies[j:j + GRAPH_STEPS]
@@ -832,7 +834,7 @@ class Ctx:
         return self.bw[key]
 
 
-def time_kernel(w, ctx, steps, warmup, min_region_ms=0.0):
+def time_kernel(w, ctx, steps, warmup, min_region_ms=0.0, ramp_ms=0.0):
     """K back-to-back steps between one CUDA-event pair on the launching
     stream, after W warm-up steps, barrier + synchronize on both sides; clocks
     sampled during the region; re-measured once on hardware/thermal throttling.
@@ -844,6 +846,10 @@ def time_kernel(w, ctx, steps, warmup, min_region_ms=0.0):
 
     world, rank, local = ctx.world, ctx.rank, ctx.local
     stream = torch.cuda.current_stream(local)
+    t_ramp = time.perf_counter()
+    while (time.perf_counter() - t_ramp) * 1e3 < ramp_ms:  # untimed: let the SM clock settle before the warm-up
+        w.step()
+        torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(warmup):
@@ -1085,7 +1091,8 @@ def run_ours(args):
         w.graphs, w.graph1s, w.copies = [], [], [w.msgs]
         w.step = gather.launch
     torch.cuda.synchronize()
-    ms_local, ms, launches, clk, wall_ms, _ = time_kernel(w, ctx, args.steps, args.warmup)
+    # the process's first GPU work: ~0.4 s of untimed steps first, so the timed region does not see the clock ramp
+    ms_local, ms, launches, clk, wall_ms, _ = time_kernel(w, ctx, args.steps, args.warmup, ramp_ms=400.0)
     if gather is not None:  # the gather wrote into rank 0's buffer; refill the local digests for the checks below
         from paper_2407_09333_b200 import device as _device
 
