@@ -495,7 +495,7 @@ template <int ALG, int L>
 static void launch_small_one_ab(const uint8_t* d_msgs, uint64_t n, uint8_t* d_out, cudaStream_t s) {
     const Tuning& T = tuning();
     const unsigned b = T.small_cta >= 128 ? 128u : T.small_cta >= 64 ? 64u : 32u;
-    const bool pair = ALG == kMd5 && n >= (1ull << 20) && L <= 32 && T.small_pair;
+    const bool pair = T.small_pair_all || (ALG == kMd5 && n >= (1ull << 20) && L <= 32 && T.small_pair);
     if (T.const_variant == 0)
         launch_pdl(k_fixed_small<ALG, L, kVarPlain>, (unsigned)((n + b - 1) / b), b, s, d_msgs, n, d_out);
     else if (pair)

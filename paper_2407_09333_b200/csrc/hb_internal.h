@@ -38,6 +38,7 @@ struct Tuning {
     bool small_kernel_ab = false;               // $HB_CONST_VARIANT=0 / $HB_SMALL_CTA set
     int const_variant = -1;                     // $HB_CONST_VARIANT
     uint32_t small_cta = 128;                   // $HB_SMALL_CTA
+    bool small_pair_all = false;                // $HB_SMALL_PAIR_ALL: two rows per thread at every width / count
     bool dec_ab = false;                        // any of $HB_DEC_PAIR / $HB_FMA_DIGITS / $HB_CONST_VARIANT set
     int dec_pair = -1;                          // $HB_DEC_PAIR
     bool fma_digits = true;                     // $HB_FMA_DIGITS

@@ -70,7 +70,8 @@ static Tuning parse_tuning() {
     t.small_kernel = !env_set("HB_NO_SMALL_KERNEL");
     t.const_variant = env_set("HB_CONST_VARIANT") ? (int)env_u64("HB_CONST_VARIANT", 1) : -1;
     t.small_cta = (uint32_t)env_u64("HB_SMALL_CTA", 128);
-    t.small_kernel_ab = t.const_variant == 0 || t.small_cta != 128;
+    t.small_pair_all = env_u64("HB_SMALL_PAIR_ALL", 0) != 0;
+    t.small_kernel_ab = t.const_variant == 0 || t.small_cta != 128 || t.small_pair_all;
     t.dec_pair = env_set("HB_DEC_PAIR") ? (int)env_u64("HB_DEC_PAIR", 0) : -1;
     t.fma_digits = env_u64("HB_FMA_DIGITS", 1) != 0;
     t.dec_ab = t.dec_pair >= 0 || !t.fma_digits || t.const_variant >= 0;
