@@ -558,8 +558,14 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
         case 5: launch_plain(k_varlen_bulk<ALG, 2, 8>, grid, 128, stream, d_data, d_offsets, offset_base, perm, n, d_out); break;
         default: launch_plain(k_varlen_bulk<ALG, 3, 1>, grid, 128, stream, d_data, d_offsets, offset_base, perm, n, d_out); break;
         }
+    } else if (T.varlen_kernel >= 10) {  // prefetch-instruction arms of the per-thread kernel (PF = kernel - 10)
+        switch (T.varlen_kernel - 10) {
+        case 2: launch_plain(k_varlen16<ALG, 2>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 3: launch_plain(k_varlen16<ALG, 3>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        default: launch_plain(k_varlen16<ALG, 4>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        }
     } else if (T.varlen_kernel == 0) {  // the per-thread kernel with md_finish tails
-        launch_plain(k_varlen16<ALG, false>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base,
+        launch_plain(k_varlen16<ALG, 0>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base,
                      perm, n, d_out);
     } else if (T.varlen_kernel == 2) {  // uniform block loop, every addition on the FMA pipe
         launch_plain(k_varlen16u<ALG, kVarBal2>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets,
@@ -568,10 +574,10 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
         launch_plain(k_varlen16u<ALG, kVarBal>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets,
                      offset_base, perm, n, d_out);
     } else if (T.varlen_prefetch) {
-        launch_plain(k_varlen16<ALG, true>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base,
+        launch_plain(k_varlen16<ALG, 1>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base,
                      perm, n, d_out);
     } else {
-        launch_plain(k_varlen16<ALG, false>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base,
+        launch_plain(k_varlen16<ALG, 0>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base,
                      perm, n, d_out);
     }
     return cudaGetLastError();

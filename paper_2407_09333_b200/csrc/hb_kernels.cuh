@@ -493,7 +493,34 @@ __device__ __forceinline__ void load_full_window(const uint4* src, bool misalign
 // straddles the end of the data buffer (only the batch's final bytes), so the
 // granules that can cross it are loaded bounded.  The common path carries no
 // bounds checks at all.
-template <int ALG, bool PF, bool EDGE>
+// PF >= 2: prefetch instructions instead of register pipelining (no
+// registers held across the compression): 2 = the window of block b+2 into L2
+// while block b is compressed, 3 = block b+1's window into L1, 4 = both.
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+template <int PF>
+__device__ __forceinline__ void varlen_prefetch(const uint4* w16, uint64_t b, uint64_t nfull) {
+    if constexpr (PF == 2 || PF == 4) {
+        if (b + 2 <= nfull) {
+            const uint8_t* p = reinterpret_cast<const uint8_t*>(w16 + 4 * (b + 2));
+            prefetch_l2(p);
+            prefetch_l2(p + 79);
+        }
+    }
+    if constexpr (PF == 3 || PF == 4) {
+        if (b + 1 <= nfull) {
+            const uint8_t* p = reinterpret_cast<const uint8_t*>(w16 + 4 * (b + 1));
+            prefetch_l1(p);
+            prefetch_l1(p + 79);
+        }
+    }
+}
+
+template <int ALG, int PF, bool EDGE>
 __device__ __forceinline__ void varlen16_message(const uint4* w16, uintptr_t a, uint64_t len, uintptr_t dend,
                                                  uint8_t* dout) {
     using H = HashAlg<ALG>;
@@ -504,7 +531,7 @@ __device__ __forceinline__ void varlen16_message(const uint4* w16, uintptr_t a, 
     uint32_t c[20];
     uint32_t raw[16];
     const uint64_t nfull = len >> 6;
-    if (PF) {
+    if (PF == 1) {
         if (nfull) load_full_window(w16, misaligned, c, EDGE, dend);
         for (uint64_t b = 0; b < nfull; ++b) {
             realign16(c, q, sh, raw);
@@ -512,8 +539,10 @@ __device__ __forceinline__ void varlen16_message(const uint4* w16, uintptr_t a, 
             compress1<ALG>(st, raw);
         }
     } else {
+        if (PF == 2 || PF == 4) varlen_prefetch<2>(w16, (uint64_t)-1, nfull);  // block 1 (b = -1: b + 2 = 1)
         for (uint64_t b = 0; b < nfull; ++b) {
             load_full_window(w16 + 4 * b, misaligned, c, EDGE, dend);
+            varlen_prefetch<PF>(w16, b, nfull);
             realign16(c, q, sh, raw);
             compress1<ALG>(st, raw);
         }
@@ -612,7 +641,7 @@ k_varlen16u(const uint8_t* __restrict__ data, const uint8_t* data_end, const uin
         varlen16u_message<ALG, V, false>(w16, a, len, dend, out + i * H::kDigestBytes);
 }
 
-template <int ALG, bool PF = false>
+template <int ALG, int PF = 0>
 __global__ void __launch_bounds__(128)
 k_varlen16(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
@@ -969,7 +998,7 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
     const uint32_t* perm = nullptr;
     cudaError_t e = launch_varlen_sort(ALG, d_data, d_offsets, offset_base, n, d_scratch, stream, flags, &perm, 4);
     if (e != cudaSuccess) return e;
-    launch_plain(k_varlen16<ALG, false>, (unsigned)((n + 127) / 128), 128, stream, d_data, d_data + data_bytes,
+    launch_plain(k_varlen16<ALG, 0>, (unsigned)((n + 127) / 128), 128, stream, d_data, d_data + data_bytes,
                  d_offsets, offset_base, perm, n, d_out);
     return cudaGetLastError();
 }
