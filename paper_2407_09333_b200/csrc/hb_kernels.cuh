@@ -477,15 +477,36 @@ __device__ __forceinline__ uint4 ld16_edge(const uint4* p, bool edge, uintptr_t 
     return (edge && reinterpret_cast<uintptr_t>(p + 1) > dend) ? ld16_bounded(p, dend) : __ldg(p);
 }
 
+// LD: 0 = plain read-only loads; 1 = with an L2 256-byte prefetch hint (a
+// miss fills the next three blocks of the message into L2); 2 = the same and
+// no L1 allocation.
+template <int LD>
+__device__ __forceinline__ uint4 ld16(const uint4* p) {
+    if constexpr (LD == 0) {
+        return __ldg(p);
+    } else {
+        uint4 v;
+        if constexpr (LD == 1)
+            asm volatile("ld.global.nc.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+        else
+            asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+        return v;
+    }
+}
+
+template <int LD = 0>
 __device__ __forceinline__ void load_full_window(const uint4* src, bool misaligned, uint32_t (&c)[20],
                                                  bool edge = false, uintptr_t dend = 0) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {  // chunks 0-3 end inside the block: never past the message
-        const uint4 v = __ldg(src + k);
+        const uint4 v = ld16<LD>(src + k);
         c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
     }
     uint4 v4 = make_uint4(0, 0, 0, 0);
-    if (misaligned) v4 = ld16_edge(src + 4, edge, dend);
+    if (misaligned) v4 = (edge && reinterpret_cast<uintptr_t>(src + 5) > dend) ? ld16_bounded(src + 4, dend)
+                                                                                 : ld16<LD>(src + 4);
     c[16] = v4.x; c[17] = v4.y; c[18] = v4.z; c[19] = v4.w;
 }
 
@@ -520,7 +541,7 @@ __device__ __forceinline__ void varlen_prefetch(const uint4* w16, uint64_t b, ui
     }
 }
 
-template <int ALG, int PF, bool EDGE>
+template <int ALG, int PF, bool EDGE, int LD = 0>
 __device__ __forceinline__ void varlen16_message(const uint4* w16, uintptr_t a, uint64_t len, uintptr_t dend,
                                                  uint8_t* dout) {
     using H = HashAlg<ALG>;
@@ -532,16 +553,16 @@ __device__ __forceinline__ void varlen16_message(const uint4* w16, uintptr_t a, 
     uint32_t raw[16];
     const uint64_t nfull = len >> 6;
     if (PF == 1) {
-        if (nfull) load_full_window(w16, misaligned, c, EDGE, dend);
+        if (nfull) load_full_window<LD>(w16, misaligned, c, EDGE, dend);
         for (uint64_t b = 0; b < nfull; ++b) {
             realign16(c, q, sh, raw);
-            if (b + 1 < nfull) load_full_window(w16 + 4 * (b + 1), misaligned, c, EDGE, dend);
+            if (b + 1 < nfull) load_full_window<LD>(w16 + 4 * (b + 1), misaligned, c, EDGE, dend);
             compress1<ALG>(st, raw);
         }
     } else {
         if (PF == 2 || PF == 4) varlen_prefetch<2>(w16, (uint64_t)-1, nfull);  // block 1 (b = -1: b + 2 = 1)
         for (uint64_t b = 0; b < nfull; ++b) {
-            load_full_window(w16 + 4 * b, misaligned, c, EDGE, dend);
+            load_full_window<LD>(w16 + 4 * b, misaligned, c, EDGE, dend);
             varlen_prefetch<PF>(w16, b, nfull);
             realign16(c, q, sh, raw);
             compress1<ALG>(st, raw);
@@ -641,7 +662,7 @@ k_varlen16u(const uint8_t* __restrict__ data, const uint8_t* data_end, const uin
         varlen16u_message<ALG, V, false>(w16, a, len, dend, out + i * H::kDigestBytes);
 }
 
-template <int ALG, int PF = 0>
+template <int ALG, int PF = 0, int LD = 0>
 __global__ void __launch_bounds__(128)
 k_varlen16(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
@@ -655,9 +676,9 @@ k_varlen16(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint
     const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
     const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
     if (((a + len + 15u) & ~uintptr_t(15)) > dend)
-        varlen16_message<ALG, PF, true>(w16, a, len, dend, out + i * H::kDigestBytes);
+        varlen16_message<ALG, PF, true, LD>(w16, a, len, dend, out + i * H::kDigestBytes);
     else
-        varlen16_message<ALG, PF, false>(w16, a, len, dend, out + i * H::kDigestBytes);
+        varlen16_message<ALG, PF, false, LD>(w16, a, len, dend, out + i * H::kDigestBytes);
 }
 
 
