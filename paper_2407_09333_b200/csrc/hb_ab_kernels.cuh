@@ -558,7 +558,7 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
         case 5: launch_plain(k_varlen_bulk<ALG, 2, 8>, grid, 128, stream, d_data, d_offsets, offset_base, perm, n, d_out); break;
         default: launch_plain(k_varlen_bulk<ALG, 3, 1>, grid, 128, stream, d_data, d_offsets, offset_base, perm, n, d_out); break;
         }
-    } else if (T.varlen_kernel >= 20) {  // load-hint arms: 20 + 3*LD + PF (PF 0 | 1)
+    } else if (T.varlen_kernel >= 20) {  // load-hint arms: 20 + 3*LD + PF (PF 0 | 1; 25 / 28: carry, LD 0 / 1)
         const unsigned blk = T.small_cta >= 128 ? 128u : 64u;  // $HB_SMALL_CTA=64: 64-thread CTAs
         const unsigned g2 = (unsigned)((n + blk - 1) / blk);
         switch (T.varlen_kernel) {
@@ -567,6 +567,8 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
         case 26: launch_plain(k_varlen16<ALG, 0, 2>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 27: launch_plain(k_varlen16<ALG, 1, 2>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 21: launch_plain(k_varlen16<ALG, 1, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 25: launch_plain(k_varlen16<ALG, 5, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 28: launch_plain(k_varlen16<ALG, 5, 1>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         default: launch_plain(k_varlen16<ALG, 0, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         }
     } else if (T.varlen_kernel >= 10) {  // prefetch-instruction arms of the per-thread kernel (PF = kernel - 10)

@@ -559,6 +559,27 @@ __device__ __forceinline__ void varlen16_message(const uint4* w16, uintptr_t a, 
             if (b + 1 < nfull) load_full_window<LD>(w16 + 4 * (b + 1), misaligned, c, EDGE, dend);
             compress1<ALG>(st, raw);
         }
+    } else if (PF == 5) {
+        // Carry: a misaligned window's fifth chunk is the next block's first,
+        // so it is kept in registers -- 4 loads per block instead of 5.
+        uint4 carry = make_uint4(0, 0, 0, 0);
+        for (uint64_t b = 0; b < nfull; ++b) {
+            const uint4* src = w16 + 4 * b;
+            const uint4 v0 = (b != 0 && misaligned) ? carry : ld16<LD>(src);
+            c[0] = v0.x; c[1] = v0.y; c[2] = v0.z; c[3] = v0.w;
+#pragma unroll
+            for (int k = 1; k < 4; ++k) {
+                const uint4 v = ld16<LD>(src + k);
+                c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+            }
+            uint4 v4 = make_uint4(0, 0, 0, 0);
+            if (misaligned) v4 = (EDGE && reinterpret_cast<uintptr_t>(src + 5) > dend) ? ld16_bounded(src + 4, dend)
+                                                                                       : ld16<LD>(src + 4);
+            c[16] = v4.x; c[17] = v4.y; c[18] = v4.z; c[19] = v4.w;
+            carry = v4;
+            realign16(c, q, sh, raw);
+            compress1<ALG>(st, raw);
+        }
     } else {
         if (PF == 2 || PF == 4) varlen_prefetch<2>(w16, (uint64_t)-1, nfull);  // block 1 (b = -1: b + 2 = 1)
         for (uint64_t b = 0; b < nfull; ++b) {
