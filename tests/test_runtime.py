@@ -267,3 +267,58 @@ def test_varlen_program_golden(golden):
             prog = lower_hash_batch_varlen(alg, off, [("gpu0", 0.4), ("gpu1", 0.6)], devs)
             rep = execute_batched(prog, devs, {"msgs": data, "offsets": off})
             assert hashlib.sha256(rep.outputs["out"]).hexdigest() == row[alg], (alg, len(lens))
+
+
+def test_sweep_grid_and_records():
+    """ratio_grid equals the reference's (sweep.py:39-48); split_ratios puts x
+    on the first binding; argmin skips failed points; CSV skips them too."""
+    from paper_2407_09333_b200.runtime import RunRecord, ratio_grid, records_to_csv, split_ratios, sweep_argmin
+
+    for step in (0.02, 0.1, 0.25, 0.3, 1.0):
+        xs = ratio_grid(step)
+        assert xs[0] == 0.0 and xs[-1] == 1.0 and xs == sorted(xs)
+    if os.path.isdir(REF_SRC):
+        sys.path.insert(0, REF_SRC)
+        try:
+            from hetoc.scheduler.sweep import ratio_grid as ref_grid
+        finally:
+            sys.path.remove(REF_SRC)
+        for step in (0.02, 0.07, 0.1, 0.25, 0.3, 1.0):
+            assert ratio_grid(step) == ref_grid(step)
+    for bad in (0.0, -0.1, 1.5):
+        with pytest.raises(ValueError):
+            ratio_grid(bad)
+    assert split_ratios(0.25, 3) == (0.25, 0.375, 0.375)
+    with pytest.raises(ValueError):
+        split_ratios(0.5, 1)
+    recs = [RunRecord((0.0, 1.0), 2.0, {"a": 1.0, "b": 2.0}, {"a": 0, "b": 3}, 10, "md5"),
+            RunRecord((0.5, 0.5), 1.0, {"a": 1.0, "b": 1.0}, {"a": 2, "b": 2}, 10, "md5"),
+            RunRecord((1.0, 0.0), float("nan"), {}, {}, 10, "md5", error="boom")]
+    assert sweep_argmin(recs).ratio_first == 0.5
+    csv = records_to_csv(recs).splitlines()
+    assert csv[0] == "ratio_first,wall_s,accel_s,batches,n_data,alg" and len(csv) == 3
+    assert csv[2] == "0.5,1,1;1,2;2,10,md5"
+    with pytest.raises(ValueError):
+        sweep_argmin(recs[2:])
+
+
+@pytest.mark.gpu
+def test_sweep_gpu_ratio_grid():
+    """The reference's duty-ratio sweep (sweep.py:75-99) over two GPU bindings
+    (aliasing GPU 0 on a one-GPU box): every point runs, the extremes put the
+    whole batch on one binding, and each point's digests equal the oracle's."""
+    import oracle
+    from paper_2407_09333_b200 import _native
+    from paper_2407_09333_b200.runtime import split_ratios, sweep, sweep_argmin
+
+    n = _native.device_count()
+    w = Workload("md5", 30011, 9)
+    host = DeviceSpec("host", kind="host", threads=os.cpu_count() or 1)
+    devs = DeviceTable(host, tuple(DeviceSpec(f"gpu{i}", ordinal=i % n, mem_bytes=1 << 20) for i in range(2)))
+    recs = sweep(w, devs, step=0.25)
+    assert [r.ratio_first for r in recs] == [0.0, 0.25, 0.5, 0.75, 1.0]
+    assert all(r.error is None and r.wall_s > 0 for r in recs)
+    assert recs[0].batches["gpu0"] == 0 and recs[-1].batches["gpu1"] == 0
+    best = sweep_argmin(recs)
+    ref = oracle.batch_fixed("md5", gen_messages(0, w.count, w.width).as_array(), threads=8).tobytes()
+    assert run_point(w, devs, split_ratios(best.ratio_first, 2), keep_digests=True).digests == ref
