@@ -498,6 +498,8 @@ static void launch_small_one_ab(const uint8_t* d_msgs, uint64_t n, uint8_t* d_ou
     const bool pair = T.small_pair_all || (ALG == kMd5 && n >= (1ull << 20) && L <= 32 && T.small_pair);
     if (T.const_variant == 0)
         launch_pdl(k_fixed_small<ALG, L, kVarPlain>, (unsigned)((n + b - 1) / b), b, s, d_msgs, n, d_out);
+    else if (T.const_variant == 3)
+        launch_pdl(k_fixed_small<ALG, L, kVarBal3>, (unsigned)((n + b - 1) / b), b, s, d_msgs, n, d_out);
     else if (pair)
         launch_pdl(k_fixed_small<ALG, L, kVarBal, 2>, (unsigned)(((n + 1) / 2 + b - 1) / b), b, s, d_msgs, n, d_out);
     else

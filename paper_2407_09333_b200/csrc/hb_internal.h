@@ -43,6 +43,7 @@ struct Tuning {
     int dec_pair = -1;                          // $HB_DEC_PAIR
     bool fma_digits = true;                     // $HB_FMA_DIGITS
     uint32_t sort_window = 8192;                // $HB_SORT_WINDOW
+    bool sort_qmajor = false;                   // $HB_SORT_QMAJOR: windowed sort key (q, block count)
     uint32_t varlen_ld = 16;                    // $HB_VARLEN_LD
     uint32_t varlen_q = 8;                      // $HB_VARLEN_Q
     uint32_t varlen_prefetch = 0;               // $HB_VARLEN_PREFETCH

@@ -71,11 +71,12 @@ static Tuning parse_tuning() {
     t.const_variant = env_set("HB_CONST_VARIANT") ? (int)env_u64("HB_CONST_VARIANT", 1) : -1;
     t.small_cta = (uint32_t)env_u64("HB_SMALL_CTA", 128);
     t.small_pair_all = env_u64("HB_SMALL_PAIR_ALL", 0) != 0;
-    t.small_kernel_ab = t.const_variant == 0 || t.small_cta != 128 || t.small_pair_all;
+    t.small_kernel_ab = t.const_variant == 0 || t.const_variant == 3 || t.small_cta != 128 || t.small_pair_all;
     t.dec_pair = env_set("HB_DEC_PAIR") ? (int)env_u64("HB_DEC_PAIR", 0) : -1;
     t.fma_digits = env_u64("HB_FMA_DIGITS", 1) != 0;
     t.dec_ab = t.dec_pair >= 0 || !t.fma_digits || t.const_variant >= 0;
     t.sort_window = (uint32_t)env_u64("HB_SORT_WINDOW", 8192);
+    t.sort_qmajor = env_u64("HB_SORT_QMAJOR", 0) != 0;
     t.varlen_ld = (uint32_t)env_u64("HB_VARLEN_LD", 16);
     t.varlen_q = (uint32_t)env_u64("HB_VARLEN_Q", 8);
     t.varlen_prefetch = (uint32_t)env_u64("HB_VARLEN_PREFETCH", 0);
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const uint64_t* _
 // other: L2 lines fetched for one message (256 B promotion) are still
 // resident when its neighbours are hashed, instead of being re-fetched from
 // HBM after a global sort scattered the neighbours across the whole batch.
-template <int kSortWindow, int Q>
+template <int kSortWindow, int Q, bool QMAJOR = false>
 __global__ void __launch_bounds__(1024) k_sort_window(const uint64_t* __restrict__ offsets, uint64_t n,
                                                       uint64_t addr_bias, uint32_t* __restrict__ perm) {
     constexpr int kBuckets = kSortNbClasses * Q;
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(1024) k_sort_window(const uint64_t* __restrict
         const uint64_t i = w0 + (uint64_t)it * 1024u + t;
         key[it] = 0xFFFFFFFFu;
         if (i < n) {
-            key[it] = sort_bucket_q<Q>(offsets, i, addr_bias);
+            key[it] = sort_bucket_q<Q, QMAJOR>(offsets, i, addr_bias);
             rank[it] = atomicAdd(&h[key[it]], 1u);
         }
     }
@@ -277,6 +278,7 @@ cudaError_t launch_varlen_sort(int alg, const uint8_t* d_data, const uint64_t* d
         const bool q8 = qclasses == 8;
 #define HB_WIN(W)                                                                                            \
     q8 ? k_sort_window<W, 8><<<(unsigned)((n + W - 1) / W), 1024, 0, stream>>>(d_offsets, n, bias0, p)     \
+    : T.sort_qmajor ? k_sort_window<W, 4, true><<<(unsigned)((n + W - 1) / W), 1024, 0, stream>>>(d_offsets, n, bias0, p) \
        : k_sort_window<W, 4><<<(unsigned)((n + W - 1) / W), 1024, 0, stream>>>(d_offsets, n, bias0, p)
         if (w >= 16384)
             HB_WIN(16384);

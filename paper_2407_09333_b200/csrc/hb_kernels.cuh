@@ -719,12 +719,18 @@ constexpr int kSortItems = 16;  // per thread
 // Sort key: block-count class (longest first) x Q word-alignment classes
 // q = (address >> 2) mod Q -- Q = 4 for the 16-byte-window kernels, 8 for the
 // 32-byte-window one -- so a warp's messages take the same realignment path.
-template <int Q>
+// QMAJOR: alignment class first, then block count -- a window of 8,192
+// messages has ~31 per (block count, q) bucket, so with the block count as
+// the major key nearly every warp straddles two q classes (the realignment
+// switch then runs two paths); q-major warps are q-uniform and straddle at
+// most two adjacent block counts instead.
+template <int Q, bool QMAJOR = false>
 __device__ __forceinline__ uint32_t sort_bucket_q(const uint64_t* offsets, uint64_t i, uint64_t addr_bias) {
     const uint64_t len = offsets[i + 1] - offsets[i];
     const uint64_t nb = (len + 8u) / 64u + 1u;
     const uint64_t c = nb < (uint64_t)(kSortNbClasses - 1) ? nb : (uint64_t)(kSortNbClasses - 1);
     const uint32_t q = (uint32_t)((offsets[i] + addr_bias) >> 2) & (uint32_t)(Q - 1);
+    if (QMAJOR) return q * (uint32_t)kSortNbClasses + ((uint32_t)(kSortNbClasses - 1) - (uint32_t)c);
     return ((uint32_t)(kSortNbClasses - 1) - (uint32_t)c) * (uint32_t)Q + q;
 }
 __device__ __forceinline__ uint32_t sort_bucket(const uint64_t* offsets, uint64_t i, uint64_t addr_bias) {
