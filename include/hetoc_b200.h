@@ -59,6 +59,14 @@ typedef enum { HB_SHA1 = 0, HB_MD5 = 1, HB_SM3 = 2 } hb_alg;
 #define HB_FLAG_NO_TMA   0x1u  /* fixed width: direct-load kernel instead of TMA staging */
 #define HB_FLAG_NO_SORT  0x2u  /* varlen: skip the length-bucket sort                    */
 #define HB_FLAG_SYNC_H2D 0x4u  /* engine: no copy/compute overlap (diagnostics)          */
+/* fixed width, hb_hash_fixed_dev: the caller guarantees the message bytes are
+ * not written by the kernel that immediately precedes this launch on the
+ * stream (e.g. they were copied in, or written earlier and synchronised).
+ * The hash kernel then starts reading them while that kernel drains
+ * (programmatic dependent launch); digests are still written only after it
+ * completes.  (The engine's own chunks follow their H2D copy, which a
+ * dependent launch never overlaps, so it does not need it.)                 */
+#define HB_FLAG_INPUT_READY 0x40u
 /* A/B kernel arms: honoured only by a library built with -DHB_AB
  * (hb_built_with_ab() == 1); the default build returns HB_ERR_CUDA with
  * hb_last_error() saying so for VARLEN_WORDS / VARLEN_COOP.                 */

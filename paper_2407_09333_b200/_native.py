@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(_HERE, os.environ.get("HETOC_B200_LIB", "libhetoc_b200.s
 HB_OK, HB_ERR_ALG, HB_ERR_INVAL, HB_ERR_CUDA, HB_ERR_NOMEM, HB_ERR_NODEV = range(6)
 HB_FLAG_NO_TMA, HB_FLAG_NO_SORT, HB_FLAG_SYNC_H2D, HB_FLAG_VARLEN_WORDS = 0x1, 0x2, 0x4, 0x8
 HB_FLAG_VARLEN_COOP_OFF, HB_FLAG_VARLEN_COOP = 0x10, 0x20
+HB_FLAG_INPUT_READY = 0x40  # fixed width, device-resident: messages not written by the preceding kernel
 ALG_ID = {"sha1": 0, "md5": 1, "sm3": 2}
 
 # Every symbol include/hetoc_b200.h declares (tests check the library exports all of them).

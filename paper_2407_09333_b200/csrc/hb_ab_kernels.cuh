@@ -497,13 +497,13 @@ static void launch_small_one_ab(const uint8_t* d_msgs, uint64_t n, uint8_t* d_ou
     const unsigned b = T.small_cta >= 128 ? 128u : T.small_cta >= 64 ? 64u : 32u;
     const bool pair = T.small_pair_all || (ALG == kMd5 && n >= (1ull << 20) && L <= 32 && T.small_pair);
     if (T.const_variant == 0)
-        launch_pdl(k_fixed_small<ALG, L, kVarPlain>, (unsigned)((n + b - 1) / b), b, s, d_msgs, n, d_out);
+        launch_pdl(k_fixed_small<ALG, L, kVarPlain>, (unsigned)((n + b - 1) / b), b, s, d_msgs, n, d_out, 0u);
     else if (T.const_variant == 3)
-        launch_pdl(k_fixed_small<ALG, L, kVarBal3>, (unsigned)((n + b - 1) / b), b, s, d_msgs, n, d_out);
+        launch_pdl(k_fixed_small<ALG, L, kVarBal3>, (unsigned)((n + b - 1) / b), b, s, d_msgs, n, d_out, 0u);
     else if (pair)
-        launch_pdl(k_fixed_small<ALG, L, kVarBal, 2>, (unsigned)(((n + 1) / 2 + b - 1) / b), b, s, d_msgs, n, d_out);
+        launch_pdl(k_fixed_small<ALG, L, kVarBal, 2>, (unsigned)(((n + 1) / 2 + b - 1) / b), b, s, d_msgs, n, d_out, 0u);
     else
-        launch_pdl(k_fixed_small<ALG, L, kVarBal>, (unsigned)((n + b - 1) / b), b, s, d_msgs, n, d_out);
+        launch_pdl(k_fixed_small<ALG, L, kVarBal>, (unsigned)((n + b - 1) / b), b, s, d_msgs, n, d_out, 0u);
 }
 
 template <int ALG>

@@ -25,6 +25,9 @@ struct Tuning {
     // kernels (hb_kernels.cuh)
     bool pdl = true;                            // $HB_PDL
     uint64_t small_n = 1ull << 18;              // $HB_SMALL_N: below it, one message per thread in TMA tiles
+    uint64_t chain_n = 1ull << 17;              // $HB_CHAIN_N: MD5 TMA batches below it use round variant 3
+    bool varlen_pf = true;                      // $HB_VARLEN_PF: MD5 varlen, software-pipelined per-thread kernel
+    bool sort_qmajor = true;                    // $HB_SORT_QMAJOR: windowed sort key (q, block count), else (block count, q)
     uint64_t direct_max_len = 128;              // $HB_DIRECT_MAX_L: rows up to it use the per-thread-load kernels
     bool small_pair = true;                     // $HB_SMALL_PAIR: MD5 <= 32 B rows, two per thread at >= 2^20
     bool dec_run = true;                        // $HB_DEC_RUN: runs-of-ten decimal kernel
@@ -39,11 +42,11 @@ struct Tuning {
     int const_variant = -1;                     // $HB_CONST_VARIANT
     uint32_t small_cta = 128;                   // $HB_SMALL_CTA
     bool small_pair_all = false;                // $HB_SMALL_PAIR_ALL: two rows per thread at every width / count
+    bool input_ready = false;                   // $HB_INPUT_READY: treat every fixed-width launch as HB_FLAG_INPUT_READY
     bool dec_ab = false;                        // any of $HB_DEC_PAIR / $HB_FMA_DIGITS / $HB_CONST_VARIANT set
     int dec_pair = -1;                          // $HB_DEC_PAIR
     bool fma_digits = true;                     // $HB_FMA_DIGITS
     uint32_t sort_window = 8192;                // $HB_SORT_WINDOW
-    bool sort_qmajor = false;                   // $HB_SORT_QMAJOR: windowed sort key (q, block count)
     uint32_t varlen_ld = 16;                    // $HB_VARLEN_LD
     uint32_t varlen_q = 8;                      // $HB_VARLEN_Q
     uint32_t varlen_prefetch = 0;               // $HB_VARLEN_PREFETCH

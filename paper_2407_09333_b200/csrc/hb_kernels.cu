@@ -52,6 +52,9 @@ static Tuning parse_tuning() {
     t.device_reserve = env_u64("HB_DEVICE_RESERVE", t.device_reserve);
     t.pdl = env_u64("HB_PDL", 1) != 0;
     t.small_n = env_u64("HB_SMALL_N", t.small_n);
+    t.chain_n = env_u64("HB_CHAIN_N", t.chain_n);
+    t.varlen_pf = env_u64("HB_VARLEN_PF", 1) != 0;
+    t.sort_qmajor = env_u64("HB_SORT_QMAJOR", 1) != 0;
     t.direct_max_len = env_u64("HB_DIRECT_MAX_L", t.direct_max_len);
     t.small_pair = env_u64("HB_SMALL_PAIR", 1) != 0;
     t.dec_run = env_u64("HB_DEC_RUN", 1) != 0;
@@ -71,12 +74,12 @@ static Tuning parse_tuning() {
     t.const_variant = env_set("HB_CONST_VARIANT") ? (int)env_u64("HB_CONST_VARIANT", 1) : -1;
     t.small_cta = (uint32_t)env_u64("HB_SMALL_CTA", 128);
     t.small_pair_all = env_u64("HB_SMALL_PAIR_ALL", 0) != 0;
+    t.input_ready = env_u64("HB_INPUT_READY", 0) != 0;
     t.small_kernel_ab = t.const_variant == 0 || t.const_variant == 3 || t.small_cta != 128 || t.small_pair_all;
     t.dec_pair = env_set("HB_DEC_PAIR") ? (int)env_u64("HB_DEC_PAIR", 0) : -1;
     t.fma_digits = env_u64("HB_FMA_DIGITS", 1) != 0;
     t.dec_ab = t.dec_pair >= 0 || !t.fma_digits || t.const_variant >= 0;
     t.sort_window = (uint32_t)env_u64("HB_SORT_WINDOW", 8192);
-    t.sort_qmajor = env_u64("HB_SORT_QMAJOR", 0) != 0;
     t.varlen_ld = (uint32_t)env_u64("HB_VARLEN_LD", 16);
     t.varlen_q = (uint32_t)env_u64("HB_VARLEN_Q", 8);
     t.varlen_prefetch = (uint32_t)env_u64("HB_VARLEN_PREFETCH", 0);
@@ -289,7 +292,10 @@ cudaError_t launch_varlen_sort(int alg, const uint8_t* d_data, const uint64_t* d
 #undef HB_WIN
 #else
         (void)qclasses;
-        k_sort_window<8192, 4><<<(unsigned)((n + 8191) / 8192), 1024, 0, stream>>>(d_offsets, n, bias0, p);
+        if (T.sort_qmajor)
+            k_sort_window<8192, 4, true><<<(unsigned)((n + 8191) / 8192), 1024, 0, stream>>>(d_offsets, n, bias0, p);
+        else
+            k_sort_window<8192, 4><<<(unsigned)((n + 8191) / 8192), 1024, 0, stream>>>(d_offsets, n, bias0, p);
 #endif
         note_launch(nullptr, false);
         perm = p;

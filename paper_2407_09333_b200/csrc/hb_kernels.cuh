@@ -125,6 +125,8 @@ template <int ALG, int NB, int STAGES, int W = kTmaWarps> struct TmaOcc {  // CT
 // `empty` -- no TMA-issue path, fence or lane-0 branch in their loop.
 // -------------------------------------------------------------------------
 constexpr int kWsComputeWarps = 4;
+constexpr uint32_t kEarlyLoad = 1u;     // read the messages before griddepcontrol.wait (HB_FLAG_INPUT_READY)
+constexpr uint32_t kEarlyTrigger = 2u;  // release the next grid right after griddepcontrol.wait
 // SLACK: reserve 1 KiB to align the ring to 1024 B at run time.  Without it
 // (the dynamic window of a kernel with no static shared memory starts 1 KiB
 // aligned -- checked in-kernel) a 3-stage CTA needs 24 KiB and 9 CTAs fit an
@@ -146,7 +148,7 @@ template <int ALG, int NB, int STAGES, bool SLACK = true> struct WsOcc {
 template <int ALG, int V, int NB, int STAGES, bool UNR = false, bool SLACK = true>
 __global__ void __launch_bounds__((kWsComputeWarps + 1) * 32, (WsOcc<ALG, NB, STAGES, SLACK>::kMinCtas))
 k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out,
-               uint32_t evict_first) {
+               uint32_t evict_first, uint32_t early) {
     using H = HashAlg<ALG, V>;
     using C = WsCfg<NB, STAGES, SLACK>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -171,14 +173,30 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
     // Programmatic dependent launch (launch_pdl_smem): the barrier setup above
     // overlaps the previous grid's tail; global memory is touched only after it
     // completes.  The next grid is triggered once the digests are computed.
+    // early & kEarlyLoad (HB_FLAG_INPUT_READY: the caller guarantees the
+    // previous grid does not write the messages): the first ring stages are
+    // loaded before the wait, so the HBM latency of this grid's first blocks
+    // overlaps the previous grid's tail.  Digests are still stored only after
+    // the wait.  early & kEarlyTrigger (a grid that leaves room for the next
+    // one on every SM): the next grid is released right after the wait, so it
+    // is resident -- barriers set up, first stages loading -- while this one runs.
+    const uint32_t pro = (early & kEarlyLoad) ? (nload < (uint32_t)STAGES ? nload : (uint32_t)STAGES) : 0u;
+    if (pro && warp == kWsComputeWarps && lane == 0) {
+        prefetch_tmap(&tmap);
+        for (uint32_t b = 0; b < pro; ++b) {
+            mbar_arrive_expect_tx(&full[b], C::kStageBytes);
+            tma_load_2d(ring + b * C::kStageBytes, &tmap, &full[b], (int)(b * 64u), (int)row0);
+        }
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (early & kEarlyTrigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == kWsComputeWarps) {  // ---------------- producer warp
         if (lane == 0) {
-            prefetch_tmap(&tmap);
+            if (!pro) prefetch_tmap(&tmap);
             const uint64_t pol = evict_first ? policy_evict_first() : 0;
-            uint32_t s = 0, ph = 0;
-            for (uint32_t b = 0; b < nload; ++b) {
+            uint32_t s = pro % (uint32_t)STAGES, ph = pro == (uint32_t)STAGES ? 1u : 0u;
+            for (uint32_t b = pro; b < nload; ++b) {
                 if (b >= (uint32_t)STAGES) mbar_wait_parity(&empty[s], ph ^ 1u);
                 mbar_arrive_expect_tx(&full[s], C::kStageBytes);
                 if (evict_first)
@@ -312,7 +330,7 @@ __host__ __device__ constexpr uint32_t bswap_c(uint32_t x) {
 
 template <int ALG, int L, int V = -1, int NB = 1>
 __global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__ msgs, uint64_t n,
-                                                     uint8_t* __restrict__ out) {
+                                                     uint8_t* __restrict__ out, uint32_t early = 0) {
     using H = HashAlg<ALG, V>;
     static_assert(L % 16 == 0 && L >= 16 && L <= 128, "width");
     static_assert(NB == 1 || NB == 2, "messages per thread");
@@ -324,12 +342,18 @@ __global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__
     // completion and memory before touching global memory; the trigger for
     // the next grid comes once this thread's hash is done (both no-ops for a
     // normal launch).  A stream of short batches then hides the launch gap.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // early: as in k_fixed_tma_ws -- kEarlyLoad reads the row before the wait
+    // (the caller guarantees the previous grid does not write it; digests are
+    // stored after the wait), kEarlyTrigger releases the next grid right after it.
+    if (!(early & kEarlyLoad)) asm volatile("griddepcontrol.wait;" ::: "memory");
     // NB = 2: rows 2t and 2t+1 (contiguous bytes) hashed as two independent
     // chains in one compress call; a missing second row re-hashes the first
     // and is not stored.
     const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * NB;
-    if (i0 >= n) return;
+    if (i0 >= n) {
+        if (early & kEarlyLoad) asm volatile("griddepcontrol.wait;" ::: "memory");
+        return;
+    }
     uint32_t w[NB][L / 4];
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
@@ -341,6 +365,8 @@ __global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__
             w[q][4 * c] = v.x; w[q][4 * c + 1] = v.y; w[q][4 * c + 2] = v.z; w[q][4 * c + 3] = v.w;
         }
     }
+    if (early & kEarlyLoad) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (early & kEarlyTrigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     uint32_t st[NB][H::kStateWords];
 #pragma unroll
     for (int q = 0; q < NB; ++q) H::init(st[q]);
@@ -935,7 +961,7 @@ static cudaError_t encode_rows_map(CUtensorMap* map, const uint8_t* d_msgs, uint
 
 template <int ALG, int V, int NB, int STAGES, bool UNR = false, bool SLACK = true>
 static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
-                                       cudaStream_t stream) {
+                                       cudaStream_t stream, bool input_ready = false) {
     using C = WsCfg<NB, STAGES, SLACK>;
     const Tuning& T = tuning();
     CUtensorMap map;
@@ -954,8 +980,12 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     // SM there and run up to 30 % slower (profiles/ab_pdl_r1.txt), so those
     // launch normally.
     const bool pdl = grid >= (uint32_t)device_sms() || (L + 8u) / 64u + 1u <= 17u;
+    // The next grid may be released early only if it fits beside this one:
+    // at most half the CTA slots of every SM.
+    const uint32_t half_wave = (uint32_t)device_sms() * (uint32_t)WsOcc<ALG, NB, STAGES, SLACK>::kMinCtas / 2u;
+    const uint32_t early = input_ready && pdl && T.pdl ? kEarlyLoad | (grid <= half_wave ? kEarlyTrigger : 0u) : 0u;
     launch_pdl_smem(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK>, grid, (kWsComputeWarps + 1) * 32, C::kSmem,
-                    stream, pdl, map, n, L, d_out, (uint32_t)T.tma_evict_first);
+                    stream, pdl, map, n, L, d_out, (uint32_t)T.tma_evict_first, early);
     return cudaGetLastError();
 }
 
@@ -971,29 +1001,43 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
 // message per thread so the grid still covers every SM (SHA-1's NB=2 tiles
 // halve the CTA count: 4096 x 64 KiB 251 vs 428 GB/s, profiles/ab_small_r1.txt).
 template <int ALG>
-static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t L, uint8_t* dst, cudaStream_t s) {
+static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t L, uint8_t* dst, cudaStream_t s,
+                                       bool input_ready) {
 #ifdef HB_AB
     if (tuning().tma_cfg >= 0 || tuning().variant >= 0) return launch_tma_ab<ALG>(src, n, L, dst, s);
 #endif
+    // MD5 batches under 2^17 messages (at most ~4.4 warps per SM sub-partition:
+    // bound by each message's dependent chain, not by issue) take round
+    // variant 3, whose shorter f -> add -> rotate chain is 4-23 % faster there
+    // and 3-5 % slower once the grid is issue-bound (profiles/ab_mid_r2c.txt).
+    if constexpr (ALG == kMd5)
+        if ((uint64_t)n < tuning().chain_n) return launch_fixed_tma_ws<ALG, kVarBal3, 1, 3>(src, n, L, dst, s, input_ready);
     if ((uint64_t)n < tuning().small_n || ALG != kSha1)
-        return launch_fixed_tma_ws<ALG, kVarBal, 1, 3>(src, n, L, dst, s);
-    return launch_fixed_tma_ws<ALG, kVarBal, 2, 3>(src, n, L, dst, s);
+        return launch_fixed_tma_ws<ALG, kVarBal, 1, 3>(src, n, L, dst, s, input_ready);
+    return launch_fixed_tma_ws<ALG, kVarBal, 2, 3>(src, n, L, dst, s, input_ready);
 }
 
 // Compile-time-width kernel for L in {16, 32, 48, 64, 128}; MD5 one-block
 // rows (<= 32 B) in batches >= 2^20 take two adjacent rows per thread (+3-4 %;
 // 48-byte rows lose 2 %, two-block rows 1-9 %, profiles/ab_small_r1d.txt).
 template <int ALG, int L>
-static void launch_small(const uint8_t* d_msgs, uint64_t n, uint8_t* d_out, cudaStream_t s) {
+static void launch_small(const uint8_t* d_msgs, uint64_t n, uint8_t* d_out, cudaStream_t s, bool input_ready) {
     constexpr unsigned kBlk = 128;
+    // early start (see k_fixed_small): the next grid is released early only
+    // when it fits beside this one (<= 8 of the SM's 16 CTA slots).
+    const auto early = [&](unsigned grid) -> uint32_t {
+        return input_ready && tuning().pdl ? kEarlyLoad | (grid <= 8u * (unsigned)device_sms() ? kEarlyTrigger : 0u)
+                                           : 0u;
+    };
     if constexpr (ALG == kMd5 && L <= 32) {
         if (n >= (1ull << 20) && tuning().small_pair) {
-            launch_pdl(k_fixed_small<ALG, L, kVarBal, 2>, (unsigned)(((n + 1) / 2 + kBlk - 1) / kBlk), kBlk, s,
-                       d_msgs, n, d_out);
+            const unsigned g = (unsigned)(((n + 1) / 2 + kBlk - 1) / kBlk);
+            launch_pdl(k_fixed_small<ALG, L, kVarBal, 2>, g, kBlk, s, d_msgs, n, d_out, early(g));
             return;
         }
     }
-    launch_pdl(k_fixed_small<ALG, L, kVarBal>, (unsigned)((n + kBlk - 1) / kBlk), kBlk, s, d_msgs, n, d_out);
+    const unsigned g = (unsigned)((n + kBlk - 1) / kBlk);
+    launch_pdl(k_fixed_small<ALG, L, kVarBal>, g, kBlk, s, d_msgs, n, d_out, early(g));
 }
 
 template <int ALG>
@@ -1004,13 +1048,17 @@ static cudaError_t launch_fixed_alg(const uint8_t* d_msgs, uint64_t n, uint64_t 
     const bool aligned = L > 0 && (L % 16) == 0 && (reinterpret_cast<uintptr_t>(d_msgs) % 16) == 0 &&
                          L < (1ull << 31);
     const bool direct = (flags & HB_FLAG_NO_TMA) || L <= T.direct_max_len;
+    bool input_ready = (flags & HB_FLAG_INPUT_READY) != 0;
+#ifdef HB_AB
+    input_ready = input_ready || T.input_ready;
+#endif
     if (aligned && !direct) {
         // TMA coordinates are int32: split very large batches into row slabs.
         const uint64_t slab = 1ull << 30;
         for (uint64_t r0 = 0; r0 < n; r0 += slab) {
             const uint64_t rn = (n - r0) < slab ? (n - r0) : slab;
             const cudaError_t e = launch_tma_dispatch<ALG>(d_msgs + r0 * L, (uint32_t)rn, (uint32_t)L,
-                                                           d_out + r0 * H::kDigestBytes, stream);
+                                                           d_out + r0 * H::kDigestBytes, stream, input_ready);
             if (e != cudaSuccess) return e;
         }
         return cudaSuccess;
@@ -1020,11 +1068,11 @@ static cudaError_t launch_fixed_alg(const uint8_t* d_msgs, uint64_t n, uint64_t 
 #endif
     const unsigned grid = (unsigned)((n + 127) / 128);
     const bool small_ok = aligned && T.small_kernel;
-    if (small_ok && L == 16) launch_small<ALG, 16>(d_msgs, n, d_out, stream);
-    else if (small_ok && L == 32) launch_small<ALG, 32>(d_msgs, n, d_out, stream);
-    else if (small_ok && L == 48) launch_small<ALG, 48>(d_msgs, n, d_out, stream);
-    else if (small_ok && L == 64) launch_small<ALG, 64>(d_msgs, n, d_out, stream);
-    else if (small_ok && L == 128) launch_small<ALG, 128>(d_msgs, n, d_out, stream);
+    if (small_ok && L == 16) launch_small<ALG, 16>(d_msgs, n, d_out, stream, input_ready);
+    else if (small_ok && L == 32) launch_small<ALG, 32>(d_msgs, n, d_out, stream, input_ready);
+    else if (small_ok && L == 48) launch_small<ALG, 48>(d_msgs, n, d_out, stream, input_ready);
+    else if (small_ok && L == 64) launch_small<ALG, 64>(d_msgs, n, d_out, stream, input_ready);
+    else if (small_ok && L == 128) launch_small<ALG, 128>(d_msgs, n, d_out, stream, input_ready);
     else if (aligned) launch_plain(k_fixed_direct<ALG>, grid, 128, stream, d_msgs, n, (uint32_t)L, d_out);
     else launch_plain(k_generic<ALG, false>, grid, 128, stream, d_msgs, d_msgs + n * L,
                       (const uint64_t*)nullptr, (uint64_t)0, (const uint32_t*)nullptr, L, n, d_out);
@@ -1046,8 +1094,16 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
     const uint32_t* perm = nullptr;
     cudaError_t e = launch_varlen_sort(ALG, d_data, d_offsets, offset_base, n, d_scratch, stream, flags, &perm, 4);
     if (e != cudaSuccess) return e;
-    launch_plain(k_varlen16<ALG, 0>, (unsigned)((n + 127) / 128), 128, stream, d_data, d_data + data_bytes,
-                 d_offsets, offset_base, perm, n, d_out);
+    // MD5 (HBM/issue ridge, windowed q-major sort): the software-pipelined
+    // per-thread kernel, block b+1's window in flight during b's compression
+    // (-6 % vs the plain kernel, profiles/ab_varlen_r2d.txt); SHA-1 / SM3 are
+    // ALU-bound and keep the plain kernel.
+    if (ALG == kMd5 && tuning().varlen_pf)
+        launch_plain(k_varlen16<ALG, 1>, (unsigned)((n + 127) / 128), 128, stream, d_data, d_data + data_bytes,
+                     d_offsets, offset_base, perm, n, d_out);
+    else
+        launch_plain(k_varlen16<ALG, 0>, (unsigned)((n + 127) / 128), 128, stream, d_data, d_data + data_bytes,
+                     d_offsets, offset_base, perm, n, d_out);
     return cudaGetLastError();
 }
 

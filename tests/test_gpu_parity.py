@@ -637,6 +637,51 @@ def test_fixed_hash_graph_replay():
             assert np.array_equal(out.cpu().numpy()[rows], oracle.batch_fixed(alg, sample)), (alg, seed)
 
 
+def test_input_ready_early_start():
+    """HB_FLAG_INPUT_READY: back-to-back launches over rotating, already
+    written inputs start reading before the previous grid completes (early
+    loads, early release of the next grid for sub-wave grids); every pass's
+    digests equal the oracle's, for the compile-time-width kernel, the TMA
+    ring (sub-wave and multi-wave grids, ragged last CTA) and a one-block
+    message.  A fill kernel that rewrites the input right before a flagged
+    launch is ordered by a plain (unflagged) launch in between."""
+    import torch
+
+    from paper_2407_09333_b200 import device
+
+    flag = _native.HB_FLAG_INPUT_READY
+    for alg, n, L in (("sha1", 65536, 64), ("md5", 65536, 1024), ("sm3", 1000, 256), ("md5", 300000, 256),
+                      ("sha1", 4099, 48), ("md5", 70000, 16)):
+        d = {"sha1": 20, "md5": 16, "sm3": 32}[alg]
+        copies = []
+        for k in range(3):
+            b = torch.empty(n * L, dtype=torch.uint8, device="cuda:0")
+            device.fill_random(b, 100 + k)
+            copies.append(b.view(n, L))
+        outs = [torch.empty((n, d), dtype=torch.uint8, device="cuda:0") for _ in copies]
+        for rep in range(2):
+            for b, o in zip(copies, outs):
+                device.hash_fixed(alg, b, out=o, flags=flag)
+        g = device.FixedHashGraph(alg, copies, flags=flag, repeats=2)
+        g.replay()
+        torch.cuda.synchronize()
+        for k, o in enumerate(outs):
+            rows = np.array([0, 1, n // 2, n - 1])
+            sample = np.stack([oracle.fill_random(L, 100 + k, int(r) * L) for r in rows])
+            ref = oracle.batch_fixed(alg, sample)
+            assert np.array_equal(o.cpu().numpy()[rows], ref), (alg, n, L, k)
+        last = len(copies) - 1
+        assert np.array_equal(g.out.cpu().numpy()[rows], ref), (alg, n, L, "graph")
+        full = oracle.batch_fixed(alg, copies[0].cpu().numpy(), threads=8)
+        assert np.array_equal(outs[0].cpu().numpy(), full), (alg, n, L, "full")
+        # rewrite an input, then hash it unflagged: the result follows the new bytes
+        device.fill_random(copies[last].view(-1), 555)
+        device.hash_fixed(alg, copies[last], out=outs[last])
+        torch.cuda.synchronize()
+        sample = np.stack([oracle.fill_random(L, 555, int(r) * L) for r in rows])
+        assert np.array_equal(outs[last].cpu().numpy()[rows], oracle.batch_fixed(alg, sample))
+
+
 def test_out_argument_reuse_and_pinned():
     """Digests written into a caller buffer (pageable or page-locked) equal a fresh result."""
     import ctypes
