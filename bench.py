@@ -63,10 +63,12 @@ ALU_OPS_PER_BLOCK = {"md5": 128, "sha1": 448, "sm3": 1084}
 # looser than the ALU-pipe bound above for SHA-1 and SM3 -- their 448 / 1,084
 # boolean/rotate ops can only issue at 64 lanes/clk/SM -- so it reads lower.
 SURVEY_C_ALG = {"md5": 324, "sha1": 613, "sm3": 1412}
-# Dependent-chain latency of one compression (cycles, one warp per SM,
-# tools/bench_configs.py r1): a batch with too few messages to overlap cannot
-# finish before (blocks per message) x this.
-CHAIN_CYCLES = {"md5": 1509, "sha1": 1116, "sm3": 2514}
+# Dependent-chain latency of one compression (cycles, one warp per SM: 4,736
+# messages of 64 KiB, profiles/r2/ab_chain_r2d.txt; the smaller of the r1 and
+# r2 measurements).  MD5 is the round-variant-3 kernel the dispatch runs below
+# 2^17 messages (variant 1: 1,462-1,509).  A batch with too few messages to
+# overlap cannot finish before (blocks per message) x this.
+CHAIN_CYCLES = {"md5": 1132, "sha1": 1116, "sm3": 2514}
 _BACKEND = os.environ.get("HB_BENCH_BACKEND", "nccl")
 
 
@@ -467,6 +469,7 @@ class PinnedPool:
 GRAPH_STEPS = 10
 L2_DEFEAT_BYTES = 2 * 126 * 10**6  # twice the B200's 126 MB L2
 PROFILE_ONLY = False  # tools/ncu_configs.py: no rotated copies, no graphs (one launch per config)
+INPUT_READY = 0x40  # HB_FLAG_INPUT_READY (include/hetoc_b200.h): inputs resident, not written by the previous kernel
 
 
 # -------------------------------------------------------------- workloads --
@@ -521,8 +524,8 @@ class FixedWorkload:
             for j in range(0, len(self.copies), GRAPH_STEPS):
                 group = self.copies[j:j + GRAPH_STEPS]
                 reps = GRAPH_STEPS // len(group) if len(group) < GRAPH_STEPS else 1
-                self.graphs.append(device.FixedHashGraph(alg, group, self.out, repeats=reps))
-            self.graph1s = [device.FixedHashGraph(alg, c, self.out) for c in self.copies]
+                self.graphs.append(device.FixedHashGraph(alg, group, self.out, flags=INPUT_READY, repeats=reps))
+            self.graph1s = [device.FixedHashGraph(alg, c, self.out, flags=INPUT_READY) for c in self.copies]
 
     def step(self):
         from paper_2407_09333_b200 import device
@@ -532,7 +535,7 @@ class FixedWorkload:
         if self.graph1s:
             self.graph1s[i].replay()
         else:
-            device.hash_fixed(self.alg, self.copies[i], out=self.out)
+            device.hash_fixed(self.alg, self.copies[i], out=self.out, flags=INPUT_READY)
 
     def run_steps(self, k):
         if self.graphs:
@@ -604,6 +607,9 @@ class FixedWorkload:
                 else f"{self.alg} {self.n} x {self.L} B fixed-width per GPU")
         return {"workload": f"{what} ({self.desc})", "alg": self.alg,
                 "msgs_per_gpu": self.n, "msg_len": self.L, "global_batch_msgs": self.total_msgs,
+                "launch_flags": "HB_FLAG_INPUT_READY: the inputs are written before the timed region and never by "
+                                "the preceding kernel, so each launch starts loading them while the previous one "
+                                "drains (programmatic dependent launch)",
                 "parallelism": f"message-range shards over {world} GPU(s), no collective",
                 "l2": ("inputs are %.2f GiB per GPU > 2 x 126 MB L2; no flush needed" % (self.n * self.L / 2**30)
                        if len(self.copies) == 1 else

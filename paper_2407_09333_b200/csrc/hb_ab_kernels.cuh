@@ -146,7 +146,7 @@ __device__ __forceinline__ void realign32(const uint32_t (&c)[24], uint32_t q, u
 #undef HB_RA
 }
 
-template <int ALG>
+template <int ALG, int PF = 0>
 __global__ void __launch_bounds__(128)
 k_varlen32(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
@@ -166,7 +166,7 @@ k_varlen32(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint
     uint32_t c[24];
     uint32_t raw[16];
     const uint64_t nfull = len >> 6;
-    for (uint64_t b = 0; b < nfull; ++b) {
+    auto load_win = [&](uint64_t b) {
         const uint8_t* src = w32 + 64 * b;
         load_chunk32(src, dend, c);
         load_chunk32(src + 32, dend, c + 8);
@@ -176,8 +176,20 @@ k_varlen32(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint
 #pragma unroll
             for (int k = 16; k < 24; ++k) c[k] = 0u;
         }
-        realign32(c, q, sh, raw);
-        compress1<ALG>(st, raw);
+    };
+    if (PF) {  // software pipelining: block b+1's window loads in flight during b's compression
+        if (nfull) load_win(0);
+        for (uint64_t b = 0; b < nfull; ++b) {
+            realign32(c, q, sh, raw);
+            if (b + 1 < nfull) load_win(b + 1);
+            compress1<ALG>(st, raw);
+        }
+    } else {
+        for (uint64_t b = 0; b < nfull; ++b) {
+            load_win(b);
+            realign32(c, q, sh, raw);
+            compress1<ALG>(st, raw);
+        }
     }
     // tail: the r = len % 64 remaining bytes (chunks overlapping [p, p + r) only)
     const uint32_t r = (uint32_t)(len & 63u);
@@ -530,7 +542,7 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
                                     uint64_t offset_base, uint64_t n, uint8_t* d_out, void* d_scratch,
                                     cudaStream_t stream, uint32_t flags) {
     const Tuning& T = tuning();
-    const bool special = (flags & (HB_FLAG_VARLEN_WORDS | HB_FLAG_VARLEN_COOP)) || T.varlen_bulk || T.varlen_prefetch;
+    const bool special = (flags & (HB_FLAG_VARLEN_WORDS | HB_FLAG_VARLEN_COOP)) || T.varlen_bulk;
     const bool wide = !special && T.varlen_ld == 32;
     const uint32_t* perm = nullptr;
     const int qcls = wide ? (int)T.varlen_q : 4;
@@ -539,8 +551,12 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((n + 127) / 128);
     if (wide) {
-        launch_plain(k_varlen32<ALG>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n,
-                     d_out);
+        if (T.varlen_prefetch)
+            launch_plain(k_varlen32<ALG, 1>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base,
+                         perm, n, d_out);
+        else
+            launch_plain(k_varlen32<ALG>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base,
+                         perm, n, d_out);
     } else if (flags & HB_FLAG_VARLEN_WORDS) {
         launch_plain(k_generic<ALG, true>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base,
                      perm, (uint64_t)0, n, d_out);

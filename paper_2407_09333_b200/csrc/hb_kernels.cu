@@ -280,7 +280,8 @@ cudaError_t launch_varlen_sort(int alg, const uint8_t* d_data, const uint64_t* d
         const uint64_t w = T.sort_window;
         const bool q8 = qclasses == 8;
 #define HB_WIN(W)                                                                                            \
-    q8 ? k_sort_window<W, 8><<<(unsigned)((n + W - 1) / W), 1024, 0, stream>>>(d_offsets, n, bias0, p)     \
+    q8 ? (T.sort_qmajor ? k_sort_window<W, 8, true><<<(unsigned)((n + W - 1) / W), 1024, 0, stream>>>(d_offsets, n, bias0, p) \
+                        : k_sort_window<W, 8><<<(unsigned)((n + W - 1) / W), 1024, 0, stream>>>(d_offsets, n, bias0, p)) \
     : T.sort_qmajor ? k_sort_window<W, 4, true><<<(unsigned)((n + W - 1) / W), 1024, 0, stream>>>(d_offsets, n, bias0, p) \
        : k_sort_window<W, 4><<<(unsigned)((n + W - 1) / W), 1024, 0, stream>>>(d_offsets, n, bias0, p)
         if (w >= 16384)
