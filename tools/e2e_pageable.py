@@ -9,13 +9,13 @@ import time
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import oracle  # noqa: E402
+import hostref  # noqa: E402
 from paper_2407_09333_b200.crypto import batch_digest  # noqa: E402
 
 alg = sys.argv[1] if len(sys.argv) > 1 else "md5"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 22
 L = int(sys.argv[3]) if len(sys.argv) > 3 else 1024
-data = oracle.fill_random(n * L, 2).reshape(n, L)  # pageable
+data = hostref.random_bytes(n * L, 2).reshape(n, L)  # pageable
 batch_digest(alg, data)  # warm
 res = {}
 for name in ("pageable_in_fresh_out", "pageable_in_reused_out"):

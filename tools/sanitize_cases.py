@@ -3,7 +3,7 @@
 
     compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_cases.py
 
-Each case is checked against the CPU oracle as well, so a clean sanitizer run
+Each case is checked against hashlib (tools/hostref.py) as well, so a clean sanitizer run
 also confirms the results.  Inputs are sized so every batch sits exactly at
 the end of its device allocation (no slack after the last message).
 """
@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import oracle  # noqa: E402
+import hostref  # noqa: E402  (hashlib checker)
 from paper_2407_09333_b200 import _native, device  # noqa: E402
 
 ALGS = ("sha1", "md5", "sm3")
@@ -29,20 +29,20 @@ def with_env(env):
 
 
 def fixed(alg, n, L, flags=0):
-    host = oracle.fill_random(n * L, n + L).reshape(n, L)
+    host = hostref.random_bytes(n * L, n + L).reshape(n, L)
     d = torch.from_numpy(host.copy()).cuda()
     got = device.hash_fixed(alg, d, flags=flags).cpu().numpy()
-    assert np.array_equal(got, oracle.batch_fixed(alg, host, 8)), (alg, n, L, flags)
+    assert np.array_equal(got, hostref.digests(alg, host)), (alg, n, L, flags)
 
 
 def varlen(alg, n, maxlen, flags=0):
     lens = np.random.default_rng(n).integers(0, maxlen + 1, n).astype(np.int64)
     off = np.zeros(n + 1, np.int64)
     off[1:] = np.cumsum(lens)
-    host = oracle.fill_random(int(off[-1]), 7)
+    host = hostref.random_bytes(int(off[-1]), 7)
     d = torch.from_numpy(host.copy()).cuda()
     got = device.hash_varlen(alg, d, torch.from_numpy(off).cuda(), flags=flags, offset_base=0).cpu().numpy()
-    assert np.array_equal(got, oracle.batch_varlen(alg, host, off.astype(np.uint64), 8)), (alg, n, maxlen, flags)
+    assert np.array_equal(got, hostref.digests_varlen(alg, host, off)), (alg, n, maxlen, flags)
 
 
 def main():
@@ -73,19 +73,19 @@ def main():
     for alg in ALGS:
         for w in (9, 12):
             out = device.hash_decimal(alg, 5, 4000, w).cpu().numpy()
-            assert np.array_equal(out, oracle.batch_fixed(alg, oracle.gen_decimal(5, 4000, w), 8))
+            assert np.array_equal(out, hostref.digests(alg, hostref.decimal_messages(5, 4000, w)))
             cases += 1
     # programmatic dependent launch: a chain of launches on one stream, each
     # consuming the previous one's digests, no host synchronisation between
     for L in (64, 1024):
         per = L // 32
         rows = per ** 3 if L > 64 else 1 << 10
-        data = oracle.fill_random(rows * L, 47).reshape(rows, L)
+        data = hostref.random_bytes(rows * L, 47).reshape(rows, L)
         cur, ref = torch.from_numpy(data).cuda(), data
         while rows >= per:
             rows //= per
             cur = device.hash_fixed("sm3", cur).reshape(rows, L)
-            ref = oracle.batch_fixed("sm3", ref, 8).reshape(rows, L)
+            ref = hostref.digests("sm3", ref).reshape(rows, L)
             cases += 1
         assert np.array_equal(cur.cpu().numpy(), ref)
     torch.cuda.synchronize()
