@@ -586,6 +586,11 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
         case 27: launch_plain(k_varlen16<ALG, 1, 2>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 21: launch_plain(k_varlen16<ALG, 1, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 25: launch_plain(k_varlen16<ALG, 5, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        // register caps: 29 / 30 = pipelined kernel at >= 8 / 9 CTAs per SM, 31 = plain kernel at 10
+        case 29: launch_plain(k_varlen16<ALG, 1, 0, 8>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 30: launch_plain(k_varlen16<ALG, 1, 0, 9>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 31: launch_plain(k_varlen16<ALG, 0, 0, 10>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 32: launch_plain(k_varlen16<ALG, 3, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 28: launch_plain(k_varlen16<ALG, 5, 1>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         default: launch_plain(k_varlen16<ALG, 0, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         }

@@ -709,8 +709,8 @@ k_varlen16u(const uint8_t* __restrict__ data, const uint8_t* data_end, const uin
         varlen16u_message<ALG, V, false>(w16, a, len, dend, out + i * H::kDigestBytes);
 }
 
-template <int ALG, int PF = 0, int LD = 0>
-__global__ void __launch_bounds__(128)
+template <int ALG, int PF = 0, int LD = 0, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB)
 k_varlen16(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
     using H = HashAlg<ALG>;
