@@ -1159,6 +1159,13 @@ def run_ours(args):
     sampler.stop()
     pool.close()
     if rank == 0:
+        if roof and clk and "sw_power_cap" in (clk.get("reasons") or []) and clk.get("sm_mhz"):
+            # The board reached its power limit (1,000 W on this pool, tools/ab_power.py): the
+            # SM clock fell below its maximum, so an issue-bound kernel runs slower than the
+            # same kernel at full clock.  Reported, not corrected.
+            roof["power_note"] = (f"sw_power_cap during the timed region: SM clock median {clk['sm_mhz']:.0f} MHz "
+                                  f"of {clk.get('sm_max_mhz') or 1965:.0f}; the ALU-pipe and chain bounds above "
+                                  "assume the maximum clock")
         line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
                 "higher_is_better": True, "scaling": head["scaling"], "vs_baseline": None, "dtype": "u32",
@@ -1209,8 +1216,22 @@ bounds = np.linspace(0, rowsp, cores + 1, dtype=np.int64)
 with Pool(cores) as p:
     p.map(part, [(0, 1)] * cores)
     t0 = time.perf_counter(); p.map(part, list(zip(bounds[:-1], bounds[1:]))); pool = time.perf_counter() - t0
-print(json.dumps({"one_core": {"value": rows1 * L / one / 1e9, "rows": rows1, "seconds": one},
-                  "pool": {"value": rowsp * L / pool / 1e9, "rows": rowsp, "seconds": pool, "cores": cores}}))
+res = {"one_core": {"value": rows1 * L / one / 1e9, "rows": rows1, "seconds": one},
+       "pool": {"value": rowsp * L / pool / 1e9, "rows": rowsp, "seconds": pool, "cores": cores}}
+# hash_batch as-is over the same rows with threads = cores (thread pool over
+# the np.linspace split, list[Digest] built), SURVEY §8(d) CPU timing 1
+from hetoc.crypto import MessageBatch, hash_batch
+mb = MessageBatch(rowsp, L, data[:rowsp].tobytes())
+t0 = time.perf_counter(); hash_batch(alg, mb, threads=cores); hb = time.perf_counter() - t0
+res["hash_batch_threads"] = {"value": rowsp * L / hb / 1e9, "rows": rowsp, "seconds": hb, "threads": cores}
+# the SHA-1 accel path (hashlib / SHA-NI, batch.py:266-271) on SHA-1 rows of the same shape, timing 3
+t0 = time.perf_counter(); batch_digest("sha1", data[:4096], accel=True); per = (time.perf_counter() - t0) / 4096
+rowsa = int(max(4096, min(n, budget / 6 / per)))
+t0 = time.perf_counter(); batch_digest("sha1", data[:rowsa], accel=True); a1 = time.perf_counter() - t0
+mba = MessageBatch(rowsa, L, data[:rowsa].tobytes())
+t0 = time.perf_counter(); hash_batch("sha1", mba, threads=cores, accel=True); at = time.perf_counter() - t0
+res["sha1_accel"] = {"one_core": rowsa * L / a1 / 1e9, "hash_batch_threads": rowsa * L / at / 1e9, "rows": rowsa}
+print(json.dumps(res))
 '''
     try:
         n, L = data
@@ -1219,6 +1240,12 @@ print(json.dumps({"one_core": {"value": rows1 * L / one / 1e9, "rows": rows1, "s
         r = json.loads(out.stdout.strip().splitlines()[-1])
         return {"one_core_gbs": round(r["one_core"]["value"], 4), "pool_gbs": round(r["pool"]["value"], 4),
                 "pool_cores": r["pool"]["cores"],
+                "hash_batch_threads_gbs": round(r["hash_batch_threads"]["value"], 4),
+                "sha1_accel_gbs": {"one_core": round(r["sha1_accel"]["one_core"], 4),
+                                   "hash_batch_threads": round(r["sha1_accel"]["hash_batch_threads"], 4),
+                                   "rows": r["sha1_accel"]["rows"],
+                                   "api": "hetoc.crypto.batch_digest / hash_batch(..., accel=True), SHA-1 rows "
+                                          "of the same shape (hashlib, SHA-NI on this host)"},
                 "sample": f"{r['one_core']['rows']} rows on 1 core, {r['pool']['rows']} rows over a process pool "
                           f"(np.linspace split, batch.py:305) of {L} B random messages",
                 "api": "hetoc.crypto.batch_digest (baseline/_ref, unmodified reference)"}
