@@ -591,6 +591,7 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
         case 30: launch_plain(k_varlen16<ALG, 1, 0, 9>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 31: launch_plain(k_varlen16<ALG, 0, 0, 10>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 32: launch_plain(k_varlen16<ALG, 3, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 33: launch_plain(k_varlen16x2<ALG>, (unsigned)(((n + 1) / 2 + blk - 1) / blk), blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 28: launch_plain(k_varlen16<ALG, 5, 1>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         default: launch_plain(k_varlen16<ALG, 0, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         }

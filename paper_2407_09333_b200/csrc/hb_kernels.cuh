@@ -631,6 +631,85 @@ __device__ __forceinline__ void varlen16_message(const uint4* w16, uintptr_t a, 
     store_digest<ALG>(dout, st);
 }
 
+// The rest of one message from full block b0 on: full blocks b0 .. len/64-1,
+// then the tail and padding (md_finish), digest stored.  `st` holds the state
+// after blocks 0 .. b0-1.
+template <int ALG, bool EDGE>
+__device__ __forceinline__ void varlen16_rest(const uint4* w16, uintptr_t a, uint64_t len, uintptr_t dend,
+                                              uint64_t b0, uint32_t* st, uint8_t* dout) {
+    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
+    const bool misaligned = (a & 15u) != 0;
+    uint32_t c[20];
+    uint32_t raw[16];
+    const uint64_t nfull = len >> 6;
+    for (uint64_t b = b0; b < nfull; ++b) {
+        load_full_window(w16 + 4 * b, misaligned, c, EDGE, dend);
+        realign16(c, q, sh, raw);
+        compress1<ALG>(st, raw);
+    }
+    const uint32_t r = (uint32_t)(len & 63u);
+    const uintptr_t tail_end = a + len;
+    const uint4* src = w16 + 4 * nfull;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (reinterpret_cast<uintptr_t>(src + k) < tail_end) v = ld16_edge(src + k, EDGE, dend);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+    realign16(c, q, sh, raw);
+    mask_tail(raw, r);
+    md_finish<ALG>(st, raw, r, len);
+    store_digest<ALG>(dout, st);
+}
+
+// Two messages per thread: sorted neighbours 2t and 2t+1 (same alignment
+// class and block count, or adjacent counts, after the q-major windowed
+// sort) compress together while both have full blocks left -- two
+// independent round chains interleaved in one instruction stream, for the
+// dependency stalls that dominate the one-message kernel (ncu: 43 % `wait`).
+// Leftover full blocks and the 1-2 finishing blocks run per message.
+template <int ALG>
+__global__ void __launch_bounds__(128)
+k_varlen16x2(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+             uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t k0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2u;
+    if (k0 >= n) return;
+    const bool two = k0 + 1 < n;
+    const uint64_t i0 = perm ? (uint64_t)perm[k0] : k0;
+    const uint64_t i1 = two ? (perm ? (uint64_t)perm[k0 + 1] : k0 + 1) : i0;
+    const uint64_t len0 = offsets[i0 + 1] - offsets[i0], len1 = offsets[i1 + 1] - offsets[i1];
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(data + (offsets[i0] - offset_base));
+    const uintptr_t a1 = reinterpret_cast<uintptr_t>(data + (offsets[i1] - offset_base));
+    const uint4* w0 = reinterpret_cast<const uint4*>(a0 & ~uintptr_t(15));
+    const uint4* w1 = reinterpret_cast<const uint4*>(a1 & ~uintptr_t(15));
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    if (((a0 + len0 + 15u) & ~uintptr_t(15)) > dend || ((a1 + len1 + 15u) & ~uintptr_t(15)) > dend) {
+        // a message whose last granule straddles the end of the data: bounded loads, one at a time
+        varlen16_message<ALG, 0, true>(w0, a0, len0, dend, out + i0 * H::kDigestBytes);
+        if (two) varlen16_message<ALG, 0, true>(w1, a1, len1, dend, out + i1 * H::kDigestBytes);
+        return;
+    }
+    const uint32_t q0 = (uint32_t)(a0 >> 2) & 3u, sh0 = (uint32_t)(a0 & 3u) * 8u;
+    const uint32_t q1 = (uint32_t)(a1 >> 2) & 3u, sh1 = (uint32_t)(a1 & 3u) * 8u;
+    const bool mis0 = (a0 & 15u) != 0, mis1 = (a1 & 15u) != 0;
+    uint32_t st[2][H::kStateWords];
+    H::init(st[0]);
+    H::init(st[1]);
+    const uint64_t nf0 = len0 >> 6, nf1 = len1 >> 6;
+    const uint64_t nmin = nf0 < nf1 ? nf0 : nf1;
+    uint32_t c0[20], c1[20], raw[2][16];
+    for (uint64_t b = 0; b < nmin; ++b) {
+        load_full_window(w0 + 4 * b, mis0, c0);
+        load_full_window(w1 + 4 * b, mis1, c1);
+        realign16(c0, q0, sh0, raw[0]);
+        realign16(c1, q1, sh1, raw[1]);
+        H::template compress_n<2>(st, raw);
+    }
+    varlen16_rest<ALG, false>(w0, a0, len0, dend, nmin, st[0], out + i0 * H::kDigestBytes);
+    if (two) varlen16_rest<ALG, false>(w1, a1, len1, dend, nmin, st[1], out + i1 * H::kDigestBytes);
+}
+
 // -------------------------------------------------------------------------
 // Variable-length kernel with a warp-uniform block loop.  After the length
 // sort a warp's 32 messages share their block count nb = (len+8)/64 + 1,
