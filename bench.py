@@ -411,6 +411,22 @@ def load_ncu(name: str):
         return json.load(f).get(name)
 
 
+def library_info():
+    """The engine library this run loaded: path, size, A/B build flag and the
+    number of kernels in its sm_100a cubins (cuobjdump, when present)."""
+    from paper_2407_09333_b200 import _native
+
+    path = _native.LIB_PATH
+    info = {"so": os.path.relpath(path, ROOT), "bytes": os.path.getsize(path), "ab_build": _native.built_with_ab()}
+    try:
+        sass = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True, timeout=60).stdout
+        info["kernels"] = sass.count("Function :")
+        info["arch"] = sorted({l.split("=")[-1].strip() for l in sass.splitlines() if "arch = " in l})
+    except Exception:
+        info["kernels"] = None
+    return info
+
+
 def cpu_info():
     """lscpu model / sockets x cores / threads and the SHA-NI flag."""
     info = {"os_cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0))}
@@ -1176,7 +1192,7 @@ def run_ours(args):
                 "mhash_per_s": round(head["total_msgs"] / (ms * 1e-3) / 1e6, 2), "clocks": clk,
                 "e2e": e2e, "e2e_pageable": e2e_pageable, "latency": latency,
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "parity": parity,
-                "ranks": ranks, "configs": configs}
+                "ranks": ranks, "library": library_info(), "configs": configs}
         print(json.dumps(line), flush=True)
     if gather is not None:
         gather.close()
