@@ -60,6 +60,17 @@ def main():
     for alg in ALGS:
         fixed(alg, 2000, 1024, _native.HB_FLAG_NO_TMA)
         cases += 1
+    # HB_FLAG_INPUT_READY: loads before griddepcontrol.wait, early release of
+    # sub-wave grids; back-to-back flagged launches over independent inputs
+    for alg in ALGS:
+        for n, L in ((3000, 1024), (300, 64), (4099, 48), (1000, 256)):
+            fixed(alg, n, L, _native.HB_FLAG_INPUT_READY)
+            cases += 1
+        ins = [torch.from_numpy(hostref.random_bytes(700 * 320, 90 + k).reshape(700, 320)).cuda() for k in range(4)]
+        outs = [device.hash_fixed(alg, x, flags=_native.HB_FLAG_INPUT_READY) for x in ins]
+        for x, o in zip(ins, outs):
+            assert np.array_equal(o.cpu().numpy(), hostref.digests(alg, x.cpu().numpy()))
+            cases += 1
     varlen_arms = [({}, 0), ({"HB_VARLEN_SORT": "global"}, 0), ({"HB_VARLEN_SORT": "window"}, 0),
                    ({}, _native.HB_FLAG_VARLEN_COOP), ({}, _native.HB_FLAG_VARLEN_WORDS),
                    ({"HB_VARLEN_LD": "32"}, 0), ({"HB_VARLEN_BULK": "3"}, 0), ({"HB_VARLEN_PREFETCH": "1"}, 0)]
