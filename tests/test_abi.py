@@ -52,6 +52,15 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
+def test_header_flags_match_python_constants():
+    """Every HB_FLAG_* the header defines has the same value in _native."""
+    flags = dict(re.findall(r"#define\s+(HB_FLAG_[A-Z0-9_]+)\s+(0x[0-9a-fA-F]+)u?", open(HEADER).read()))
+    assert "HB_FLAG_INPUT_READY" in flags and len(flags) >= 7
+    for name, val in flags.items():
+        assert getattr(_native, name) == int(val, 16), name
+    assert len(set(flags.values())) == len(flags)  # distinct bits
+
+
 def test_abi_basics():
     lib = _native.lib()
     assert lib.hb_abi_version() == 2
