@@ -19,13 +19,15 @@ from paper_2407_09333_b200 import _native, device  # noqa: E402
 
 ALGS = ("sha1", "md5", "sm3")
 ENV_KEYS = ("HB_TMA_CFG", "HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_VARLEN_SORT", "HB_VARLEN_LD",
-            "HB_VARLEN_BULK", "HB_VARLEN_PREFETCH", "HB_VC_STAGES")
+            "HB_VARLEN_BULK", "HB_VARLEN_PREFETCH", "HB_VC_STAGES", "HB_CHAIN_N", "HB_SORT_QMAJOR", "HB_VARLEN_PF",
+            "HB_VARLEN_KERNEL")
 
 
 def with_env(env):
     for k in ENV_KEYS:
         os.environ.pop(k, None)
     os.environ.update(env)
+    _native.reload_tuning()  # the engine parses its knobs once; re-read them
 
 
 def fixed(alg, n, L, flags=0):
@@ -48,9 +50,10 @@ def varlen(alg, n, maxlen, flags=0):
 def main():
     cases = 0
     fixed_shapes = [({}, [(3000, 1024), (700, 1040), (300, 64), (300, 16), (300, 96), (257, 7), (129, 0)]),
-                    ({"HB_TMA_CFG": "ws3x2"}, [(3000, 1024), (513, 80)]),
-                    ({"HB_TMA_CFG": "1x3"}, [(3000, 1024)]),
+                    ({"HB_CHAIN_N": "0"}, [(3000, 1024)]),
                     ({"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"}, [(5000, 64), (5000, 144)])]
+    if _native.built_with_ab():
+        fixed_shapes += [({"HB_TMA_CFG": "ws3x2"}, [(3000, 1024), (513, 80)]), ({"HB_TMA_CFG": "1x3"}, [(3000, 1024)])]
     for env, shapes in fixed_shapes:
         with_env(env)
         for alg in ALGS:
@@ -72,8 +75,11 @@ def main():
             assert np.array_equal(o.cpu().numpy(), hostref.digests(alg, x.cpu().numpy()))
             cases += 1
     varlen_arms = [({}, 0), ({"HB_VARLEN_SORT": "global"}, 0), ({"HB_VARLEN_SORT": "window"}, 0),
-                   ({}, _native.HB_FLAG_VARLEN_COOP), ({}, _native.HB_FLAG_VARLEN_WORDS),
-                   ({"HB_VARLEN_LD": "32"}, 0), ({"HB_VARLEN_BULK": "3"}, 0), ({"HB_VARLEN_PREFETCH": "1"}, 0)]
+                   ({"HB_SORT_QMAJOR": "0"}, 0), ({"HB_VARLEN_PF": "0"}, 0)]
+    if _native.built_with_ab():  # the A/B arms exist only in libhetoc_b200_ab.so
+        varlen_arms += [({}, _native.HB_FLAG_VARLEN_COOP), ({}, _native.HB_FLAG_VARLEN_WORDS),
+                        ({"HB_VARLEN_LD": "32"}, 0), ({"HB_VARLEN_BULK": "3"}, 0), ({"HB_VARLEN_PREFETCH": "1"}, 0),
+                        ({"HB_VARLEN_KERNEL": "33"}, 0)]
     for env, fl in varlen_arms:
         with_env(env)
         for alg in ALGS:
