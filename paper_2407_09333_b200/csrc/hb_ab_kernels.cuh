@@ -465,6 +465,10 @@ static cudaError_t launch_tma_ab(const uint8_t* src, uint32_t n, uint32_t L, uin
     case kCfgWs2: return v == 0 ? launch_fixed_tma_ws<ALG, 0, 1, 2>(src, n, L, dst, s)
                                 : launch_fixed_tma_ws<ALG, 1, 1, 2>(src, n, L, dst, s);
     case kCfgWs3:
+        if constexpr (ALG == kMd5) {
+            if (v == 4) return launch_fixed_tma_ws<ALG, 4, 1, 3>(src, n, L, dst, s);
+            if (v == 5) return launch_fixed_tma_ws<ALG, 5, 1, 3>(src, n, L, dst, s);
+        }
         switch (v) {
         case 0: return launch_fixed_tma_ws<ALG, 0, 1, 3>(src, n, L, dst, s);
         case 2: return launch_fixed_tma_ws<ALG, 2, 1, 3>(src, n, L, dst, s);

@@ -141,6 +141,18 @@ __host__ __device__ constexpr uint32_t md5_k(int i) {
         0x6fa87e4f, 0xfe2ce6e0, 0xa3014314, 0x4e0811a1, 0xf7537e82, 0xbd3af235, 0x2ad7d2bb, 0xeb86d391};
     return K[i];
 }
+// The same K table in constant memory: an opaque operand keeps ptxas from
+// splitting a + M + K into VIADD + IMAD.IADD, so variants 4 / 5 get one
+// IADD3 R, R, c[..], R per round for the off-chain sum.
+__constant__ uint32_t c_md5k[64] = {
+    0xd76aa478, 0xe8c7b756, 0x242070db, 0xc1bdceee, 0xf57c0faf, 0x4787c62a, 0xa8304613, 0xfd469501,
+    0x698098d8, 0x8b44f7af, 0xffff5bb1, 0x895cd7be, 0x6b901122, 0xfd987193, 0xa679438e, 0x49b40821,
+    0xf61e2562, 0xc040b340, 0x265e5a51, 0xe9b6c7aa, 0xd62f105d, 0x02441453, 0xd8a1e681, 0xe7d3fbc8,
+    0x21e1cde6, 0xc33707d6, 0xf4d50d87, 0x455a14ed, 0xa9e3e905, 0xfcefa3f8, 0x676f02d9, 0x8d2a4c8a,
+    0xfffa3942, 0x8771f681, 0x6d9d6122, 0xfde5380c, 0xa4beea44, 0x4bdecfa9, 0xf6bb4b60, 0xbebfbc70,
+    0x289b7ec6, 0xeaa127fa, 0xd4ef3085, 0x04881d05, 0xd9d4d039, 0xe6db99e5, 0x1fa27cf8, 0xc4ac5665,
+    0xf4292244, 0x432aff97, 0xab9423a7, 0xfc93a039, 0x655b59c3, 0x8f0ccc92, 0xffeff47d, 0x85845dd1,
+    0x6fa87e4f, 0xfe2ce6e0, 0xa3014314, 0x4e0811a1, 0xf7537e82, 0xbd3af235, 0x2ad7d2bb, 0xeb86d391};
 __host__ __device__ constexpr int md5_s(int i) {
     constexpr int S[4][4] = {{7, 12, 17, 22}, {5, 9, 14, 20}, {4, 11, 16, 23}, {6, 10, 15, 21}};
     return S[i / 16][i % 4];
@@ -191,6 +203,10 @@ template <int V> struct HashAlg<kMd5, V> {
                 // keeps K attached to M (shorter dependency chain, 2 IMADs).
                 uint32_t u;
                 if (kV == kVarBal3) u = use_fma(i) ? add_g(f, add_f(a[q], mg + md5_k(i))) : add_g(f, a[q] + (mg + md5_k(i)));
+                // 4: variant 3's chain; one round in three sums a + M + K in one IADD3 (ALU)
+                // 5: every round does (fewest instructions: LOP3, IADD3, IMAD, LEA.HI)
+                else if (kV == 4) u = (i % 3) == 2 ? add_g(f, a[q] + mg + c_md5k[i]) : add_g(f, add_f(a[q], mg + md5_k(i)));
+                else if (kV == 5) u = add_g(f, a[q] + mg + c_md5k[i]);
                 else if (use_fma(i)) u = add_f(f, add_f(a[q], mg) + md5_k(i));
                 else u = a[q] + f + mg + md5_k(i);
                 const uint32_t nb = b[q] + rotl(u, md5_s(i));         // one LEA.HI

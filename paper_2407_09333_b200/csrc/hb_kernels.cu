@@ -66,7 +66,7 @@ static Tuning parse_tuning() {
         for (int k = 0; k < (int)(sizeof kCfgNames / sizeof *kCfgNames); ++k)
             if (!strcmp(v, kCfgNames[k])) t.tma_cfg = k;
     if (const char* v = getenv("HB_VARIANT"))
-        if (*v >= '0' && *v <= '3' && v[1] == '\0') t.variant = *v - '0';
+        if (*v >= '0' && *v <= '5' && v[1] == '\0') t.variant = *v - '0';
     if (t.tma_cfg >= 0) t.direct_max_len = env_u64("HB_DIRECT_MAX_L", 0);  // a forced tile applies to every width
     t.tma_l2 = (uint32_t)env_u64("HB_TMA_L2", 256);
     t.tma_evict_first = (uint32_t)env_u64("HB_TMA_EVICT_FIRST", 0);
