@@ -433,7 +433,11 @@ k_varlen_coop(const uint8_t* __restrict__ data, const uint64_t* __restrict__ off
 // profiles/variant_sweep_r1*.txt, selected through the Tuning A/B fields.
 // =========================================================================
 enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4, kCfg1x2 = 5, kCfgWs2x2 = 6,
-                kCfgWs3x2 = 7, kCfgWs3u = 8, kCfgWs3x2u = 9, kCfgWs3n = 10 };
+                kCfgWs3x2 = 7, kCfgWs3u = 8, kCfgWs3x2u = 9, kCfgWs3n = 10,
+                // single-warp CTAs (per-warp ring, W = 1) with NB messages per thread: a
+                // mid-size batch (2^16 messages, 3.46 warps per scheduler at NB = 1) as
+                // <= 1 warp per scheduler carrying NB independent round chains
+                kCfgW1x1 = 11, kCfgW1x2 = 12, kCfgW1x4 = 13, kCfgW1x4s2 = 14 };
 
 template <int ALG, int V, int NB, int STAGES, int W = kTmaWarps>
 static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
@@ -475,6 +479,16 @@ static cudaError_t launch_tma_ab(const uint8_t* src, uint32_t n, uint32_t L, uin
         case 3: return launch_fixed_tma_ws<ALG, 3, 1, 3>(src, n, L, dst, s);
         default: return launch_fixed_tma_ws<ALG, 1, 1, 3>(src, n, L, dst, s);
         }
+    case kCfgW1x1: return v == 3 ? launch_fixed_tma_alg<ALG, 3, 1, 3, 1>(src, n, L, dst, s)
+                                 : launch_fixed_tma_alg<ALG, 1, 1, 3, 1>(src, n, L, dst, s);
+    case kCfgW1x2: return v == 3 ? launch_fixed_tma_alg<ALG, 3, 2, 3, 1>(src, n, L, dst, s)
+                                 : launch_fixed_tma_alg<ALG, 1, 2, 3, 1>(src, n, L, dst, s);
+    case kCfgW1x4:
+        if constexpr (ALG == kMd5)
+            if (v == 5) return launch_fixed_tma_alg<ALG, 5, 4, 3, 1>(src, n, L, dst, s);
+        return v == 3 ? launch_fixed_tma_alg<ALG, 3, 4, 3, 1>(src, n, L, dst, s)
+                      : launch_fixed_tma_alg<ALG, 1, 4, 3, 1>(src, n, L, dst, s);
+    case kCfgW1x4s2: return launch_fixed_tma_alg<ALG, 1, 4, 2, 1>(src, n, L, dst, s);
     case kCfgWs3u: return launch_fixed_tma_ws<ALG, kVarBal, 1, 3, true>(src, n, L, dst, s);
     case kCfgWs3n: return launch_fixed_tma_ws<ALG, kVarBal, 1, 3, false, false>(src, n, L, dst, s);
     case kCfgWs3x2u: return launch_fixed_tma_ws<ALG, kVarBal, 2, 3, true>(src, n, L, dst, s);

@@ -111,7 +111,7 @@ template <int NB, int STAGES, int W = kTmaWarps> struct TmaCfg {
 };
 template <int ALG, int NB, int STAGES, int W = kTmaWarps> struct TmaOcc {  // CTAs per SM the budget targets
     static constexpr int kMinCtas =
-        W == 1 ? 16
+        W == 1 ? (NB >= 4 ? 6 : NB == 2 ? 12 : 16)
         : NB == 1 ? (STAGES == 2 ? (ALG == kMd5 ? 12 : ALG == kSha1 ? 9 : 8) : (ALG == kSm3 ? 6 : 8))
                   : (STAGES == 2 && ALG != kSm3 ? 6 : 4);
 };
