@@ -472,6 +472,8 @@ static cudaError_t launch_tma_ab(const uint8_t* src, uint32_t n, uint32_t L, uin
         if constexpr (ALG == kMd5) {
             if (v == 4) return launch_fixed_tma_ws<ALG, 4, 1, 3>(src, n, L, dst, s);
             if (v == 5) return launch_fixed_tma_ws<ALG, 5, 1, 3>(src, n, L, dst, s);
+            if (v == 6) return launch_fixed_tma_ws<ALG, 6, 1, 3>(src, n, L, dst, s);
+            if (v == 7) return launch_fixed_tma_ws<ALG, 7, 1, 3>(src, n, L, dst, s);
         }
         switch (v) {
         case 0: return launch_fixed_tma_ws<ALG, 0, 1, 3>(src, n, L, dst, s);
@@ -481,7 +483,10 @@ static cudaError_t launch_tma_ab(const uint8_t* src, uint32_t n, uint32_t L, uin
         }
     case kCfgW1x1: return v == 3 ? launch_fixed_tma_alg<ALG, 3, 1, 3, 1>(src, n, L, dst, s)
                                  : launch_fixed_tma_alg<ALG, 1, 1, 3, 1>(src, n, L, dst, s);
-    case kCfgW1x2: return v == 3 ? launch_fixed_tma_alg<ALG, 3, 2, 3, 1>(src, n, L, dst, s)
+    case kCfgW1x2:
+        if constexpr (ALG == kMd5)
+            if (v == 4) return launch_fixed_tma_alg<ALG, 4, 2, 3, 1>(src, n, L, dst, s);
+        return v == 3 ? launch_fixed_tma_alg<ALG, 3, 2, 3, 1>(src, n, L, dst, s)
                                  : launch_fixed_tma_alg<ALG, 1, 2, 3, 1>(src, n, L, dst, s);
     case kCfgW1x4:
         if constexpr (ALG == kMd5)
@@ -530,6 +535,8 @@ static void launch_small_one_ab(const uint8_t* d_msgs, uint64_t n, uint8_t* d_ou
         launch_pdl(k_fixed_small<ALG, L, kVarPlain>, (unsigned)((n + b - 1) / b), b, s, d_msgs, n, d_out, 0u);
     else if (T.const_variant == 3)
         launch_pdl(k_fixed_small<ALG, L, kVarBal3>, (unsigned)((n + b - 1) / b), b, s, d_msgs, n, d_out, 0u);
+    else if (T.const_variant == 4)
+        launch_pdl(k_fixed_small<ALG, L, ALG == kMd5 ? 4 : kVarBal3>, (unsigned)((n + b - 1) / b), b, s, d_msgs, n, d_out, 0u);
     else if (pair)
         launch_pdl(k_fixed_small<ALG, L, kVarBal, 2>, (unsigned)(((n + 1) / 2 + b - 1) / b), b, s, d_msgs, n, d_out, 0u);
     else
@@ -611,6 +618,14 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
         case 32: launch_plain(k_varlen16<ALG, 3, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 33: launch_plain(k_varlen16x2<ALG>, (unsigned)(((n + 1) / 2 + blk - 1) / blk), blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 28: launch_plain(k_varlen16<ALG, 5, 1>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        // lean block loop: 40 = one loop (runtime realignment switch), 41 = one loop per alignment class
+        case 40: launch_plain(k_varlen16l<ALG, false>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 41: launch_plain(k_varlen16l<ALG, true>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        // ... with MD5 round variant 4 / 6 / 7 (one round in three / two / four sums a + M + K in one IADD3)
+        case 42: launch_plain(k_varlen16l<ALG, false, ALG == kMd5 ? 4 : -1>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 43: launch_plain(k_varlen16l<ALG, true, ALG == kMd5 ? 4 : -1>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 44: launch_plain(k_varlen16l<ALG, true, ALG == kMd5 ? 6 : -1>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 45: launch_plain(k_varlen16l<ALG, true, ALG == kMd5 ? 7 : -1>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         default: launch_plain(k_varlen16<ALG, 0, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         }
     } else if (T.varlen_kernel >= 10) {  // prefetch-instruction arms of the per-thread kernel (PF = kernel - 10)
@@ -650,6 +665,8 @@ static void dec_launch_ab(uint64_t start, uint64_t count, uint8_t* d_out, cudaSt
             const unsigned g = (unsigned)((threads + 127) / 128);
             if (T.const_variant == 3)
                 launch_plain(k_decimal_run<ALG, W, kVarBal3>, g, 128, s, start, count, d_out);
+            else if (T.const_variant == 4 && ALG == kMd5)
+                launch_plain(k_decimal_run<ALG, W, ALG == kMd5 ? 4 : kVarBal, true>, g, 128, s, start, count, d_out);
             else if (T.dec_pair >= 0 ? T.dec_pair : ALG == kMd5)
                 launch_plain(k_decimal_run<ALG, W, kVarBal, true>, g, 128, s, start, count, d_out);
             else

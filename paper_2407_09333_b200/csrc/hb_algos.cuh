@@ -207,6 +207,9 @@ template <int V> struct HashAlg<kMd5, V> {
                 // 5: every round does (fewest instructions: LOP3, IADD3, IMAD, LEA.HI)
                 else if (kV == 4) u = (i % 3) == 2 ? add_g(f, a[q] + mg + c_md5k[i]) : add_g(f, add_f(a[q], mg + md5_k(i)));
                 else if (kV == 5) u = add_g(f, a[q] + mg + c_md5k[i]);
+                // 6 / 7: as 4 with one round in two / in four through the IADD3
+                else if (kV == 6) u = (i % 2) == 1 ? add_g(f, a[q] + mg + c_md5k[i]) : add_g(f, add_f(a[q], mg + md5_k(i)));
+                else if (kV == 7) u = (i % 4) == 3 ? add_g(f, a[q] + mg + c_md5k[i]) : add_g(f, add_f(a[q], mg + md5_k(i)));
                 else if (use_fma(i)) u = add_f(f, add_f(a[q], mg) + md5_k(i));
                 else u = a[q] + f + mg + md5_k(i);
                 const uint32_t nb = b[q] + rotl(u, md5_s(i));         // one LEA.HI

@@ -66,7 +66,7 @@ static Tuning parse_tuning() {
         for (int k = 0; k < (int)(sizeof kCfgNames / sizeof *kCfgNames); ++k)
             if (!strcmp(v, kCfgNames[k])) t.tma_cfg = k;
     if (const char* v = getenv("HB_VARIANT"))
-        if (*v >= '0' && *v <= '5' && v[1] == '\0') t.variant = *v - '0';
+        if (*v >= '0' && *v <= '9' && v[1] == '\0') t.variant = *v - '0';
     if (t.tma_cfg >= 0) t.direct_max_len = env_u64("HB_DIRECT_MAX_L", 0);  // a forced tile applies to every width
     t.tma_l2 = (uint32_t)env_u64("HB_TMA_L2", 256);
     t.tma_evict_first = (uint32_t)env_u64("HB_TMA_EVICT_FIRST", 0);
@@ -75,7 +75,8 @@ static Tuning parse_tuning() {
     t.small_cta = (uint32_t)env_u64("HB_SMALL_CTA", 128);
     t.small_pair_all = env_u64("HB_SMALL_PAIR_ALL", 0) != 0;
     t.input_ready = env_u64("HB_INPUT_READY", 0) != 0;
-    t.small_kernel_ab = t.const_variant == 0 || t.const_variant == 3 || t.small_cta != 128 || t.small_pair_all;
+    t.small_kernel_ab = t.const_variant == 0 || t.const_variant == 3 || t.const_variant == 4 || t.small_cta != 128 ||
+                        t.small_pair_all;
     t.dec_pair = env_set("HB_DEC_PAIR") ? (int)env_u64("HB_DEC_PAIR", 0) : -1;
     t.fma_digits = env_u64("HB_FMA_DIGITS", 1) != 0;
     t.dec_ab = t.dec_pair >= 0 || !t.fma_digits || t.const_variant >= 0;

@@ -807,6 +807,106 @@ k_varlen16(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint
         varlen16_message<ALG, PF, false, LD>(w16, a, len, dend, out + i * H::kDigestBytes);
 }
 
+// -------------------------------------------------------------------------
+// Variable-length kernel with a lean block loop.  MD5's varlen kernel is
+// issue-bound (ncu: issue 75 %, ALU 77 %, LSU 81 %), and around the ~315
+// instructions of a compression k_varlen16 spends ~45 per block: the
+// realignment switch (7 branch instructions), a bounds branch for the fifth
+// granule, 64-bit block counters.  Here the fifth granule is one predicated
+// load (a 16-byte-aligned window does not use it, and for an aligned message
+// it may lie past the data end), the block counters are 32-bit, and with QT
+// the word offset q = (a >> 2) & 3 is a template parameter of the whole
+// block loop -- entered once per message, warp-uniform after the q-major
+// sort -- so the loop body has no realignment branches at all (four copies
+// of the loop).  Block b+1's window is in flight during b's compression.
+// -------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ld16_pred(const uint4* p, uint32_t pred) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t@p ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}"
+        : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+        : "l"(p), "r"(pred));
+    return v;
+}
+
+__device__ __forceinline__ void load_window5(const uint4* src, uint32_t mis, uint32_t (&c)[20]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint4 v = __ldg(src + k);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+    const uint4 v4 = ld16_pred(src + 4, mis);
+    c[16] = v4.x; c[17] = v4.y; c[18] = v4.z; c[19] = v4.w;
+}
+
+template <int Q>
+__device__ __forceinline__ void realign_q(const uint32_t (&c)[20], uint32_t sh, uint32_t (&raw)[16]) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) raw[j] = __funnelshift_r(c[j + Q], c[j + Q + 1], sh);
+}
+
+// Full blocks 0 .. nfull-1 of one message (not at the data end).  Q < 0: the
+// realignment class is read at run time (one loop for every class).
+template <int ALG, int Q, int V>
+__device__ __forceinline__ void varlen16l_blocks(const uint4* w16, uint32_t mis, uint32_t q, uint32_t sh,
+                                                 uint32_t nfull, uint32_t* st) {
+    uint32_t c[20], raw[16];
+    if (nfull) load_window5(w16, mis, c);
+    for (uint32_t b = 0; b < nfull; ++b) {
+        if constexpr (Q < 0) realign16(c, q, sh, raw);
+        else realign_q<Q>(c, sh, raw);
+        if (b + 1 < nfull) load_window5(w16 + 4 * (b + 1), mis, c);
+        compress1<ALG, V>(st, raw);
+    }
+}
+
+template <int ALG, bool QT, int V = -1>
+__global__ void __launch_bounds__(128)
+k_varlen16l(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = perm ? (uint64_t)perm[t] : t;
+    const uint64_t start = offsets[i] - offset_base;
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
+    const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    uint8_t* dout = out + i * H::kDigestBytes;
+    if (((a + len + 15u) & ~uintptr_t(15)) > dend || (len >> 38)) {  // the batch's last bytes, or > 2^32 blocks
+        varlen16_message<ALG, 1, true>(w16, a, len, dend, dout);
+        return;
+    }
+    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
+    const uint32_t mis = (a & 15u) != 0;
+    const uint32_t nfull = (uint32_t)(len >> 6);
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    if constexpr (QT) {
+        switch (q) {
+        case 0: varlen16l_blocks<ALG, 0, V>(w16, mis, q, sh, nfull, st); break;
+        case 1: varlen16l_blocks<ALG, 1, V>(w16, mis, q, sh, nfull, st); break;
+        case 2: varlen16l_blocks<ALG, 2, V>(w16, mis, q, sh, nfull, st); break;
+        default: varlen16l_blocks<ALG, 3, V>(w16, mis, q, sh, nfull, st); break;
+        }
+    } else {
+        varlen16l_blocks<ALG, -1, V>(w16, mis, q, sh, nfull, st);
+    }
+    // tail: the r = len % 64 remaining bytes (granules that overlap [.., a + len) only)
+    const uint32_t r = (uint32_t)(len & 63u);
+    const uintptr_t tail_end = a + len;
+    const uint4* src = w16 + 4 * (uint64_t)nfull;
+    uint32_t c[20], raw[16];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const uint4 v = ld16_pred(src + k, reinterpret_cast<uintptr_t>(src + k) < tail_end);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+    realign16(c, q, sh, raw);
+    mask_tail(raw, r);
+    md_finish<ALG, V>(st, raw, r, len);
+    store_digest<ALG>(dout, st);
+}
 
 // ---------------------------------------------------- length-bucket sort --
 // Counting sort of message indices by block count, longest first.  Three

@@ -18,6 +18,12 @@ POINTS = [(1 << 24, 16), (1 << 24, 32), (1 << 24, 64), (1 << 24, 128)] if os.env
      (1 << 16, 1024), (1 << 16, 65536), (1 << 12, 65536), (1 << 14, 16384), (1 << 17, 4096)]
 ARMS = {"default": ({}, 0), "const_v1": ({"HB_CONST_VARIANT": "1"}, 0), "direct": ({"HB_NO_SMALL_KERNEL": "1"}, _native.HB_FLAG_NO_TMA), "ws_forced": ({"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"}, 0),
         "small_forced": ({"HB_SMALL_N": str(1 << 40), "HB_DIRECT_MAX_L": "0"}, 0)}
+if os.environ.get("AB_ARMS"):  # {name: {env}} (flags 0)
+    ARMS = {k: (v, 0) for k, v in json.loads(os.environ["AB_ARMS"]).items()}
+if os.environ.get("AB_POINTS"):  # n:L,n:L,...
+    POINTS = [tuple(int(x) for x in p.split(":")) for p in os.environ["AB_POINTS"].split(",")]
+KEYS = sorted({k for env, _ in ARMS.values() for k in env} | {"HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL",
+                                                              "HB_CONST_VARIANT"})
 rounds = int(os.environ.get("AB_ROUNDS", 3))
 for n, L in POINTS:
     buf = torch.empty(n * L, dtype=torch.uint8, device="cuda:0")
@@ -28,9 +34,10 @@ for n, L in POINTS:
         ref, times = None, {}
         for _ in range(rounds):
             for arm, (env, flags) in ARMS.items():
-                for k in ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_CONST_VARIANT"):
+                for k in KEYS:
                     os.environ.pop(k, None)
                 os.environ.update(env)
+                _native.reload_tuning()  # the library parses $HB_* once
                 out = torch.empty((n, DLEN[alg]), dtype=torch.uint8, device="cuda:0")
                 device.hash_fixed(alg, msgs, out=out, flags=flags)
                 torch.cuda.synchronize()
