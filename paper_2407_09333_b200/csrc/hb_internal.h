@@ -25,7 +25,7 @@ struct Tuning {
     // kernels (hb_kernels.cuh)
     bool pdl = true;                            // $HB_PDL
     uint64_t small_n = 1ull << 18;              // $HB_SMALL_N: below it, one message per thread in TMA tiles
-    uint64_t chain_n = 1ull << 17;              // $HB_CHAIN_N: MD5 TMA batches below it use round variant 3
+    uint64_t chain_n = 1ull << 16;              // $HB_CHAIN_N: MD5 TMA batches below it: 4+1-warp tile, variant 6
     bool varlen_pf = true;                      // $HB_VARLEN_PF: MD5 varlen, software-pipelined per-thread kernel
     bool sort_qmajor = true;                    // $HB_SORT_QMAJOR: windowed sort key (q, block count), else (block count, q)
     uint64_t direct_max_len = 128;              // $HB_DIRECT_MAX_L: rows up to it use the per-thread-load kernels

@@ -280,6 +280,115 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
     }
 }
 
+// -------------------------------------------------------------------------
+// Single-warp CTAs, NB messages per thread (MD5 from 2^16 messages).  Each
+// CTA is one warp with its own STAGES-deep ring of {64 B, 32·NB rows} TMA
+// tiles; lane 0 refills a stage right after the warp has read it.  Against
+// the 4+1-warp tile: two independent round chains per thread (MD5's rounds
+// are a 3-op dependency chain, ncu: 35-42 % `wait` stalls), and 32-thread
+// CTAs spread a batch evenly over the SMs' sub-partitions (a 2^16-message
+// batch is 3.46 warps per scheduler: 4-warp CTAs put 4 on some, 3 on others).
+// -9 / -13 / -9 / -5 % at 2^16 x 1 KiB / 2^16 x 4 KiB / 2^18 x 1 KiB /
+// 2^20 x 1 KiB with round variant 4 (profiles/r2/ab_v467_r2o.txt).  Chain-
+// bound grids (< 2^16 messages) keep the 4+1-warp tile: halving the thread
+// count there lengthens the critical path.  Programmatic dependent launch
+// and early loads as in k_fixed_tma_ws.
+// -------------------------------------------------------------------------
+template <int ALG, int V, int NB, int STAGES>
+__global__ void __launch_bounds__(32, (TmaOcc<ALG, NB, STAGES, 1>::kMinCtas))
+k_fixed_tma_w1(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out,
+               uint32_t early) {
+    using H = HashAlg<ALG, V>;
+    using C = TmaCfg<NB, STAGES, 1>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t lane = threadIdx.x;
+    const uint32_t row0 = blockIdx.x * C::kRows;
+    const uint32_t base_s = smem_u32(smem_raw);
+    uint8_t* ring = smem_raw + (((base_s + 1023u) & ~1023u) - base_s);  // SWIZZLE_64B needs 1 KiB alignment
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + STAGES * C::kStageBytes);
+    const uint32_t nload = (msg_len + 63u) >> 6;
+    const uint32_t pro = nload < (uint32_t)STAGES ? nload : (uint32_t)STAGES;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        if (early & kEarlyLoad) {  // HB_FLAG_INPUT_READY: the first stages load before the wait
+            prefetch_tmap(&tmap);
+            for (uint32_t b = 0; b < pro; ++b) {
+                mbar_arrive_expect_tx(&bars[b], C::kStageBytes);
+                tma_load_2d(ring + b * C::kStageBytes, &tmap, &bars[b], (int)(b * 64u), (int)row0);
+            }
+        }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (early & kEarlyTrigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (lane == 0 && !(early & kEarlyLoad)) {
+        prefetch_tmap(&tmap);
+        for (uint32_t b = 0; b < pro; ++b) {
+            mbar_arrive_expect_tx(&bars[b], C::kStageBytes);
+            tma_load_2d(ring + b * C::kStageBytes, &tmap, &bars[b], (int)(b * 64u), (int)row0);
+        }
+    }
+    __syncwarp();
+
+    uint32_t st[NB][H::kStateWords];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) H::init(st[q]);
+    const uint32_t swz = (lane >> 1) & 3u;  // SWIZZLE_64B: rows lane and lane + 32q share it
+    uint32_t choff[NB][4];
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+#pragma unroll
+        for (uint32_t c = 0; c < 4; ++c) choff[q][c] = smem_u32(ring) + (lane + 32u * q) * 64u + ((c ^ swz) << 4);
+    uint32_t raw[NB][16];
+    auto read_stage = [&](uint32_t s) {
+        const uint32_t sbase = s * C::kStageBytes;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+#pragma unroll
+            for (uint32_t c = 0; c < 4; ++c) {
+                uint32_t x, y, z, w;
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+                             : "r"(choff[q][c] + sbase)
+                             : "memory");
+                raw[q][4 * c + 0] = x; raw[q][4 * c + 1] = y; raw[q][4 * c + 2] = z; raw[q][4 * c + 3] = w;
+            }
+        }
+    };
+    const uint32_t nfull = msg_len >> 6;
+    uint32_t stage = 0, phase = 0;
+    for (uint32_t b = 0; b < nfull; ++b) {
+        mbar_wait_parity(&bars[stage], phase);
+        read_stage(stage);
+        __syncwarp();  // every lane has its registers: the stage may be refilled
+        if (lane == 0 && b + STAGES < nload) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&bars[stage], C::kStageBytes);
+            tma_load_2d(ring + stage * C::kStageBytes, &tmap, &bars[stage], (int)((b + STAGES) * 64u), (int)row0);
+        }
+        H::template compress_n<NB>(st, raw);
+        if (++stage == (uint32_t)STAGES) { stage = 0; phase ^= 1u; }
+    }
+    const uint32_t r = msg_len & 63u;
+    if (r) {  // partial data block: TMA zero-filled the columns >= msg_len
+        mbar_wait_parity(&bars[stage], phase);
+        read_stage(stage);
+    } else {
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) raw[q][j] = 0u;
+    }
+    md_finish_n<ALG, V, NB>(st, raw, r, msg_len);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+        const uint32_t row = row0 + lane + 32u * q;
+        if (row < n) store_digest<ALG>(out + (uint64_t)row * H::kDigestBytes, st[q]);
+    }
+}
+
 // =========================================================================
 // Fixed-width direct-load kernel (HB_FLAG_NO_TMA; 16B-aligned rows only).
 // Kept as the A/B baseline for the TMA staging: each thread streams its own
@@ -828,6 +937,24 @@ __device__ __forceinline__ uint4 ld16_pred(const uint4* p, uint32_t pred) {
     return v;
 }
 
+// ... with an L2 cache policy (createpolicy) on every granule.
+__device__ __forceinline__ uint4 ld16_pred_hint(const uint4* p, uint32_t pred, uint64_t pol) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t"
+        "@p ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %6;\n\t}"
+        : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+        : "l"(p), "r"(pred), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ void load_window5_hint(const uint4* src, uint32_t mis, uint32_t (&c)[20], uint64_t pol) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const uint4 v = ld16_pred_hint(src + k, k < 4 ? 1u : mis, pol);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+}
+
 __device__ __forceinline__ void load_window5(const uint4* src, uint32_t mis, uint32_t (&c)[20]) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -846,11 +973,18 @@ __device__ __forceinline__ void realign_q(const uint32_t (&c)[20], uint32_t sh, 
 
 // Full blocks 0 .. nfull-1 of one message (not at the data end).  Q < 0: the
 // realignment class is read at run time (one loop for every class).
-template <int ALG, int Q, int V>
+// HINT: the first window (whose leading granule holds the previous message's
+// last bytes, read by that message's thread much later) is loaded evict_last,
+// so the shared granule is still in L2 then instead of coming from HBM twice.
+template <int ALG, int Q, int V, bool HINT = false>
 __device__ __forceinline__ void varlen16l_blocks(const uint4* w16, uint32_t mis, uint32_t q, uint32_t sh,
                                                  uint32_t nfull, uint32_t* st) {
     uint32_t c[20], raw[16];
-    if (nfull) load_window5(w16, mis, c);
+    if (HINT) {
+        if (nfull) load_window5_hint(w16, mis, c, policy_evict_last());
+    } else {
+        if (nfull) load_window5(w16, mis, c);
+    }
     for (uint32_t b = 0; b < nfull; ++b) {
         if constexpr (Q < 0) realign16(c, q, sh, raw);
         else realign_q<Q>(c, sh, raw);
@@ -859,7 +993,7 @@ __device__ __forceinline__ void varlen16l_blocks(const uint4* w16, uint32_t mis,
     }
 }
 
-template <int ALG, bool QT, int V = -1>
+template <int ALG, bool QT, int V = -1, bool HINT = false>
 __global__ void __launch_bounds__(128)
 k_varlen16l(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
             uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
@@ -884,22 +1018,24 @@ k_varlen16l(const uint8_t* __restrict__ data, const uint8_t* data_end, const uin
     H::init(st);
     if constexpr (QT) {
         switch (q) {
-        case 0: varlen16l_blocks<ALG, 0, V>(w16, mis, q, sh, nfull, st); break;
-        case 1: varlen16l_blocks<ALG, 1, V>(w16, mis, q, sh, nfull, st); break;
-        case 2: varlen16l_blocks<ALG, 2, V>(w16, mis, q, sh, nfull, st); break;
-        default: varlen16l_blocks<ALG, 3, V>(w16, mis, q, sh, nfull, st); break;
+        case 0: varlen16l_blocks<ALG, 0, V, HINT>(w16, mis, q, sh, nfull, st); break;
+        case 1: varlen16l_blocks<ALG, 1, V, HINT>(w16, mis, q, sh, nfull, st); break;
+        case 2: varlen16l_blocks<ALG, 2, V, HINT>(w16, mis, q, sh, nfull, st); break;
+        default: varlen16l_blocks<ALG, 3, V, HINT>(w16, mis, q, sh, nfull, st); break;
         }
     } else {
-        varlen16l_blocks<ALG, -1, V>(w16, mis, q, sh, nfull, st);
+        varlen16l_blocks<ALG, -1, V, HINT>(w16, mis, q, sh, nfull, st);
     }
     // tail: the r = len % 64 remaining bytes (granules that overlap [.., a + len) only)
     const uint32_t r = (uint32_t)(len & 63u);
     const uintptr_t tail_end = a + len;
     const uint4* src = w16 + 4 * (uint64_t)nfull;
     uint32_t c[20], raw[16];
+    const uint64_t pol_tail = HINT ? policy_evict_first() : 0;
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
-        const uint4 v = ld16_pred(src + k, reinterpret_cast<uintptr_t>(src + k) < tail_end);
+        const uint32_t live = reinterpret_cast<uintptr_t>(src + k) < tail_end;
+        const uint4 v = HINT ? ld16_pred_hint(src + k, live, pol_tail) : ld16_pred(src + k, live);
         c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
     }
     realign16(c, q, sh, raw);
@@ -1168,6 +1304,28 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     return cudaGetLastError();
 }
 
+template <int ALG, int V, int NB, int STAGES>
+static cudaError_t launch_fixed_tma_w1(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
+                                       cudaStream_t stream, bool input_ready = false) {
+    using C = TmaCfg<NB, STAGES, 1>;
+    const Tuning& T = tuning();
+    CUtensorMap map;
+    cudaError_t e = encode_rows_map(&map, d_msgs, n, L, (uint32_t)C::kRows, T.tma_l2);
+    if (e != cudaSuccess) return e;
+    static std::atomic<uint64_t> attr_done{0};
+    e = set_smem_attr_once(attr_done, [] {
+        return cudaFuncSetAttribute(k_fixed_tma_w1<ALG, V, NB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    C::kSmem);
+    });
+    if (e != cudaSuccess) return e;
+    const uint32_t grid = (n + C::kRows - 1) / C::kRows;
+    const bool pdl = grid >= (uint32_t)device_sms() || (L + 8u) / 64u + 1u <= 17u;  // as launch_fixed_tma_ws
+    const uint32_t half_wave = (uint32_t)device_sms() * (uint32_t)TmaOcc<ALG, NB, STAGES, 1>::kMinCtas / 2u;
+    const uint32_t early = input_ready && pdl && T.pdl ? kEarlyLoad | (grid <= half_wave ? kEarlyTrigger : 0u) : 0u;
+    launch_pdl_smem(k_fixed_tma_w1<ALG, V, NB, STAGES>, grid, 32, C::kSmem, stream, pdl, map, n, L, d_out, early);
+    return cudaGetLastError();
+}
+
 #ifdef HB_AB
 #include "hb_ab_kernels.cuh"
 #endif
@@ -1185,12 +1343,17 @@ static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t 
 #ifdef HB_AB
     if (tuning().tma_cfg >= 0 || tuning().variant >= 0) return launch_tma_ab<ALG>(src, n, L, dst, s);
 #endif
-    // MD5 batches under 2^17 messages (at most ~4.4 warps per SM sub-partition:
-    // bound by each message's dependent chain, not by issue) take round
-    // variant 3, whose shorter f -> add -> rotate chain is 4-23 % faster there
-    // and 3-5 % slower once the grid is issue-bound (profiles/ab_mid_r2c.txt).
-    if constexpr (ALG == kMd5)
-        if ((uint64_t)n < tuning().chain_n) return launch_fixed_tma_ws<ALG, kVarBal3, 1, 3>(src, n, L, dst, s, input_ready);
+    // MD5: from 2^16 messages single-warp CTAs with two messages per thread and
+    // round variant 4 (one round in three sums a + M + K in one IADD3: 4
+    // instead of 5 instructions there), 5-13 % faster than the 4+1-warp tile
+    // from 2^16 to 2^22 x 1 KiB (profiles/r2/ab_v467_r2o.txt).  Smaller,
+    // chain-bound batches keep one message per thread in the 4+1-warp tile
+    // with variant 6 (variant 3's short f -> add -> rotate chain, every other
+    // round's off-chain sum in one IADD3): -7 % against variant 3 there.
+    if constexpr (ALG == kMd5) {
+        if ((uint64_t)n < tuning().chain_n) return launch_fixed_tma_ws<ALG, 6, 1, 3>(src, n, L, dst, s, input_ready);
+        return launch_fixed_tma_w1<ALG, 4, 2, 3>(src, n, L, dst, s, input_ready);
+    }
     if ((uint64_t)n < tuning().small_n || ALG != kSha1)
         return launch_fixed_tma_ws<ALG, kVarBal, 1, 3>(src, n, L, dst, s, input_ready);
     return launch_fixed_tma_ws<ALG, kVarBal, 2, 3>(src, n, L, dst, s, input_ready);
@@ -1273,12 +1436,13 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
     const uint32_t* perm = nullptr;
     cudaError_t e = launch_varlen_sort(ALG, d_data, d_offsets, offset_base, n, d_scratch, stream, flags, &perm, 4);
     if (e != cudaSuccess) return e;
-    // MD5 (HBM/issue ridge, windowed q-major sort): the software-pipelined
-    // per-thread kernel, block b+1's window in flight during b's compression
-    // (-6 % vs the plain kernel, profiles/ab_varlen_r2d.txt); SHA-1 / SM3 are
-    // ALU-bound and keep the plain kernel.
+    // MD5 (issue-bound, windowed q-major sort): the lean software-pipelined
+    // block loop -- block b+1's window in flight during b's compression (-6 %
+    // vs the plain kernel, profiles/ab_varlen_r2d.txt), ~18 fewer instructions
+    // per block than k_varlen16<MD5, 1> (-1.4 %, profiles/r2/ab_varlen_r2o.txt);
+    // SHA-1 / SM3 are ALU-bound and keep the plain kernel.
     if (ALG == kMd5 && tuning().varlen_pf)
-        launch_plain(k_varlen16<ALG, 1>, (unsigned)((n + 127) / 128), 128, stream, d_data, d_data + data_bytes,
+        launch_plain(k_varlen16l<ALG, false>, (unsigned)((n + 127) / 128), 128, stream, d_data, d_data + data_bytes,
                      d_offsets, offset_base, perm, n, d_out);
     else
         launch_plain(k_varlen16<ALG, 0>, (unsigned)((n + 127) / 128), 128, stream, d_data, d_data + data_bytes,

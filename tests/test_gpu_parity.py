@@ -249,16 +249,16 @@ def test_pdl_stream_order(L):
 
     from paper_2407_09333_b200 import device
 
-    n = 20000
-    buf = torch.empty((n, L), dtype=torch.uint8, device="cuda:0")
-    outs = []
-    for k in range(6):
-        buf.fill_(k + 1)
-        outs.append(device.hash_fixed("md5", buf))
-    torch.cuda.synchronize()
-    for k, o in enumerate(outs):
-        ref = oracle.batch_fixed("md5", np.full((1, L), k + 1, np.uint8))
-        assert np.array_equal(o.cpu().numpy(), np.repeat(ref, n, axis=0)), k
+    for n in (20000, 70000):  # MD5: the 4+1-warp tile below 2^16 messages, single-warp tiles above
+        buf = torch.empty((n, L), dtype=torch.uint8, device="cuda:0")
+        outs = []
+        for k in range(6):
+            buf.fill_(k + 1)
+            outs.append(device.hash_fixed("md5", buf))
+        torch.cuda.synchronize()
+        for k, o in enumerate(outs):
+            ref = oracle.batch_fixed("md5", np.full((1, L), k + 1, np.uint8))
+            assert np.array_equal(o.cpu().numpy(), np.repeat(ref, n, axis=0)), (n, k)
     per = L // 32  # SM3 digests per L-byte row of the next round
     rows = per ** 3 if L > 64 else 1 << 14
     data = oracle.fill_random(rows * L, 41).reshape(rows, L)
@@ -498,12 +498,16 @@ def test_full_size_sampled_and_cross_path():
 
 
 @pytest.mark.ab
-@pytest.mark.parametrize("cfg", ["1x3", "2x2", "2x3", "ws2", "ws3", "ws2x2", "ws3x2", "ws3u", "ws3x2u", "ws3n"])
+@pytest.mark.parametrize("cfg", ["1x3", "2x2", "2x3", "ws2", "ws3", "ws2x2", "ws3x2", "ws3u", "ws3x2u", "ws3n",
+                                 "w1x1", "w1x2", "w1x4", "w1x4s2", "w1x2p", "ws3v6"])
 def test_tma_tile_configs_and_variants(cfg, hb_env):
     """Every compiled TMA tile configuration x round variant is bit-exact
     (the tuned default is only one of them; $HB_TMA_CFG/$HB_VARIANT select)."""
-    variants = (["0", "1", "2", "3"] if cfg == "1x3" else ["1", "3"] if cfg.endswith("x2") and cfg.startswith("ws")
-                else ["0", "1", "2", "3"] if cfg == "ws3" else ["0", "1"] if cfg.startswith("ws") else ["0", "1", "2"])
+    variants = {"1x3": ["0", "1", "2", "3"], "ws3": ["0", "1", "2", "3", "4", "5", "6", "7"],
+                "w1x1": ["1", "3"], "w1x2": ["1", "3", "4"], "w1x4": ["1", "3", "5"], "w1x4s2": ["1"],
+                "w1x2p": ["1", "4", "6"], "ws3v6": ["6"]}.get(
+        cfg, ["1", "3"] if cfg.endswith("x2") and cfg.startswith("ws") else ["0", "1"] if cfg.startswith("ws")
+        else ["0", "1", "2"])
     hb_env.set(HB_TMA_CFG=cfg)
     for L in (16, 48, 64, 112, 128, 1024, 1040):
         n = 333
@@ -530,7 +534,7 @@ def test_duty_ratio_invariance():
             assert np.array_equal(got, ref), (alg, x)
 
 
-GEOMETRY_KEYS = ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_CONST_VARIANT")
+GEOMETRY_KEYS = ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_CONST_VARIANT", "HB_CHAIN_N")
 
 
 def _geometry_arms(alg, arms, hb_env):
@@ -549,7 +553,9 @@ def test_batch_geometry_dispatch_matches(alg, hb_env):
     loads for short rows, one message per thread below $HB_SMALL_N, the tuned
     tiles otherwise); every shape must give the oracle's digests."""
     _geometry_arms(alg, [{}, {"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"},
-                         {"HB_SMALL_N": str(1 << 40), "HB_DIRECT_MAX_L": "0"}], hb_env)
+                         {"HB_SMALL_N": str(1 << 40), "HB_DIRECT_MAX_L": "0"},
+                         # MD5's single-warp two-messages-per-thread tile at every width
+                         {"HB_CHAIN_N": "0", "HB_DIRECT_MAX_L": "0"}], hb_env)
 
 
 @pytest.mark.ab
@@ -592,7 +598,11 @@ def test_varlen_every_length_and_alignment_ab(alg, hb_env):
         for env, fl in (({"HB_VC_STAGES": "3"}, C), ({"HB_VC_STAGES": "2"}, C), ({"HB_VC_PF": "128"}, C),
                         ({"HB_VC_PF": "0"}, C), ({"HB_VARLEN_PREFETCH": "1"}, 0), ({"HB_VARLEN_BULK": "3"}, 0),
                         ({"HB_VARLEN_BULK": "5"}, 0), ({"HB_VARLEN_LD": "32"}, 0), ({"HB_VARLEN_LD": "16"}, 0),
-                        ({"HB_VARLEN_LD": "32", "HB_VARLEN_Q": "4"}, 0)):
+                        ({"HB_VARLEN_LD": "32", "HB_VARLEN_Q": "4"}, 0),
+                        # lean block loop: runtime / per-class realignment, round variants, L2 policies
+                        ({"HB_VARLEN_KERNEL": "40"}, 0), ({"HB_VARLEN_KERNEL": "41"}, 0),
+                        ({"HB_VARLEN_KERNEL": "42"}, 0), ({"HB_VARLEN_KERNEL": "44"}, 0),
+                        ({"HB_VARLEN_KERNEL": "46"}, 0), ({"HB_VARLEN_KERNEL": "47"}, 0)):
             hb_env.set(**env)
             got = batch_digest_varlen(alg, buf, off, flags=fl)
             assert np.array_equal(got, ref), (alg, shift, env)
@@ -822,10 +832,12 @@ def test_engine_budget():
     assert 0 < b["chunk_cap_bytes"] <= 256 << 20
 
 
-@pytest.mark.parametrize("n,L,expect", [(1 << 18, 1024, "k_fixed_tma_ws"), (4096, 1024, "k_fixed_tma_ws"),
-                                        (4096, 64, "k_fixed_small"), (4096, 96, "k_fixed_direct"),
-                                        (4096, 100, "k_generic")])
-def test_last_kernel_name(n, L, expect):
+@pytest.mark.parametrize("n,L,expect,expect_md5", [(1 << 18, 1024, "k_fixed_tma_ws", "k_fixed_tma_w1"),
+                                                   (4096, 1024, "k_fixed_tma_ws", "k_fixed_tma_ws"),
+                                                   (4096, 64, "k_fixed_small", "k_fixed_small"),
+                                                   (4096, 96, "k_fixed_direct", "k_fixed_direct"),
+                                                   (4096, 100, "k_generic", "k_generic")])
+def test_last_kernel_name(n, L, expect, expect_md5):
     """hb_last_kernel_name names the kernel that actually ran (what the bench
     reports as roofline.kernel), for the device and host-buffer paths."""
     import torch
@@ -837,7 +849,7 @@ def test_last_kernel_name(n, L, expect):
     name = _native.last_kernel_name()
     assert name.startswith(f"void hb::{expect}<") or expect in name, name
     batch_digest("md5", np.zeros((n, L), np.uint8), gpus=[0, 0])  # two shards on the workers
-    assert expect in _native.last_kernel_name()
+    assert expect_md5 in _native.last_kernel_name()
     device.hash_decimal("md5", 0, 1000, 9)
     assert "k_decimal_run" in _native.last_kernel_name()
 
