@@ -437,7 +437,7 @@ enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4,
                 // single-warp CTAs (per-warp ring, W = 1) with NB messages per thread: a
                 // mid-size batch (2^16 messages, 3.46 warps per scheduler at NB = 1) as
                 // <= 1 warp per scheduler carrying NB independent round chains
-                kCfgW1x1 = 11, kCfgW1x2 = 12, kCfgW1x4 = 13, kCfgW1x4s2 = 14, kCfgW1x2p = 15, kCfgWs3v6 = 16 };
+                kCfgW1x1 = 11, kCfgW1x2 = 12, kCfgW1x4 = 13, kCfgW1x4s2 = 14, kCfgW1x2p = 15, kCfgWs3v6 = 16, kCfgW1x2s4 = 17 };
 
 template <int ALG, int V, int NB, int STAGES, int W = kTmaWarps>
 static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
@@ -500,6 +500,9 @@ static cudaError_t launch_tma_ab(const uint8_t* src, uint32_t n, uint32_t L, uin
             if (v == 6) return launch_fixed_tma_w1<ALG, 6, 2, 3>(src, n, L, dst, s);
         }
         return launch_fixed_tma_w1<ALG, 1, 2, 3>(src, n, L, dst, s);
+    case kCfgW1x2s4:
+        if constexpr (ALG == kMd5) return launch_fixed_tma_w1<ALG, 4, 2, 4>(src, n, L, dst, s);
+        return launch_fixed_tma_w1<ALG, 1, 2, 4>(src, n, L, dst, s);
     case kCfgWs3v6:
         if constexpr (ALG == kMd5) return launch_fixed_tma_ws<ALG, 6, 1, 3>(src, n, L, dst, s);
         return launch_fixed_tma_ws<ALG, 1, 1, 3>(src, n, L, dst, s);
@@ -638,6 +641,8 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
         // 46: per-class loops + variant 4 + L2 policies (first window evict_last, tail evict_first); 47: runtime switch + L2 policies
         case 46: launch_plain(k_varlen16l<ALG, true, ALG == kMd5 ? 4 : -1, true>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 47: launch_plain(k_varlen16l<ALG, false, -1, true>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        // lean loop, uniform finish (nb compressions per warp, not nb + 1)
+        case 48: launch_plain(k_varlen16f<ALG>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         default: launch_plain(k_varlen16<ALG, 0, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         }
     } else if (T.varlen_kernel >= 10) {  // prefetch-instruction arms of the per-thread kernel (PF = kernel - 10)

@@ -289,7 +289,7 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
 // CTAs spread a batch evenly over the SMs' sub-partitions (a 2^16-message
 // batch is 3.46 warps per scheduler: 4-warp CTAs put 4 on some, 3 on others).
 // -9 / -13 / -9 / -5 % at 2^16 x 1 KiB / 2^16 x 4 KiB / 2^18 x 1 KiB /
-// 2^20 x 1 KiB with round variant 4 (profiles/r2/ab_v467_r2o.txt).  Chain-
+// 2^20 x 1 KiB with round variants 4 / 6 (profiles/r2/ab_v467_r2o.txt).  Chain-
 // bound grids (< 2^16 messages) keep the 4+1-warp tile: halving the thread
 // count there lengthens the critical path.  Programmatic dependent launch
 // and early loads as in k_fixed_tma_ws.
@@ -1044,6 +1044,81 @@ k_varlen16l(const uint8_t* __restrict__ data, const uint8_t* data_end, const uin
     store_digest<ALG>(dout, st);
 }
 
+// -------------------------------------------------------------------------
+// Lean block loop with a uniform finish.  A message of block count nb (data
+// + 0x80 + length) needs nb compressions, but k_varlen16(l) runs its full-
+// block loop to len/64 and then md_finish's one or two: a lane whose last
+// r = len % 64 bytes are >= 56 has one full block fewer and one tail block
+// more, so a warp holding both kinds (nearly every warp: P(r >= 56) = 1/8 per
+// lane) executes nb + 1 compressions.  Here every lane runs nb - 1 loop
+// iterations -- the r >= 56 lanes' partial block, with its 0x80, is the last
+// one, masked in place (a branch taken once per message) -- and then one
+// final block: the remaining data, 0x80 (r < 56) and the bit length.  The
+// window after the last full block is loaded with per-granule predicates
+// (never past the message's last granule).
+// -------------------------------------------------------------------------
+__device__ __forceinline__ void load_window_tail(const uint4* src, uintptr_t tail_end, uint32_t (&c)[20]) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const uint4 v = ld16_pred(src + k, reinterpret_cast<uintptr_t>(src + k) < tail_end);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(128)
+k_varlen16f(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = perm ? (uint64_t)perm[t] : t;
+    const uint64_t start = offsets[i] - offset_base;
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
+    const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    uint8_t* dout = out + i * H::kDigestBytes;
+    if (((a + len + 15u) & ~uintptr_t(15)) > dend || (len >> 38)) {  // the batch's last bytes, or > 2^32 blocks
+        varlen16_message<ALG, 1, true>(w16, a, len, dend, dout);
+        return;
+    }
+    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
+    const uint32_t mis = (a & 15u) != 0;
+    const uint32_t nfull = (uint32_t)(len >> 6), r = (uint32_t)(len & 63u);
+    const uint32_t nmain = nfull + (r >= 56u ? 1u : 0u);  // every block but the final one
+    const uint32_t pad = 0x80u << ((r & 3u) * 8u), pw = r >> 2;
+    const uintptr_t tail_end = a + len;
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    uint32_t c[20], raw[16];
+    if (nfull) load_window5(w16, mis, c);
+    else load_window_tail(w16, tail_end, c);
+    for (uint32_t b = 0; b < nmain; ++b) {
+        realign16(c, q, sh, raw);
+        if (b + 1 < nfull) load_window5(w16 + 4 * (b + 1), mis, c);
+        else load_window_tail(w16 + 4 * (b + 1), tail_end, c);
+        if (b == nfull) {  // r >= 56: the partial data block carries the 0x80
+            mask_tail(raw, r);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) raw[j] |= (pw == (uint32_t)j) ? pad : 0u;
+        }
+        compress1<ALG>(st, raw);
+    }
+    // final block: r < 56 -> the last r data bytes, 0x80 and the length; r >= 56 -> zeros and the length
+    realign16(c, q, sh, raw);
+    mask_tail(raw, r < 56u ? r : 0u);
+    if (r < 56u) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) raw[j] |= (pw == (uint32_t)j) ? pad : 0u;
+    }
+    const uint64_t bits = len * 8ull;
+    raw[14] = H::kBigEndian ? bswap((uint32_t)(bits >> 32)) : (uint32_t)bits;
+    raw[15] = H::kBigEndian ? bswap((uint32_t)bits) : (uint32_t)(bits >> 32);
+    compress1<ALG>(st, raw);
+    store_digest<ALG>(dout, st);
+}
+
 // ---------------------------------------------------- length-bucket sort --
 // Counting sort of message indices by block count, longest first.  Three
 // small kernels: per-CTA shared-memory histograms -> global histogram, one
@@ -1249,8 +1324,35 @@ static cudaError_t set_smem_attr_once(std::atomic<uint64_t>& done, F set) {
 // The (n, L) byte matrix as a 2-D TMA tensor: dim0 = bytes of a row
 // (contiguous), dim1 = rows with stride L.  Box = one 64-byte block of `rows`
 // rows, 64-byte swizzle, L2 promotion `l2` bytes.
+static cudaError_t encode_rows_map_uncached(CUtensorMap* map, const uint8_t* d_msgs, uint32_t n, uint32_t L,
+                                            uint32_t rows, uint32_t l2);
 static cudaError_t encode_rows_map(CUtensorMap* map, const uint8_t* d_msgs, uint32_t n, uint32_t L, uint32_t rows,
                                    uint32_t l2) {
+    // The last few descriptors of this thread, reused when a caller hashes the
+    // same buffer shape again (rotating input copies, graph capture, the
+    // reference executor's repeated chunks): the encode is ~1 us of host time
+    // on a launch that can be shorter than that.
+    struct Entry { const uint8_t* p; uint32_t n, L, rows, l2; CUtensorMap map; };
+    constexpr int kCache = 8;
+    thread_local Entry cache[kCache] = {};
+    thread_local int next = 0;
+    for (int k = 0; k < kCache; ++k) {
+        const Entry& c = cache[k];
+        if (c.p == d_msgs && c.n == n && c.L == L && c.rows == rows && c.l2 == l2 && c.p) {
+            *map = c.map;
+            return cudaSuccess;
+        }
+    }
+    const cudaError_t e = encode_rows_map_uncached(map, d_msgs, n, L, rows, l2);
+    if (e == cudaSuccess) {
+        cache[next] = Entry{d_msgs, n, L, rows, l2, *map};
+        next = (next + 1) % kCache;
+    }
+    return e;
+}
+
+static cudaError_t encode_rows_map_uncached(CUtensorMap* map, const uint8_t* d_msgs, uint32_t n, uint32_t L,
+                                            uint32_t rows, uint32_t l2) {
     PFN_encodeTiled enc = get_encode_tiled();
     if (!enc) {
         snprintf(tma_error_buf(), kTmaErrLen, "cuTensorMapEncodeTiled unavailable");
@@ -1318,9 +1420,19 @@ static cudaError_t launch_fixed_tma_w1(const uint8_t* d_msgs, uint32_t n, uint32
                                     C::kSmem);
     });
     if (e != cudaSuccess) return e;
+    // resident CTAs per SM (shared memory bounds it, ~17 at 3 stages), queried once per device
+    static std::atomic<int> occ_cache[64];
+    int dev = 0, occ = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) occ = occ_cache[dev].load(std::memory_order_relaxed);
+    if (!occ) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fixed_tma_w1<ALG, V, NB, STAGES>, 32, C::kSmem) !=
+                cudaSuccess || occ <= 0)
+            occ = TmaOcc<ALG, NB, STAGES, 1>::kMinCtas;
+        if (dev >= 0 && dev < 64) occ_cache[dev].store(occ, std::memory_order_relaxed);
+    }
     const uint32_t grid = (n + C::kRows - 1) / C::kRows;
     const bool pdl = grid >= (uint32_t)device_sms() || (L + 8u) / 64u + 1u <= 17u;  // as launch_fixed_tma_ws
-    const uint32_t half_wave = (uint32_t)device_sms() * (uint32_t)TmaOcc<ALG, NB, STAGES, 1>::kMinCtas / 2u;
+    const uint32_t half_wave = (uint32_t)device_sms() * (uint32_t)occ / 2u;
     const uint32_t early = input_ready && pdl && T.pdl ? kEarlyLoad | (grid <= half_wave ? kEarlyTrigger : 0u) : 0u;
     launch_pdl_smem(k_fixed_tma_w1<ALG, V, NB, STAGES>, grid, 32, C::kSmem, stream, pdl, map, n, L, d_out, early);
     return cudaGetLastError();
@@ -1344,15 +1456,16 @@ static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t 
     if (tuning().tma_cfg >= 0 || tuning().variant >= 0) return launch_tma_ab<ALG>(src, n, L, dst, s);
 #endif
     // MD5: from 2^16 messages single-warp CTAs with two messages per thread and
-    // round variant 4 (one round in three sums a + M + K in one IADD3: 4
+    // round variant 6 (every other round sums a + M + K in one IADD3: 4
     // instead of 5 instructions there), 5-13 % faster than the 4+1-warp tile
-    // from 2^16 to 2^22 x 1 KiB (profiles/r2/ab_v467_r2o.txt).  Smaller,
+    // from 2^16 to 2^22 x 1 KiB (profiles/r2/ab_v467_r2o.txt, ab_mid_r2p.txt:
+    // variant 6 beats 4 by 2-5 % in this tile from 2^20 messages).  Smaller,
     // chain-bound batches keep one message per thread in the 4+1-warp tile
     // with variant 6 (variant 3's short f -> add -> rotate chain, every other
     // round's off-chain sum in one IADD3): -7 % against variant 3 there.
     if constexpr (ALG == kMd5) {
         if ((uint64_t)n < tuning().chain_n) return launch_fixed_tma_ws<ALG, 6, 1, 3>(src, n, L, dst, s, input_ready);
-        return launch_fixed_tma_w1<ALG, 4, 2, 3>(src, n, L, dst, s, input_ready);
+        return launch_fixed_tma_w1<ALG, 6, 2, 3>(src, n, L, dst, s, input_ready);
     }
     if ((uint64_t)n < tuning().small_n || ALG != kSha1)
         return launch_fixed_tma_ws<ALG, kVarBal, 1, 3>(src, n, L, dst, s, input_ready);

@@ -6,6 +6,7 @@ import json
 import os
 import statistics
 import sys
+import time
 
 import numpy as np
 import torch
@@ -36,6 +37,9 @@ for alg in sys.argv[1:] or ["md5", "sha1", "sm3"]:
                 os.environ.pop(k, None)
             os.environ.update(env)
             _native.reload_tuning()
+            if float(os.environ.get("AB_COOL", 0)) > 0:  # idle first: every arm starts from the same power state
+                torch.cuda.synchronize()
+                time.sleep(float(os.environ["AB_COOL"]))
             out = torch.empty((n, DLEN[alg]), dtype=torch.uint8, device="cuda:0")
             f = lambda: device.hash_varlen(alg, data, d_off, out=out, scratch=scratch, flags=flags,  # noqa: E731
                                            offset_base=0)
