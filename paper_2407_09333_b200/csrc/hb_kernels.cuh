@@ -1119,6 +1119,79 @@ k_varlen16f(const uint8_t* __restrict__ data, const uint8_t* data_end, const uin
     store_digest<ALG>(dout, st);
 }
 
+// Uniform finish with unpredicated windows: as k_varlen16f, but every window
+// -- including the one after the last full block -- is loaded whole (its bytes
+// past the message are masked off; they belong to the next message), so the
+// hot loop carries no tail-specific loads.  A message whose final window can
+// reach past the data end takes the bounded path.  HINT: L2 policies as in
+// k_varlen16l -- the first window evict_last (its leading granule holds the
+// previous message's last bytes, read by that message's thread much later),
+// the final window evict_first (it releases that granule).
+template <int ALG, bool HINT = false>
+__global__ void __launch_bounds__(128)
+k_varlen16g(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = perm ? (uint64_t)perm[t] : t;
+    const uint64_t start = offsets[i] - offset_base;
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
+    const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    uint8_t* dout = out + i * H::kDigestBytes;
+    // the final window ends before (a & ~15) + 64 * (len / 64 + 1) + 80
+    if ((a & ~uintptr_t(15)) + (len & ~uint64_t(63)) + 144u > dend || (len >> 38)) {
+        varlen16_message<ALG, 1, true>(w16, a, len, dend, dout);
+        return;
+    }
+    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
+    const uint32_t mis = (a & 15u) != 0;
+    const uint32_t nfull = (uint32_t)(len >> 6), r = (uint32_t)(len & 63u);
+    const uint32_t nmain = nfull + (r >= 56u ? 1u : 0u);  // every block but the final one
+    const uint32_t pad = 0x80u << ((r & 3u) * 8u), pw = r >> 2;
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    uint32_t c[20], raw[16];
+    uint64_t pol_norm = 0, pol_last = 0;
+    if (HINT) {
+        pol_norm = policy_evict_normal();
+        pol_last = policy_evict_first();
+        load_window5_hint(w16, mis, c, nmain ? policy_evict_last() : pol_last);
+    } else {
+        load_window5(w16, mis, c);
+    }
+    for (uint32_t b = 0; b < nmain; ++b) {
+        realign16(c, q, sh, raw);
+        if (HINT) load_window5_hint(w16 + 4 * (b + 1), mis, c, b + 1 == nmain ? pol_last : pol_norm);
+        else load_window5(w16 + 4 * (b + 1), mis, c);
+        if (b == nfull) {
+            // r >= 56: the partial data block carries the 0x80.  Only words 14-15
+            // change (bytes 56 .. r-1 are data, byte r is 0x80, the rest zero): a
+            // few predicated instructions, no full mask_tail in the hot loop.
+            const uint32_t k = r - 56u;
+            const uint64_t w = ((uint64_t)raw[15] << 32) | raw[14];
+            const uint64_t m = k ? (~0ull >> (64u - 8u * k)) : 0ull;
+            const uint64_t v = (w & m) | (0x80ull << (8u * k));
+            raw[14] = (uint32_t)v;
+            raw[15] = (uint32_t)(v >> 32);
+        }
+        compress1<ALG>(st, raw);
+    }
+    realign16(c, q, sh, raw);
+    mask_tail(raw, r < 56u ? r : 0u);
+    if (r < 56u) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) raw[j] |= (pw == (uint32_t)j) ? pad : 0u;
+    }
+    const uint64_t bits = len * 8ull;
+    raw[14] = H::kBigEndian ? bswap((uint32_t)(bits >> 32)) : (uint32_t)bits;
+    raw[15] = H::kBigEndian ? bswap((uint32_t)bits) : (uint32_t)(bits >> 32);
+    compress1<ALG>(st, raw);
+    store_digest<ALG>(dout, st);
+}
+
 // ---------------------------------------------------- length-bucket sort --
 // Counting sort of message indices by block count, longest first.  Three
 // small kernels: per-CTA shared-memory histograms -> global histogram, one
@@ -1552,11 +1625,21 @@ static cudaError_t launch_varlen_alg(const uint8_t* d_data, uint64_t data_bytes,
     // MD5 (issue-bound, windowed q-major sort): the lean software-pipelined
     // block loop -- block b+1's window in flight during b's compression (-6 %
     // vs the plain kernel, profiles/ab_varlen_r2d.txt), ~18 fewer instructions
-    // per block than k_varlen16<MD5, 1> (-1.4 %, profiles/r2/ab_varlen_r2o.txt);
-    // SHA-1 / SM3 are ALU-bound and keep the plain kernel.
+    // per block than k_varlen16<MD5, 1> (-1.4 %, profiles/r2/ab_varlen_r2o.txt)
+    // -- with L2 policies on the first window (evict_last: its leading granule
+    // is the previous message's tail, read by that message's thread much later)
+    // and on the tail (evict_first): DRAM traffic 1.063 -> 1.040 x algorithmic
+    // at equal time (profiles/r2/ncu_varlen_r2.md).  SM3 (ALU-bound): the
+    // uniform-finish loop, nb compressions per warp instead of nb + 1 (-3 %,
+    // profiles/r2/ab_varlen_r2s.txt).  SHA-1 keeps the plain kernel (the
+    // uniform finish costs it 12 %).
+    const unsigned grid = (unsigned)((n + 127) / 128);
     if (ALG == kMd5 && tuning().varlen_pf)
-        launch_plain(k_varlen16l<ALG, false>, (unsigned)((n + 127) / 128), 128, stream, d_data, d_data + data_bytes,
-                     d_offsets, offset_base, perm, n, d_out);
+        launch_plain(k_varlen16l<ALG, false, -1, true>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets,
+                     offset_base, perm, n, d_out);
+    else if (ALG == kSm3)
+        launch_plain(k_varlen16g<ALG>, grid, 128, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm,
+                     n, d_out);
     else
         launch_plain(k_varlen16<ALG, 0>, (unsigned)((n + 127) / 128), 128, stream, d_data, d_data + data_bytes,
                      d_offsets, offset_base, perm, n, d_out);

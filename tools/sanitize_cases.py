@@ -74,12 +74,20 @@ def main():
         for x, o in zip(ins, outs):
             assert np.array_equal(o.cpu().numpy(), hostref.digests(alg, x.cpu().numpy()))
             cases += 1
+    # MD5's single-warp two-messages-per-thread tile at any batch size, flagged
+    # (early loads before griddepcontrol.wait) and unflagged
+    with_env({"HB_CHAIN_N": "0"})
+    for alg in ALGS:
+        for n, L in ((3000, 1024), (700, 1040), (129, 144)):
+            fixed(alg, n, L, _native.HB_FLAG_INPUT_READY)
+            cases += 1
     varlen_arms = [({}, 0), ({"HB_VARLEN_SORT": "global"}, 0), ({"HB_VARLEN_SORT": "window"}, 0),
                    ({"HB_SORT_QMAJOR": "0"}, 0), ({"HB_VARLEN_PF": "0"}, 0)]
     if _native.built_with_ab():  # the A/B arms exist only in libhetoc_b200_ab.so
         varlen_arms += [({}, _native.HB_FLAG_VARLEN_COOP), ({}, _native.HB_FLAG_VARLEN_WORDS),
                         ({"HB_VARLEN_LD": "32"}, 0), ({"HB_VARLEN_BULK": "3"}, 0), ({"HB_VARLEN_PREFETCH": "1"}, 0),
-                        ({"HB_VARLEN_KERNEL": "33"}, 0)]
+                        ({"HB_VARLEN_KERNEL": "33"}, 0), ({"HB_VARLEN_KERNEL": "40"}, 0),
+                        ({"HB_VARLEN_KERNEL": "47"}, 0), ({"HB_VARLEN_KERNEL": "49"}, 0)]
     for env, fl in varlen_arms:
         with_env(env)
         for alg in ALGS:
