@@ -401,14 +401,33 @@ def load_peaks():
     return peaks, "fallback (B200_PROFILING.md; MEASURED_PEAKS.json unreadable or without hbm_gbs)"
 
 
-def load_ncu(name: str):
+# bench workloads whose shape is a suite entry: the suite's ncu record is the one
+# tools/ncu_configs.py refreshes with every capture
+NCU_ALIASES = {"sha1_64": "C1_sha1_64", "sm3_1k": "C3_sm3_1k", "sha1_1k": "C5_sha1_1024x16777216",
+               "varlen_md5": "C4_varlen_md5", "varlen_sha1": "C4_varlen_sha1", "varlen_sm3": "C4_varlen_sm3"}
+
+
+def _kernel_key(name):
+    """'void hb::k_x<1, false, -1>(...)' and 'void k_x<1, 0, (int)-1>(...)' -> 'k_x<1,0,-1>'."""
+    base = (name or "").replace("(int)", "").split("(")[0].replace("void ", "").replace("hb::", "")
+    head, _, args = base.partition("<")
+    vals = [a.strip().replace("false", "0").replace("true", "1") for a in args.rstrip(">").split(",")]
+    return head.strip() + "<" + ",".join(vals) + ">"
+
+
+def load_ncu(name: str, kernel: str = None):
     """The committed ncu --set full record of this config's dominant kernel
-    (profiles/ncu_summary.json, tools/ncu_configs.py): dram bytes per launch."""
+    (profiles/ncu_summary.json, tools/ncu_configs.py): dram bytes per launch.
+    A record of a different kernel than the one that ran is not used."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
-        return json.load(f).get(name)
+        summ = json.load(f)
+    rec = summ.get(NCU_ALIASES.get(name, name)) or summ.get(name)
+    if rec and kernel and _kernel_key(rec.get("kernel")) != _kernel_key(kernel):
+        return None
+    return rec
 
 
 def library_info():
@@ -946,7 +965,7 @@ def roofline(w, ctx, ms_local, kernel, name):
         roof["survey_issue_model"] = {
             "c_alg": SURVEY_C_ALG[w.alg], "issue_peak_tops": round(ctx.sms * 128 * f_max * 1e6 / 1e12, 3),
             "t_roof_ms": round(max(t_int, t_hbm) * 1e3, 4), "frac": round(max(t_int, t_hbm) / t, 4)}
-    ncu = load_ncu(name)
+    ncu = load_ncu(name, kernel)
     roof.update({"traffic": ncu.get("dram_bytes") if ncu else None,
                  "traffic_over_algorithmic": round(ncu["dram_bytes"] / w.alg_bytes, 4) if ncu else None,
                  "ncu_kernel": ncu.get("kernel") if ncu else None, "kernel": kernel,

@@ -21,3 +21,15 @@ def test_decimal_alu_ops_bounded_by_block_model():
             # exceeds the arbitrary-data count (which adds 16 byte swaps for SHA-1/SM3)
             assert prev <= ops <= bench.ALU_OPS_PER_BLOCK[alg]
             prev = ops
+
+
+def test_ncu_record_matches_the_kernel_that_ran():
+    """roofline.traffic comes from the committed ncu record of the same kernel:
+    ncu's demangled names and the library's are normalised alike, a workload
+    reads its suite entry, and a record of another kernel is not used."""
+    assert bench._kernel_key("void hb::k_varlen16l<1, false, -1, true>(unsigned char const*)") == \
+        bench._kernel_key("void k_varlen16l<1, 0, (int)-1, 1>(const unsigned char *, const unsigned char *)")
+    rec = bench.load_ncu("md5_1k")
+    assert rec is not None and bench.load_ncu("md5_1k", rec["kernel"]) == rec
+    assert bench.load_ncu("md5_1k", "void hb::k_generic<1, false>(unsigned char const*)") is None
+    assert bench.load_ncu("varlen_md5")["kernel"] == bench.load_ncu("C4_varlen_md5")["kernel"]
