@@ -64,11 +64,12 @@ ALU_OPS_PER_BLOCK = {"md5": 128, "sha1": 448, "sm3": 1084}
 # boolean/rotate ops can only issue at 64 lanes/clk/SM -- so it reads lower.
 SURVEY_C_ALG = {"md5": 324, "sha1": 613, "sm3": 1412}
 # Dependent-chain latency of one compression (cycles, one warp per SM: 4,736
-# messages of 64 KiB, profiles/r2/ab_chain_r2d.txt; the smaller of the r1 and
-# r2 measurements).  MD5 is the round-variant-3 kernel the dispatch runs below
-# 2^17 messages (variant 1: 1,462-1,509).  A batch with too few messages to
-# overlap cannot finish before (blocks per message) x this.
-CHAIN_CYCLES = {"md5": 1132, "sha1": 1116, "sm3": 2514}
+# messages of 64 KiB, profiles/r2/ab_chain_r2d.txt and ab_mid_r2p.txt; the
+# smallest measurement).  MD5 is the round-variant-6 tile the dispatch runs
+# below 2^16 messages (548.4 us for 1,025 blocks at 1,965 MHz; variant 3:
+# 1,132, variant 1: 1,462-1,509).  A batch with too few messages to overlap
+# cannot finish before (blocks per message) x this.
+CHAIN_CYCLES = {"md5": 1051, "sha1": 1116, "sm3": 2514}
 _BACKEND = os.environ.get("HB_BENCH_BACKEND", "nccl")
 
 

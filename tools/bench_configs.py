@@ -35,7 +35,7 @@ ALU_OPS = {"md5": 128, "sha1": 448, "sm3": 1084}
 # message's blocks are compressed in sequence, so no batch finishes faster than
 # (blocks per message) x this -- the binding bound when there are fewer
 # messages than the GPU has lanes to overlap.
-CHAIN_CYCLES = {"md5": 1132, "sha1": 1116, "sm3": 2514}
+CHAIN_CYCLES = bench.CHAIN_CYCLES  # one set of measured constants (bench.py)
 SMS = 148
 
 

@@ -19,7 +19,7 @@ def main():
           "max(T_hbm, T_alu, T_chain) / T_measured with T_hbm at the HBM peak (6,650 GB/s fallback unless "
           "MEASURED_PEAKS.json), T_alu = blocks x ALU-only ops / (64 lanes/clk x 148 SMs x clock) and "
           "T_chain = blocks per message x the measured dependent-chain latency of one compression "
-          "(MD5 1,509 / SHA-1 1,116 / SM3 2,514 cycles, one warp per SM) -- the bound when the batch has too "
+          "(MD5 1,051 / SHA-1 1,116 / SM3 2,514 cycles, one warp per SM) -- the bound when the batch has too "
           "few messages to overlap.\n")
     print("| config | alg | messages | size | ms | GB/s | Mhash/s | bound | fraction | bit-exact |")
     print("|---|---|---|---|---|---|---|---|---|---|")
