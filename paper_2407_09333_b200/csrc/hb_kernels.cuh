@@ -1536,8 +1536,12 @@ static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t 
     // chain-bound batches keep one message per thread in the 4+1-warp tile
     // with variant 6 (variant 3's short f -> add -> rotate chain, every other
     // round's off-chain sum in one IADD3): -7 % against variant 3 there.
+    // From 2^22 messages (>= 14 warps per scheduler) three messages per thread:
+    // -2 % at configs[1] (profiles/r2/ab_headline_r2y.txt), even at 2^18-2^22,
+    // -20 % at 2^16 (too few warps left).
     if constexpr (ALG == kMd5) {
         if ((uint64_t)n < tuning().chain_n) return launch_fixed_tma_ws<ALG, 6, 1, 3>(src, n, L, dst, s, input_ready);
+        if ((uint64_t)n >= tuning().md5_nb3_n) return launch_fixed_tma_w1<ALG, 6, 3, 3>(src, n, L, dst, s, input_ready);
         return launch_fixed_tma_w1<ALG, 6, 2, 3>(src, n, L, dst, s, input_ready);
     }
     if ((uint64_t)n < tuning().small_n || ALG != kSha1)

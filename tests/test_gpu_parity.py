@@ -534,7 +534,8 @@ def test_duty_ratio_invariance():
             assert np.array_equal(got, ref), (alg, x)
 
 
-GEOMETRY_KEYS = ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_CONST_VARIANT", "HB_CHAIN_N")
+GEOMETRY_KEYS = ("HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_CONST_VARIANT", "HB_CHAIN_N",
+                 "HB_MD5_NB3_N")
 
 
 def _geometry_arms(alg, arms, hb_env):
@@ -554,8 +555,9 @@ def test_batch_geometry_dispatch_matches(alg, hb_env):
     tiles otherwise); every shape must give the oracle's digests."""
     _geometry_arms(alg, [{}, {"HB_SMALL_N": "0", "HB_DIRECT_MAX_L": "0"},
                          {"HB_SMALL_N": str(1 << 40), "HB_DIRECT_MAX_L": "0"},
-                         # MD5's single-warp two-messages-per-thread tile at every width
-                         {"HB_CHAIN_N": "0", "HB_DIRECT_MAX_L": "0"}], hb_env)
+                         # MD5's single-warp two- and three-messages-per-thread tiles at every width
+                         {"HB_CHAIN_N": "0", "HB_DIRECT_MAX_L": "0"},
+                         {"HB_CHAIN_N": "0", "HB_MD5_NB3_N": "0", "HB_DIRECT_MAX_L": "0"}], hb_env)
 
 
 @pytest.mark.ab

@@ -5,6 +5,12 @@
 TAG=${1:-r2t}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv > gpurun_out/smi_$TAG.txt 2>&1
+# ncu --set full of the headline kernel first (bench.py reads its traffic from profiles/ncu_summary.json;
+# fold here with: python tools/ncu_configs.py fold $TAG gpurun_out/ncu_cfg_${TAG}_raw.csv gpurun_out/ncu_cfg_${TAG}_order.json)
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_fixed|k_varlen|k_generic|k_decimal" \
+  -o /tmp/ncu_cfg_$TAG python tools/ncu_configs.py run gpurun_out/ncu_cfg_${TAG}_order.json ${NCU_CONFIGS:-md5_1k} > gpurun_out/ncu_cfg_$TAG.log 2>&1
+ncu -i /tmp/ncu_cfg_$TAG.ncu-rep --page raw --csv > gpurun_out/ncu_cfg_${TAG}_raw.csv 2>/dev/null
+ncu -i /tmp/ncu_cfg_$TAG.ncu-rep --page source --csv > gpurun_out/ncu_cfg_${TAG}_source.csv 2>/dev/null
 timeout 900 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu_$TAG.log
 HETOC_B200_LIB=libhetoc_b200_ab.so timeout 900 python -m pytest tests -q -m "gpu and ab" > gpurun_out/pytest_ab_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_ab_$TAG.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/smoke_$TAG.log

@@ -20,7 +20,7 @@ from paper_2407_09333_b200 import _native, device  # noqa: E402
 ALGS = ("sha1", "md5", "sm3")
 ENV_KEYS = ("HB_TMA_CFG", "HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_VARLEN_SORT", "HB_VARLEN_LD",
             "HB_VARLEN_BULK", "HB_VARLEN_PREFETCH", "HB_VC_STAGES", "HB_CHAIN_N", "HB_SORT_QMAJOR", "HB_VARLEN_PF",
-            "HB_VARLEN_KERNEL")
+            "HB_VARLEN_KERNEL", "HB_MD5_NB3_N")
 
 
 def with_env(env):
@@ -76,11 +76,12 @@ def main():
             cases += 1
     # MD5's single-warp two-messages-per-thread tile at any batch size, flagged
     # (early loads before griddepcontrol.wait) and unflagged
-    with_env({"HB_CHAIN_N": "0"})
-    for alg in ALGS:
-        for n, L in ((3000, 1024), (700, 1040), (129, 144)):
-            fixed(alg, n, L, _native.HB_FLAG_INPUT_READY)
-            cases += 1
+    for env in ({"HB_CHAIN_N": "0"}, {"HB_CHAIN_N": "0", "HB_MD5_NB3_N": "0"}):
+        with_env(env)
+        for alg in ALGS:
+            for n, L in ((3000, 1024), (700, 1040), (129, 144)):
+                fixed(alg, n, L, _native.HB_FLAG_INPUT_READY)
+                cases += 1
     varlen_arms = [({}, 0), ({"HB_VARLEN_SORT": "global"}, 0), ({"HB_VARLEN_SORT": "window"}, 0),
                    ({"HB_SORT_QMAJOR": "0"}, 0), ({"HB_VARLEN_PF": "0"}, 0)]
     if _native.built_with_ab():  # the A/B arms exist only in libhetoc_b200_ab.so
