@@ -652,6 +652,8 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
         case 48: launch_plain(k_varlen16f<ALG>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 49: launch_plain(k_varlen16g<ALG>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         case 50: launch_plain(k_varlen16g<ALG, true>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        // lean loop unrolled by two, fifth granule carried (4 loads per block), L2 policies
+        case 51: launch_plain(k_varlen16c<ALG>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         default: launch_plain(k_varlen16<ALG, 0, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         }
     } else if (T.varlen_kernel >= 10) {  // prefetch-instruction arms of the per-thread kernel (PF = kernel - 10)

@@ -88,7 +88,8 @@ def main():
         varlen_arms += [({}, _native.HB_FLAG_VARLEN_COOP), ({}, _native.HB_FLAG_VARLEN_WORDS),
                         ({"HB_VARLEN_LD": "32"}, 0), ({"HB_VARLEN_BULK": "3"}, 0), ({"HB_VARLEN_PREFETCH": "1"}, 0),
                         ({"HB_VARLEN_KERNEL": "33"}, 0), ({"HB_VARLEN_KERNEL": "40"}, 0),
-                        ({"HB_VARLEN_KERNEL": "47"}, 0), ({"HB_VARLEN_KERNEL": "49"}, 0)]
+                        ({"HB_VARLEN_KERNEL": "47"}, 0), ({"HB_VARLEN_KERNEL": "49"}, 0),
+                        ({"HB_VARLEN_KERNEL": "51"}, 0)]
     for env, fl in varlen_arms:
         with_env(env)
         for alg in ALGS:
