@@ -700,7 +700,10 @@ class VarlenWorkload:
     def step(self):
         from paper_2407_09333_b200 import device
 
-        device.hash_varlen(self.alg, self.buf, self.d_off, out=self.out, scratch=self.scratch, offset_base=0)
+        # HB_FLAG_INPUT_READY: data and offsets are written before the timed region, never by
+        # the preceding kernel (MD5: the length sort may start while the previous step drains)
+        device.hash_varlen(self.alg, self.buf, self.d_off, out=self.out, scratch=self.scratch, offset_base=0,
+                           flags=INPUT_READY)
 
     def probe_kernel(self):
         from paper_2407_09333_b200 import _native
@@ -745,7 +748,10 @@ class VarlenWorkload:
                 "global_batch_msgs": world * self.n,
                 "parallelism": f"message-range shards over {world} GPU(s), no collective",
                 "l2": "inputs are %.1f GiB per GPU >> 126 MB L2; no flush needed" % (self.total / 2**30),
-                "step": "length sort (k_sort_window / k_sort_hist..scatter) + hash kernel, both timed"}
+                "step": "length sort (k_sort_window / k_sort_hist..scatter) + hash kernel, both timed",
+                "launch_flags": "HB_FLAG_INPUT_READY: data and offsets are written before the timed region and "
+                                "never by the preceding kernel (MD5's windowed sort may start while the previous "
+                                "step's hash kernel drains)"}
 
 
 class DecimalWorkload:

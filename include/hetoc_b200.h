@@ -65,7 +65,12 @@ typedef enum { HB_SHA1 = 0, HB_MD5 = 1, HB_SM3 = 2 } hb_alg;
  * The hash kernel then starts reading them while that kernel drains
  * (programmatic dependent launch); digests are still written only after it
  * completes.  (The engine's own chunks follow their H2D copy, which a
- * dependent launch never overlaps, so it does not need it.)                 */
+ * dependent launch never overlaps, so it does not need it.)
+ * varlen, hb_hash_varlen_dev (MD5's windowed length sort): the same guarantee
+ * for `offsets` -- the sort then starts while the preceding varlen hash
+ * kernel drains (that kernel releases it once every thread has read its
+ * permutation entry, so the scratch may be the same); the hash kernel itself
+ * still starts only after the sort completes.                               */
 #define HB_FLAG_INPUT_READY 0x40u
 /* A/B kernel arms: honoured only by a library built with -DHB_AB
  * (hb_built_with_ab() == 1); the default build returns HB_ERR_CUDA with

@@ -295,10 +295,31 @@ cudaError_t launch_varlen_sort(int alg, const uint8_t* d_data, const uint64_t* d
 #undef HB_WIN
 #else
         (void)qclasses;
-        if (T.sort_qmajor)
-            k_sort_window<8192, 4, true><<<(unsigned)((n + 8191) / 8192), 1024, 0, stream>>>(d_offsets, n, bias0, p);
-        else
-            k_sort_window<8192, 4><<<(unsigned)((n + 8191) / 8192), 1024, 0, stream>>>(d_offsets, n, bias0, p);
+        const unsigned g = (unsigned)((n + 8191) / 8192);
+        if (T.sort_qmajor && (flags & HB_FLAG_INPUT_READY) && T.pdl) {
+            // HB_FLAG_INPUT_READY: the offsets are not written by the preceding
+            // kernel, so the sort may start while it drains (programmatic
+            // dependent launch without griddepcontrol.wait).  A preceding
+            // k_varlen16l releases it once all its threads have read their
+            // permutation entries, so overwriting perm here is safe; any other
+            // preceding kernel releases it at its end or after its last read of
+            // the scratch.  41 us of a 1.93 ms configs[3] step
+            // (profiles/r2/launches_varlen_r2ab.csv) overlap the previous step.
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(g);
+            cfg.blockDim = dim3(1024);
+            cfg.stream = stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            cudaLaunchKernelEx(&cfg, k_sort_window<8192, 4, true>, d_offsets, n, bias0, p);
+        } else if (T.sort_qmajor) {
+            k_sort_window<8192, 4, true><<<g, 1024, 0, stream>>>(d_offsets, n, bias0, p);
+        } else {
+            k_sort_window<8192, 4><<<g, 1024, 0, stream>>>(d_offsets, n, bias0, p);
+        }
 #endif
         note_launch(nullptr, false);
         perm = p;

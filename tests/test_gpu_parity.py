@@ -696,6 +696,43 @@ def test_input_ready_early_start():
         assert np.array_equal(outs[last].cpu().numpy()[rows], oracle.batch_fixed(alg, sample))
 
 
+def test_varlen_input_ready_sort_overlap():
+    """HB_FLAG_INPUT_READY on varlen launches: MD5's windowed sort starts while
+    the preceding kernel drains (no griddepcontrol.wait), released by the
+    previous varlen hash kernel once its threads have read their permutation
+    entries -- here three different batches back to back on ONE scratch buffer
+    (each sort overwrites the permutation the previous hash kernel read), after
+    a fixed-width launch, with no synchronisation in between; every digest
+    equals the oracle's."""
+    import torch
+
+    from paper_2407_09333_b200 import device
+
+    flag = _native.HB_FLAG_INPUT_READY
+    rng = np.random.default_rng(31)
+    cases = []
+    for k, (n, maxlen) in enumerate(((20000, 3000), (70000, 700), (5000, 9000))):
+        lens = rng.integers(0, maxlen + 1, n).astype(np.int64)
+        off = np.zeros(n + 1, np.int64)
+        off[1:] = np.cumsum(lens)
+        host = oracle.fill_random(int(off[-1]), 70 + k)
+        cases.append((torch.from_numpy(host).cuda(), torch.from_numpy(off).cuda(), host, off))
+    scratch = torch.empty(int(_native.lib().hb_varlen_scratch_bytes(70000)), dtype=torch.uint8, device="cuda:0")
+    fixed = torch.zeros((100000, 1024), dtype=torch.uint8, device="cuda:0")
+    for alg in ALGS:
+        torch.cuda.synchronize()
+        outs = []
+        for rep in range(2):
+            device.hash_fixed(alg, fixed, flags=flag)
+            for d, o, _, _ in cases:
+                outs.append(device.hash_varlen(alg, d, o, scratch=scratch, flags=flag, offset_base=0))
+        torch.cuda.synchronize()
+        for k, (_, _, host, off) in enumerate(cases):
+            ref = oracle.batch_varlen(alg, host, off.astype(np.uint64), threads=8)
+            for rep in range(2):
+                assert np.array_equal(outs[rep * len(cases) + k].cpu().numpy(), ref), (alg, k, rep)
+
+
 def test_out_argument_reuse_and_pinned():
     """Digests written into a caller buffer (pageable or page-locked) equal a fresh result."""
     import ctypes
