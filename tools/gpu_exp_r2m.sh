@@ -6,7 +6,7 @@ timeout 600 python -m pytest tests -q -m gpu -k "varlen" > gpurun_out/pytest_var
 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_cases.py > gpurun_out/sanitize_memcheck_$T.log 2>&1; echo "rc=$?" >> gpurun_out/sanitize_memcheck_$T.log
 timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python tools/sanitize_cases.py > gpurun_out/sanitize_racecheck_$T.log 2>&1; echo "rc=$?" >> gpurun_out/sanitize_racecheck_$T.log
 for k in 1 2; do
-timeout 600 python bench.py --workload varlen_md5 --steps 20 --warmup 5 --configs none --no-e2e > gpurun_out/bench_vl_$T_$k.json 2> gpurun_out/bench_vl_${T}_$k.err
+timeout 600 python bench.py --workload varlen_md5 --steps 20 --warmup 5 --configs none --no-e2e > gpurun_out/bench_vl_${T}_$k.json 2> gpurun_out/bench_vl_${T}_$k.err
 HB_PDL=0 timeout 600 python bench.py --workload varlen_md5 --steps 20 --warmup 5 --configs none --no-e2e > gpurun_out/bench_vl_nopdl_${T}_$k.json 2> gpurun_out/bench_vl_nopdl_${T}_$k.err
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_varlen_$T.csv \
