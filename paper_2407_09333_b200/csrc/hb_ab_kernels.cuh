@@ -590,7 +590,9 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
     const bool wide = !special && T.varlen_ld == 32;
     const uint32_t* perm = nullptr;
     const int qcls = wide ? (int)T.varlen_q : 4;
-    cudaError_t e = launch_varlen_sort(ALG, d_data, d_offsets, offset_base, n, d_scratch, stream, flags, &perm,
+    // k_varlen16m groups warps by the word class of byte a-1: sort on a bias one lower
+    const uint64_t sort_base = T.varlen_kernel == 52 ? offset_base + 1 : offset_base;
+    cudaError_t e = launch_varlen_sort(ALG, d_data, d_offsets, sort_base, n, d_scratch, stream, flags, &perm,
                                        qcls == 4 ? 4 : 8);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((n + 127) / 128);
@@ -654,6 +656,8 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
         case 50: launch_plain(k_varlen16g<ALG, true>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         // lean loop unrolled by two, fifth granule carried (4 loads per block), L2 policies
         case 51: launch_plain(k_varlen16c<ALG>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        // realignment on the FMA pipe (IMAD.HI + IMAD instead of funnel shifts), sort keyed on a-1
+        case 52: launch_plain(k_varlen16m<ALG>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         default: launch_plain(k_varlen16<ALG, 0, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         }
     } else if (T.varlen_kernel >= 10) {  // prefetch-instruction arms of the per-thread kernel (PF = kernel - 10)

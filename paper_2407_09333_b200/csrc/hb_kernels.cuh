@@ -1050,6 +1050,80 @@ k_varlen16l(const uint8_t* __restrict__ data, const uint8_t* data_end, const uin
 }
 
 // -------------------------------------------------------------------------
+// Realignment on the FMA pipe (ALU-bound SHA-1 / SM3).  The funnel shifts of
+// realign16 are ALU-pipe ops, 16 per block, on top of an ALU pipe the
+// compression already keeps ~95 % busy.  Here the window is based at the
+// granule holding byte a-1, so the shift s = 8 * ((a-1) % 4) + 8 lies in
+// 8..32 and never is 0, and word j = (c[j+q+1]:c[j+q]) >> s =
+// umulhi(c[j+q], m) + c[j+q+1] * m with m = 2^(32-s): one IMAD.HI (with the
+// addend) and one IMAD, both FMA-pipe.  The word class q = ((a-1) >> 2) % 4
+// must be warp-uniform, so the length sort keys on a-1 (bias shifted by one).
+// -------------------------------------------------------------------------
+__device__ __forceinline__ void realign16m(const uint32_t (&c)[20], uint32_t q, uint32_t m, uint32_t (&raw)[16]) {
+#define HB_RM(Q) \
+    _Pragma("unroll") for (int j = 0; j < 16; ++j) raw[j] = __umulhi(c[j + Q], m) + c[j + Q + 1] * m;
+    switch (q) {
+    case 0: HB_RM(0) break;
+    case 1: HB_RM(1) break;
+    case 2: HB_RM(2) break;
+    default: HB_RM(3) break;
+    }
+#undef HB_RM
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(128)
+k_varlen16m(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = perm ? (uint64_t)perm[t] : t;
+    const uint64_t start = offsets[i] - offset_base;
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    uint8_t* dout = out + i * H::kDigestBytes;
+    const uintptr_t wb = (a - 1u) & ~uintptr_t(15);
+    if (wb < reinterpret_cast<uintptr_t>(data) || ((a + len + 15u) & ~uintptr_t(15)) > dend || (len >> 38)) {
+        // a message at the very start (its window would begin before the data) or at the end
+        varlen16_message<ALG, 0, true>(reinterpret_cast<const uint4*>(a & ~uintptr_t(15)), a, len, dend, dout);
+        return;
+    }
+    const uint4* w = reinterpret_cast<const uint4*>(wb);
+    const uint32_t q = (uint32_t)((a - 1u) >> 2) & 3u;
+    // m = 2^(32 - s), s = 8 ((a-1) % 4) + 8, read from constant memory: a shift
+    // ptxas can see is a power of two would be strength-reduced back to SHF
+    const uint32_t m = c_opaque[24u - 8u * ((uint32_t)(a - 1u) & 3u)];
+    const uint32_t nfull = (uint32_t)(len >> 6);
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    uint32_t c[20], raw[16];
+    for (uint32_t b = 0; b < nfull; ++b) {
+        const uint4* src = w + 4 * (uint64_t)b;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const uint4 v = __ldg(src + k);
+            c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+        }
+        realign16m(c, q, m, raw);
+        compress1<ALG>(st, raw);
+    }
+    const uint32_t r = (uint32_t)(len & 63u);
+    const uintptr_t tail_end = a + len;
+    const uint4* src = w + 4 * (uint64_t)nfull;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const uint4 v = ld16_pred(src + k, reinterpret_cast<uintptr_t>(src + k) < tail_end);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+    realign16m(c, q, m, raw);
+    mask_tail(raw, r);
+    md_finish<ALG>(st, raw, r, len);
+    store_digest<ALG>(dout, st);
+}
+
+// -------------------------------------------------------------------------
 // Lean loop unrolled by two with the shared granule carried: window b+1's
 // first granule is window b's fifth, so after the first window every block
 // loads four granules instead of five (-20 % L1 wavefronts), and the loop

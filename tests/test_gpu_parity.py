@@ -606,7 +606,8 @@ def test_varlen_every_length_and_alignment_ab(alg, hb_env):
                         ({"HB_VARLEN_KERNEL": "42"}, 0), ({"HB_VARLEN_KERNEL": "44"}, 0),
                         ({"HB_VARLEN_KERNEL": "46"}, 0), ({"HB_VARLEN_KERNEL": "47"}, 0),
                         ({"HB_VARLEN_KERNEL": "48"}, 0), ({"HB_VARLEN_KERNEL": "49"}, 0),
-                        ({"HB_VARLEN_KERNEL": "50"}, 0), ({"HB_VARLEN_KERNEL": "51"}, 0)):
+                        ({"HB_VARLEN_KERNEL": "50"}, 0), ({"HB_VARLEN_KERNEL": "51"}, 0),
+                        ({"HB_VARLEN_KERNEL": "52"}, 0)):
             hb_env.set(**env)
             got = batch_digest_varlen(alg, buf, off, flags=fl)
             assert np.array_equal(got, ref), (alg, shift, env)

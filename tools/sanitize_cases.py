@@ -89,7 +89,7 @@ def main():
                         ({"HB_VARLEN_LD": "32"}, 0), ({"HB_VARLEN_BULK": "3"}, 0), ({"HB_VARLEN_PREFETCH": "1"}, 0),
                         ({"HB_VARLEN_KERNEL": "33"}, 0), ({"HB_VARLEN_KERNEL": "40"}, 0),
                         ({"HB_VARLEN_KERNEL": "47"}, 0), ({"HB_VARLEN_KERNEL": "49"}, 0),
-                        ({"HB_VARLEN_KERNEL": "51"}, 0)]
+                        ({"HB_VARLEN_KERNEL": "51"}, 0), ({"HB_VARLEN_KERNEL": "52"}, 0)]
     for env, fl in varlen_arms:
         with_env(env)
         for alg in ALGS:
