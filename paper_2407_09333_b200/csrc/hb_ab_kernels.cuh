@@ -7,6 +7,394 @@
 //   k_varlen_bulk     per-lane cp.async.bulk (TMA engine)   profiles/ab_varlen_r1e.txt
 //   k_varlen_coop     warp-cooperative cp.async staging     profiles/ab_varlen_r1.txt, _r1b.txt
 #pragma once
+// Round-2 varlen arms that lost to the shipped kernels (interleaved B200 A/B,
+// profiles/r2/): two messages per thread (k_varlen16x2, ab_varlen_r2i.txt),
+// the uniform-finish loops with predicated windows for every algorithm
+// (k_varlen16u, k_varlen16f; ab_varlen_r2q.txt), the FMA-pipe realignment
+// (k_varlen16m, ab_varlen_r2ae.txt) and the two-block carry loop (k_varlen16c,
+// ab_varlen_r2ab.txt).  They build on the shipped helpers of hb_kernels.cuh.
+// The rest of one message from full block b0 on: full blocks b0 .. len/64-1,
+// then the tail and padding (md_finish), digest stored.  `st` holds the state
+// after blocks 0 .. b0-1.
+template <int ALG, bool EDGE>
+__device__ __forceinline__ void varlen16_rest(const uint4* w16, uintptr_t a, uint64_t len, uintptr_t dend,
+                                              uint64_t b0, uint32_t* st, uint8_t* dout) {
+    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
+    const bool misaligned = (a & 15u) != 0;
+    uint32_t c[20];
+    uint32_t raw[16];
+    const uint64_t nfull = len >> 6;
+    for (uint64_t b = b0; b < nfull; ++b) {
+        load_full_window(w16 + 4 * b, misaligned, c, EDGE, dend);
+        realign16(c, q, sh, raw);
+        compress1<ALG>(st, raw);
+    }
+    const uint32_t r = (uint32_t)(len & 63u);
+    const uintptr_t tail_end = a + len;
+    const uint4* src = w16 + 4 * nfull;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (reinterpret_cast<uintptr_t>(src + k) < tail_end) v = ld16_edge(src + k, EDGE, dend);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+    realign16(c, q, sh, raw);
+    mask_tail(raw, r);
+    md_finish<ALG>(st, raw, r, len);
+    store_digest<ALG>(dout, st);
+}
+
+// Two messages per thread: sorted neighbours 2t and 2t+1 (same alignment
+// class and block count, or adjacent counts, after the q-major windowed
+// sort) compress together while both have full blocks left -- two
+// independent round chains interleaved in one instruction stream, for the
+// dependency stalls that dominate the one-message kernel (ncu: 43 % `wait`).
+// Leftover full blocks and the 1-2 finishing blocks run per message.
+template <int ALG>
+__global__ void __launch_bounds__(128)
+k_varlen16x2(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+             uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t k0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2u;
+    if (k0 >= n) return;
+    const bool two = k0 + 1 < n;
+    const uint64_t i0 = perm ? (uint64_t)perm[k0] : k0;
+    const uint64_t i1 = two ? (perm ? (uint64_t)perm[k0 + 1] : k0 + 1) : i0;
+    const uint64_t len0 = offsets[i0 + 1] - offsets[i0], len1 = offsets[i1 + 1] - offsets[i1];
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(data + (offsets[i0] - offset_base));
+    const uintptr_t a1 = reinterpret_cast<uintptr_t>(data + (offsets[i1] - offset_base));
+    const uint4* w0 = reinterpret_cast<const uint4*>(a0 & ~uintptr_t(15));
+    const uint4* w1 = reinterpret_cast<const uint4*>(a1 & ~uintptr_t(15));
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    if (((a0 + len0 + 15u) & ~uintptr_t(15)) > dend || ((a1 + len1 + 15u) & ~uintptr_t(15)) > dend) {
+        // a message whose last granule straddles the end of the data: bounded loads, one at a time
+        varlen16_message<ALG, 0, true>(w0, a0, len0, dend, out + i0 * H::kDigestBytes);
+        if (two) varlen16_message<ALG, 0, true>(w1, a1, len1, dend, out + i1 * H::kDigestBytes);
+        return;
+    }
+    const uint32_t q0 = (uint32_t)(a0 >> 2) & 3u, sh0 = (uint32_t)(a0 & 3u) * 8u;
+    const uint32_t q1 = (uint32_t)(a1 >> 2) & 3u, sh1 = (uint32_t)(a1 & 3u) * 8u;
+    const bool mis0 = (a0 & 15u) != 0, mis1 = (a1 & 15u) != 0;
+    uint32_t st[2][H::kStateWords];
+    H::init(st[0]);
+    H::init(st[1]);
+    const uint64_t nf0 = len0 >> 6, nf1 = len1 >> 6;
+    const uint64_t nmin = nf0 < nf1 ? nf0 : nf1;
+    uint32_t c0[20], c1[20], raw[2][16];
+    for (uint64_t b = 0; b < nmin; ++b) {
+        load_full_window(w0 + 4 * b, mis0, c0);
+        load_full_window(w1 + 4 * b, mis1, c1);
+        realign16(c0, q0, sh0, raw[0]);
+        realign16(c1, q1, sh1, raw[1]);
+        H::template compress_n<2>(st, raw);
+    }
+    varlen16_rest<ALG, false>(w0, a0, len0, dend, nmin, st[0], out + i0 * H::kDigestBytes);
+    if (two) varlen16_rest<ALG, false>(w1, a1, len1, dend, nmin, st[1], out + i1 * H::kDigestBytes);
+}
+
+// -------------------------------------------------------------------------
+// Variable-length kernel with a warp-uniform block loop.  After the length
+// sort a warp's 32 messages share their block count nb = (len+8)/64 + 1,
+// but not whether the final data bytes and the padding need one block or
+// two (r = len % 64 >= 56 needs two): k_varlen16 runs the full-block loop to
+// len/64 and then md_finish's 1-2 compressions, so a warp with both kinds of
+// lanes executes nb + 1 compressions.  Here every lane runs exactly nb:
+// blocks 0 .. nb-3 are full data blocks for every lane, and the last two go
+// through one branch-free tail body (bytes past the message masked to zero,
+// 0x80 where the message ends, the bit length in the last block) -- one
+// compress call site per loop, no divergence when nb is warp-uniform.
+// V: round variant (1 = the tuned ALU/FMA balance, 2 = every addition on the
+// FMA pipe: the realignment's funnel shifts load the ALU pipe here).
+// -------------------------------------------------------------------------
+template <int ALG, int V, bool EDGE>
+__device__ __forceinline__ void varlen16u_message(const uint4* w16, uintptr_t a, uint64_t len, uintptr_t dend,
+                                                  uint8_t* dout) {
+    using H = HashAlg<ALG, V>;
+    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
+    const bool misaligned = (a & 15u) != 0;
+    uint32_t st[1][H::kStateWords];
+    H::init(st[0]);
+    uint32_t c[20];
+    uint32_t raw[1][16];
+    const uint64_t nb = (len + 8u) / 64u + 1u;
+    const uint64_t nmain = nb >= 2u ? nb - 2u : 0u;  // every lane: full data blocks
+    for (uint64_t b = 0; b < nmain; ++b) {
+        load_full_window(w16 + 4 * b, misaligned, c, EDGE, dend);
+        realign16(c, q, sh, raw[0]);
+        H::template compress_n<1>(st, raw);
+    }
+    const uint64_t bits = len * 8ull;
+    const uint32_t l14 = H::kBigEndian ? bswap((uint32_t)(bits >> 32)) : (uint32_t)bits;
+    const uint32_t l15 = H::kBigEndian ? bswap((uint32_t)bits) : (uint32_t)(bits >> 32);
+    const uintptr_t mend = a + len;
+#pragma unroll 1
+    for (uint64_t k = nmain; k < nb; ++k) {
+        const uint4* src = w16 + 4 * k;
+#pragma unroll
+        for (int kk = 0; kk < 5; ++kk) {  // the chunks that overlap the message's bytes of block k
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (reinterpret_cast<uintptr_t>(src + kk) < mend) v = ld16_edge(src + kk, EDGE, dend);
+            c[4 * kk] = v.x; c[4 * kk + 1] = v.y; c[4 * kk + 2] = v.z; c[4 * kk + 3] = v.w;
+        }
+        realign16(c, q, sh, raw[0]);
+        const int64_t rem = (int64_t)len - 64 * (int64_t)k;  // message bytes from this block's start
+        if (rem < 64) {
+            const uint32_t r = rem > 0 ? (uint32_t)rem : 0u;
+            mask_tail(raw[0], r);
+            const uint32_t pad = rem >= 0 ? 0x80u << ((r & 3u) * 8u) : 0u, pw = r >> 2;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) raw[0][j] |= (pw == (uint32_t)j) ? pad : 0u;
+        }
+        if (k == nb - 1u) { raw[0][14] = l14; raw[0][15] = l15; }
+        H::template compress_n<1>(st, raw);
+    }
+    store_digest<ALG>(dout, st[0]);
+}
+
+template <int ALG, int V>
+__global__ void __launch_bounds__(128)
+k_varlen16u(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = perm ? (uint64_t)perm[t] : t;
+    const uint64_t start = offsets[i] - offset_base;
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
+    const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    if (((a + len + 15u) & ~uintptr_t(15)) > dend)
+        varlen16u_message<ALG, V, true>(w16, a, len, dend, out + i * H::kDigestBytes);
+    else
+        varlen16u_message<ALG, V, false>(w16, a, len, dend, out + i * H::kDigestBytes);
+}
+
+// -------------------------------------------------------------------------
+// Realignment on the FMA pipe (ALU-bound SHA-1 / SM3).  The funnel shifts of
+// realign16 are ALU-pipe ops, 16 per block, on top of an ALU pipe the
+// compression already keeps ~95 % busy.  Here the window is based at the
+// granule holding byte a-1, so the shift s = 8 * ((a-1) % 4) + 8 lies in
+// 8..32 and never is 0, and word j = (c[j+q+1]:c[j+q]) >> s =
+// umulhi(c[j+q], m) + c[j+q+1] * m with m = 2^(32-s): one IMAD.HI (with the
+// addend) and one IMAD, both FMA-pipe.  The word class q = ((a-1) >> 2) % 4
+// must be warp-uniform, so the length sort keys on a-1 (bias shifted by one).
+// -------------------------------------------------------------------------
+__device__ __forceinline__ void realign16m(const uint32_t (&c)[20], uint32_t q, uint32_t m, uint32_t (&raw)[16]) {
+#define HB_RM(Q) \
+    _Pragma("unroll") for (int j = 0; j < 16; ++j) raw[j] = __umulhi(c[j + Q], m) + c[j + Q + 1] * m;
+    switch (q) {
+    case 0: HB_RM(0) break;
+    case 1: HB_RM(1) break;
+    case 2: HB_RM(2) break;
+    default: HB_RM(3) break;
+    }
+#undef HB_RM
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(128)
+k_varlen16m(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = perm ? (uint64_t)perm[t] : t;
+    const uint64_t start = offsets[i] - offset_base;
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    uint8_t* dout = out + i * H::kDigestBytes;
+    const uintptr_t wb = (a - 1u) & ~uintptr_t(15);
+    if (wb < reinterpret_cast<uintptr_t>(data) || ((a + len + 15u) & ~uintptr_t(15)) > dend || (len >> 38)) {
+        // a message at the very start (its window would begin before the data) or at the end
+        varlen16_message<ALG, 0, true>(reinterpret_cast<const uint4*>(a & ~uintptr_t(15)), a, len, dend, dout);
+        return;
+    }
+    const uint4* w = reinterpret_cast<const uint4*>(wb);
+    const uint32_t q = (uint32_t)((a - 1u) >> 2) & 3u;
+    // m = 2^(32 - s), s = 8 ((a-1) % 4) + 8, read from constant memory: a shift
+    // ptxas can see is a power of two would be strength-reduced back to SHF
+    const uint32_t m = c_opaque[24u - 8u * ((uint32_t)(a - 1u) & 3u)];
+    const uint32_t nfull = (uint32_t)(len >> 6);
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    uint32_t c[20], raw[16];
+    for (uint32_t b = 0; b < nfull; ++b) {
+        const uint4* src = w + 4 * (uint64_t)b;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const uint4 v = __ldg(src + k);
+            c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+        }
+        realign16m(c, q, m, raw);
+        compress1<ALG>(st, raw);
+    }
+    const uint32_t r = (uint32_t)(len & 63u);
+    const uintptr_t tail_end = a + len;
+    const uint4* src = w + 4 * (uint64_t)nfull;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const uint4 v = ld16_pred(src + k, reinterpret_cast<uintptr_t>(src + k) < tail_end);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+    realign16m(c, q, m, raw);
+    mask_tail(raw, r);
+    md_finish<ALG>(st, raw, r, len);
+    store_digest<ALG>(dout, st);
+}
+
+// -------------------------------------------------------------------------
+// Lean loop unrolled by two with the shared granule carried: window b+1's
+// first granule is window b's fifth, so after the first window every block
+// loads four granules instead of five (-20 % L1 wavefronts), and the loop
+// bookkeeping and the realignment switch's branches are paid once per two
+// blocks.  The carry is a register renaming in the unrolled body (cA[16..19]
+// becomes cB[0..3] and back), not a copy.  Every window's fifth granule is
+// loaded (a 16-byte-aligned message does not use it for its own block), so a
+// message whose last granule ends within 16 bytes of the data end takes the
+// bounded path.  L2 policies as in k_varlen16l<.., HINT>.
+// -------------------------------------------------------------------------
+__device__ __forceinline__ void load_granules_1to4(const uint4* src, uint32_t (&c)[20]) {
+#pragma unroll
+    for (int k = 1; k < 5; ++k) {
+        const uint4 v = __ldg(src + k);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(128)
+k_varlen16c(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = perm ? (uint64_t)perm[t] : t;
+    const uint64_t start = offsets[i] - offset_base;
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
+    const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    uint8_t* dout = out + i * H::kDigestBytes;
+    if (((a + len + 15u) & ~uintptr_t(15)) + 16u > dend || (len >> 38)) {  // near the data end, or > 2^32 blocks
+        varlen16_message<ALG, 1, true>(w16, a, len, dend, dout);
+        return;
+    }
+    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
+    const uint32_t nfull = (uint32_t)(len >> 6);
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    uint32_t cA[20], cB[20], raw[16];
+    if (nfull) load_window5_hint(w16, 1u, cA, policy_evict_last());
+    uint32_t b = 0;
+    for (; b + 2 <= nfull; b += 2) {
+        realign16(cA, q, sh, raw);
+        cB[0] = cA[16]; cB[1] = cA[17]; cB[2] = cA[18]; cB[3] = cA[19];
+        load_granules_1to4(w16 + 4 * (b + 1), cB);  // block b+1 is full
+        compress1<ALG>(st, raw);
+        realign16(cB, q, sh, raw);
+        if (b + 2 < nfull) {
+            cA[0] = cB[16]; cA[1] = cB[17]; cA[2] = cB[18]; cA[3] = cB[19];
+            load_granules_1to4(w16 + 4 * (b + 2), cA);
+        }
+        compress1<ALG>(st, raw);
+    }
+    if (b < nfull) {  // an odd block count: the last full block's window is in cA
+        realign16(cA, q, sh, raw);
+        compress1<ALG>(st, raw);
+    }
+    const uint32_t r = (uint32_t)(len & 63u);
+    const uintptr_t tail_end = a + len;
+    const uint4* src = w16 + 4 * (uint64_t)nfull;
+    uint32_t c[20];
+    const uint64_t pol_tail = policy_evict_first();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const uint4 v = ld16_pred_hint(src + k, reinterpret_cast<uintptr_t>(src + k) < tail_end, pol_tail);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+    realign16(c, q, sh, raw);
+    mask_tail(raw, r);
+    md_finish<ALG>(st, raw, r, len);
+    store_digest<ALG>(dout, st);
+}
+
+// -------------------------------------------------------------------------
+// Lean block loop with a uniform finish.  A message of block count nb (data
+// + 0x80 + length) needs nb compressions, but k_varlen16(l) runs its full-
+// block loop to len/64 and then md_finish's one or two: a lane whose last
+// r = len % 64 bytes are >= 56 has one full block fewer and one tail block
+// more, so a warp holding both kinds (nearly every warp: P(r >= 56) = 1/8 per
+// lane) executes nb + 1 compressions.  Here every lane runs nb - 1 loop
+// iterations -- the r >= 56 lanes' partial block, with its 0x80, is the last
+// one, masked in place (a branch taken once per message) -- and then one
+// final block: the remaining data, 0x80 (r < 56) and the bit length.  The
+// window after the last full block is loaded with per-granule predicates
+// (never past the message's last granule).
+// -------------------------------------------------------------------------
+__device__ __forceinline__ void load_window_tail(const uint4* src, uintptr_t tail_end, uint32_t (&c)[20]) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const uint4 v = ld16_pred(src + k, reinterpret_cast<uintptr_t>(src + k) < tail_end);
+        c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+    }
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(128)
+k_varlen16f(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint64_t* __restrict__ offsets,
+            uint64_t offset_base, const uint32_t* __restrict__ perm, uint64_t n, uint8_t* __restrict__ out) {
+    using H = HashAlg<ALG>;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t i = perm ? (uint64_t)perm[t] : t;
+    const uint64_t start = offsets[i] - offset_base;
+    const uint64_t len = offsets[i + 1] - offsets[i];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
+    const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
+    const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
+    uint8_t* dout = out + i * H::kDigestBytes;
+    if (((a + len + 15u) & ~uintptr_t(15)) > dend || (len >> 38)) {  // the batch's last bytes, or > 2^32 blocks
+        varlen16_message<ALG, 1, true>(w16, a, len, dend, dout);
+        return;
+    }
+    const uint32_t q = (uint32_t)(a >> 2) & 3u, sh = (uint32_t)(a & 3u) * 8u;
+    const uint32_t mis = (a & 15u) != 0;
+    const uint32_t nfull = (uint32_t)(len >> 6), r = (uint32_t)(len & 63u);
+    const uint32_t nmain = nfull + (r >= 56u ? 1u : 0u);  // every block but the final one
+    const uint32_t pad = 0x80u << ((r & 3u) * 8u), pw = r >> 2;
+    const uintptr_t tail_end = a + len;
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    uint32_t c[20], raw[16];
+    if (nfull) load_window5(w16, mis, c);
+    else load_window_tail(w16, tail_end, c);
+    for (uint32_t b = 0; b < nmain; ++b) {
+        realign16(c, q, sh, raw);
+        if (b + 1 < nfull) load_window5(w16 + 4 * (b + 1), mis, c);
+        else load_window_tail(w16 + 4 * (b + 1), tail_end, c);
+        if (b == nfull) {  // r >= 56: the partial data block carries the 0x80
+            mask_tail(raw, r);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) raw[j] |= (pw == (uint32_t)j) ? pad : 0u;
+        }
+        compress1<ALG>(st, raw);
+    }
+    // final block: r < 56 -> the last r data bytes, 0x80 and the length; r >= 56 -> zeros and the length
+    realign16(c, q, sh, raw);
+    mask_tail(raw, r < 56u ? r : 0u);
+    if (r < 56u) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) raw[j] |= (pw == (uint32_t)j) ? pad : 0u;
+    }
+    const uint64_t bits = len * 8ull;
+    raw[14] = H::kBigEndian ? bswap((uint32_t)(bits >> 32)) : (uint32_t)bits;
+    raw[15] = H::kBigEndian ? bswap((uint32_t)bits) : (uint32_t)(bits >> 32);
+    compress1<ALG>(st, raw);
+    store_digest<ALG>(dout, st);
+}
+
 template <int ALG, int V, int NB, int STAGES, int W = kTmaWarps>
 __global__ void __launch_bounds__(W * 32, (TmaOcc<ALG, NB, STAGES, W>::kMinCtas))
 k_fixed_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out) {
