@@ -826,8 +826,7 @@ enum TmaCfgId { kCfg1x3 = 0, kCfg2x2 = 1, kCfg2x3 = 2, kCfgWs2 = 3, kCfgWs3 = 4,
                 // mid-size batch (2^16 messages, 3.46 warps per scheduler at NB = 1) as
                 // <= 1 warp per scheduler carrying NB independent round chains
                 kCfgW1x1 = 11, kCfgW1x2 = 12, kCfgW1x4 = 13, kCfgW1x4s2 = 14, kCfgW1x2p = 15, kCfgWs3v6 = 16, kCfgW1x2s4 = 17,
-                kCfgW1x2s2 = 18, kCfgW1x3 = 19, kCfgW1x4p = 20,
-                kCfgW1x3r1 = 21, kCfgW1x3r2 = 22, kCfgW1x2r1 = 23, kCfgW1x2r2 = 24 };
+                kCfgW1x2s2 = 18, kCfgW1x3 = 19, kCfgW1x4p = 20 };
 
 template <int ALG, int V, int NB, int STAGES, int W = kTmaWarps>
 static cudaError_t launch_fixed_tma_alg(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
@@ -896,18 +895,6 @@ static cudaError_t launch_tma_ab(const uint8_t* src, uint32_t n, uint32_t L, uin
     case kCfgW1x3:
         if constexpr (ALG == kMd5) return launch_fixed_tma_w1<ALG, 6, 3, 3>(src, n, L, dst, s);
         return launch_fixed_tma_w1<ALG, 1, 3, 3>(src, n, L, dst, s);
-    case kCfgW1x3r1:  // refill-order arms of the shipping tile (see k_fixed_tma_w1's RF)
-        if constexpr (ALG == kMd5) return launch_fixed_tma_w1<ALG, 6, 3, 3, 1>(src, n, L, dst, s);
-        return launch_fixed_tma_w1<ALG, 1, 3, 3, 1>(src, n, L, dst, s);
-    case kCfgW1x3r2:
-        if constexpr (ALG == kMd5) return launch_fixed_tma_w1<ALG, 6, 3, 3, 2>(src, n, L, dst, s);
-        return launch_fixed_tma_w1<ALG, 1, 3, 3, 2>(src, n, L, dst, s);
-    case kCfgW1x2r1:
-        if constexpr (ALG == kMd5) return launch_fixed_tma_w1<ALG, 6, 2, 3, 1>(src, n, L, dst, s);
-        return launch_fixed_tma_w1<ALG, 1, 2, 3, 1>(src, n, L, dst, s);
-    case kCfgW1x2r2:
-        if constexpr (ALG == kMd5) return launch_fixed_tma_w1<ALG, 6, 2, 3, 2>(src, n, L, dst, s);
-        return launch_fixed_tma_w1<ALG, 1, 2, 3, 2>(src, n, L, dst, s);
     case kCfgW1x4p:  // shipping single-warp kernel, 4 messages per thread
         if constexpr (ALG == kMd5) return launch_fixed_tma_w1<ALG, 6, 4, 3>(src, n, L, dst, s);
         return launch_fixed_tma_w1<ALG, 1, 4, 3>(src, n, L, dst, s);

@@ -62,7 +62,7 @@ static Tuning parse_tuning() {
     if (const char* v = getenv("HB_VARLEN_SORT")) t.varlen_sort = strcmp(v, "global") == 0 ? 0 : 1;
 #ifdef HB_AB
     static const char* const kCfgNames[] = {"1x3", "2x2", "2x3", "ws2", "ws3", "1x2", "ws2x2", "ws3x2",
-                                            "ws3u", "ws3x2u", "ws3n", "w1x1", "w1x2", "w1x4", "w1x4s2", "w1x2p", "ws3v6", "w1x2s4", "w1x2s2", "w1x3", "w1x4p", "w1x3r1", "w1x3r2", "w1x2r1", "w1x2r2"};
+                                            "ws3u", "ws3x2u", "ws3n", "w1x1", "w1x2", "w1x4", "w1x4s2", "w1x2p", "ws3v6", "w1x2s4", "w1x2s2", "w1x3", "w1x4p"};
     if (const char* v = getenv("HB_TMA_CFG"))
         for (int k = 0; k < (int)(sizeof kCfgNames / sizeof *kCfgNames); ++k)
             if (!strcmp(v, kCfgNames[k])) t.tma_cfg = k;

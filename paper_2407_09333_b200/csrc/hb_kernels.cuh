@@ -294,14 +294,7 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
 // count there lengthens the critical path.  Programmatic dependent launch
 // and early loads as in k_fixed_tma_ws.
 // -------------------------------------------------------------------------
-// RF (stage refill, A/B): 0 = lane 0 refills right after the warp has read
-// the stage, behind a proxy fence (fence.proxy.async: MEMBAR.ALL.CTA +
-// FENCE.VIEW.ASYNC, the warp waits for lane 0's shared loads); 1 = the same
-// slot, no fence -- the refill's expect_tx is made to depend on the loaded
-// words, which orders lane 0's reads, __syncwarp the other lanes'; 2 = refill
-// after the compression (the loads are long consumed; one block less
-// lookahead).
-template <int ALG, int V, int NB, int STAGES, int RF = 0>
+template <int ALG, int V, int NB, int STAGES>
 __global__ void __launch_bounds__(32, (TmaOcc<ALG, NB, STAGES, 1>::kMinCtas))
 k_fixed_tma_w1(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t msg_len, uint8_t* __restrict__ out,
                uint32_t early) {
@@ -369,23 +362,12 @@ k_fixed_tma_w1(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
         mbar_wait_parity(&bars[stage], phase);
         read_stage(stage);
         __syncwarp();  // every lane has its registers: the stage may be refilled
-        if (RF != 2 && lane == 0 && b + STAGES < nload) {
-            uint32_t bytes = C::kStageBytes;
-            if (RF == 0) fence_proxy_async_smem();
-            else bytes += raw[0][0] & (blockIdx.x >> 31);  // + 0, but only once lane 0's loads are back
-            mbar_arrive_expect_tx(&bars[stage], bytes);
+        if (lane == 0 && b + STAGES < nload) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&bars[stage], C::kStageBytes);
             tma_load_2d(ring + stage * C::kStageBytes, &tmap, &bars[stage], (int)((b + STAGES) * 64u), (int)row0);
         }
         H::template compress_n<NB>(st, raw);
-        if (RF == 2) {
-            __syncwarp();
-            if (lane == 0 && b + STAGES < nload) {
-                fence_proxy_async_smem();
-                mbar_arrive_expect_tx(&bars[stage], C::kStageBytes);
-                tma_load_2d(ring + stage * C::kStageBytes, &tmap, &bars[stage], (int)((b + STAGES) * 64u),
-                            (int)row0);
-            }
-        }
         if (++stage == (uint32_t)STAGES) { stage = 0; phase ^= 1u; }
     }
     const uint32_t r = msg_len & 63u;
@@ -1279,7 +1261,7 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     return cudaGetLastError();
 }
 
-template <int ALG, int V, int NB, int STAGES, int RF = 0>
+template <int ALG, int V, int NB, int STAGES>
 static cudaError_t launch_fixed_tma_w1(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
                                        cudaStream_t stream, bool input_ready = false) {
     using C = TmaCfg<NB, STAGES, 1>;
@@ -1289,7 +1271,7 @@ static cudaError_t launch_fixed_tma_w1(const uint8_t* d_msgs, uint32_t n, uint32
     if (e != cudaSuccess) return e;
     static std::atomic<uint64_t> attr_done{0};
     e = set_smem_attr_once(attr_done, [] {
-        return cudaFuncSetAttribute(k_fixed_tma_w1<ALG, V, NB, STAGES, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        return cudaFuncSetAttribute(k_fixed_tma_w1<ALG, V, NB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     C::kSmem);
     });
     if (e != cudaSuccess) return e;
@@ -1298,7 +1280,7 @@ static cudaError_t launch_fixed_tma_w1(const uint8_t* d_msgs, uint32_t n, uint32
     int dev = 0, occ = 0;
     if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) occ = occ_cache[dev].load(std::memory_order_relaxed);
     if (!occ) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fixed_tma_w1<ALG, V, NB, STAGES, RF>, 32, C::kSmem) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fixed_tma_w1<ALG, V, NB, STAGES>, 32, C::kSmem) !=
                 cudaSuccess || occ <= 0)
             occ = TmaOcc<ALG, NB, STAGES, 1>::kMinCtas;
         if (dev >= 0 && dev < 64) occ_cache[dev].store(occ, std::memory_order_relaxed);
@@ -1307,7 +1289,7 @@ static cudaError_t launch_fixed_tma_w1(const uint8_t* d_msgs, uint32_t n, uint32
     const bool pdl = grid >= (uint32_t)device_sms() || (L + 8u) / 64u + 1u <= 17u;  // as launch_fixed_tma_ws
     const uint32_t half_wave = (uint32_t)device_sms() * (uint32_t)occ / 2u;
     const uint32_t early = input_ready && pdl && T.pdl ? kEarlyLoad | (grid <= half_wave ? kEarlyTrigger : 0u) : 0u;
-    launch_pdl_smem(k_fixed_tma_w1<ALG, V, NB, STAGES, RF>, grid, 32, C::kSmem, stream, pdl, map, n, L, d_out, early);
+    launch_pdl_smem(k_fixed_tma_w1<ALG, V, NB, STAGES>, grid, 32, C::kSmem, stream, pdl, map, n, L, d_out, early);
     return cudaGetLastError();
 }
 
