@@ -127,6 +127,13 @@ template <int ALG, int NB, int STAGES, int W = kTmaWarps> struct TmaOcc {  // CT
 constexpr int kWsComputeWarps = 4;
 constexpr uint32_t kEarlyLoad = 1u;     // read the messages before griddepcontrol.wait (HB_FLAG_INPUT_READY)
 constexpr uint32_t kEarlyTrigger = 2u;  // release the next grid right after griddepcontrol.wait
+// kLateWait (with kEarlyLoad, HB_FLAG_INPUT_READY): compute before
+// griddepcontrol.wait, wait only before the digest stores.  Under the flag the
+// previous grid writes none of this grid's inputs, so the only ordering left
+// is on `out` (this grid's stores after everything the previous one did), and
+// consecutive batches then compute concurrently -- a batch too small to fill
+// the GPU (2^16 messages: 3.5 warps per scheduler) overlaps its successor.
+constexpr uint32_t kLateWait = 4u;
 // SLACK: reserve 1 KiB to align the ring to 1024 B at run time.  Without it
 // (the dynamic window of a kernel with no static shared memory starts 1 KiB
 // aligned -- checked in-kernel) a 3-stage CTA needs 24 KiB and 9 CTAs fit an
@@ -188,7 +195,7 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
             tma_load_2d(ring + b * C::kStageBytes, &tmap, &full[b], (int)(b * 64u), (int)row0);
         }
     }
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (!(early & kLateWait)) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (early & kEarlyTrigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == kWsComputeWarps) {  // ---------------- producer warp
@@ -273,6 +280,7 @@ k_fixed_tma_ws(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
     }
     md_finish_n<ALG, V, NB>(st, raw, r, msg_len);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (early & kLateWait) asm volatile("griddepcontrol.wait;" ::: "memory");
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
         const uint32_t grow = row0 + row + 128u * q;
@@ -320,7 +328,7 @@ k_fixed_tma_w1(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
             }
         }
     }
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (!(early & kLateWait)) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (early & kEarlyTrigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (lane == 0 && !(early & kEarlyLoad)) {
         prefetch_tmap(&tmap);
@@ -382,6 +390,7 @@ k_fixed_tma_w1(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t ms
     }
     md_finish_n<ALG, V, NB>(st, raw, r, msg_len);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (early & kLateWait) asm volatile("griddepcontrol.wait;" ::: "memory");
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
         const uint32_t row = row0 + lane + 32u * q;
@@ -474,7 +483,7 @@ __global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__
             w[q][4 * c] = v.x; w[q][4 * c + 1] = v.y; w[q][4 * c + 2] = v.z; w[q][4 * c + 3] = v.w;
         }
     }
-    if (early & kEarlyLoad) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if ((early & kEarlyLoad) && !(early & kLateWait)) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (early & kEarlyTrigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     uint32_t st[NB][H::kStateWords];
 #pragma unroll
@@ -497,6 +506,7 @@ __global__ void __launch_bounds__(128) k_fixed_small(const uint8_t* __restrict__
             H::template compress_n<NB>(st, raw);
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (early & kLateWait) asm volatile("griddepcontrol.wait;" ::: "memory");
 #pragma unroll
     for (int q = 0; q < NB; ++q)
         if (i0 + q < n) store_digest<ALG>(out + (i0 + q) * H::kDigestBytes, st[q]);
@@ -1255,7 +1265,9 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     // The next grid may be released early only if it fits beside this one:
     // at most half the CTA slots of every SM.
     const uint32_t half_wave = (uint32_t)device_sms() * (uint32_t)WsOcc<ALG, NB, STAGES, SLACK>::kMinCtas / 2u;
-    const uint32_t early = input_ready && pdl && T.pdl ? kEarlyLoad | (grid <= half_wave ? kEarlyTrigger : 0u) : 0u;
+    const uint32_t early = input_ready && pdl && T.pdl
+                               ? kEarlyLoad | (grid <= half_wave ? kEarlyTrigger : 0u) | (T.late_wait ? kLateWait : 0u)
+                               : 0u;
     launch_pdl_smem(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK>, grid, (kWsComputeWarps + 1) * 32, C::kSmem,
                     stream, pdl, map, n, L, d_out, (uint32_t)T.tma_evict_first, early);
     return cudaGetLastError();
@@ -1288,7 +1300,9 @@ static cudaError_t launch_fixed_tma_w1(const uint8_t* d_msgs, uint32_t n, uint32
     const uint32_t grid = (n + C::kRows - 1) / C::kRows;
     const bool pdl = grid >= (uint32_t)device_sms() || (L + 8u) / 64u + 1u <= 17u;  // as launch_fixed_tma_ws
     const uint32_t half_wave = (uint32_t)device_sms() * (uint32_t)occ / 2u;
-    const uint32_t early = input_ready && pdl && T.pdl ? kEarlyLoad | (grid <= half_wave ? kEarlyTrigger : 0u) : 0u;
+    const uint32_t early = input_ready && pdl && T.pdl
+                               ? kEarlyLoad | (grid <= half_wave ? kEarlyTrigger : 0u) | (T.late_wait ? kLateWait : 0u)
+                               : 0u;
     launch_pdl_smem(k_fixed_tma_w1<ALG, V, NB, STAGES>, grid, 32, C::kSmem, stream, pdl, map, n, L, d_out, early);
     return cudaGetLastError();
 }
@@ -1340,7 +1354,8 @@ static void launch_small(const uint8_t* d_msgs, uint64_t n, uint8_t* d_out, cuda
     // early start (see k_fixed_small): the next grid is released early only
     // when it fits beside this one (<= 8 of the SM's 16 CTA slots).
     const auto early = [&](unsigned grid) -> uint32_t {
-        return input_ready && tuning().pdl ? kEarlyLoad | (grid <= 8u * (unsigned)device_sms() ? kEarlyTrigger : 0u)
+        return input_ready && tuning().pdl ? kEarlyLoad | (grid <= 8u * (unsigned)device_sms() ? kEarlyTrigger : 0u) |
+                                                 (tuning().late_wait ? kLateWait : 0u)
                                            : 0u;
     };
     if constexpr (ALG == kMd5 && L <= 32) {

@@ -652,6 +652,41 @@ def test_fixed_hash_graph_replay():
             assert np.array_equal(out.cpu().numpy()[rows], oracle.batch_fixed(alg, sample)), (alg, seed)
 
 
+@pytest.mark.parametrize("late", ["1", "0"])
+def test_input_ready_shared_out_order(late, hb_env):
+    """HB_FLAG_INPUT_READY launches compute before griddepcontrol.wait
+    ($HB_LATE_WAIT=1: consecutive batches overlap) and store only after it, so
+    back-to-back launches over DIFFERENT inputs into the SAME digest buffer
+    leave exactly the last launch's digests -- for the compile-time-width
+    kernel, the 4+1-warp tile and the single-warp tiles (2 and 3 messages per
+    thread), sub-wave grids (released at entry) and multi-wave ones."""
+    import torch
+
+    from paper_2407_09333_b200 import device
+
+    hb_env.set(HB_LATE_WAIT=late)
+    flag = _native.HB_FLAG_INPUT_READY
+    for alg, n, L, env in (("sha1", 65536, 64, {}), ("md5", 20000, 1024, {}), ("md5", 70000, 1024, {}),
+                           ("md5", 300000, 256, {}), ("md5", 70000, 320, {"HB_MD5_NB3_N": "0"}),
+                           ("sm3", 9000, 512, {})):
+        hb_env.set(HB_LATE_WAIT=late, **env)
+        d = {"sha1": 20, "md5": 16, "sm3": 32}[alg]
+        copies = []
+        for k in range(6):
+            b = torch.empty(n * L, dtype=torch.uint8, device="cuda:0")
+            device.fill_random(b, 300 + k)
+            copies.append(b.view(n, L))
+        out = torch.empty((n, d), dtype=torch.uint8, device="cuda:0")
+        torch.cuda.synchronize()
+        for rep in range(3):
+            for c in copies:
+                device.hash_fixed(alg, c, out=out, flags=flag)
+        torch.cuda.synchronize()
+        full = oracle.batch_fixed(alg, copies[-1].cpu().numpy(), threads=8)
+        assert np.array_equal(out.cpu().numpy(), full), (alg, n, L, env, late)
+        hb_env.clear(*env)
+
+
 def test_input_ready_early_start():
     """HB_FLAG_INPUT_READY: back-to-back launches over rotating, already
     written inputs start reading before the previous grid completes (early

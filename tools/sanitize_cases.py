@@ -20,7 +20,7 @@ from paper_2407_09333_b200 import _native, device  # noqa: E402
 ALGS = ("sha1", "md5", "sm3")
 ENV_KEYS = ("HB_TMA_CFG", "HB_SMALL_N", "HB_DIRECT_MAX_L", "HB_NO_SMALL_KERNEL", "HB_VARLEN_SORT", "HB_VARLEN_LD",
             "HB_VARLEN_BULK", "HB_VARLEN_PREFETCH", "HB_VC_STAGES", "HB_CHAIN_N", "HB_SORT_QMAJOR", "HB_VARLEN_PF",
-            "HB_VARLEN_KERNEL", "HB_MD5_NB3_N")
+            "HB_VARLEN_KERNEL", "HB_MD5_NB3_N", "HB_LATE_WAIT")
 
 
 def with_env(env):
@@ -76,7 +76,7 @@ def main():
             cases += 1
     # MD5's single-warp two-messages-per-thread tile at any batch size, flagged
     # (early loads before griddepcontrol.wait) and unflagged
-    for env in ({"HB_CHAIN_N": "0"}, {"HB_CHAIN_N": "0", "HB_MD5_NB3_N": "0"}):
+    for env in ({"HB_CHAIN_N": "0"}, {"HB_CHAIN_N": "0", "HB_MD5_NB3_N": "0"}, {"HB_LATE_WAIT": "0"}):
         with_env(env)
         for alg in ALGS:
             for n, L in ((3000, 1024), (700, 1040), (129, 144)):
