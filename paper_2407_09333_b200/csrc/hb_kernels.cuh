@@ -1241,6 +1241,20 @@ static cudaError_t encode_rows_map_uncached(CUtensorMap* map, const uint8_t* d_m
     return cudaSuccess;
 }
 
+// Resident CTAs per SM of `kernel` at this launch shape (the occupancy API,
+// cached per device in `cache`; `fallback` if the query fails).
+template <class K>
+static int resident_ctas(K kernel, int threads, size_t smem, int fallback, std::atomic<int> (&cache)[64]) {
+    int dev = 0, occ = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) occ = cache[dev].load(std::memory_order_relaxed);
+    if (!occ) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess || occ <= 0)
+            occ = fallback;
+        if (dev >= 0 && dev < 64) cache[dev].store(occ, std::memory_order_relaxed);
+    }
+    return occ;
+}
+
 template <int ALG, int V, int NB, int STAGES, bool UNR = false, bool SLACK = true>
 static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32_t L, uint8_t* d_out,
                                        cudaStream_t stream, bool input_ready = false) {
@@ -1263,8 +1277,11 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     // launch normally.
     const bool pdl = grid >= (uint32_t)device_sms() || (L + 8u) / 64u + 1u <= 17u;
     // The next grid may be released early only if it fits beside this one:
-    // at most half the CTA slots of every SM.
-    const uint32_t half_wave = (uint32_t)device_sms() * (uint32_t)WsOcc<ALG, NB, STAGES, SLACK>::kMinCtas / 2u;
+    // at most $HB_TRIGGER_WAVE_PCT (50) % of the SMs' resident CTA slots.
+    static std::atomic<int> occ_cache[64];
+    const int occ = resident_ctas(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK>, (kWsComputeWarps + 1) * 32,
+                                  C::kSmem, WsOcc<ALG, NB, STAGES, SLACK>::kMinCtas, occ_cache);
+    const uint32_t half_wave = (uint32_t)((uint64_t)device_sms() * (uint64_t)occ * T.trigger_wave_pct / 100u);
     const uint32_t early = input_ready && pdl && T.pdl
                                ? kEarlyLoad | (grid <= half_wave ? kEarlyTrigger : 0u) | (T.late_wait ? kLateWait : 0u)
                                : 0u;
@@ -1289,17 +1306,11 @@ static cudaError_t launch_fixed_tma_w1(const uint8_t* d_msgs, uint32_t n, uint32
     if (e != cudaSuccess) return e;
     // resident CTAs per SM (shared memory bounds it, ~17 at 3 stages), queried once per device
     static std::atomic<int> occ_cache[64];
-    int dev = 0, occ = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) occ = occ_cache[dev].load(std::memory_order_relaxed);
-    if (!occ) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fixed_tma_w1<ALG, V, NB, STAGES>, 32, C::kSmem) !=
-                cudaSuccess || occ <= 0)
-            occ = TmaOcc<ALG, NB, STAGES, 1>::kMinCtas;
-        if (dev >= 0 && dev < 64) occ_cache[dev].store(occ, std::memory_order_relaxed);
-    }
+    const int occ = resident_ctas(k_fixed_tma_w1<ALG, V, NB, STAGES>, 32, C::kSmem,
+                                  TmaOcc<ALG, NB, STAGES, 1>::kMinCtas, occ_cache);
     const uint32_t grid = (n + C::kRows - 1) / C::kRows;
     const bool pdl = grid >= (uint32_t)device_sms() || (L + 8u) / 64u + 1u <= 17u;  // as launch_fixed_tma_ws
-    const uint32_t half_wave = (uint32_t)device_sms() * (uint32_t)occ / 2u;
+    const uint32_t half_wave = (uint32_t)((uint64_t)device_sms() * (uint64_t)occ * T.trigger_wave_pct / 100u);
     const uint32_t early = input_ready && pdl && T.pdl
                                ? kEarlyLoad | (grid <= half_wave ? kEarlyTrigger : 0u) | (T.late_wait ? kLateWait : 0u)
                                : 0u;
@@ -1352,9 +1363,11 @@ template <int ALG, int L>
 static void launch_small(const uint8_t* d_msgs, uint64_t n, uint8_t* d_out, cudaStream_t s, bool input_ready) {
     constexpr unsigned kBlk = 128;
     // early start (see k_fixed_small): the next grid is released early only
-    // when it fits beside this one (<= 8 of the SM's 16 CTA slots).
+    // when it fits beside this one ($HB_TRIGGER_WAVE_PCT of the SM's 16 CTA slots: 8).
     const auto early = [&](unsigned grid) -> uint32_t {
-        return input_ready && tuning().pdl ? kEarlyLoad | (grid <= 8u * (unsigned)device_sms() ? kEarlyTrigger : 0u) |
+        return input_ready && tuning().pdl ? kEarlyLoad |
+                                                 (grid <= 16u * tuning().trigger_wave_pct / 100u * (unsigned)device_sms()
+                                                      ? kEarlyTrigger : 0u) |
                                                  (tuning().late_wait ? kLateWait : 0u)
                                            : 0u;
     };
