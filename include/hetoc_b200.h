@@ -62,9 +62,9 @@ typedef enum { HB_SHA1 = 0, HB_MD5 = 1, HB_SM3 = 2 } hb_alg;
 /* fixed width, hb_hash_fixed_dev: the caller guarantees the message bytes are
  * not written by the kernel that immediately precedes this launch on the
  * stream (e.g. they were copied in, or written earlier and synchronised).
- * The hash kernel then starts reading them while that kernel drains
- * (programmatic dependent launch); digests are still written only after it
- * completes.  (The engine's own chunks follow their H2D copy, which a
+ * The hash kernel then starts -- reading and hashing its messages -- while
+ * that kernel is still running (programmatic dependent launch): consecutive
+ * batches overlap; only the digest stores wait until it completes.  (The engine's own chunks follow their H2D copy, which a
  * dependent launch never overlaps, so it does not need it.)
  * varlen, hb_hash_varlen_dev (MD5's windowed length sort): the same guarantee
  * for `offsets` -- the sort then starts while the preceding varlen hash

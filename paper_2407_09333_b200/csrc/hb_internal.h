@@ -27,7 +27,7 @@ struct Tuning {
     uint64_t small_n = 1ull << 18;              // $HB_SMALL_N: below it, one message per thread in TMA tiles
     uint64_t chain_n = 1ull << 16;              // $HB_CHAIN_N: MD5 TMA batches below it: 4+1-warp tile, variant 6
     bool late_wait = true;                      // $HB_LATE_WAIT: INPUT_READY launches wait only before their stores
-    uint32_t trigger_wave_pct = 50;             // $HB_TRIGGER_WAVE_PCT: early release if the grid fits this share of the slots
+    uint32_t trigger_wave_pct = 100;            // $HB_TRIGGER_WAVE_PCT: early release if the grid fits this share of the slots
     uint64_t md5_nb3_n = 1ull << 22;            // $HB_MD5_NB3_N: from it, three messages per thread in the single-warp tile
     bool varlen_pf = true;                      // $HB_VARLEN_PF: MD5 varlen, software-pipelined per-thread kernel
     bool sort_qmajor = true;                    // $HB_SORT_QMAJOR: windowed sort key (q, block count), else (block count, q)

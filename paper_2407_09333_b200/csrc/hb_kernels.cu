@@ -55,7 +55,7 @@ static Tuning parse_tuning() {
     t.chain_n = env_u64("HB_CHAIN_N", t.chain_n);
     t.md5_nb3_n = env_u64("HB_MD5_NB3_N", t.md5_nb3_n);
     t.late_wait = env_u64("HB_LATE_WAIT", 1) != 0;
-    t.trigger_wave_pct = (uint32_t)env_u64("HB_TRIGGER_WAVE_PCT", 50);
+    t.trigger_wave_pct = (uint32_t)env_u64("HB_TRIGGER_WAVE_PCT", 100);
     t.varlen_pf = env_u64("HB_VARLEN_PF", 1) != 0;
     t.sort_qmajor = env_u64("HB_SORT_QMAJOR", 1) != 0;
     t.direct_max_len = env_u64("HB_DIRECT_MAX_L", t.direct_max_len);

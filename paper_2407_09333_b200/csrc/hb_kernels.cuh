@@ -1276,8 +1276,12 @@ static cudaError_t launch_fixed_tma_ws(const uint8_t* d_msgs, uint32_t n, uint32
     // SM there and run up to 30 % slower (profiles/ab_pdl_r1.txt), so those
     // launch normally.
     const bool pdl = grid >= (uint32_t)device_sms() || (L + 8u) / 64u + 1u <= 17u;
-    // The next grid may be released early only if it fits beside this one:
-    // at most $HB_TRIGGER_WAVE_PCT (50) % of the SMs' resident CTA slots.
+    // The next grid is released early (at entry) if this one is resident in a
+    // single wave: at most $HB_TRIGGER_WAVE_PCT (100) % of the SMs' resident
+    // CTA slots.  With the late wait the released grid computes beside this
+    // one; half a wave (the round-1 rule) kept SM3 / SHA-1's 512-CTA grids of
+    // 2^16 messages out: 0.74 -> 0.92 of the ALU bound at 2^16 x 1 KiB SM3
+    // (profiles/r2/trigger_r2al/).
     static std::atomic<int> occ_cache[64];
     const int occ = resident_ctas(k_fixed_tma_ws<ALG, V, NB, STAGES, UNR, SLACK>, (kWsComputeWarps + 1) * 32,
                                   C::kSmem, WsOcc<ALG, NB, STAGES, SLACK>::kMinCtas, occ_cache);
@@ -1362,8 +1366,9 @@ static cudaError_t launch_tma_dispatch(const uint8_t* src, uint32_t n, uint32_t 
 template <int ALG, int L>
 static void launch_small(const uint8_t* d_msgs, uint64_t n, uint8_t* d_out, cudaStream_t s, bool input_ready) {
     constexpr unsigned kBlk = 128;
-    // early start (see k_fixed_small): the next grid is released early only
-    // when it fits beside this one ($HB_TRIGGER_WAVE_PCT of the SM's 16 CTA slots: 8).
+    // early start (see k_fixed_small): the next grid is released early when
+    // this one is resident in one wave ($HB_TRIGGER_WAVE_PCT of the SM's 16
+    // CTA slots).
     const auto early = [&](unsigned grid) -> uint32_t {
         return input_ready && tuning().pdl ? kEarlyLoad |
                                                  (grid <= 16u * tuning().trigger_wave_pct / 100u * (unsigned)device_sms()
