@@ -668,7 +668,7 @@ def test_input_ready_shared_out_order(late, hb_env):
     flag = _native.HB_FLAG_INPUT_READY
     for alg, n, L, env in (("sha1", 65536, 64, {}), ("md5", 20000, 1024, {}), ("md5", 70000, 1024, {}),
                            ("md5", 300000, 256, {}), ("md5", 70000, 320, {"HB_MD5_NB3_N": "0"}),
-                           ("sm3", 9000, 512, {})):
+                           ("sm3", 9000, 512, {}), ("sm3", 65536, 1024, {})):
         hb_env.set(HB_LATE_WAIT=late, **env)
         d = {"sha1": 20, "md5": 16, "sm3": 32}[alg]
         copies = []
