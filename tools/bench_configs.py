@@ -25,6 +25,7 @@ import hostref  # noqa: E402  (hashlib checker)
 from paper_2407_09333_b200 import _native, device  # noqa: E402
 
 DLEN = {"sha1": 20, "md5": 16, "sm3": 32}
+READY = _native.HB_FLAG_INPUT_READY
 import bench  # noqa: E402  (the same defensive MEASURED_PEAKS.json reader)
 
 PEAK = bench.load_peaks()[0]["hbm_gbs"]
@@ -107,13 +108,15 @@ def fixed_point(alg, n, L, seed, steps, out, tag):
     if n * L <= (64 << 20):
         # launch-bound sizes: CUDA-graph replays of 10 passes over 10 identical
         # copies, L2 flushed before each replay, so every pass reads HBM
+        # (HB_FLAG_INPUT_READY, as bench.py passes it: the inputs are written
+        # before the timed region, never by the preceding kernel)
         copies = [msgs] + [msgs.clone() for _ in range(9)]
-        g = device.FixedHashGraph(alg, copies, dig)
+        g = device.FixedHashGraph(alg, copies, dig, flags=READY)
         ms = timed_cold(g.replay, max(3, steps // 10), 10)
     elif n * L < bench.L2_DEFEAT_BYTES:  # fits (partly) in L2: flush between launches
-        ms = timed_cold(lambda: device.hash_fixed(alg, msgs, out=dig), max(3, steps), 1)
+        ms = timed_cold(lambda: device.hash_fixed(alg, msgs, out=dig, flags=READY), max(3, steps), 1)
     else:  # larger than 2 x L2: back-to-back launches already read HBM
-        ms = timed(lambda: device.hash_fixed(alg, msgs, out=dig), steps)
+        ms = timed(lambda: device.hash_fixed(alg, msgs, out=dig, flags=READY), steps)
     del copies
     rows = np.unique(np.concatenate([np.random.default_rng(seed).integers(0, n, 256), [0, n - 1]]))
     sample = msgs[torch.from_numpy(rows).cuda()].cpu().numpy()

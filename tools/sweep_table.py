@@ -14,7 +14,8 @@ def main():
     other = [r for r in rows if r["config"] != "C5"]
     print(f"# BASELINE configs on 1 B200 ({sys.argv[1].split('/')[-1]})\n")
     print("Kernel-only, inputs resident in HBM and read from HBM at every timed pass (batches under 2 x L2: "
-          "10-copy graph replays with the L2 flushed before each; larger: back-to-back launches), CUDA events; every point's "
+          "10-copy graph replays with the L2 flushed before each; larger: back-to-back launches; launches flagged "
+          "HB_FLAG_INPUT_READY as in bench.py, so consecutive passes overlap), CUDA events; every point's "
           "digests checked against a CPU reference on a row sample (`bit_exact_sample`). Fraction = "
           "max(T_hbm, T_alu, T_chain) / T_measured with T_hbm at the HBM peak (6,650 GB/s fallback unless "
           "MEASURED_PEAKS.json), T_alu = blocks x ALU-only ops / (64 lanes/clk x 148 SMs x clock) and "
