@@ -66,10 +66,10 @@ SURVEY_C_ALG = {"md5": 324, "sha1": 613, "sm3": 1412}
 # Dependent-chain latency of one compression (cycles, one warp per SM: 4,736
 # messages of 64 KiB, profiles/r2/ab_chain_r2d.txt and ab_mid_r2p.txt; the
 # smallest measurement).  MD5 is the round-variant-6 tile the dispatch runs
-# below 2^16 messages (548.4 us for 1,025 blocks at 1,965 MHz; variant 3:
+# below 2^16 messages (544.6 us for 1,025 blocks at 1,965 MHz, the best of the final passes; variant 3:
 # 1,132, variant 1: 1,462-1,509).  A batch with too few messages to overlap
 # cannot finish before (blocks per message) x this.
-CHAIN_CYCLES = {"md5": 1051, "sha1": 1116, "sm3": 2514}
+CHAIN_CYCLES = {"md5": 1044, "sha1": 1116, "sm3": 2514}
 _BACKEND = os.environ.get("HB_BENCH_BACKEND", "nccl")
 
 
@@ -942,6 +942,16 @@ def time_kernel(w, ctx, steps, warmup, min_region_ms=0.0, ramp_ms=0.0):
     return ms_local, ms, launches, clk, t_wall * 1e3 / steps, steps
 
 
+def pdl_overlap(kind, n, blocks_per_msg):
+    """Whether consecutive flagged fixed-width steps overlap on the GPU
+    (HB_FLAG_INPUT_READY + programmatic dependent launch; the engine uses PDL
+    for rows of <= 128 B and for TMA grids of short messages or of at least one
+    CTA per SM).  A stream of such steps is not bound by one batch's
+    dependent chain -- several batches' chains run side by side -- so the
+    chain bound does not enter its roofline."""
+    return kind == "fixed" and (blocks_per_msg <= 17 or n >= 148 * 128)
+
+
 def roofline(w, ctx, ms_local, kernel, name):
     peaks = ctx.peaks
     f_max = peaks.get("sm_max_mhz", 1965.0)
@@ -951,22 +961,25 @@ def roofline(w, ctx, ms_local, kernel, name):
     achieved = w.alg_bytes / t / 1e9
     t_hbm = w.alg_bytes / (peaks["hbm_gbs"] * 1e9)
     t_alu = w.blocks * ops / alu_peak
-    # a batch too small to overlap its messages' dependent chains is bound by one chain
+    # a batch too small to overlap its messages' dependent chains is bound by one
+    # chain -- unless consecutive steps overlap (pdl_overlap), then only HBM / ALU bind
     t_chain = w.blocks_per_msg * CHAIN_CYCLES[w.alg] / (f_max * 1e6)
+    chain_applies = not pdl_overlap(w.kind, getattr(w, "n", 0), w.blocks_per_msg)
+    t_chain_b = t_chain if chain_applies else 0.0
     alu = {"achieved": round(w.blocks * ops / t / 1e12, 3), "peak": round(alu_peak / 1e12, 3), "unit": "Tops/s",
            "frac": round(t_alu / t, 4), "alu_ops_per_block": ops, "blocks_per_launch": w.blocks,
            "clock_mhz": f_max}
-    bound = max((("hbm", t_hbm), ("alu", t_alu), ("chain", t_chain)), key=lambda x: x[1])[0]
+    bound = max((("hbm", t_hbm), ("alu", t_alu), ("chain", t_chain_b)), key=lambda x: x[1])[0]
     if bound == "hbm" or (bound == "chain" and t_hbm >= t_alu):
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved / peaks["hbm_gbs"], 4)}
     else:  # integer (ALU-pipe) bound: report against the ALU-pipe roofline, HBM alongside
         roof = {"bound": "alu", "achieved": alu["achieved"], "peak": alu["peak"], "unit": "Tops/s",
                 "frac": alu["frac"], "hbm_achieved_gbs": round(achieved, 1), "hbm_peak_gbs": peaks["hbm_gbs"]}
-    t_roof = max(t_hbm, t_alu, t_chain)
+    t_roof = max(t_hbm, t_alu, t_chain_b)
     roof["max_bound"] = {"bound": bound, "t_ms": {"hbm": round(t_hbm * 1e3, 5), "alu": round(t_alu * 1e3, 5),
                                                   "chain": round(t_chain * 1e3, 5)},
-                         "frac": round(t_roof / t, 4)}
+                         "chain_applies": chain_applies, "frac": round(t_roof / t, 4)}
     if w.kind != "decimal":  # the survey's per-block counts assume arbitrary message words
         t_int = w.blocks * SURVEY_C_ALG[w.alg] / (ctx.sms * 128 * f_max * 1e6)
         roof["survey_issue_model"] = {

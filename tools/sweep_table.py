@@ -20,8 +20,10 @@ def main():
           "max(T_hbm, T_alu, T_chain) / T_measured with T_hbm at the HBM peak (6,650 GB/s fallback unless "
           "MEASURED_PEAKS.json), T_alu = blocks x ALU-only ops / (64 lanes/clk x 148 SMs x clock) and "
           "T_chain = blocks per message x the measured dependent-chain latency of one compression "
-          "(MD5 1,051 / SHA-1 1,116 / SM3 2,514 cycles, one warp per SM) -- the bound when the batch has too "
-          "few messages to overlap.\n")
+          "(MD5 1,044 / SHA-1 1,116 / SM3 2,514 cycles, one warp per SM) -- the bound when the batch has too "
+          "few messages to overlap; it is left out where consecutive flagged passes overlap on the GPU "
+          "(`chain_applies`: false -- rows of <= 128 B, messages of <= 17 blocks, grids of >= one CTA per SM), "
+          "since several batches' chains then run side by side.\n")
     print("| config | alg | messages | size | ms | GB/s | Mhash/s | bound | fraction | bit-exact |")
     print("|---|---|---|---|---|---|---|---|---|---|")
     for r in other:
