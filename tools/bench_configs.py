@@ -130,8 +130,11 @@ def fixed_point(alg, n, L, seed, steps, out, tag):
           "L2 flushed before each launch" if n * L < bench.L2_DEFEAT_BYTES else "inputs > 2 x L2, back-to-back")
     rec = {"config": tag, "alg": alg, "n": n, "msg_len": L, "l2": l2, "ms": round(ms, 4),
            "GBps": round(n * L / ms / 1e6, 2), "Mhash_s": round(n / ms / 1e3, 2),
+           # passes overlap only when launched back to back (graph replays, or launches with no
+           # L2-flush kernel in between)
            "roofline": roof(alg, blocks, n * (L + DLEN[alg]), ms, f, (L + 8) // 64 + 1,
-                            bench.pdl_overlap("fixed", n, (L + 8) // 64 + 1)), "sm_mhz": f,
+                            bench.pdl_overlap("fixed", n, (L + 8) // 64 + 1) and
+                            (n * L <= (64 << 20) or n * L >= bench.L2_DEFEAT_BYTES)), "sm_mhz": f,
            "bit_exact_sample": ok}
     print(json.dumps(rec), flush=True)
     out.write(json.dumps(rec) + "\n")
