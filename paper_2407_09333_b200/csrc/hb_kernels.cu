@@ -127,8 +127,20 @@ const void* last_hash_kernel() { return t_last_hash_kernel; }
 void set_last_hash_kernel(const void* kernel) { t_last_hash_kernel = kernel; }
 uint64_t launches_total() { return g_launches.load(std::memory_order_relaxed); }
 
+// The global sort's four kernels may run as programmatic dependents
+// (HB_FLAG_INPUT_READY, launch_varlen_sort): k_sort_zero starts while the
+// previous varlen hash kernel drains (released once every thread of it has
+// read its permutation entry); each later kernel does its offsets-only work
+// first and calls griddepcontrol.wait before touching the shared counters or
+// the permutation.  Launched normally, the waits and triggers are no-ops.
+__global__ void __launch_bounds__(1024) k_sort_zero(uint32_t* __restrict__ hist) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    for (int k = threadIdx.x; k < kSortBuckets; k += 1024) hist[k] = 0;
+}
+
 __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __restrict__ offsets, uint64_t n,
                                                             uint64_t addr_bias, uint32_t* __restrict__ hist) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __shared__ uint32_t h[kSortBuckets];
     for (int k = threadIdx.x; k < kSortBuckets; k += kSortThreads) h[k] = 0;
     __syncthreads();
@@ -139,12 +151,15 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __re
         if (i < n) atomicAdd(&h[sort_bucket(offsets, i, addr_bias)], 1u);
     }
     __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the counters are zeroed
     for (int k = threadIdx.x; k < kSortBuckets; k += kSortThreads)
         if (h[k]) atomicAdd(&hist[k], h[k]);
 }
 
 __global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* __restrict__ hist) {
     // exclusive scan of kSortBuckets in place; thread t owns kPer consecutive buckets
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     constexpr int kPer = kSortBuckets / 1024;
     __shared__ uint32_t warp_sums[32];
     const int t = threadIdx.x;
@@ -191,6 +206,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const uint64_t* _
         if (i < n) atomicAdd(&h[bucket[it]], 1u);
     }
     __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the cursors are scanned
     for (int k = threadIdx.x; k < kSortBuckets; k += kSortThreads) {
         base[k] = h[k] ? atomicAdd(&cursor[k], h[k]) : 0u;
         h[k] = 0;
@@ -328,15 +344,30 @@ cudaError_t launch_varlen_sort(int alg, const uint8_t* d_data, const uint64_t* d
     } else if (!(flags & HB_FLAG_NO_SORT) && n >= 1024 && d_scratch) {
         uint32_t* hist = static_cast<uint32_t*>(d_scratch);
         uint32_t* p = hist + kSortBuckets;
-        cudaError_t e = cudaMemsetAsync(hist, 0, kSortBuckets * sizeof(uint32_t), stream);
-        if (e != cudaSuccess) return e;
         const uint64_t per_cta = (uint64_t)kSortThreads * kSortItems;
         const unsigned g = (unsigned)((n + per_cta - 1) / per_cta);
         const uint64_t bias = reinterpret_cast<uintptr_t>(d_data) - offset_base;  // address = offsets[i] + bias
-        k_sort_hist<<<g, kSortThreads, 0, stream>>>(d_offsets, n, bias, hist);
-        k_sort_scan<<<1, 1024, 0, stream>>>(hist);
-        k_sort_scatter<<<g, kSortThreads, 0, stream>>>(d_offsets, n, bias, hist, p);
-        note_launches(3);
+        // HB_FLAG_INPUT_READY: programmatic dependents, so the sort runs while the
+        // previous varlen step drains (see k_sort_zero); otherwise plain launches.
+        const bool pdl = (flags & HB_FLAG_INPUT_READY) && T.pdl;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        const auto launch = [&](auto kernel, unsigned grid, unsigned block, auto... args) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(block);
+            cfg.stream = stream;
+            cfg.attrs = at;
+            cfg.numAttrs = pdl ? 1 : 0;
+            return cudaLaunchKernelEx(&cfg, kernel, args...);
+        };
+        cudaError_t e = launch(k_sort_zero, 1u, 1024u, hist);
+        if (e == cudaSuccess) e = launch(k_sort_hist, g, (unsigned)kSortThreads, d_offsets, n, bias, hist);
+        if (e == cudaSuccess) e = launch(k_sort_scan, 1u, 1024u, hist);
+        if (e == cudaSuccess) e = launch(k_sort_scatter, g, (unsigned)kSortThreads, d_offsets, n, bias, hist, p);
+        if (e != cudaSuccess) return e;
+        note_launches(4);
         perm = p;
     }
     *perm_out = perm;

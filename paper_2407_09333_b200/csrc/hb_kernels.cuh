@@ -760,6 +760,9 @@ k_varlen16(const uint8_t* __restrict__ data, const uint8_t* data_end, const uint
     const uint64_t i = perm ? (uint64_t)perm[t] : t;
     const uint64_t start = offsets[i] - offset_base;
     const uint64_t len = offsets[i + 1] - offsets[i];
+    // perm[t] read (see k_varlen16l): a length sort launched after this kernel
+    // with HB_FLAG_INPUT_READY may now overwrite the permutation
+    if (len != ~0ull) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
     const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
     const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
@@ -929,6 +932,9 @@ k_varlen16g(const uint8_t* __restrict__ data, const uint8_t* data_end, const uin
     const uint64_t i = perm ? (uint64_t)perm[t] : t;
     const uint64_t start = offsets[i] - offset_base;
     const uint64_t len = offsets[i + 1] - offsets[i];
+    // perm[t] read (see k_varlen16l): a length sort launched after this kernel
+    // with HB_FLAG_INPUT_READY may now overwrite the permutation
+    if (len != ~0ull) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uintptr_t a = reinterpret_cast<uintptr_t>(data + start);
     const uint4* w16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
     const uintptr_t dend = reinterpret_cast<uintptr_t>(data_end);
