@@ -33,3 +33,15 @@ def test_ncu_record_matches_the_kernel_that_ran():
     assert rec is not None and bench.load_ncu("md5_1k", rec["kernel"]) == rec
     assert bench.load_ncu("md5_1k", "void hb::k_generic<1, false>(unsigned char const*)") is None
     assert bench.load_ncu("varlen_md5")["kernel"] == bench.load_ncu("C4_varlen_md5")["kernel"]
+
+
+def test_chain_bound_only_for_non_overlapping_steps():
+    """The one-batch dependent-chain bound enters a fixed-width entry's
+    roofline only when consecutive flagged steps cannot overlap on the GPU
+    (long messages in a grid of fewer CTAs than SMs); varlen steps (the hash
+    waits for its own sort) always keep it."""
+    assert bench.pdl_overlap("fixed", 65536, 17)          # short messages: programmatic launches
+    assert bench.pdl_overlap("fixed", 1 << 16, 1025)      # >= one CTA per SM
+    assert not bench.pdl_overlap("fixed", 4096, 1025)     # sub-wave grid of long messages: plain launches
+    assert not bench.pdl_overlap("varlen", 1 << 22, 65)
+    assert not bench.pdl_overlap("decimal", 10 ** 9, 1)
