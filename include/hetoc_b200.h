@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 2
+#define HB_ABI_VERSION 3
 
 typedef enum {
     HB_OK = 0,
@@ -153,6 +153,15 @@ int hb_hash_fixed_split(int alg, const uint8_t *msgs, uint64_t n, uint64_t msg_l
  * non-decreasing entries, offsets[0] may be non-zero.                        */
 int hb_hash_varlen(int alg, const uint8_t *data, const uint64_t *offsets, uint64_t n, uint8_t *out,
                    const int *gpus, int n_gpus, uint32_t flags, hb_timing *t);
+
+/* One message (digest, pkg/src/hetoc/crypto/batch.py:102-109), len <=
+ * HB_DIGEST_SMALL_MAX bytes, synchronously: the bytes are passed inside the
+ * kernel launch and the digest is written to mapped pinned host memory, so a
+ * call is one launch + one stream synchronise (no staging copies).  gpu < 0
+ * picks the calling thread's default GPU as hb_hash_varlen does for a small
+ * call.  Thread-safe; HB_ERR_INVAL for longer messages (use hb_hash_varlen). */
+#define HB_DIGEST_SMALL_MAX 4096u
+int hb_digest_small(int alg, const uint8_t *msg, uint64_t len, uint8_t *out, int gpu);
 
 /* Paper workload (gen_messages): digests of the zero-padded decimal strings
  * of start .. start+count-1, width bytes each, generated on the GPU.

@@ -20,13 +20,14 @@ LIB_PATH = os.path.join(_HERE, os.environ.get("HETOC_B200_LIB", "libhetoc_b200.s
 HB_OK, HB_ERR_ALG, HB_ERR_INVAL, HB_ERR_CUDA, HB_ERR_NOMEM, HB_ERR_NODEV = range(6)
 HB_FLAG_NO_TMA, HB_FLAG_NO_SORT, HB_FLAG_SYNC_H2D, HB_FLAG_VARLEN_WORDS = 0x1, 0x2, 0x4, 0x8
 HB_FLAG_VARLEN_COOP_OFF, HB_FLAG_VARLEN_COOP = 0x10, 0x20
+HB_DIGEST_SMALL_MAX = 4096  # hb_digest_small: longest message passed inside the launch
 HB_FLAG_INPUT_READY = 0x40  # fixed width, device-resident: messages not written by the preceding kernel
 ALG_ID = {"sha1": 0, "md5": 1, "sm3": 2}
 
 # Every symbol include/hetoc_b200.h declares (tests check the library exports all of them).
 EXPORTS = (
     "hb_abi_version", "hb_last_error", "hb_digest_len", "hb_device_count", "hb_device_info", "hb_launch_count",
-    "hb_hash_fixed", "hb_hash_fixed_split", "hb_hash_varlen", "hb_hash_decimal", "hb_hash_fixed_dev", "hb_hash_varlen_dev",
+    "hb_hash_fixed", "hb_hash_fixed_split", "hb_hash_varlen", "hb_digest_small", "hb_hash_decimal", "hb_hash_fixed_dev", "hb_hash_varlen_dev",
     "hb_varlen_scratch_bytes", "hb_hash_decimal_dev", "hb_fill_random_dev", "hb_gen_decimal_dev",
     "hb_alloc_pinned", "hb_free_pinned", "hb_sync_device", "hb_shutdown", "hb_partition_range",
     "hb_ipc_handle", "hb_ipc_open", "hb_ipc_close",
@@ -98,6 +99,7 @@ _SIGS = {
     "hb_hash_fixed_split": (_int, [_int, _vp, _u64, _u64, _vp, _intp, ctypes.POINTER(ctypes.c_double), _int, _u32,
                                    ctypes.POINTER(HbTiming)]),
     "hb_hash_varlen": (_int, [_int, _vp, _vp, _u64, _vp, _intp, _int, _u32, ctypes.POINTER(HbTiming)]),
+    "hb_digest_small": (_int, [_int, _vp, _u64, _vp, _int]),
     "hb_hash_decimal": (_int, [_int, _u64, _u64, _int, _vp, _intp, _int, _u32, ctypes.POINTER(HbTiming)]),
     "hb_hash_fixed_dev": (_int, [_int, _int, _vp, _u64, _u64, _vp, _vp, _u32]),
     "hb_hash_varlen_dev": (_int, [_int, _int, _vp, _u64, _vp, _u64, _u64, _vp, _vp, _vp, _u32]),

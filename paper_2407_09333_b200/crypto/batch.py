@@ -272,9 +272,18 @@ def hash_decimal(alg: str, start_index: int, count: int, width: int = 9, *, gpus
 
 
 def digest(alg: str, message: bytes) -> Digest:
-    """Single-message digest (batch.py:102-109), computed on the GPU."""
+    """Single-message digest (batch.py:102-109), computed on the GPU.  Up to
+    HB_DIGEST_SMALL_MAX (4 KiB) bytes it is one launch with the message in the
+    kernel's parameters (hb_digest_small); longer messages take the varlen path."""
     _check_alg(alg)
-    m = np.frombuffer(bytes(message), np.uint8)
+    message = bytes(message)
+    if len(message) <= _native.HB_DIGEST_SMALL_MAX:
+        garr, ng = _native.gpu_array(None)
+        out = ctypes.create_string_buffer(DIGEST_LEN[alg])
+        rc = _native.lib().hb_digest_small(_native.ALG_ID[alg], message, len(message), out, garr[0] if ng else -1)
+        _native.check(rc, "hb_digest_small")
+        return Digest(alg, out.raw)
+    m = np.frombuffer(message, np.uint8)
     out = batch_digest_varlen(alg, m, np.array([0, m.shape[0]], np.uint64))
     return Digest(alg, out[0].tobytes())
 

@@ -607,6 +607,19 @@ static Worker* get_worker(int dev) {
     return g_workers[dev];
 }
 
+// hb_digest_small's per-device pool of (non-blocking stream, 64-byte mapped
+// pinned digest slot): a call takes one and returns it, so concurrent callers
+// never share a slot and pool threads that come and go leak nothing.
+// hb_shutdown frees them.
+struct SmallSlot {
+    cudaStream_t stream = nullptr;
+    uint8_t* h_out = nullptr;
+    uint8_t* d_out = nullptr;
+    uint32_t seq = 0;  // last value the kernel published at h_out + 48
+};
+static std::mutex g_small_mu;
+static std::vector<std::vector<SmallSlot>> g_small;
+
 // partition_range, pkg/src/hetoc/passes/partition.py:17-31 (same double
 // arithmetic as the Python: cum += r; b = lb + floor(n*cum + 0.5)).
 static int partition(int64_t lb, int64_t ub, const double* ratios, int k, int64_t* bounds) {
@@ -885,6 +898,62 @@ int hb_hash_varlen(int alg, const uint8_t* data, const uint64_t* offsets, uint64
     return rc;
 }
 
+int hb_digest_small(int alg, const uint8_t* msg, uint64_t len, uint8_t* out, int gpu) {
+    const int dlen = digest_len(alg);
+    if (dlen < 0) return fail(HB_ERR_ALG, "unknown hash algorithm id %d", alg);
+    if (len > HB_DIGEST_SMALL_MAX)
+        return fail(HB_ERR_INVAL, "message of %llu bytes exceeds HB_DIGEST_SMALL_MAX (%u)", (unsigned long long)len,
+                    HB_DIGEST_SMALL_MAX);
+    if (!out || (!msg && len)) return fail(HB_ERR_INVAL, "null buffer");
+    const int nd = device_count();
+    if (nd == 0) return fail(HB_ERR_NODEV, "no CUDA device visible");
+    if (gpu < 0) gpu = nd > 1 ? pick_default_gpu(nd) : 0;
+    else if (gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
+    DeviceGuard g(gpu);
+    SmallSlot sl;
+    {
+        std::lock_guard<std::mutex> lk(g_small_mu);
+        if ((int)g_small.size() <= gpu) g_small.resize(gpu + 1);
+        if (!g_small[gpu].empty()) {
+            sl = g_small[gpu].back();
+            g_small[gpu].pop_back();
+        }
+    }
+    if (!sl.stream) {
+        HB_CK(cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking));
+        HB_CK(cudaHostAlloc(reinterpret_cast<void**>(&sl.h_out), 64, cudaHostAllocMapped | cudaHostAllocPortable));
+        HB_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sl.d_out), sl.h_out, 0));
+        memset(sl.h_out, 0, 64);  // seq word starts at 0, the value no launch publishes
+    }
+    if (tuning().small_poll) {
+        // Spin on the slot's sequence word (a few us sooner than a stream
+        // synchronise); a launch that fails never publishes, so the stream is
+        // queried now and then and its error returned.
+        sl.seq = sl.seq + 1 ? sl.seq + 1 : 1;
+        HB_CK(launch_digest_small(alg, msg, len, sl.d_out, sl.seq, sl.stream));
+        const volatile uint32_t* flag = reinterpret_cast<const volatile uint32_t*>(sl.h_out + 48);
+        for (uint32_t k = 1; *flag != sl.seq; ++k) {
+#if defined(__x86_64__)
+            __builtin_ia32_pause();
+#endif
+            if ((k & 1023u) == 0) {
+                const cudaError_t e = cudaStreamQuery(sl.stream);
+                if (e == cudaSuccess && *flag != sl.seq)
+                    return fail(HB_ERR_CUDA, "hb_digest_small: kernel completed without publishing its digest");
+                if (e != cudaSuccess && e != cudaErrorNotReady) HB_CK(e);
+            }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+    } else {
+        HB_CK(launch_digest_small(alg, msg, len, sl.d_out, 0, sl.stream));
+        HB_CK(cudaStreamSynchronize(sl.stream));
+    }
+    memcpy(out, sl.h_out, (size_t)dlen);
+    std::lock_guard<std::mutex> lk(g_small_mu);
+    g_small[gpu].push_back(sl);
+    return HB_OK;
+}
+
 int hb_hash_decimal(int alg, uint64_t start, uint64_t count, int width, uint8_t* out, const int* gpus, int n_gpus,
                     uint32_t flags, hb_timing* t) {
     const int dlen = digest_len(alg);
@@ -1114,6 +1183,19 @@ int hb_shutdown(void) {
         w->cv.notify_one();
         w->th.join();
         delete w;
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_small_mu);
+        for (size_t d = 0; d < g_small.size(); ++d) {
+            if (g_small[d].empty()) continue;
+            DeviceGuard g((int)d);
+            for (SmallSlot& sl : g_small[d]) {
+                cudaStreamSynchronize(sl.stream);
+                cudaStreamDestroy(sl.stream);
+                cudaFreeHost(sl.h_out);
+            }
+        }
+        g_small.clear();
     }
     std::lock_guard<std::mutex> lk(g_ctx_mu);
     for (auto& cp : g_ctx) {

@@ -34,6 +34,7 @@ struct Tuning {
     uint64_t direct_max_len = 128;              // $HB_DIRECT_MAX_L: rows up to it use the per-thread-load kernels
     bool small_pair = true;                     // $HB_SMALL_PAIR: MD5 <= 32 B rows, two per thread at >= 2^20
     bool dec_run = true;                        // $HB_DEC_RUN: runs-of-ten decimal kernel
+    bool small_poll = true;                     // $HB_SMALL_POLL: hb_digest_small polls its mapped slot, else syncs the stream
     int varlen_sort = -1;                       // $HB_VARLEN_SORT: -1 per algorithm, 0 global, 1 window
     // A/B (-DHB_AB)
     int tma_cfg = -1;                           // $HB_TMA_CFG
@@ -92,6 +93,13 @@ uint64_t varlen_scratch_bytes(uint64_t n);
 cudaError_t launch_varlen(int alg, const uint8_t* d_data, uint64_t data_bytes, const uint64_t* d_offsets,
                           uint64_t offset_base, uint64_t n, uint8_t* d_out, void* d_scratch, cudaStream_t stream,
                           uint32_t flags);
+
+// One message of len <= HB_DIGEST_SMALL_MAX host bytes, passed by value in
+// the launch; the digest is stored at `out` (device-visible, e.g. mapped
+// pinned host memory) and then, when seq != 0, the u32 seq at out + 48
+// (release, system scope).
+cudaError_t launch_digest_small(int alg, const uint8_t* msg, uint64_t len, uint8_t* out, uint32_t seq,
+                                cudaStream_t stream);
 
 // Counter-based synthetic bytes (same stream as oracle/orc_fill_random).
 cudaError_t launch_fill_random(uint8_t* d_buf, uint64_t nbytes, uint64_t seed, uint64_t byte_offset,

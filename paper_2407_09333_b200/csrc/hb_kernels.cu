@@ -61,6 +61,7 @@ static Tuning parse_tuning() {
     t.direct_max_len = env_u64("HB_DIRECT_MAX_L", t.direct_max_len);
     t.small_pair = env_u64("HB_SMALL_PAIR", 1) != 0;
     t.dec_run = env_u64("HB_DEC_RUN", 1) != 0;
+    t.small_poll = env_u64("HB_SMALL_POLL", 1) != 0;
     if (const char* v = getenv("HB_VARLEN_SORT")) t.varlen_sort = strcmp(v, "global") == 0 ? 0 : 1;
 #ifdef HB_AB
     static const char* const kCfgNames[] = {"1x3", "2x2", "2x3", "ws2", "ws3", "1x2", "ws2x2", "ws3x2",
@@ -485,6 +486,56 @@ cudaError_t launch_decimal(int alg, uint64_t start, uint64_t count, int width, u
     case kSm3: return launch_decimal_sm3(start, count, width, d_out, stream);
     default: return cudaErrorInvalidValue;
     }
+}
+
+// hb_digest_small: the message rides in the parameter block (k_digest_small).
+// One thread's latency is the block chain, so the round variant is the one
+// with the shortest dependency chain, not the batch kernels' issue-balanced
+// one (tools/digest_probe.py; the A/B build takes $HB_VARIANT).
+template <int ALG, int CAP, int V>
+static void digest_small_launch(const SmallMsg<CAP>& m, uint8_t* out, cudaStream_t s) {
+    launch_plain(k_digest_small<ALG, CAP, V>, 1, 32, s, m, out);
+}
+
+template <int ALG, int CAP>
+static void digest_small_alg(const SmallMsg<CAP>& m, uint8_t* out, cudaStream_t s) {
+#ifdef HB_AB
+    switch (tuning().variant) {
+    case 0: return digest_small_launch<ALG, CAP, 0>(m, out, s);
+    case 1: return digest_small_launch<ALG, CAP, 1>(m, out, s);
+    case 2: return digest_small_launch<ALG, CAP, 2>(m, out, s);
+    case 3: return digest_small_launch<ALG, CAP, 3>(m, out, s);
+    case 5: if constexpr (ALG == kMd5) return digest_small_launch<ALG, CAP, 5>(m, out, s);
+    default: break;
+    }
+#endif
+    digest_small_launch<ALG, CAP, kSmallVariant<ALG>>(m, out, s);
+}
+
+template <int CAP>
+static cudaError_t digest_small_cap(int alg, const uint8_t* msg, uint64_t len, uint8_t* out, uint32_t seq,
+                                    cudaStream_t s) {
+    SmallMsg<CAP> m;
+    if (len) memcpy(m.w, msg, len);
+    // Zero the rest of the tail block (md_finish expects bytes >= r clear);
+    // words past it are never read.
+    memset(reinterpret_cast<uint8_t*>(m.w) + len, 0, (len / 64u + 1u) * 64u - len);
+    m.len = len;
+    m.seq = seq;
+    switch (alg) {
+    case kSha1: digest_small_alg<kSha1>(m, out, s); break;
+    case kMd5: digest_small_alg<kMd5>(m, out, s); break;
+    case kSm3: digest_small_alg<kSm3>(m, out, s); break;
+    default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_digest_small(int alg, const uint8_t* msg, uint64_t len, uint8_t* out, uint32_t seq,
+                                cudaStream_t stream) {
+    if (len > HB_DIGEST_SMALL_MAX) return cudaErrorInvalidValue;
+    if (len <= 256) return digest_small_cap<256>(alg, msg, len, out, seq, stream);
+    return digest_small_cap<HB_DIGEST_SMALL_MAX>(alg, msg, len, out, seq, stream);
 }
 
 cudaError_t launch_gen_decimal(uint64_t start, uint64_t count, int width, uint8_t* d_out, cudaStream_t stream) {

@@ -1508,4 +1508,59 @@ static cudaError_t launch_decimal_alg(uint64_t start, uint64_t count, int width,
     return cudaGetLastError();
 }
 
+// -------------------------------------------------------------------------
+// One short message (hb_digest_small, crypto.digest: batch.py:102-109).  The
+// latency of a single digest is copies and launches, not hashing: the bytes
+// travel in the kernel's parameter block (host-zero-padded little-endian
+// words, so no H2D copy and no tail masking) and the digest is stored
+// straight into mapped pinned host memory (no D2H copy) -- one launch and
+// one stream synchronise per call.  One thread runs the block chain, as the
+// batch kernels do per message.  Two parameter sizes so a short
+// message does not ship 4 KiB of zeros with its launch.
+template <int ALG> constexpr int kSmallVariant = ALG == kMd5 ? 5 : kVarBal;
+
+template <int CAP>
+struct SmallMsg {
+    uint32_t w[CAP / 4 + 16];  // message bytes, then zeros through the tail block
+    uint64_t len;
+    uint32_t seq;  // != 0: publish seq at out + kSmallSeqOffset after the digest
+};
+constexpr int kSmallSeqOffset = 48;
+
+template <int ALG, int CAP, int V>
+__global__ void __launch_bounds__(32) k_digest_small(const __grid_constant__ SmallMsg<CAP> m, uint8_t* out) {
+    using H = HashAlg<ALG, V>;
+    // The parameter bank is read through the constant cache: a dependent
+    // per-block read there costs a miss in the chain (1.5x at 4 KiB), so the
+    // warp first stages the used words in shared memory (8-byte loads), then
+    // lane 0 runs the chain with the next block's words loaded ahead.
+    __shared__ uint2 sw[(CAP / 4 + 16) / 2];
+    const uint32_t nfull = (uint32_t)(m.len >> 6);
+    const uint2* pw = reinterpret_cast<const uint2*>(m.w);
+    for (uint32_t i = threadIdx.x; i < 8u * (nfull + 1u); i += 32u) sw[i] = pw[i];
+    __syncwarp();
+    if (threadIdx.x != 0) return;
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(sw);
+    uint32_t st[H::kStateWords];
+    H::init(st);
+    uint32_t nxt[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) nxt[j] = w[j];
+#pragma unroll 1
+    for (uint32_t b = 0; b < nfull; ++b) {
+        uint32_t raw[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            raw[j] = nxt[j];
+            nxt[j] = w[16 * (b + 1) + j];
+        }
+        compress1<ALG, V>(st, raw);
+    }
+    md_finish<ALG, V>(st, nxt, (uint32_t)(m.len & 63u), m.len);
+    store_digest<ALG>(out, st);
+    // The host polls this word instead of synchronising the stream; the
+    // release orders the digest stores before it at system scope.
+    if (m.seq) asm volatile("st.release.sys.u32 [%0], %1;" ::"l"(out + kSmallSeqOffset), "r"(m.seq) : "memory");
+}
+
 }  // namespace hb

@@ -20,6 +20,7 @@ from paper_2407_09333_b200.crypto import (
     UnknownAlgorithmError,
     batch_digest,
     batch_digest_varlen,
+    digest,
     gen_messages,
     hash_batch,
 )
@@ -63,7 +64,7 @@ def test_header_flags_match_python_constants():
 
 def test_abi_basics():
     lib = _native.lib()
-    assert lib.hb_abi_version() == 2
+    assert lib.hb_abi_version() == 3
     assert [lib.hb_digest_len(i) for i in range(3)] == [20, 16, 32]
     assert lib.hb_digest_len(7) == -1
     assert hb.launch_count() >= 0
@@ -161,6 +162,23 @@ def test_no_cpu_fallback_without_gpu():
         batch_digest("md5", np.zeros((4, 16), np.uint8))
     lib = _native.lib()
     assert lib.hb_hash_fixed_dev(1, 0, ctypes.c_void_p(16), 1, 16, ctypes.c_void_p(16), None, 0) == _native.HB_ERR_NODEV
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        digest("md5", b"abc")
+
+
+def test_digest_small_validation():
+    """hb_digest_small rejects a bad alg, an over-long message and null
+    buffers before touching a device; the header's limit matches _native."""
+    hdr = open(HEADER).read()
+    assert int(re.search(r"#define\s+HB_DIGEST_SMALL_MAX\s+(\d+)u", hdr).group(1)) == _native.HB_DIGEST_SMALL_MAX
+    lib = _native.lib()
+    out = ctypes.create_string_buffer(32)
+    assert lib.hb_digest_small(9, b"a", 1, out, -1) == _native.HB_ERR_ALG
+    big = b"x" * (_native.HB_DIGEST_SMALL_MAX + 1)
+    assert lib.hb_digest_small(1, big, len(big), out, -1) == _native.HB_ERR_INVAL
+    assert "HB_DIGEST_SMALL_MAX" in _native.last_error()
+    assert lib.hb_digest_small(1, None, 4, out, -1) == _native.HB_ERR_INVAL
+    assert lib.hb_digest_small(1, b"abcd", 4, None, -1) == _native.HB_ERR_INVAL
 
 
 def test_ratio_validation_matches_reference_verifier():

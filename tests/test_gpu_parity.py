@@ -49,6 +49,42 @@ def test_kats(golden):
     assert digest_sha1_accel(b"").hex() == "da39a3ee5e6b4b0d3255bfef95601890afd80709"
 
 
+def test_digest_small_every_length():
+    """crypto.digest's one-launch path (hb_digest_small): every length 0..300,
+    the 55/56/64-byte padding edges of later blocks, both parameter sizes
+    (<=256 and <=4096 B) and the limit, against the oracle; one byte past the
+    limit takes the varlen path and must agree too."""
+    lens = list(range(301)) + [439, 440, 447, 448, 511, 512, 1000, 2047, 2048, 4031, 4032, 4095, 4096, 4097, 6000]
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    data = oracle.fill_random(int(off[-1]), 61)
+    lib = _native.lib()
+    k0 = _native.launch_count()
+    for alg in ALGS:
+        ref = oracle.batch_varlen(alg, data, off, 8)
+        for i, L in enumerate(lens):
+            m = data[int(off[i]):int(off[i + 1])].tobytes()
+            assert digest(alg, m).data == ref[i].tobytes(), (alg, L)
+        out = ctypes.create_string_buffer(32)
+        assert lib.hb_digest_small(_native.ALG_ID[alg], data.ctypes.data, 4096, out, 0) == _native.HB_OK
+        assert out.raw[:ref.shape[1]] == oracle.batch_varlen(alg, data[:4096], np.array([0, 4096], np.uint64))[0].tobytes()
+        assert "k_digest_small" in _native.last_kernel_name()
+    assert _native.launch_count() > k0
+    assert lib.hb_digest_small(1, b"a", 1, ctypes.create_string_buffer(16), _native.device_count()) == _native.HB_ERR_NODEV
+
+
+def test_digest_small_concurrent_callers():
+    """Pool threads calling digest at once (the executor's per-index
+    crypto.digest) each get their own stream/slot: no crossed results."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    msgs = [bytes([i % 251]) * (i % 700) for i in range(2000)]
+    with ThreadPoolExecutor(16) as ex:
+        got = list(ex.map(lambda m: digest("sm3", m).data, msgs))
+    off = np.concatenate([[0], np.cumsum([len(m) for m in msgs])]).astype(np.uint64)
+    ref = oracle.batch_varlen("sm3", np.frombuffer(b"".join(msgs), np.uint8), off, 8)
+    assert got == [r.tobytes() for r in ref]
+
+
 def test_boundary_lengths_single(golden):
     for row in golden("boundary.json"):
         m = np.frombuffer(bytes.fromhex(row["msg_hex"]), np.uint8).reshape(1, -1)
