@@ -19,6 +19,8 @@ timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/
 for w in paper_md5 paper_sha1 paper_sm3; do
   timeout 600 python bench.py --workload $w --steps 10 --warmup 3 --configs none > gpurun_out/bench_${w}_$TAG.json 2> gpurun_out/bench_${w}_$TAG.err
 done
+{ for a in md5 sha1 sm3; do python tools/digest_probe.py $a 0 55 1024 4096; done
+  HB_SMALL_POLL=0 python tools/digest_probe.py md5 55 1024 | sed "s/^/HB_SMALL_POLL=0 /"; } > gpurun_out/digest_probe_$TAG.txt 2>&1
 for tool in memcheck racecheck synccheck; do
   timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_cases.py > gpurun_out/sanitize_${tool}_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/sanitize_${tool}_$TAG.log
 done

@@ -130,6 +130,14 @@ def main():
             ref = hostref.digests("sm3", ref).reshape(rows, L)
             cases += 1
         assert np.array_equal(cur.cpu().numpy(), ref)
+    # hb_digest_small: message in the launch parameters, digest + polled sequence word in mapped pinned memory
+    from paper_2407_09333_b200.crypto import digest
+    msg = hostref.random_bytes(4096, 53).tobytes()
+    for alg in ALGS:
+        for L in (0, 55, 56, 64, 256, 257, 4096):
+            want = hostref.digests_varlen(alg, np.frombuffer(msg[:L], np.uint8), np.array([0, L], np.uint64))[0]
+            assert digest(alg, msg[:L]).data == want.tobytes(), (alg, L)
+            cases += 1
     torch.cuda.synchronize()
     print(f"sanitize cases ok: {cases} invocations bit-exact")
 
