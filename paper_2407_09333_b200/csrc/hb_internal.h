@@ -34,6 +34,7 @@ struct Tuning {
     uint64_t direct_max_len = 128;              // $HB_DIRECT_MAX_L: rows up to it use the per-thread-load kernels
     bool small_pair = true;                     // $HB_SMALL_PAIR: MD5 <= 32 B rows, two per thread at >= 2^20
     bool dec_run = true;                        // $HB_DEC_RUN: runs-of-ten decimal kernel
+    uint64_t zc_max_bytes = 256u << 10;         // $HB_ZERO_COPY_MAX: single-GPU untimed calls up to it read host memory directly (0 = off)
     bool small_poll = true;                     // $HB_SMALL_POLL: hb_digest_small polls its mapped slot, else syncs the stream
     int varlen_sort = -1;                       // $HB_VARLEN_SORT: -1 per algorithm, 0 global, 1 window
     // A/B (-DHB_AB)

@@ -62,6 +62,7 @@ static Tuning parse_tuning() {
     t.small_pair = env_u64("HB_SMALL_PAIR", 1) != 0;
     t.dec_run = env_u64("HB_DEC_RUN", 1) != 0;
     t.small_poll = env_u64("HB_SMALL_POLL", 1) != 0;
+    t.zc_max_bytes = std::min<uint64_t>(env_u64("HB_ZERO_COPY_MAX", t.zc_max_bytes), 16ull << 20);
     if (const char* v = getenv("HB_VARLEN_SORT")) t.varlen_sort = strcmp(v, "global") == 0 ? 0 : 1;
 #ifdef HB_AB
     static const char* const kCfgNames[] = {"1x3", "2x2", "2x3", "ws2", "ws3", "1x2", "ws2x2", "ws3x2",

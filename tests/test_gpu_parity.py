@@ -72,6 +72,34 @@ def test_digest_small_every_length():
     assert lib.hb_digest_small(1, b"a", 1, ctypes.create_string_buffer(16), _native.device_count()) == _native.HB_ERR_NODEV
 
 
+@pytest.mark.parametrize("zc_max", ["65536", "262144"])
+def test_small_batch_zero_copy(hb_env, zc_max):
+    """Small untimed single-GPU calls read mapped host memory directly
+    (small_batch in hb_engine.cu).  Against the oracle and against the chunk
+    ring (HB_ZERO_COPY_MAX=0) at the size limits: input bytes, 128 KiB of
+    digests, 64 KiB of offsets; varlen with offsets[0] != 0; every kernel
+    family (TMA widths fall back to the direct loads)."""
+    cases = [(1, 64), (4096, 16), (4096, 32), (1024, 64), (64, 1024), (63, 1000), (16, 4096), (1, 65536), (4000, 7)]
+    for alg in ALGS:
+        for n, L in cases:
+            data = oracle.fill_random(n * L, n + L).reshape(n, L)
+            ref = oracle.batch_fixed(alg, data, threads=8)
+            hb_env.set(HB_ZERO_COPY_MAX=zc_max)
+            assert np.array_equal(batch_digest(alg, data), ref), (alg, n, L)
+            hb_env.set(HB_ZERO_COPY_MAX=0)
+            assert np.array_equal(batch_digest(alg, data), ref), (alg, n, L)
+        rng = np.random.default_rng(5)
+        for n in (1, 7, 1000, 8190, 8191):
+            lens = rng.integers(0, 40, n)
+            off = (np.concatenate([[0], np.cumsum(lens)]) + 13).astype(np.uint64)
+            data = oracle.fill_random(int(off[-1]) + 5, n)
+            ref = oracle.batch_varlen(alg, data, off, 8)
+            hb_env.set(HB_ZERO_COPY_MAX=zc_max)
+            assert np.array_equal(batch_digest_varlen(alg, data, off), ref), (alg, n)
+            hb_env.set(HB_ZERO_COPY_MAX=0)
+            assert np.array_equal(batch_digest_varlen(alg, data, off), ref), (alg, n)
+
+
 def test_digest_small_concurrent_callers():
     """Pool threads calling digest at once (the executor's per-index
     crypto.digest) each get their own stream/slot: no crossed results."""

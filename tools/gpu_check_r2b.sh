@@ -21,6 +21,7 @@ for w in paper_md5 paper_sha1 paper_sm3; do
 done
 { for a in md5 sha1 sm3; do python tools/digest_probe.py $a 0 55 1024 4096; done
   HB_SMALL_POLL=0 python tools/digest_probe.py md5 55 1024 | sed "s/^/HB_SMALL_POLL=0 /"; } > gpurun_out/digest_probe_$TAG.txt 2>&1
+python tools/zero_copy_probe.py > gpurun_out/zero_copy_$TAG.txt 2>&1
 for tool in memcheck racecheck synccheck; do
   timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_cases.py > gpurun_out/sanitize_${tool}_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/sanitize_${tool}_$TAG.log
 done

@@ -138,6 +138,17 @@ def main():
             want = hostref.digests_varlen(alg, np.frombuffer(msg[:L], np.uint8), np.array([0, L], np.uint64))[0]
             assert digest(alg, msg[:L]).data == want.tobytes(), (alg, L)
             cases += 1
+    # small untimed host calls: zero-copy reads of mapped pinned memory (hb_engine.cu small_batch)
+    from paper_2407_09333_b200.crypto import batch_digest, batch_digest_varlen
+    for alg in ALGS:
+        for n, L in ((1, 64), (1000, 64), (64, 1024), (4096, 32), (33, 7)):
+            rows = hostref.random_bytes(n * L, n * L).reshape(n, L)
+            assert np.array_equal(batch_digest(alg, rows), hostref.digests(alg, rows)), (alg, n, L)
+            cases += 1
+        off = np.array([3, 3, 20, 21, 120, 4000], np.uint64)
+        buf = hostref.random_bytes(4007, 3)
+        assert np.array_equal(batch_digest_varlen(alg, buf, off), hostref.digests_varlen(alg, buf, off)), alg
+        cases += 1
     torch.cuda.synchronize()
     print(f"sanitize cases ok: {cases} invocations bit-exact")
 
