@@ -62,6 +62,7 @@ static int fail(int code, const char* fmt, ...) {
     do {                                                                                                   \
         cudaError_t e_ = (expr);                                                                           \
         if (e_ != cudaSuccess) {                                                                           \
+            cudaGetLastError(); /* clear a non-sticky error so the next launch check does not report it */ \
             const char* extra_ = (e_ == cudaErrorNotSupported || e_ == cudaErrorInvalidValue) ? tma_error() : ""; \
             return fail(e_ == cudaErrorMemoryAllocation ? HB_ERR_NOMEM : HB_ERR_CUDA, "%s failed: %s %s (%s:%d)", \
                         #expr, cudaGetErrorString(e_), extra_, __FILE__, __LINE__);                        \
@@ -668,7 +669,7 @@ static int small_batch(int kind, int alg, const uint8_t* data, uint64_t in_bytes
     SmallSlot sl;
     if (int rc = take_slot(gpu, sl)) return rc;
     const uint64_t cap = std::max<uint64_t>(tuning().zc_max_bytes, 4096);
-    if (sl.zc_in_cap < in_bytes) {
+    if (!sl.zc || sl.zc_in_cap < in_bytes) {  // (an all-empty batch still needs the digest buffer)
         if (sl.zc) HB_CK(cudaFreeHost(sl.zc));
         sl.zc = nullptr;
         sl.zc_in_cap = 0;

@@ -79,7 +79,7 @@ def test_small_batch_zero_copy(hb_env, zc_max):
     ring (HB_ZERO_COPY_MAX=0) at the size limits: input bytes, 128 KiB of
     digests, 64 KiB of offsets; varlen with offsets[0] != 0; every kernel
     family (TMA widths fall back to the direct loads)."""
-    cases = [(1, 64), (4096, 16), (4096, 32), (1024, 64), (64, 1024), (63, 1000), (16, 4096), (1, 65536), (4000, 7)]
+    cases = [(1, 64), (5, 0), (4096, 16), (4096, 32), (1024, 64), (64, 1024), (63, 1000), (16, 4096), (1, 65536), (4000, 7)]
     for alg in ALGS:
         for n, L in cases:
             data = oracle.fill_random(n * L, n + L).reshape(n, L)
