@@ -637,10 +637,13 @@ static int take_slot(int gpu, SmallSlot& sl) {  // on the current device == gpu
             return HB_OK;
         }
     }
-    HB_CK(cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking));
-    HB_CK(cudaHostAlloc(reinterpret_cast<void**>(&sl.h_out), 64, cudaHostAllocMapped | cudaHostAllocPortable));
-    HB_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sl.d_out), sl.h_out, 0));
-    memset(sl.h_out, 0, 64);  // seq word starts at 0, the value no launch publishes
+    // Built in a local: the lease returns only complete slots to the pool.
+    SmallSlot n;
+    HB_CK(cudaHostAlloc(reinterpret_cast<void**>(&n.h_out), 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(n.h_out, 0, 64);  // seq word starts at 0, the value no launch publishes
+    HB_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&n.d_out), n.h_out, 0));
+    HB_CK(cudaStreamCreateWithFlags(&n.stream, cudaStreamNonBlocking));
+    sl = n;
     return HB_OK;
 }
 
@@ -648,6 +651,18 @@ static void give_slot(int gpu, const SmallSlot& sl) {
     std::lock_guard<std::mutex> lk(g_small_mu);
     g_small[gpu].push_back(sl);
 }
+
+// Returns the slot to the pool on every exit, error paths included (a call
+// rejected at launch, e.g. for bad flags, leaves the slot usable; after a
+// sticky error the context is gone anyway).
+struct SlotLease {
+    int gpu;
+    SmallSlot sl;
+    explicit SlotLease(int g) : gpu(g) {}
+    ~SlotLease() {
+        if (sl.stream) give_slot(gpu, sl);
+    }
+};
 
 // Small batches (at most tuning().zc_max_bytes of messages, kZcOutBytes of
 // digests, kZcOffBytes of offsets) skip the chunk ring: the bytes are copied
@@ -666,7 +681,8 @@ static bool small_batch_fits(uint64_t in_bytes, uint64_t n, uint64_t out_bytes, 
 static int small_batch(int kind, int alg, const uint8_t* data, uint64_t in_bytes, const uint64_t* offsets, uint64_t n,
                        uint64_t msg_len, uint8_t* out, uint64_t out_bytes, int gpu, uint32_t flags) {
     DeviceGuard g(gpu);
-    SmallSlot sl;
+    SlotLease lease(gpu);
+    SmallSlot& sl = lease.sl;
     if (int rc = take_slot(gpu, sl)) return rc;
     const uint64_t cap = std::max<uint64_t>(tuning().zc_max_bytes, 4096);
     if (!sl.zc || sl.zc_in_cap < in_bytes) {  // (an all-empty batch still needs the digest buffer)
@@ -696,7 +712,6 @@ static int small_batch(int kind, int alg, const uint8_t* data, uint64_t in_bytes
     }
     HB_CK(cudaStreamSynchronize(sl.stream));
     memcpy(out, h_dig, out_bytes);
-    give_slot(gpu, sl);
     return HB_OK;
 }
 
@@ -995,7 +1010,8 @@ int hb_digest_small(int alg, const uint8_t* msg, uint64_t len, uint8_t* out, int
     if (gpu < 0) gpu = nd > 1 ? pick_default_gpu(nd) : 0;
     else if (gpu >= nd) return fail(HB_ERR_NODEV, "device ordinal %d out of range (%d devices)", gpu, nd);
     DeviceGuard g(gpu);
-    SmallSlot sl;
+    SlotLease lease(gpu);
+    SmallSlot& sl = lease.sl;
     if (int rc = take_slot(gpu, sl)) return rc;
     if (tuning().small_poll) {
         // Spin on the slot's sequence word (a few us sooner than a stream
@@ -1021,7 +1037,6 @@ int hb_digest_small(int alg, const uint8_t* msg, uint64_t len, uint8_t* out, int
         HB_CK(cudaStreamSynchronize(sl.stream));
     }
     memcpy(out, sl.h_out, (size_t)dlen);
-    give_slot(gpu, sl);
     return HB_OK;
 }
 

@@ -100,6 +100,21 @@ def test_small_batch_zero_copy(hb_env, zc_max):
             assert np.array_equal(batch_digest_varlen(alg, data, off), ref), (alg, n)
 
 
+def test_small_call_error_leaves_engine_usable():
+    """A small call rejected at launch (an A/B-only flag on the shipped
+    library) raises, and the next calls on the same slots still succeed: the
+    slot goes back to the pool and the non-sticky error is cleared."""
+    if _native.built_with_ab():
+        pytest.skip("the A/B library accepts the A/B varlen flags")
+    data = oracle.fill_random(300, 4)
+    off = np.array([0, 100, 300], np.uint64)
+    for _ in range(3):
+        with pytest.raises(RuntimeError, match="A/B"):
+            batch_digest_varlen("md5", data, off, flags=_native.HB_FLAG_VARLEN_WORDS)
+        assert np.array_equal(batch_digest_varlen("md5", data, off), oracle.batch_varlen("md5", data, off))
+        assert digest("sm3", b"abc").hex().startswith("66c7f0f4")
+
+
 def test_digest_small_concurrent_callers():
     """Pool threads calling digest at once (the executor's per-index
     crypto.digest) each get their own stream/slot: no crossed results."""
