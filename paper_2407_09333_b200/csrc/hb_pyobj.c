@@ -65,8 +65,22 @@ done:
     return list;
 }
 
+/* addr(obj) -> int: the address of a C-contiguous buffer (numpy array,
+ * bytes, ...) -- what `ndarray.ctypes.data` returns, without building the
+ * ctypes helper object (1.4 us per call, several per small engine call).  The
+ * caller keeps obj alive while the address is in use. */
+static PyObject* addr(PyObject* self, PyObject* obj) {
+    (void)self;
+    Py_buffer view;
+    if (PyObject_GetBuffer(obj, &view, PyBUF_ANY_CONTIGUOUS) < 0) return NULL;
+    PyObject* r = PyLong_FromVoidPtr(view.buf);
+    PyBuffer_Release(&view);
+    return r;
+}
+
 static PyMethodDef methods[] = {
     {"digest_list", digest_list, METH_VARARGS, "Digest objects over consecutive dlen-byte slices of a buffer."},
+    {"addr", addr, METH_O, "Address of a contiguous buffer (ndarray.ctypes.data without the ctypes object)."},
     {NULL, NULL, 0, NULL},
 };
 
