@@ -256,3 +256,18 @@ def test_digest_list_matches_constructor():
         helper.digest_list(Digest, "md5", b"x" * 31, 16, 2)  # buffer shorter than count * dlen
     with pytest.raises(TypeError):
         helper.digest_list(int, "md5", b"x" * 32, 16, 2)  # not a Python class
+
+
+def test_buffer_address_helper():
+    """crypto's _addr (the C helper) returns what ndarray.ctypes.data does,
+    for writable, read-only, empty and offset views; non-contiguous buffers
+    are rejected rather than passed as a wrong address."""
+    from paper_2407_09333_b200.crypto import batch
+
+    assert batch._hb_pyobj is not None, "csrc/hb_pyobj.c not built"
+    base = np.arange(512, dtype=np.uint8).reshape(8, 64)
+    for a in (base, base[3:], np.frombuffer(b"abcdef", np.uint8), np.zeros((0, 16), np.uint8),
+              np.zeros(9, np.uint64)):
+        assert batch._addr(a) == a.ctypes.data
+    with pytest.raises((BufferError, ValueError)):
+        batch._hb_pyobj.addr(base[:, ::2])
