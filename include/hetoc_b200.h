@@ -137,7 +137,10 @@ uint64_t hb_launch_count(void);           /* kernels launched by this process so
  * ~30 us per call on small batches).  msg_len 0 hashes empty messages.
  * Each GPU stages through kSlots = 3 chunk buffers whose size is capped by
  * that GPU's budget (free HBM at first use minus $HB_DEVICE_RESERVE, 2 GiB):
- * hb_engine_budget reports it.                                              */
+ * hb_engine_budget reports it.  An untimed (t == NULL) single-GPU call of at
+ * most $HB_ZERO_COPY_MAX (256 KiB) message bytes and 128 KiB of digests skips
+ * the ring: the batch is copied into a mapped pinned buffer that the kernel
+ * reads over PCIe, and the digests are stored straight into mapped memory. */
 int hb_hash_fixed(int alg, const uint8_t *msgs, uint64_t n, uint64_t msg_len, uint8_t *out,
                   const int *gpus, int n_gpus, uint32_t flags, hb_timing *t);
 
