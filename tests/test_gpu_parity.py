@@ -115,6 +115,19 @@ def test_small_call_error_leaves_engine_usable():
         assert digest("sm3", b"abc").hex().startswith("66c7f0f4")
 
 
+def test_small_batch_concurrent_callers():
+    """Pool threads issuing small batches at once (hash_batch / _fast_digest
+    slices) each lease their own zero-copy slot: no crossed digests."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    jobs = [(ALGS[i % 3], 1 + (i * 37) % 900, (16, 64, 100, 1024)[i % 4]) for i in range(240)]
+    datas = [oracle.fill_random(n * L, i).reshape(n, L) for i, (_, n, L) in enumerate(jobs)]
+    with ThreadPoolExecutor(16) as ex:
+        got = list(ex.map(lambda k: batch_digest(jobs[k][0], datas[k]), range(len(jobs))))
+    for (alg, n, L), d, g in zip(jobs, datas, got):
+        assert np.array_equal(g, oracle.batch_fixed(alg, d)), (alg, n, L)
+
+
 def test_digest_small_concurrent_callers():
     """Pool threads calling digest at once (the executor's per-index
     crypto.digest) each get their own stream/slot: no crossed results."""
