@@ -1049,6 +1049,11 @@ static cudaError_t launch_varlen_ab(const uint8_t* d_data, uint64_t data_bytes, 
         case 51: launch_plain(k_varlen16c<ALG>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         // realignment on the FMA pipe (IMAD.HI + IMAD instead of funnel shifts), sort keyed on a-1
         case 52: launch_plain(k_varlen16m<ALG>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        // the shipping MD5 loop (runtime alignment switch + L2 policies) at MD5 round variants 3 / 4 / 5 / 6
+        case 53: launch_plain(k_varlen16l<ALG, false, ALG == kMd5 ? 3 : -1, true>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 54: launch_plain(k_varlen16l<ALG, false, ALG == kMd5 ? 4 : -1, true>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 55: launch_plain(k_varlen16l<ALG, false, ALG == kMd5 ? 5 : -1, true>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
+        case 56: launch_plain(k_varlen16l<ALG, false, ALG == kMd5 ? 6 : -1, true>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         default: launch_plain(k_varlen16<ALG, 0, 0>, g2, blk, stream, d_data, d_data + data_bytes, d_offsets, offset_base, perm, n, d_out); break;
         }
     } else if (T.varlen_kernel >= 10) {  // prefetch-instruction arms of the per-thread kernel (PF = kernel - 10)
