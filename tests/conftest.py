@@ -13,6 +13,8 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
     config.addinivalue_line("markers", "ab: exercises an A/B kernel arm; needs the -DHB_AB library "
                                        "(HETOC_B200_LIB=libhetoc_b200_ab.so, `make -C paper_2407_09333_b200/csrc ab`)")
+    config.addinivalue_line("markers", "zero_copy: test_gpu_parity runs it with the small-call zero-copy path at "
+                                       "its default (every other test there pins $HB_ZERO_COPY_MAX=0)")
 
 
 def _gpu_visible() -> bool:

@@ -28,6 +28,22 @@ from paper_2407_09333_b200.crypto import (
 pytestmark = pytest.mark.gpu
 ALGS = ("sha1", "md5", "sm3")
 FLAGS = {"tma": 0, "direct": _native.HB_FLAG_NO_TMA}
+ZC_DEFAULT = 256 << 10  # $HB_ZERO_COPY_MAX default (hb_internal.h)
+
+
+@pytest.fixture(autouse=True)
+def _ring_unless_zero_copy(request, monkeypatch):
+    """These tests cover kernel shapes (TMA tiles, the length sort, exact-size
+    device buffers) that small host calls no longer reach: small untimed calls
+    take the zero-copy path (kernels reading mapped host memory, direct loads,
+    unsorted).  So every test here runs with $HB_ZERO_COPY_MAX=0 unless it is
+    marked zero_copy; the zero-copy path has its own tests below."""
+    if request.node.get_closest_marker("zero_copy") is None:
+        monkeypatch.setenv("HB_ZERO_COPY_MAX", "0")
+        _native.reload_tuning()
+    yield
+    monkeypatch.undo()
+    _native.reload_tuning()
 
 
 def sha(a):
@@ -40,6 +56,7 @@ def test_device_visible_and_native_loaded():
     assert info["cc_major"] == 10, info  # sm_100
 
 
+@pytest.mark.zero_copy
 def test_kats(golden):
     for row in golden("kats.json"):
         assert digest(row["alg"], bytes.fromhex(row["msg_hex"])).hex() == row["digest"]
@@ -49,6 +66,7 @@ def test_kats(golden):
     assert digest_sha1_accel(b"").hex() == "da39a3ee5e6b4b0d3255bfef95601890afd80709"
 
 
+@pytest.mark.zero_copy
 def test_digest_small_every_length():
     """crypto.digest's one-launch path (hb_digest_small): every length 0..300,
     the 55/56/64-byte padding edges of later blocks, both parameter sizes
@@ -72,6 +90,7 @@ def test_digest_small_every_length():
     assert lib.hb_digest_small(1, b"a", 1, ctypes.create_string_buffer(16), _native.device_count()) == _native.HB_ERR_NODEV
 
 
+@pytest.mark.zero_copy
 @pytest.mark.parametrize("zc_max", ["65536", "262144"])
 def test_small_batch_zero_copy(hb_env, zc_max):
     """Small untimed single-GPU calls read mapped host memory directly
@@ -100,6 +119,7 @@ def test_small_batch_zero_copy(hb_env, zc_max):
             assert np.array_equal(batch_digest_varlen(alg, data, off), ref), (alg, n)
 
 
+@pytest.mark.zero_copy
 def test_small_call_error_leaves_engine_usable():
     """A small call rejected at launch (an A/B-only flag on the shipped
     library) raises, and the next calls on the same slots still succeed: the
@@ -115,6 +135,7 @@ def test_small_call_error_leaves_engine_usable():
         assert digest("sm3", b"abc").hex().startswith("66c7f0f4")
 
 
+@pytest.mark.zero_copy
 def test_small_batch_concurrent_callers():
     """Pool threads issuing small batches at once (hash_batch / _fast_digest
     slices) each lease their own zero-copy slot: no crossed digests."""
@@ -128,6 +149,7 @@ def test_small_batch_concurrent_callers():
         assert np.array_equal(g, oracle.batch_fixed(alg, d)), (alg, n, L)
 
 
+@pytest.mark.zero_copy
 def test_digest_small_concurrent_callers():
     """Pool threads calling digest at once (the executor's per-index
     crypto.digest) each get their own stream/slot: no crossed results."""
@@ -159,9 +181,13 @@ def test_fixed_golden_batches(golden):
                 assert sha(out) == row[alg], (alg, n, L, fl)
 
 
+@pytest.mark.zero_copy
+@pytest.mark.parametrize("path", ["ring", "zero_copy"])
 @pytest.mark.parametrize("alg", ALGS)
-def test_every_width_0_to_300(alg):
-    # every tail shape r = L % 64 (incl. 55/56/63/64/65 boundaries), partial warps/CTAs (n=133)
+def test_every_width_0_to_300(alg, path, hb_env):
+    # every tail shape r = L % 64 (incl. 55/56/63/64/65 boundaries), partial warps/CTAs (n=133);
+    # the ring reaches the TMA tiles from L = 144, the zero-copy path the direct loads at every width
+    hb_env.set(HB_ZERO_COPY_MAX=0 if path == "ring" else ZC_DEFAULT)
     for L in range(0, 301):
         n = 133
         data = oracle.fill_random(n * L, 77 + L).reshape(n, L)
@@ -668,11 +694,16 @@ def _every_length_cases():
         yield shift, off, oracle.fill_random(int(off[-1]) + 5, 17 + shift)
 
 
+@pytest.mark.zero_copy
+@pytest.mark.parametrize("path", ["ring", "zero_copy"])
 @pytest.mark.parametrize("alg", ALGS)
-def test_varlen_every_length_and_alignment(alg):
+def test_varlen_every_length_and_alignment(alg, path, hb_env):
     """Every length 0..260 (x3, shuffled, so message starts take every
     alignment mod 16) in one batch and in partial warps (n not a multiple of
-    32), with several leading offsets, sorted and unsorted."""
+    32), with several leading offsets, sorted and unsorted (the ring: device
+    buffers, length sort from 1,024 messages) and through the small-call
+    zero-copy path (mapped host memory, unsorted)."""
+    hb_env.set(HB_ZERO_COPY_MAX=0 if path == "ring" else ZC_DEFAULT)
     for shift, off, buf in _every_length_cases():
         ref = oracle.batch_varlen(alg, buf, off, threads=8)
         for k in (len(off) - 1, 31, 33, 1):
@@ -685,6 +716,7 @@ def test_varlen_every_length_and_alignment(alg):
 @pytest.mark.parametrize("alg", ALGS)
 def test_varlen_every_length_and_alignment_ab(alg, hb_env):
     C = _native.HB_FLAG_VARLEN_COOP
+    hb_env.set(HB_ZERO_COPY_MAX=0)  # device buffers and the length sort, as the arms were measured
     for shift, off, buf in _every_length_cases():
         ref = oracle.batch_varlen(alg, buf, off, threads=8)
         for k in (len(off) - 1, 31, 33, 1):
@@ -699,7 +731,9 @@ def test_varlen_every_length_and_alignment_ab(alg, hb_env):
                         ({"HB_VARLEN_KERNEL": "46"}, 0), ({"HB_VARLEN_KERNEL": "47"}, 0),
                         ({"HB_VARLEN_KERNEL": "48"}, 0), ({"HB_VARLEN_KERNEL": "49"}, 0),
                         ({"HB_VARLEN_KERNEL": "50"}, 0), ({"HB_VARLEN_KERNEL": "51"}, 0),
-                        ({"HB_VARLEN_KERNEL": "52"}, 0)):
+                        ({"HB_VARLEN_KERNEL": "52"}, 0), ({"HB_VARLEN_KERNEL": "53"}, 0),
+                        ({"HB_VARLEN_KERNEL": "54"}, 0), ({"HB_VARLEN_KERNEL": "55"}, 0),
+                        ({"HB_VARLEN_KERNEL": "56"}, 0)):
             hb_env.set(**env)
             got = batch_digest_varlen(alg, buf, off, flags=fl)
             assert np.array_equal(got, ref), (alg, shift, env)
