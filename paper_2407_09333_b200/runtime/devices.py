@@ -32,19 +32,15 @@ class DeviceSpec:
     host_mapped: bool = False
 
     def __post_init__(self):
-        problems = []
-        if not self.id:
-            problems.append("id must be non-empty")
-        if self.kind not in _KINDS:
-            problems.append(f"kind must be one of {_KINDS}, got {self.kind!r}")
-        if self.threads < 1:
-            problems.append(f"threads must be >= 1, got {self.threads}")
-        if self.mem_bytes <= 0:
-            problems.append(f"mem_bytes must be > 0, got {self.mem_bytes}")
-        if self.kind == "cuda" and self.ordinal < 0:
-            problems.append(f"ordinal must be >= 0, got {self.ordinal}")
-        if problems:
-            raise DeviceConfigError(f"device {self.id!r}: " + "; ".join(problems))
+        bad = [what for ok, what in (
+            (bool(self.id), "empty id"),
+            (self.kind in _KINDS, f"kind {self.kind!r} not in {_KINDS}"),
+            (self.threads >= 1, f"threads={self.threads} (need at least one)"),
+            (self.mem_bytes > 0, f"mem_bytes={self.mem_bytes} (need a positive capacity)"),
+            (self.kind != "cuda" or self.ordinal >= 0, f"ordinal={self.ordinal} (need a GPU index)"),
+        ) if not ok]
+        if bad:
+            raise DeviceConfigError(f"bad device spec {self.id!r}: {', '.join(bad)}")
 
 
 @dataclass(frozen=True)
@@ -54,13 +50,15 @@ class DeviceTable:
 
     def __post_init__(self):
         if self.host.kind != "host":
-            raise DeviceConfigError("host entry must have kind 'host'")
-        ids = [self.host.id] + [a.id for a in self.accels]
-        if len(set(ids)) != len(ids):
-            raise DeviceConfigError(f"duplicate device ids in {ids}")
-        for a in self.accels:
-            if a.kind != "cuda":
-                raise DeviceConfigError(f"accelerator {a.id!r} must have kind 'cuda'")
+            raise DeviceConfigError(f"table host {self.host.id!r} is of kind {self.host.kind!r}, expected 'host'")
+        seen = set()
+        for d in self.all_devices():
+            if d.id in seen:
+                raise DeviceConfigError(f"device id {d.id!r} appears more than once")
+            seen.add(d.id)
+        wrong = [a.id for a in self.accels if a.kind != "cuda"]
+        if wrong:
+            raise DeviceConfigError(f"accelerators {wrong} are not GPUs (kind 'cuda')")
 
     def all_devices(self) -> tuple[DeviceSpec, ...]:
         return (self.host, *self.accels)
@@ -72,10 +70,10 @@ class DeviceTable:
         return None
 
     def resolve(self, device_id: str) -> DeviceSpec:
-        d = self.get(device_id)
-        if d is None:
-            raise DeviceConfigError(f"unknown device {device_id!r}")
-        return d
+        found = self.get(device_id)
+        if found is None:
+            raise DeviceConfigError(f"no device {device_id!r} in this table")
+        return found
 
     def is_host_mapped(self, device_id: str) -> bool:
         d = self.resolve(device_id)

@@ -164,6 +164,25 @@ def test_from_reference_device_table():
         from_reference(RTable(RSpec("host", kind="host"), (RSpec("acc", host_mapped=True),)))
 
 
+@pytest.mark.parametrize("make", [
+    lambda: DeviceSpec(""),
+    lambda: DeviceSpec("g", kind="simulated_accel"),
+    lambda: DeviceSpec("g", threads=0),
+    lambda: DeviceSpec("g", mem_bytes=0),
+    lambda: DeviceSpec("g", ordinal=-1),
+    lambda: DeviceTable(DeviceSpec("h", kind="cuda")),
+    lambda: DeviceTable(DeviceSpec("h", kind="host"), (DeviceSpec("h"),)),
+    lambda: DeviceTable(DeviceSpec("h", kind="host"), (DeviceSpec("g"), DeviceSpec("g", ordinal=1))),
+    lambda: DeviceTable(DeviceSpec("h", kind="host"), (DeviceSpec("g", kind="host"),)),
+    lambda: DeviceTable(DeviceSpec("h", kind="host")).resolve("gpu9"),
+])
+def test_device_table_rejects(make):
+    """Every malformed spec or table, and an unknown id, raises DeviceConfigError."""
+    from paper_2407_09333_b200.runtime import DeviceConfigError
+    with pytest.raises(DeviceConfigError):
+        make()
+
+
 # ------------------------------------------------- variable length (§8(f) 3)
 def _var_table(mem=1 << 30, k=3, ordinals=None):
     host = DeviceSpec("host", kind="host", threads=4)
